@@ -1,0 +1,216 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * mggcn.h — C ABI of the B200-native MG-GCN full-batch training step (libmggcn.so).
+ *
+ * This is the drop-in boundary for the reference's training API (rowgcn, proj/include/rowgcn/):
+ * plain pointers and sizes, no C++ or torch types. Every entry point cites the reference interface it
+ * replaces. C++ callers use include/mggcn/rowgcn.hpp (same names and exceptions as rowgcn); Python
+ * callers use paper_2110_08688_b200 (ctypes). All calls return an mg_status; the message of the last
+ * failure on the calling thread is mg_last_error(). Status codes map 1:1 onto the reference's
+ * exception taxonomy (inc/errors.hpp:10-39) plus CUDA/NCCL failures.
+ *
+ * Ownership: objects returned through `**out` are owned by the caller and released with the matching
+ * *_free / *_destroy. Input arrays are borrowed for the duration of the call (copied when kept).
+ * Threading: calls on one object are not re-entrant (like train_run, inc/driver.hpp:140); distinct
+ * objects may be used from distinct threads.
+ */
+#ifndef MGGCN_H_
+#define MGGCN_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MG_ABI_VERSION 1
+
+typedef enum mg_status {
+  MG_OK = 0,
+  MG_SHAPE_ERROR = 1,    /* rowgcn::ShapeError    inc/errors.hpp:10 */
+  MG_VALUE_ERROR = 2,    /* rowgcn::ValueError    inc/errors.hpp:15 */
+  MG_PROTOCOL_ERROR = 3, /* rowgcn::ProtocolError inc/errors.hpp:20 */
+  MG_SHUTDOWN_ERROR = 4, /* rowgcn::ShutdownError inc/errors.hpp:25 */
+  MG_PARSE_ERROR = 5,    /* rowgcn::ParseError    inc/errors.hpp:30 */
+  MG_CONFIG_ERROR = 6,   /* rowgcn::ConfigError   inc/errors.hpp:35 */
+  MG_IO_ERROR = 7,       /* rowgcn::IoError       inc/errors.hpp:39 */
+  MG_CUDA_ERROR = 8,     /* CUDA runtime / launch failure (no reference analogue) */
+  MG_NCCL_ERROR = 9,     /* NCCL failure (the reference's collectives are in-process) */
+  MG_INTERNAL_ERROR = 10
+} mg_status;
+
+/* Borrowed CSR view, entry (u, v) = edge u -> v in row u (rowgcn::CsrMatrix, inc/sparse.hpp:25-55). */
+typedef struct mg_csr {
+  int64_t rows, cols;
+  const int64_t* row_ptr; /* rows + 1 */
+  const int64_t* col_idx; /* nnz, strictly increasing per row */
+  const float* values;    /* nnz */
+} mg_csr;
+
+/* Arithmetic modes of the device kernels (reported next to every number). */
+typedef enum mg_gemm_mode {
+  MG_GEMM_EXACT = 0,  /* SIMT, k-ascending separate mul/add: bitwise equal to rowgcn::gemm (f32) */
+  MG_GEMM_TF32X3 = 1, /* tcgen05 kind::tf32, 3-term split (hi*hi + hi*lo + lo*hi): fp32-level accuracy */
+  MG_GEMM_TF32 = 2    /* tcgen05 kind::tf32, single term (reported separately, rel ~1e-3) */
+} mg_gemm_mode;
+
+typedef enum mg_spmm_mode {
+  MG_SPMM_EXACT = 0, /* per-row column-order separate mul/add: bitwise equal to rowgcn::spmm (f32) */
+  MG_SPMM_FAST = 1   /* long rows split across warps + fixed-order second pass (deterministic, tolerance) */
+} mg_spmm_mode;
+
+/* rowgcn::GcnConfig (inc/gcn.hpp:14-36) plus the device arithmetic modes. */
+typedef struct mg_config {
+  const int64_t* layer_dims; /* [d0, d1, ..., dL] */
+  int32_t n_dims;
+  double lr, beta1, beta2, epsilon;
+  int32_t epochs;
+  uint64_t seed;
+  uint8_t permute, overlap, skip_first_backward_spmm, order_swap;
+  int32_t gemm_mode; /* mg_gemm_mode */
+  int32_t spmm_mode; /* mg_spmm_mode */
+} mg_config;
+
+/* Fills the reference defaults (inc/gcn.hpp:16-25): lr 0.01, betas 0.9/0.999, eps 1e-8, 100 epochs,
+ * seed 1, flags off; gemm_mode TF32X3, spmm_mode EXACT. layer_dims left NULL. */
+void mg_config_defaults(mg_config* cfg);
+/* GcnConfig::validate (inc/gcn.hpp:29-35) -> MG_CONFIG_ERROR. */
+mg_status mg_config_validate(const mg_config* cfg);
+
+const char* mg_last_error(void);
+int32_t mg_abi_version(void);
+/* Process-wide tuning knobs (no reference analogue; defaults in DESIGN.md):
+ *   "heavy_row"  nonzeros from which a tile row takes the cp.async hub-row SpMM path (default 4096)
+ *   "profile"    1 = record per-kernel CUDA events during steps (mg_group_last_profile). */
+mg_status mg_set_tuning(const char* key, int64_t value);
+
+/* ---------------------------------------------------------------- host datasets
+ * rowgcn::Dataset (inc/dataset.hpp:19-56). Held in host memory, float32. */
+typedef struct mg_dataset mg_dataset;
+
+/* rowgcn::synth_graph<float> (inc/dataset.hpp:287-334), bit-identical output. */
+mg_status mg_dataset_synth(int64_t n, double avg_degree, double exponent, uint64_t seed, int64_t feature_dim,
+                           int32_t classes, mg_dataset** out);
+/* Copies caller arrays into a dataset (the Dataset struct fields). train_mask may be NULL (= all). */
+mg_status mg_dataset_from_arrays(const mg_csr* graph, const float* features, int64_t d0, const int32_t* labels,
+                                 const uint8_t* train_mask, mg_dataset** out);
+/* Borrowed views into the dataset (valid until mg_dataset_free). *train_mask is NULL when absent. */
+mg_status mg_dataset_view(const mg_dataset* ds, mg_csr* graph, const float** features, int64_t* d0,
+                          const int32_t** labels, const uint8_t** train_mask);
+/* Dataset::num_classes (inc/dataset.hpp:51-55). */
+int32_t mg_dataset_num_classes(const mg_dataset* ds);
+/* Dataset::validate (inc/dataset.hpp:30-44) + CsrMatrix::validate (inc/sparse.hpp:37-54). */
+mg_status mg_dataset_validate(const mg_dataset* ds);
+void mg_dataset_free(mg_dataset* ds);
+
+/* ---------------------------------------------------------------- partitioner
+ * rowgcn::prepare_data (inc/driver.hpp:87-117): random_permutation (partition.hpp:69-79), permute
+ * rows/graph (:101-140), uniform_partition (:42-49), normalize_in_degree (sparse.hpp:94-107),
+ * transpose (:110-129), tile_rows (partition.hpp:173-225). Bit-identical to the reference.
+ * only_rank = -1 builds every row block's tiles; r >= 0 builds only row block r (one process per GPU). */
+typedef struct mg_partition mg_partition;
+
+mg_status mg_prepare(const mg_dataset* ds, const mg_config* cfg, int32_t workers, int32_t only_rank,
+                     mg_partition** out);
+/* n, global mask count and the P+1 part bounds (PartitionVector::bounds). */
+mg_status mg_partition_info(const mg_partition* p, int64_t* n, int64_t* mask_count, int64_t* bounds);
+/* dir 0 = forward tiles of A_hat^T, dir 1 = backward tiles of A_hat (PreparedData::fwd/bwd_tiles). */
+mg_status mg_partition_tile_info(const mg_partition* p, int32_t dir, int32_t i, int32_t j, int64_t* rows,
+                                 int64_t* cols, int64_t* nnz);
+mg_status mg_partition_tile_export(const mg_partition* p, int32_t dir, int32_t i, int32_t j, int64_t* row_ptr,
+                                   int64_t* col_idx, float* values);
+/* Permuted features (n x d0), labels, mask and the permutation's forward map (old id -> new id). */
+mg_status mg_partition_rows_export(const mg_partition* p, float* features, int32_t* labels, uint8_t* mask,
+                                   int64_t* perm_forward);
+void mg_partition_free(mg_partition* p);
+
+/* ---------------------------------------------------------------- device training group
+ * The set of GcnWorkers (inc/gcn.hpp:101-398) living in this process, plus their communicator
+ * (the reference's DeviceGroup, inc/collectives.hpp:58-203). One compute stream (lane 0) and one comm
+ * stream (lane 1) per worker; the staged SpMM's dependency graph (inc/dist_spmm.hpp:57-103) is
+ * reproduced with CUDA events.
+ *   world      total number of workers P (all processes)
+ *   n_local    workers driven by this process, with their ranks and CUDA devices
+ *   nccl_id    128-byte ncclUniqueId shared by all processes (mg_nccl_unique_id on one process), or
+ *              NULL when every rank is local.
+ *   transport  MG_TRANSPORT_AUTO picks NCCL when each local worker owns a distinct device (or the group
+ *              spans processes) and the in-process peer-copy transport otherwise (several workers per
+ *              device — the reference's DeviceGroup semantics, used to test P > #GPUs). */
+typedef struct mg_group mg_group;
+
+typedef enum mg_transport { MG_TRANSPORT_AUTO = 0, MG_TRANSPORT_NCCL = 1, MG_TRANSPORT_LOCAL = 2 } mg_transport;
+
+mg_status mg_nccl_unique_id(uint8_t id[128]);
+mg_status mg_group_create(const mg_config* cfg, const mg_partition* p, int32_t world, int32_t n_local,
+                          const int32_t* local_ranks, const int32_t* devices, const uint8_t* nccl_id,
+                          int32_t transport, mg_group** out);
+/* GcnWorker::init_params (inc/gcn.hpp:163-173): Glorot from Rng(seed) on the host, replicated. */
+mg_status mg_group_init_params(mg_group* g);
+/* GcnWorker::train_step(t) (inc/gcn.hpp:175-184). Synchronous; loss = global masked mean, acc =
+ * correct / mask count. wall_us (nullable) = device time from step start to optimizer completion on the
+ * first local worker (the reference's epoch wall_us, inc/driver.hpp:170-173). */
+mg_status mg_group_train_step(mg_group* g, int32_t t, double* loss, double* acc, double* wall_us);
+/* GcnWorker::compute_gradients (inc/gcn.hpp:208-217): W_G materialised, no update. */
+mg_status mg_group_compute_gradients(mg_group* g, double* loss, double* acc);
+/* GcnWorker::loss_only (inc/gcn.hpp:189-205): forward + masked loss, logits left in place. */
+mg_status mg_group_loss_only(mg_group* g, double* loss);
+/* GcnWorker::submit_forward (inc/gcn.hpp:238-267), synchronous. */
+mg_status mg_group_forward(mg_group* g);
+/* Asynchronous train step: enqueue only (no host sync). Results via mg_group_sync + mg_group_last_stats. */
+mg_status mg_group_train_step_async(mg_group* g, int32_t t);
+mg_status mg_group_sync(mg_group* g);
+mg_status mg_group_last_stats(mg_group* g, double* loss, double* acc);
+
+typedef enum mg_tensor {
+  MG_T_W = 0,      /* d_l x d_{l+1}      LayerParams::w      */
+  MG_T_WGRAD = 1,  /* d_l x d_{l+1}      LayerParams::w_grad */
+  MG_T_AHW = 2,    /* local_rows x d_{l+1}  BufferPool::ahw[l] */
+  MG_T_HW = 3,     /* local_rows x width    BufferPool::hw (width = d_{layer+1}, caller's view) */
+  MG_T_X = 4,      /* local_rows x d0     x_local */
+  MG_T_ADAM_M = 5,
+  MG_T_ADAM_V = 6,
+  MG_T_WSTAGE = 7  /* 8 d_l x d_{l+1}   the canonical-block W-grad staging buffer */
+} mg_tensor;
+
+/* Copies a tensor of local worker `rank` to/from host memory in the reference's dense layout
+ * (row-major, leading dimension = cols); count must equal the tensor's element count. */
+mg_status mg_group_read(mg_group* g, int32_t rank, int32_t which, int32_t layer, float* dst, int64_t count);
+mg_status mg_group_write(mg_group* g, int32_t rank, int32_t which, int32_t layer, const float* src, int64_t count);
+/* GcnWorker::w_hash (inc/gcn.hpp:221-226): FNV-1a over the W bytes of local worker `rank`. */
+mg_status mg_group_w_hash(mg_group* g, int32_t rank, uint64_t* hash);
+/* Local rows of worker `rank`: [row_begin, row_begin + rows). */
+mg_status mg_group_rows(mg_group* g, int32_t rank, int64_t* row_begin, int64_t* rows);
+/* BufferPool::large_buffer_count (inc/gcn.hpp:57) and the device allocation counter used by the L+3
+ * buffer audit (tests/test_gcn.cpp:350-368): allocations made inside steps must stay 0. */
+mg_status mg_group_buffer_audit(mg_group* g, int32_t* large_buffers, int64_t* step_allocations,
+                                int64_t* device_bytes);
+/* Device time accumulated since the previous call (then reset), in microseconds, measured with CUDA
+ * events on the launching stream of the first local worker when mg_set_tuning("profile", 1) is on:
+ * SpMM stages (light + hub-row kernels), GeMMs, and other kernels (loss, finalize/Adam); plus the number
+ * of kernels this library launched over the same steps (always counted). */
+mg_status mg_group_last_profile(mg_group* g, double* spmm_us, double* gemm_us, double* other_us,
+                                int64_t* kernels);
+void mg_group_destroy(mg_group* g);
+
+/* ---------------------------------------------------------------- kernel-level entry points
+ * Device pointers, caller's stream (cudaStream_t passed as void*, NULL = legacy default stream).
+ * Used by the parity tests and the micro-benchmarks (the reference's bench-spmm, proj/tools/main.cpp:120-178). */
+
+/* rowgcn::spmm (inc/sparse.hpp:161-188) on one tile: out[u, :w] = (accumulate ? out[u] : 0) +
+ * sum_e val_e * h[col_e, :w] over row u in column order. h and out are row-major with leading dimension
+ * ld (ld % 4 == 0, ld >= w, 16-byte aligned). edges = nnz {int32 col, float val} pairs. relu applies
+ * max(0, x) to the final value (the fused relu_forward of the last forward stage, dense.hpp:208-215). */
+mg_status mg_dev_spmm(int64_t rows, const int32_t* row_ptr, const void* edges, const float* h, float* out,
+                      int64_t w, int64_t ld, int32_t accumulate, int32_t relu, int32_t mode, void* stream);
+/* rowgcn::gemm (inc/dense.hpp:140-204) for the three step shapes, row-major with leading dims:
+ *   NN: C[M,N] = A[M,K] B[K,N]     TN: C[M,N] = A[K,M]^T B[K,N]     NT: C[M,N] = A[M,K] B[N,K]^T
+ * epilogue 0 = store, 1 = relu_backward mask: C = (C_old > 0 ? result : 0) (dense.hpp:221-231),
+ * 2 = relu_forward on the result. mode = mg_gemm_mode. */
+mg_status mg_dev_gemm(int32_t ta, int32_t tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                      const float* B, int64_t ldb, float* Cm, int64_t ldc, int32_t epilogue, int32_t mode,
+                      void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+#endif /* MGGCN_H_ */

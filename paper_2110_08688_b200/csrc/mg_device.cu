@@ -1,0 +1,1106 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Device half of libmggcn.so: the per-GPU GcnWorker state (L+3 buffer plan in HBM), the
+// communicator (NCCL, or the in-process rank-order transport when several workers share a device),
+// the staged 1D row-broadcast SpMM schedule on two streams with CUDA events, and the training step.
+// Reference: rowgcn inc/gcn.hpp (GcnWorker), inc/dist_spmm.hpp (staged SpMM), inc/collectives.hpp.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "mg_internal.hpp"
+#include "mg_kernels.cuh"
+#include "mg_tc_gemm.cuh"
+
+namespace mg {
+
+#define MG_CUDA(x)                                                                                     \
+  do {                                                                                                 \
+    cudaError_t _e = (x);                                                                              \
+    if (_e != cudaSuccess)                                                                             \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(_e) + " (" + __FILE__ + ":" +        \
+                      std::to_string(__LINE__) + ")");                                                 \
+  } while (0)
+#define MG_NCCL(x)                                                                                     \
+  do {                                                                                                 \
+    ncclResult_t _r = (x);                                                                             \
+    if (_r != ncclSuccess) throw NcclError(std::string(#x) + ": " + ncclGetErrorString(_r));          \
+  } while (0)
+#define MG_LAUNCHED() MG_CUDA(cudaGetLastError())
+
+namespace {
+
+inline index_t pad4(index_t d) { return (d + 3) / 4 * 4; }
+inline int ceil_div(index_t a, index_t b) { return static_cast<int>((a + b - 1) / b); }
+
+std::atomic<int> g_heavy_row{4096};
+std::atomic<int> g_profile{0};
+int heavy_threshold() { return g_heavy_row.load(); }
+
+int num_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+// ---------------------------------------------------------------- device CSR tile
+struct DevTile {
+  index_t rows = 0, cols = 0, nnz = 0;
+  int* row_ptr = nullptr;   // rows + 1 (int32)
+  int2* edges = nullptr;    // {col, float bits}
+  int* light = nullptr;     // rows with nnz < heavy threshold, by decreasing length
+  int n_light = 0;
+  int* heavy = nullptr;     // rows with nnz >= heavy threshold
+  int n_heavy = 0;
+};
+
+// Host-side construction of the launch lists for a tile (row order by decreasing length).
+void build_orders(const std::vector<index_t>& rp, std::vector<int>& light, std::vector<int>& heavy) {
+  const index_t rows = static_cast<index_t>(rp.size()) - 1;
+  const int ht = heavy_threshold();
+  light.clear();
+  heavy.clear();
+  for (index_t r = 0; r < rows; ++r) ((rp[r + 1] - rp[r]) >= ht ? heavy : light).push_back(static_cast<int>(r));
+  std::stable_sort(light.begin(), light.end(),
+                   [&](int a, int b) { return (rp[a + 1] - rp[a]) > (rp[b + 1] - rp[b]); });
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- kernel launchers (shared with C ABI)
+struct SpmmLaunch {
+  const int* row_ptr;
+  const int2* edges;
+  const int* light;
+  int n_light;
+  const int* heavy;
+  int n_heavy;
+};
+
+template <int G, int CPL>
+static void launch_rows(const SpmmLaunch& t, const float* h, float* out, int ld, int nchunk, int acc, int relu,
+                        cudaStream_t s) {
+  if (t.n_light <= 0) return;
+  const int gpb = 256 / G;
+  const int blocks = std::min(ceil_div(t.n_light, gpb), num_sms() * 16);
+  k::spmm_exact_rows<G, CPL><<<blocks, 256, 0, s>>>(t.row_ptr, t.edges, t.light, t.n_light, h, out, ld, nchunk, acc,
+                                                    relu);
+  MG_LAUNCHED();
+}
+
+// Light rows: pick the lane-group size G and chunks-per-lane CPL from the float4 width; widths above
+// 1024 floats are processed in column slabs (each slab re-walks the row's nonzeros).
+static int spmm_light(const SpmmLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, cudaStream_t s) {
+  const int nchunk_all = static_cast<int>(ld / 4);
+  int launches = 0;
+  for (int c0 = 0; c0 < nchunk_all; c0 += 256) {
+    const int nchunk = std::min(256, nchunk_all - c0);
+    const float* hs = h + 4 * c0;
+    float* os = out + 4 * c0;
+    const int L = static_cast<int>(ld);
+    if (nchunk <= 1) launch_rows<1, 1>(t, hs, os, L, nchunk, acc, relu, s);
+    else if (nchunk <= 2) launch_rows<2, 1>(t, hs, os, L, nchunk, acc, relu, s);
+    else if (nchunk <= 4) launch_rows<4, 1>(t, hs, os, L, nchunk, acc, relu, s);
+    else if (nchunk <= 8) launch_rows<8, 1>(t, hs, os, L, nchunk, acc, relu, s);
+    else if (nchunk <= 16) launch_rows<16, 1>(t, hs, os, L, nchunk, acc, relu, s);
+    else if (nchunk <= 32) launch_rows<32, 1>(t, hs, os, L, nchunk, acc, relu, s);
+    else if (nchunk <= 64) launch_rows<32, 2>(t, hs, os, L, nchunk, acc, relu, s);
+    else if (nchunk <= 96) launch_rows<32, 3>(t, hs, os, L, nchunk, acc, relu, s);
+    else if (nchunk <= 128) launch_rows<32, 4>(t, hs, os, L, nchunk, acc, relu, s);
+    else if (nchunk <= 192) launch_rows<32, 6>(t, hs, os, L, nchunk, acc, relu, s);
+    else launch_rows<32, 8>(t, hs, os, L, nchunk, acc, relu, s);
+    ++launches;
+  }
+  return launches;
+}
+
+static int spmm_heavy(const SpmmLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, cudaStream_t s) {
+  if (t.n_heavy <= 0) return 0;
+  static bool attr = false;
+  if (!attr) {
+    MG_CUDA(cudaFuncSetAttribute(k::spmm_exact_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(k::kHeavySmem)));
+    attr = true;
+  }
+  const int nslab = ceil_div(ld, k::kHeavySlab);
+  k::spmm_exact_heavy<<<t.n_heavy * nslab, 256, k::kHeavySmem, s>>>(t.row_ptr, t.edges, t.heavy, nslab, h, out,
+                                                                   static_cast<int>(ld), acc, relu);
+  MG_LAUNCHED();
+  return 1;
+}
+
+// GeMM dispatch: exact SIMT or tcgen05 (mg_tc_gemm.cuh).
+static int gemm_launch(int mode, bool ta, bool tb, index_t M, index_t N, index_t K, const float* A, index_t lda,
+                       const float* B, index_t ldb, float* Cm, index_t ldc, int epi, cudaStream_t s) {
+  if (M <= 0 || N <= 0) return 0;
+  if (mode != MG_GEMM_EXACT) return tc::gemm(mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, s);
+  dim3 grid(ceil_div(M, k::kGBM), ceil_div(N, k::kGBN));
+#define MG_G(TA, TB, E) k::gemm_exact<TA, TB, E><<<grid, 256, 0, s>>>((int)M, (int)N, (int)K, A, lda, B, ldb, Cm, ldc)
+  if (!ta && !tb) {
+    if (epi == 0) MG_G(false, false, 0); else if (epi == 1) MG_G(false, false, 1); else MG_G(false, false, 2);
+  } else if (ta && !tb) {
+    if (epi == 0) MG_G(true, false, 0); else if (epi == 1) MG_G(true, false, 1); else MG_G(true, false, 2);
+  } else if (!ta && tb) {
+    if (epi == 0) MG_G(false, true, 0); else if (epi == 1) MG_G(false, true, 1); else MG_G(false, true, 2);
+  } else {
+    throw ValueError("gemm: transposed A and B together is not on the training path");
+  }
+#undef MG_G
+  MG_LAUNCHED();
+  return 1;
+}
+
+// ======================================================================== worker
+struct Worker {
+  int rank = 0, device = 0;
+  index_t r0 = 0, rows = 0;
+  cudaStream_t s0 = nullptr, s1 = nullptr, s2 = nullptr;  // compute (lane 0), comm (lane 1), heavy-row side
+  std::vector<DevTile> tiles[2];
+  float* x = nullptr;
+  int* labels = nullptr;
+  uint8_t* mask = nullptr;
+  std::vector<float*> ahw;
+  float *hw = nullptr, *bc1 = nullptr, *bc2 = nullptr;
+  std::vector<float*> W, WG, M, V, stage;
+  double* partials = nullptr;
+  double* stats = nullptr;
+  double* h_stats = nullptr;  // pinned
+  int loss_blocks = 0;
+  ncclComm_t comm = nullptr;
+  // events (reused every step)
+  cudaEvent_t prior, heavy_fork, heavy_join, loss_done, stats_done, src_ready, copy_done, ar_ready, ar_done;
+  std::vector<cudaEvent_t> bc_done, mult, wg_done, red_done;
+  cudaEvent_t t_start, t_end;
+  std::vector<void*> allocs;
+  index_t bytes = 0;
+};
+
+}  // namespace mg
+
+struct mg_group {
+  mg::Config cfg;
+  int world = 1;
+  int transport = MG_TRANSPORT_NCCL;
+  mg::index_t n = 0, mask_count = 0;
+  std::vector<mg::index_t> bounds;
+  mg::index_t wblocks[9] = {};  // canonical W-grad blocks uniform_partition(n, 8), driver.hpp:156
+  std::vector<mg::index_t> ld;  // padded widths per dim
+  mg::index_t ld_max = 4, max_part = 0;
+  std::vector<std::unique_ptr<mg::Worker>> workers;
+  bool sealed = false;  // set after construction: allocations afterwards count as step allocations
+  mg::index_t step_allocs = 0;
+  bool labels_ok = true;
+  std::string label_error;
+  int kernels_last = 0;
+  int64_t kernels_total = 0;  // since the last mg_group_last_profile
+  std::vector<cudaEvent_t> prof_pool;
+  size_t prof_used = 0;
+  std::vector<std::pair<int, int>> prof_pending;  // (kind, index of the start event)
+  double last_loss = 0, last_acc = 0;
+  bool stats_pending = false;
+};
+
+namespace mg {
+namespace {
+
+void* dalloc(mg_group& g, Worker& w, size_t bytes) {
+  if (g.sealed) g.step_allocs++;
+  void* p = nullptr;
+  MG_CUDA(cudaSetDevice(w.device));
+  MG_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+  MG_CUDA(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
+  w.allocs.push_back(p);
+  w.bytes += static_cast<index_t>(bytes);
+  return p;
+}
+
+template <class T>
+T* dalloc_t(mg_group& g, Worker& w, size_t count) {
+  return static_cast<T*>(dalloc(g, w, sizeof(T) * count));
+}
+
+void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
+  d.rows = t.rows;
+  d.cols = t.cols;
+  d.nnz = t.nnz();
+  if (d.nnz >= (index_t(1) << 31)) throw ValueError("tile has >= 2^31 nonzeros; split the graph over more workers");
+  std::vector<int> rp32(t.rows + 1);
+  for (index_t r = 0; r <= t.rows; ++r) rp32[r] = static_cast<int>(t.row_ptr[r]);
+  std::vector<int2> ed(d.nnz);
+  parallel_for(d.nnz, [&](index_t b, index_t e) {
+    for (index_t i = b; i < e; ++i) {
+      int bits;
+      std::memcpy(&bits, &t.val[i], 4);
+      ed[i] = make_int2(t.col[i], bits);
+    }
+  });
+  std::vector<int> light, heavy;
+  build_orders(t.row_ptr, light, heavy);
+  d.row_ptr = dalloc_t<int>(g, w, rp32.size());
+  d.edges = dalloc_t<int2>(g, w, std::max<index_t>(1, d.nnz));
+  d.light = dalloc_t<int>(g, w, std::max<size_t>(1, light.size()));
+  d.heavy = dalloc_t<int>(g, w, std::max<size_t>(1, heavy.size()));
+  d.n_light = static_cast<int>(light.size());
+  d.n_heavy = static_cast<int>(heavy.size());
+  MG_CUDA(cudaMemcpy(d.row_ptr, rp32.data(), sizeof(int) * rp32.size(), cudaMemcpyHostToDevice));
+  if (d.nnz) MG_CUDA(cudaMemcpy(d.edges, ed.data(), sizeof(int2) * d.nnz, cudaMemcpyHostToDevice));
+  if (!light.empty()) MG_CUDA(cudaMemcpy(d.light, light.data(), sizeof(int) * light.size(), cudaMemcpyHostToDevice));
+  if (!heavy.empty()) MG_CUDA(cudaMemcpy(d.heavy, heavy.data(), sizeof(int) * heavy.size(), cudaMemcpyHostToDevice));
+}
+
+// Copies rows x cols (host, dense) into a device buffer with leading dimension ld (padding = 0).
+void upload_padded(float* dst, const float* src, index_t rows, index_t cols, index_t ld) {
+  if (cols == ld) {
+    MG_CUDA(cudaMemcpy(dst, src, sizeof(float) * rows * cols, cudaMemcpyHostToDevice));
+    return;
+  }
+  MG_CUDA(cudaMemcpy2D(dst, sizeof(float) * ld, src, sizeof(float) * cols, sizeof(float) * cols, rows,
+                       cudaMemcpyHostToDevice));
+}
+
+void download_padded(float* dst, const float* src, index_t rows, index_t cols, index_t ld) {
+  if (cols == ld) {
+    MG_CUDA(cudaMemcpy(dst, src, sizeof(float) * rows * cols, cudaMemcpyDeviceToHost));
+    return;
+  }
+  MG_CUDA(cudaMemcpy2D(dst, sizeof(float) * cols, src, sizeof(float) * ld, sizeof(float) * cols, rows,
+                       cudaMemcpyDeviceToHost));
+}
+
+cudaEvent_t mk_event(bool timing = false) {
+  cudaEvent_t e;
+  MG_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+  return e;
+}
+
+// ---------------------------------------------------------------- the step (one process, all local workers)
+class Step {
+ public:
+  explicit Step(mg_group& g) : g_(g), cfg_(g.cfg), L_(g.cfg.layers()), P_(g.world) {}
+
+  Worker& W(size_t k) { return *g_.workers[k]; }
+  size_t nloc() const { return g_.workers.size(); }
+  void dev(Worker& w) { MG_CUDA(cudaSetDevice(w.device)); }
+
+  // -------------------------------------------------------------- collectives
+  // DeviceGroup::broadcast_bytes (collectives.cpp:110-125) on the comm streams.
+  void bcast(int root, size_t count, const std::vector<float*>& bufs) {
+    if (P_ == 1) return;
+    if (g_.transport == MG_TRANSPORT_NCCL) {
+      MG_NCCL(ncclGroupStart());
+      for (size_t k = 0; k < nloc(); ++k) {
+        Worker& w = W(k);
+        dev(w);
+        MG_NCCL(ncclBroadcast(bufs[k], bufs[k], count, ncclFloat, root, w.comm, w.s1));
+      }
+      MG_NCCL(ncclGroupEnd());
+      return;
+    }
+    // in-process: receivers copy from the root's buffer once it is ready; the root's comm stream then
+    // waits for every copy so nothing downstream of the broadcast can overwrite the source early.
+    size_t rk = 0;
+    for (size_t k = 0; k < nloc(); ++k)
+      if (W(k).rank == root) rk = k;
+    Worker& R = W(rk);
+    dev(R);
+    MG_CUDA(cudaEventRecord(R.src_ready, R.s1));
+    for (size_t k = 0; k < nloc(); ++k) {
+      if (k == rk) continue;
+      Worker& w = W(k);
+      dev(w);
+      MG_CUDA(cudaStreamWaitEvent(w.s1, R.src_ready, 0));
+      MG_CUDA(cudaMemcpyAsync(bufs[k], bufs[rk], sizeof(float) * count, cudaMemcpyDeviceToDevice, w.s1));
+      MG_CUDA(cudaEventRecord(w.copy_done, w.s1));
+      dev(R);
+      MG_CUDA(cudaStreamWaitEvent(R.s1, w.copy_done, 0));
+    }
+  }
+
+  // DeviceGroup::all_reduce_sum (collectives.hpp:76-94), no-op at P == 1.
+  template <class T>
+  void allreduce(size_t count, const std::vector<T*>& bufs) {
+    if (P_ == 1 || count == 0) return;
+    if (g_.transport == MG_TRANSPORT_NCCL) {
+      MG_NCCL(ncclGroupStart());
+      for (size_t k = 0; k < nloc(); ++k) {
+        Worker& w = W(k);
+        dev(w);
+        MG_NCCL(ncclAllReduce(bufs[k], bufs[k], count, sizeof(T) == 8 ? ncclDouble : ncclFloat, ncclSum, w.comm, w.s1));
+      }
+      MG_NCCL(ncclGroupEnd());
+      return;
+    }
+    Worker& R = W(0);
+    for (size_t k = 1; k < nloc(); ++k) {
+      Worker& w = W(k);
+      dev(w);
+      MG_CUDA(cudaEventRecord(w.ar_ready, w.s1));
+      dev(R);
+      MG_CUDA(cudaStreamWaitEvent(R.s1, w.ar_ready, 0));
+    }
+    dev(R);
+    k::PtrList<T> pl{};
+    for (size_t k = 0; k < nloc(); ++k) pl.p[W(k).rank] = bufs[k];
+    const int blocks = std::min<long>(1024, (static_cast<long>(count) + 255) / 256);
+    k::rank_order_allreduce<T><<<blocks, 256, 0, R.s1>>>(pl, P_, static_cast<long>(count));
+    MG_LAUNCHED();
+    ++g_.kernels_last;
+    MG_CUDA(cudaEventRecord(R.ar_done, R.s1));
+    for (size_t k = 1; k < nloc(); ++k) {
+      Worker& w = W(k);
+      dev(w);
+      MG_CUDA(cudaStreamWaitEvent(w.s1, R.ar_done, 0));
+    }
+  }
+
+  // -------------------------------------------------------------- staged SpMM
+  // staged_spmm_submit (inc/dist_spmm.hpp:57-103): stage j broadcasts worker j's rows of `src` into
+  // bc[j % 2] (or bc1 without overlap) on the comm stream, then every worker multiplies its (me, j)
+  // tile on the compute stream, accumulating for j > 0. Event edges:
+  //   spmm(j) <- broadcast(j);   broadcast(j) <- spmm(j-2) overlapped / spmm(j-1) otherwise / prior.
+  // relu_last fuses the forward ReLU into the final stage's epilogue.
+  void staged_spmm(int dir, index_t width, const std::vector<float*>& src, const std::vector<float*>& out,
+                   bool relu_last) {
+    const index_t ld = pad4(width);
+    const bool ov = cfg_.overlap;
+    for (size_t k = 0; k < nloc(); ++k) {
+      dev(W(k));
+      MG_CUDA(cudaEventRecord(W(k).prior, W(k).s0));
+    }
+    for (int j = 0; j < P_; ++j) {
+      std::vector<float*> recv(nloc());
+      for (size_t k = 0; k < nloc(); ++k) {
+        Worker& w = W(k);
+        dev(w);
+        cudaEvent_t dep = ov ? (j >= 2 ? w.mult[j - 2] : w.prior) : (j >= 1 ? w.mult[j - 1] : w.prior);
+        MG_CUDA(cudaStreamWaitEvent(w.s1, dep, 0));
+        recv[k] = (w.rank == j) ? src[k] : ((!ov || j % 2 == 0) ? w.bc1 : w.bc2);
+      }
+      const size_t count = static_cast<size_t>((g_.bounds[j + 1] - g_.bounds[j]) * ld);
+      bcast(j, count, recv);
+      for (size_t k = 0; k < nloc(); ++k) {
+        Worker& w = W(k);
+        dev(w);
+        MG_CUDA(cudaEventRecord(w.bc_done[j], w.s1));
+        MG_CUDA(cudaStreamWaitEvent(w.s0, w.bc_done[j], 0));
+        const DevTile& t = w.tiles[dir][j];
+        SpmmLaunch sl{t.row_ptr, t.edges, t.light, t.n_light, t.heavy, t.n_heavy};
+        const int acc = j > 0, relu = relu_last && j == P_ - 1;
+        const int pi = prof_begin(w);
+        if (t.n_heavy > 0) {  // hub rows run beside the light rows on the side stream
+          MG_CUDA(cudaEventRecord(w.heavy_fork, w.s0));
+          MG_CUDA(cudaStreamWaitEvent(w.s2, w.heavy_fork, 0));
+          g_.kernels_last += spmm_heavy(sl, recv[k], out[k], ld, acc, relu, w.s2);
+          MG_CUDA(cudaEventRecord(w.heavy_join, w.s2));
+        }
+        g_.kernels_last += spmm_light(sl, recv[k], out[k], ld, acc, relu, w.s0);
+        if (t.n_heavy > 0) MG_CUDA(cudaStreamWaitEvent(w.s0, w.heavy_join, 0));
+        prof_end(w, pi, 0);
+        MG_CUDA(cudaEventRecord(w.mult[j], w.s0));
+      }
+    }
+  }
+
+  void gemm(Worker& w, bool ta, bool tb, index_t M, index_t N, index_t K, const float* A, index_t lda, const float* B,
+            index_t ldb, float* Cm, index_t ldc, int epi) {
+    const int pi = prof_begin(w);
+    g_.kernels_last += gemm_launch(cfg_.gemm_mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, w.s0);
+    prof_end(w, pi, 1);
+  }
+
+  // -------------------------------------------------------------- optional per-kernel timing
+  // Event pairs on the launching (compute) stream of the first local worker; enabled with
+  // mg_set_tuning("profile", 1), summed by mg_group_last_profile. kind 0 = SpMM stage, 1 = GeMM, 2 = other.
+  int prof_begin(Worker& w) {
+    if (!g_profile.load() || &w != g_.workers[0].get()) return -1;
+    if (g_.prof_used + 2 > g_.prof_pool.size()) {
+      for (int i = 0; i < 512; ++i) g_.prof_pool.push_back(mk_event(true));
+    }
+    const int idx = static_cast<int>(g_.prof_used);
+    g_.prof_used += 2;
+    MG_CUDA(cudaEventRecord(g_.prof_pool[idx], w.s0));
+    return idx;
+  }
+  void prof_end(Worker& w, int idx, int kind) {
+    if (idx < 0) return;
+    MG_CUDA(cudaEventRecord(g_.prof_pool[idx + 1], w.s0));
+    g_.prof_pending.emplace_back(kind, idx);
+  }
+
+  // -------------------------------------------------------------- forward (gcn.hpp:238-267)
+  void forward() {
+    for (int l = 0; l < L_; ++l) {
+      const index_t dl = cfg_.dims[l], dl1 = cfg_.dims[l + 1];
+      const index_t ldl = g_.ld[l], ldl1 = g_.ld[l + 1];
+      const bool swap = cfg_.order_swap && dl < dl1;  // gcn.hpp:145-148
+      std::vector<float*> src(nloc()), out(nloc());
+      for (size_t k = 0; k < nloc(); ++k) {
+        Worker& w = W(k);
+        dev(w);
+        const float* h_in = l == 0 ? w.x : w.ahw[l - 1];
+        if (!swap) {
+          gemm(w, false, false, w.rows, ldl1, dl, h_in, ldl, w.W[l], ldl1, w.hw, ldl1, 0);
+          src[k] = w.hw;
+        } else {
+          src[k] = const_cast<float*>(h_in);
+        }
+        out[k] = swap ? w.hw : w.ahw[l];
+      }
+      staged_spmm(0, swap ? dl : dl1, src, out, !swap && l < L_ - 1);
+      if (swap) {
+        for (size_t k = 0; k < nloc(); ++k) {
+          Worker& w = W(k);
+          dev(w);
+          gemm(w, false, false, w.rows, ldl1, dl, w.hw, ldl, w.W[l], ldl1, w.ahw[l], ldl1, l < L_ - 1 ? 2 : 0);
+        }
+      }
+    }
+  }
+
+  // -------------------------------------------------------------- loss (gcn.hpp:271-290)
+  void loss_grad() {
+    const index_t C = cfg_.dims[L_];
+    const float inv_denom = 1.0f / static_cast<float>(g_.mask_count);
+    std::vector<double*> st(nloc());
+    for (size_t k = 0; k < nloc(); ++k) {
+      Worker& w = W(k);
+      dev(w);
+      const int pi = prof_begin(w);
+      if (w.rows > 0) {
+        k::softmax_xent<<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
+                                                         static_cast<int>(w.rows), static_cast<int>(C), w.labels,
+                                                         w.mask, inv_denom, w.partials);
+        MG_LAUNCHED();
+        ++g_.kernels_last;
+      }
+      k::finalize_stats<<<1, 32, 0, w.s0>>>(w.partials, w.rows > 0 ? w.loss_blocks : 0, w.stats);
+      MG_LAUNCHED();
+      ++g_.kernels_last;
+      prof_end(w, pi, 2);
+      MG_CUDA(cudaEventRecord(w.loss_done, w.s0));
+      MG_CUDA(cudaStreamWaitEvent(w.s1, w.loss_done, 0));
+      st[k] = w.stats;
+    }
+    allreduce<double>(2, st);
+    for (size_t k = 0; k < nloc(); ++k) {
+      Worker& w = W(k);
+      dev(w);
+      MG_CUDA(cudaMemcpyAsync(w.h_stats, w.stats, 2 * sizeof(double), cudaMemcpyDeviceToHost, w.s1));
+      MG_CUDA(cudaEventRecord(w.stats_done, w.s1));
+    }
+  }
+
+  // -------------------------------------------------------------- backward (gcn.hpp:292-350)
+  void backward() {
+    for (int l = L_ - 1; l >= 0; --l) {
+      const index_t dl = cfg_.dims[l], dl1 = cfg_.dims[l + 1];
+      const index_t ldl = g_.ld[l], ldl1 = g_.ld[l + 1];
+      const bool skip = l == 0 && cfg_.skip_first_backward_spmm;
+      std::vector<float*> grad_rows(nloc());
+      if (!skip) {
+        std::vector<float*> src(nloc()), out(nloc());
+        for (size_t k = 0; k < nloc(); ++k) {
+          src[k] = W(k).ahw[l];
+          out[k] = W(k).hw;
+        }
+        staged_spmm(1, dl1, src, out, false);
+        grad_rows = out;
+      } else {
+        for (size_t k = 0; k < nloc(); ++k) grad_rows[k] = W(k).ahw[l];
+      }
+      // W_G staging over the 8 canonical row blocks (gcn.hpp:309-331), then one all-reduce.
+      std::vector<float*> stg(nloc());
+      const index_t bs = ldl * ldl1;
+      for (size_t k = 0; k < nloc(); ++k) {
+        Worker& w = W(k);
+        dev(w);
+        const float* h_in = l == 0 ? w.x : w.ahw[l - 1];
+        for (int b = 0; b < 8; ++b) {
+          const index_t a = std::max(g_.wblocks[b], w.r0), e = std::min(g_.wblocks[b + 1], w.r0 + w.rows);
+          float* dst = w.stage[l] + b * bs;
+          if (a >= e) {
+            MG_CUDA(cudaMemsetAsync(dst, 0, sizeof(float) * bs, w.s0));
+            continue;
+          }
+          gemm(w, true, false, ldl, ldl1, e - a, h_in + (a - w.r0) * ldl, ldl, grad_rows[k] + (a - w.r0) * ldl1, ldl1,
+               dst, ldl1, 0);
+        }
+        MG_CUDA(cudaEventRecord(w.wg_done[l], w.s0));
+        MG_CUDA(cudaStreamWaitEvent(w.s1, w.wg_done[l], 0));
+        stg[k] = w.stage[l];
+      }
+      allreduce<float>(static_cast<size_t>(8 * bs), stg);
+      for (size_t k = 0; k < nloc(); ++k) {
+        Worker& w = W(k);
+        dev(w);
+        MG_CUDA(cudaEventRecord(w.red_done[l], w.s1));
+      }
+      if (l > 0) {  // H_G = HW_G W^T fused with relu_backward into ahw[l-1] (gcn.hpp:337-348)
+        for (size_t k = 0; k < nloc(); ++k) {
+          Worker& w = W(k);
+          dev(w);
+          gemm(w, false, true, w.rows, ldl, dl1, grad_rows[k], ldl1, w.W[l], ldl1, w.ahw[l - 1], ldl, 1);
+        }
+      }
+      (void)dl;
+    }
+  }
+
+  // -------------------------------------------------------------- finalize (gcn.hpp:354-377 + adam :61-85)
+  void finalize(bool adam, int t) {
+    k::AdamConsts c{};
+    if (adam) {
+      if (t < 1) throw ValueError("adam_step: step index must be >= 1, got " + std::to_string(t));
+      c.b1 = static_cast<float>(cfg_.beta1);
+      c.b2 = static_cast<float>(cfg_.beta2);
+      c.one_m_b1 = 1.0f - c.b1;
+      c.one_m_b2 = 1.0f - c.b2;
+      c.lr = static_cast<float>(cfg_.lr);
+      c.eps = static_cast<float>(cfg_.epsilon);
+      c.corr1 = 1.0f - static_cast<float>(std::pow(cfg_.beta1, t));
+      c.corr2 = 1.0f - static_cast<float>(std::pow(cfg_.beta2, t));
+    }
+    for (size_t k = 0; k < nloc(); ++k) {
+      Worker& w = W(k);
+      dev(w);
+      for (int l = 0; l < L_; ++l) MG_CUDA(cudaStreamWaitEvent(w.s0, w.red_done[l], 0));
+      const int pi = prof_begin(w);
+      for (int l = 0; l < L_; ++l) {
+        const int size = static_cast<int>(g_.ld[l] * g_.ld[l + 1]);
+        k::finalize_adam<<<std::min(1024, (size + 255) / 256), 256, 0, w.s0>>>(size, 8, w.stage[l], w.W[l], w.WG[l],
+                                                                              w.M[l], w.V[l], adam ? 1 : 0, c);
+        MG_LAUNCHED();
+        ++g_.kernels_last;
+      }
+      prof_end(w, pi, 2);
+    }
+  }
+
+  void begin() {
+    g_.kernels_last = 0;
+    if (!g_.labels_ok) throw ValueError(g_.label_error);
+    for (size_t k = 0; k < nloc(); ++k) {
+      Worker& w = W(k);
+      dev(w);
+      // the previous step's stats read-back (comm stream) must finish before the stats are rewritten
+      MG_CUDA(cudaStreamWaitEvent(w.s0, w.stats_done, 0));
+      MG_CUDA(cudaEventRecord(w.t_start, w.s0));
+    }
+  }
+
+  void end() {
+    for (size_t k = 0; k < nloc(); ++k) {
+      Worker& w = W(k);
+      dev(w);
+      MG_CUDA(cudaEventRecord(w.t_end, w.s0));
+    }
+    g_.kernels_total += g_.kernels_last;
+  }
+
+ private:
+  mg_group& g_;
+  const Config& cfg_;
+  int L_, P_;
+};
+
+void sync_all(mg_group& g) {
+  for (auto& wp : g.workers) {
+    MG_CUDA(cudaSetDevice(wp->device));
+    MG_CUDA(cudaStreamSynchronize(wp->s0));
+    MG_CUDA(cudaStreamSynchronize(wp->s1));
+    MG_CUDA(cudaStreamSynchronize(wp->s2));
+  }
+}
+
+void read_stats(mg_group& g) {
+  Worker& w = *g.workers[0];
+  MG_CUDA(cudaSetDevice(w.device));
+  MG_CUDA(cudaEventSynchronize(w.stats_done));
+  g.last_loss = w.h_stats[0] / static_cast<double>(g.mask_count);
+  g.last_acc = w.h_stats[1] / static_cast<double>(g.mask_count);
+}
+
+}  // namespace
+}  // namespace mg
+
+using namespace mg;
+
+// ======================================================================== C ABI (device half)
+extern "C" {
+
+mg_status mg_set_tuning(const char* key, int64_t value) {
+  return guarded([&] {
+    const std::string k = key ? key : "";
+    if (k == "heavy_row") {
+      if (value < 1) throw ValueError("tuning: heavy_row must be >= 1");
+      g_heavy_row = static_cast<int>(std::min<int64_t>(value, 1 << 30));
+    } else if (k == "profile") {
+      g_profile = value != 0 ? 1 : 0;
+    } else {
+      throw ValueError("tuning: unknown key '" + k + "'");
+    }
+  });
+}
+
+mg_status mg_nccl_unique_id(uint8_t id[128]) {
+  return guarded([&] {
+    ncclUniqueId u;
+    MG_NCCL(ncclGetUniqueId(&u));
+    static_assert(sizeof(u) == 128, "ncclUniqueId size");
+    std::memcpy(id, &u, 128);
+  });
+}
+
+mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t world, int32_t n_local,
+                          const int32_t* local_ranks, const int32_t* devices, const uint8_t* nccl_id,
+                          int32_t transport, mg_group** out) {
+  return guarded([&] {
+    if (!p || !out || n_local < 1 || !local_ranks || !devices) throw ValueError("group: bad arguments");
+    auto g = std::make_unique<mg_group>();
+    g->cfg = to_config(cfgp);
+    const Config& cfg = g->cfg;
+    if (cfg.dims.front() != p->d0)
+      throw ConfigError("config: layer_dims[0]=" + std::to_string(cfg.dims.front()) +
+                        " but dataset features have width " + std::to_string(p->d0));
+    if (world != p->parts)
+      throw ValueError("group: world " + std::to_string(world) + " but the partition has P=" +
+                       std::to_string(p->parts));
+    if (cfg.dims.back() > 32 * k::kLossCpl)
+      throw ValueError("loss: more than " + std::to_string(32 * k::kLossCpl) + " classes is not supported");
+    if (cfg.gemm_mode != MG_GEMM_EXACT && !tc::available())
+      throw ValueError("gemm_mode " + std::to_string(cfg.gemm_mode) + " needs the tcgen05 kernels (sm_100a)");
+    g->world = world;
+    g->n = p->n;
+    g->mask_count = p->mask_count;
+    g->bounds = p->bounds;
+    for (index_t d : cfg.dims) g->ld.push_back(pad4(d));
+    for (size_t i = 1; i < g->ld.size(); ++i) g->ld_max = std::max(g->ld_max, g->ld[i]);
+    if (cfg.order_swap) g->ld_max = std::max(g->ld_max, g->ld[0]);
+    for (int i = 0; i < world; ++i) g->max_part = std::max(g->max_part, p->bounds[i + 1] - p->bounds[i]);
+    for (int b = 0; b <= 8; ++b) g->wblocks[b] = static_cast<index_t>(b) * p->n / 8;  // driver.hpp:156
+    // transport
+    std::vector<int> devs(devices, devices + n_local);
+    std::vector<int> sorted = devs;
+    std::sort(sorted.begin(), sorted.end());
+    const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+    if (transport == MG_TRANSPORT_AUTO) transport = (distinct || n_local < world) ? MG_TRANSPORT_NCCL : MG_TRANSPORT_LOCAL;
+    if (transport == MG_TRANSPORT_LOCAL && n_local != world)
+      throw ValueError("group: the in-process transport needs every rank local");
+    if (transport == MG_TRANSPORT_LOCAL && world > k::kMaxLocal)
+      throw ValueError("group: the in-process transport supports at most " + std::to_string(k::kMaxLocal) + " workers");
+    if (transport == MG_TRANSPORT_NCCL && !distinct)
+      throw ValueError("group: NCCL needs one device per local worker");
+    if (transport == MG_TRANSPORT_NCCL && n_local < world && !nccl_id)
+      throw ValueError("group: ranks in other processes need the shared nccl_id");
+    g->transport = transport;
+    // labels in range for masked rows (checked where the reference checks, at the loss: dense.hpp:263)
+    const index_t C = cfg.dims.back();
+    for (index_t v = 0; v < p->n && g->labels_ok; ++v)
+      if (p->mask[v] && (p->labels[v] < 0 || p->labels[v] >= C)) {
+        g->labels_ok = false;
+        g->label_error = "softmax_xent: label " + std::to_string(p->labels[v]) + " out of range [0, " +
+                         std::to_string(C) + ") at row " + std::to_string(v);
+      }
+    const int L = cfg.layers();
+    for (int k = 0; k < n_local; ++k) {
+      auto wp = std::make_unique<Worker>();
+      Worker& w = *wp;
+      w.rank = local_ranks[k];
+      w.device = devices[k];
+      if (w.rank < 0 || w.rank >= world) throw ValueError("group: rank out of range");
+      if (!p->has_row(w.rank)) throw ValueError("group: partition lacks row block " + std::to_string(w.rank));
+      w.r0 = p->bounds[w.rank];
+      w.rows = p->bounds[w.rank + 1] - w.r0;
+      MG_CUDA(cudaSetDevice(w.device));
+      MG_CUDA(cudaStreamCreateWithFlags(&w.s0, cudaStreamNonBlocking));
+      MG_CUDA(cudaStreamCreateWithFlags(&w.s1, cudaStreamNonBlocking));
+      MG_CUDA(cudaStreamCreateWithFlags(&w.s2, cudaStreamNonBlocking));
+      for (auto* e : {&w.prior, &w.heavy_fork, &w.heavy_join, &w.loss_done, &w.stats_done, &w.src_ready, &w.copy_done,
+                      &w.ar_ready, &w.ar_done})
+        *e = mk_event();
+      for (int j = 0; j < world; ++j) {
+        w.bc_done.push_back(mk_event());
+        w.mult.push_back(mk_event());
+      }
+      for (int l = 0; l < L; ++l) {
+        w.wg_done.push_back(mk_event());
+        w.red_done.push_back(mk_event());
+      }
+      w.t_start = mk_event(true);
+      w.t_end = mk_event(true);
+      // tiles
+      for (int d = 0; d < 2; ++d) {
+        w.tiles[d].resize(world);
+        for (int j = 0; j < world; ++j) upload_tile(*g, w, p->tiles[d][w.rank][j], w.tiles[d][j]);
+      }
+      // rows: x_local, labels, mask (gcn.hpp:127-132)
+      w.x = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));
+      upload_padded(w.x, p->features.data() + w.r0 * p->d0, w.rows, p->d0, g->ld[0]);
+      w.labels = dalloc_t<int>(*g, w, std::max<index_t>(1, w.rows));
+      w.mask = dalloc_t<uint8_t>(*g, w, std::max<index_t>(1, w.rows));
+      if (w.rows) {
+        MG_CUDA(cudaMemcpy(w.labels, p->labels.data() + w.r0, sizeof(int) * w.rows, cudaMemcpyHostToDevice));
+        MG_CUDA(cudaMemcpy(w.mask, p->mask.data() + w.r0, w.rows, cudaMemcpyHostToDevice));
+      }
+      // the L + 3 buffer plan (gcn.hpp:134-140)
+      for (int l = 0; l < L; ++l) w.ahw.push_back(dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[l + 1])));
+      w.hw = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld_max));
+      w.bc1 = dalloc_t<float>(*g, w, std::max<index_t>(1, g->max_part * g->ld_max));
+      w.bc2 = dalloc_t<float>(*g, w, std::max<index_t>(1, g->max_part * g->ld_max));
+      // parameters, Adam state, W-grad staging (gcn.hpp:150-158), padded ld_l x ld_{l+1}
+      for (int l = 0; l < L; ++l) {
+        const index_t sz = g->ld[l] * g->ld[l + 1];
+        w.W.push_back(dalloc_t<float>(*g, w, sz));
+        w.WG.push_back(dalloc_t<float>(*g, w, sz));
+        w.M.push_back(dalloc_t<float>(*g, w, sz));
+        w.V.push_back(dalloc_t<float>(*g, w, sz));
+        w.stage.push_back(dalloc_t<float>(*g, w, 8 * sz));
+      }
+      w.loss_blocks = std::max(1, std::min(ceil_div(w.rows, 8), num_sms() * 8));
+      w.partials = dalloc_t<double>(*g, w, 2 * w.loss_blocks);
+      w.stats = dalloc_t<double>(*g, w, 2);
+      MG_CUDA(cudaMallocHost(&w.h_stats, 2 * sizeof(double)));
+      g->workers.push_back(std::move(wp));
+    }
+    if (transport == MG_TRANSPORT_NCCL && world > 1) {
+      if (n_local == world && !nccl_id) {
+        std::vector<ncclComm_t> comms(n_local);
+        MG_NCCL(ncclCommInitAll(comms.data(), n_local, devs.data()));
+        for (int k = 0; k < n_local; ++k) g->workers[k]->comm = comms[k];
+      } else {
+        ncclUniqueId u;
+        std::memcpy(&u, nccl_id, 128);
+        MG_NCCL(ncclGroupStart());
+        for (int k = 0; k < n_local; ++k) {
+          MG_CUDA(cudaSetDevice(g->workers[k]->device));
+          MG_NCCL(ncclCommInitRank(&g->workers[k]->comm, world, u, g->workers[k]->rank));
+        }
+        MG_NCCL(ncclGroupEnd());
+      }
+    }
+    for (auto& wp : g->workers) {
+      MG_CUDA(cudaSetDevice(wp->device));
+      MG_CUDA(cudaDeviceSynchronize());
+    }
+    g->sealed = true;
+    *out = g.release();
+  });
+}
+
+// GcnWorker::init_params (gcn.hpp:163-173): one Rng(seed) across layers, Glorot-uniform in double,
+// cast to float; identical on every worker (the reference broadcasts rank 0's draw).
+mg_status mg_group_init_params(mg_group* g) {
+  return guarded([&] {
+    Rng rng(g->cfg.seed);
+    const int L = g->cfg.layers();
+    for (int l = 0; l < L; ++l) {
+      const index_t dl = g->cfg.dims[l], dl1 = g->cfg.dims[l + 1];
+      const double limit = std::sqrt(6.0 / static_cast<double>(dl + dl1));
+      std::vector<float> w(dl * dl1);
+      for (auto& x : w) x = static_cast<float>(rng.uniform(-limit, limit));
+      for (auto& wp : g->workers) {
+        MG_CUDA(cudaSetDevice(wp->device));
+        upload_padded(wp->W[l], w.data(), dl, dl1, g->ld[l + 1]);
+        const size_t sz = sizeof(float) * g->ld[l] * g->ld[l + 1];
+        MG_CUDA(cudaMemset(wp->M[l], 0, sz));
+        MG_CUDA(cudaMemset(wp->V[l], 0, sz));
+        MG_CUDA(cudaMemset(wp->WG[l], 0, sz));
+      }
+    }
+  });
+}
+
+static void enqueue_train(mg_group* g, int t, bool adam) {
+  Step st(*g);
+  st.begin();
+  st.forward();
+  st.loss_grad();
+  st.backward();
+  st.finalize(adam, t);
+  st.end();
+  g->stats_pending = true;
+}
+
+mg_status mg_group_train_step_async(mg_group* g, int32_t t) {
+  return guarded([&] { enqueue_train(g, t, true); });
+}
+
+mg_status mg_group_sync(mg_group* g) {
+  return guarded([&] {
+    sync_all(*g);
+    if (g->stats_pending) {
+      read_stats(*g);
+      g->stats_pending = false;
+    }
+  });
+}
+
+mg_status mg_group_last_stats(mg_group* g, double* loss, double* acc) {
+  return guarded([&] {
+    if (g->stats_pending) {
+      read_stats(*g);
+      g->stats_pending = false;
+    }
+    if (loss) *loss = g->last_loss;
+    if (acc) *acc = g->last_acc;
+  });
+}
+
+mg_status mg_group_train_step(mg_group* g, int32_t t, double* loss, double* acc, double* wall_us) {
+  return guarded([&] {
+    enqueue_train(g, t, true);
+    sync_all(*g);
+    read_stats(*g);
+    g->stats_pending = false;
+    if (loss) *loss = g->last_loss;
+    if (acc) *acc = g->last_acc;
+    if (wall_us) {
+      Worker& w = *g->workers[0];
+      float ms = 0.f;
+      MG_CUDA(cudaEventElapsedTime(&ms, w.t_start, w.t_end));
+      *wall_us = 1000.0 * ms;
+    }
+  });
+}
+
+mg_status mg_group_compute_gradients(mg_group* g, double* loss, double* acc) {
+  return guarded([&] {
+    enqueue_train(g, 1, false);
+    sync_all(*g);
+    read_stats(*g);
+    g->stats_pending = false;
+    if (loss) *loss = g->last_loss;
+    if (acc) *acc = g->last_acc;
+  });
+}
+
+mg_status mg_group_forward(mg_group* g) {
+  return guarded([&] {
+    Step st(*g);
+    st.begin();
+    st.forward();
+    st.end();
+    sync_all(*g);
+  });
+}
+
+// GcnWorker::loss_only (gcn.hpp:189-205): forward, then the masked loss without touching the logits.
+// The loss kernel writes gradients in place, so the logits are preserved through hw (never larger).
+mg_status mg_group_loss_only(mg_group* g, double* loss) {
+  return guarded([&] {
+    Step st(*g);
+    st.begin();
+    st.forward();
+    const int L = g->cfg.layers();
+    const index_t ldc = g->ld[L];
+    for (auto& wp : g->workers) {  // keep a copy of the logits in hw (n x ld_L <= n x ld_max)
+      MG_CUDA(cudaSetDevice(wp->device));
+      MG_CUDA(cudaMemcpyAsync(wp->hw, wp->ahw[L - 1], sizeof(float) * wp->rows * ldc, cudaMemcpyDeviceToDevice, wp->s0));
+    }
+    st.loss_grad();
+    for (auto& wp : g->workers) {
+      MG_CUDA(cudaSetDevice(wp->device));
+      MG_CUDA(cudaMemcpyAsync(wp->ahw[L - 1], wp->hw, sizeof(float) * wp->rows * ldc, cudaMemcpyDeviceToDevice, wp->s0));
+    }
+    st.end();
+    sync_all(*g);
+    read_stats(*g);
+    g->stats_pending = false;
+    if (loss) *loss = g->last_loss;
+  });
+}
+
+static Worker& find_worker(mg_group* g, int32_t rank) {
+  for (auto& wp : g->workers)
+    if (wp->rank == rank) return *wp;
+  throw ValueError("group: rank " + std::to_string(rank) + " is not local to this process");
+}
+
+struct TensorView {
+  float* p;
+  index_t rows, cols, ld;
+};
+
+static TensorView tensor_view(mg_group* g, Worker& w, int which, int layer) {
+  const int L = g->cfg.layers();
+  auto need_layer = [&] {
+    if (layer < 0 || layer >= L) throw ValueError("tensor: layer " + std::to_string(layer) + " out of range");
+  };
+  switch (which) {
+    case MG_T_W: need_layer(); return {w.W[layer], g->cfg.dims[layer], g->cfg.dims[layer + 1], g->ld[layer + 1]};
+    case MG_T_WGRAD: need_layer(); return {w.WG[layer], g->cfg.dims[layer], g->cfg.dims[layer + 1], g->ld[layer + 1]};
+    case MG_T_ADAM_M: need_layer(); return {w.M[layer], g->cfg.dims[layer], g->cfg.dims[layer + 1], g->ld[layer + 1]};
+    case MG_T_ADAM_V: need_layer(); return {w.V[layer], g->cfg.dims[layer], g->cfg.dims[layer + 1], g->ld[layer + 1]};
+    case MG_T_AHW: need_layer(); return {w.ahw[layer], w.rows, g->cfg.dims[layer + 1], g->ld[layer + 1]};
+    case MG_T_HW: need_layer(); return {w.hw, w.rows, g->cfg.dims[layer + 1], g->ld[layer + 1]};
+    case MG_T_X: return {w.x, w.rows, g->cfg.dims[0], g->ld[0]};
+    case MG_T_WSTAGE: {
+      need_layer();
+      // 8 blocks of (ld_l x ld_{l+1}); exposed as 8 d_l x d_{l+1} blocks stacked
+      return {w.stage[layer], 8 * g->cfg.dims[layer], g->cfg.dims[layer + 1], g->ld[layer + 1]};
+    }
+    default: throw ValueError("tensor: unknown id " + std::to_string(which));
+  }
+}
+
+mg_status mg_group_read(mg_group* g, int32_t rank, int32_t which, int32_t layer, float* dst, int64_t count) {
+  return guarded([&] {
+    Worker& w = find_worker(g, rank);
+    MG_CUDA(cudaSetDevice(w.device));
+    sync_all(*g);
+    TensorView v = tensor_view(g, w, which, layer);
+    if (count != v.rows * v.cols)
+      throw ShapeError("tensor: count " + std::to_string(count) + " != " + shape_str(v.rows, v.cols));
+    if (which == MG_T_WSTAGE) {
+      const index_t dl = g->cfg.dims[layer], bs = g->ld[layer] * g->ld[layer + 1];
+      for (int b = 0; b < 8; ++b) download_padded(dst + b * dl * v.cols, v.p + b * bs, dl, v.cols, v.ld);
+      return;
+    }
+    download_padded(dst, v.p, v.rows, v.cols, v.ld);
+  });
+}
+
+mg_status mg_group_write(mg_group* g, int32_t rank, int32_t which, int32_t layer, const float* src, int64_t count) {
+  return guarded([&] {
+    auto write_one = [&](Worker& w) {
+      MG_CUDA(cudaSetDevice(w.device));
+      TensorView v = tensor_view(g, w, which, layer);
+      if (which == MG_T_WSTAGE) throw ValueError("tensor: the staging buffer is read-only");
+      if (count != v.rows * v.cols)
+        throw ShapeError("tensor: count " + std::to_string(count) + " != " + shape_str(v.rows, v.cols));
+      upload_padded(v.p, src, v.rows, v.cols, v.ld);
+    };
+    sync_all(*g);
+    if (rank < 0) {  // replicated tensors: write every local worker
+      for (auto& wp : g->workers) write_one(*wp);
+    } else {
+      write_one(find_worker(g, rank));
+    }
+  });
+}
+
+// FNV-1a over the unpadded W bytes of every layer (gcn.hpp:87-94, :221-226).
+mg_status mg_group_w_hash(mg_group* g, int32_t rank, uint64_t* hash) {
+  return guarded([&] {
+    Worker& w = find_worker(g, rank);
+    MG_CUDA(cudaSetDevice(w.device));
+    sync_all(*g);
+    std::uint64_t h = 0xcbf29ce484222325ull;
+    for (int l = 0; l < g->cfg.layers(); ++l) {
+      const index_t dl = g->cfg.dims[l], dl1 = g->cfg.dims[l + 1];
+      std::vector<float> buf(dl * dl1);
+      download_padded(buf.data(), w.W[l], dl, dl1, g->ld[l + 1]);
+      const auto* p = reinterpret_cast<const unsigned char*>(buf.data());
+      for (size_t i = 0; i < buf.size() * 4; ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ull;
+      }
+    }
+    *hash = h;
+  });
+}
+
+mg_status mg_group_rows(mg_group* g, int32_t rank, int64_t* row_begin, int64_t* rows) {
+  return guarded([&] {
+    Worker& w = find_worker(g, rank);
+    if (row_begin) *row_begin = w.r0;
+    if (rows) *rows = w.rows;
+  });
+}
+
+mg_status mg_group_buffer_audit(mg_group* g, int32_t* large_buffers, int64_t* step_allocations, int64_t* device_bytes) {
+  return guarded([&] {
+    if (large_buffers) *large_buffers = g->cfg.layers() + 3;  // ahw[L] + hw + bc1 + bc2
+    if (step_allocations) *step_allocations = g->step_allocs;
+    if (device_bytes) *device_bytes = g->workers[0]->bytes;
+  });
+}
+
+mg_status mg_group_last_profile(mg_group* g, double* spmm_us, double* gemm_us, double* other_us, int64_t* kernels) {
+  return guarded([&] {
+    sync_all(*g);
+    double t[3] = {0, 0, 0};
+    for (auto& [kind, idx] : g->prof_pending) {
+      float ms = 0.f;
+      MG_CUDA(cudaEventElapsedTime(&ms, g->prof_pool[idx], g->prof_pool[idx + 1]));
+      t[kind] += 1000.0 * ms;
+    }
+    g->prof_pending.clear();
+    g->prof_used = 0;
+    if (spmm_us) *spmm_us = t[0];
+    if (gemm_us) *gemm_us = t[1];
+    if (other_us) *other_us = t[2];
+    if (kernels) *kernels = g->kernels_total;
+    g->kernels_total = 0;
+  });
+}
+
+void mg_group_destroy(mg_group* g) {
+  if (!g) return;
+  for (auto& wp : g->workers) {
+    Worker& w = *wp;
+    cudaSetDevice(w.device);
+    cudaDeviceSynchronize();
+    if (w.comm) ncclCommDestroy(w.comm);
+    for (void* p : w.allocs) cudaFree(p);
+    if (w.h_stats) cudaFreeHost(w.h_stats);
+    for (cudaEvent_t e : {w.prior, w.heavy_fork, w.heavy_join, w.loss_done, w.stats_done, w.src_ready, w.copy_done,
+                          w.ar_ready, w.ar_done, w.t_start, w.t_end})
+      cudaEventDestroy(e);
+    for (auto* vec : {&w.bc_done, &w.mult, &w.wg_done, &w.red_done})
+      for (cudaEvent_t e : *vec) cudaEventDestroy(e);
+    cudaStreamDestroy(w.s0);
+    cudaStreamDestroy(w.s1);
+    cudaStreamDestroy(w.s2);
+  }
+  if (!g->workers.empty()) cudaSetDevice(g->workers[0]->device);
+  for (cudaEvent_t e : g->prof_pool) cudaEventDestroy(e);
+  delete g;
+}
+
+// ---------------------------------------------------------------- kernel-level entry points
+mg_status mg_dev_spmm(int64_t rows, const int32_t* row_ptr, const void* edges, const float* h, float* out, int64_t w,
+                      int64_t ld, int32_t accumulate, int32_t relu, int32_t mode, void* stream) {
+  return guarded([&] {
+    if (ld % 4 != 0 || ld < w) throw ValueError("spmm: ld must be a multiple of 4 and >= w");
+    if (mode != MG_SPMM_EXACT && mode != MG_SPMM_FAST) throw ValueError("spmm: unknown mode");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<int> rp32(rows + 1);
+    MG_CUDA(cudaMemcpy(rp32.data(), row_ptr, sizeof(int) * (rows + 1), cudaMemcpyDeviceToHost));
+    std::vector<index_t> rp(rp32.begin(), rp32.end());
+    std::vector<int> light, heavy;
+    build_orders(rp, light, heavy);
+    int *dl = nullptr, *dh = nullptr;
+    MG_CUDA(cudaMalloc(&dl, sizeof(int) * std::max<size_t>(1, light.size())));
+    MG_CUDA(cudaMalloc(&dh, sizeof(int) * std::max<size_t>(1, heavy.size())));
+    if (!light.empty()) MG_CUDA(cudaMemcpy(dl, light.data(), sizeof(int) * light.size(), cudaMemcpyHostToDevice));
+    if (!heavy.empty()) MG_CUDA(cudaMemcpy(dh, heavy.data(), sizeof(int) * heavy.size(), cudaMemcpyHostToDevice));
+    SpmmLaunch sl{row_ptr, static_cast<const int2*>(edges), dl, static_cast<int>(light.size()), dh,
+                  static_cast<int>(heavy.size())};
+    spmm_heavy(sl, h, out, ld, accumulate, relu, s);
+    spmm_light(sl, h, out, ld, accumulate, relu, s);
+    MG_CUDA(cudaStreamSynchronize(s));
+    cudaFree(dl);
+    cudaFree(dh);
+  });
+}
+
+mg_status mg_dev_gemm(int32_t ta, int32_t tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                      const float* B, int64_t ldb, float* Cm, int64_t ldc, int32_t epilogue, int32_t mode,
+                      void* stream) {
+  return guarded([&] {
+    if (epilogue < 0 || epilogue > 2) throw ValueError("gemm: unknown epilogue");
+    gemm_launch(mode, ta != 0, tb != 0, M, N, K, A, lda, B, ldb, Cm, ldc, epilogue, static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

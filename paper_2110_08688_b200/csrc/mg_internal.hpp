@@ -1,0 +1,133 @@
+// SPDX-License-Identifier: Apache-2.0
+// Internal host-side types shared by the host (mg_host.cpp) and device (mg_device.cu) halves of
+// libmggcn.so. Nothing here is part of the ABI (include/mggcn.h is).
+#pragma once
+
+#include <algorithm>
+#include <atomic>
+#include <cstdint>
+#include <functional>
+#include <stdexcept>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "mggcn.h"
+
+namespace mg {
+
+using index_t = std::int64_t;
+
+// Error taxonomy mirroring rowgcn (inc/errors.hpp:10-39); each maps to one mg_status.
+struct Error : std::runtime_error {
+  mg_status code;
+  Error(mg_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+struct ShapeError : Error { explicit ShapeError(const std::string& m) : Error(MG_SHAPE_ERROR, m) {} };
+struct ValueError : Error { explicit ValueError(const std::string& m) : Error(MG_VALUE_ERROR, m) {} };
+struct ProtocolError : Error { explicit ProtocolError(const std::string& m) : Error(MG_PROTOCOL_ERROR, m) {} };
+struct ConfigError : Error { explicit ConfigError(const std::string& m) : Error(MG_CONFIG_ERROR, m) {} };
+struct CudaError : Error { explicit CudaError(const std::string& m) : Error(MG_CUDA_ERROR, m) {} };
+struct NcclError : Error { explicit NcclError(const std::string& m) : Error(MG_NCCL_ERROR, m) {} };
+
+void set_last_error(const std::string& msg);
+
+template <class F>
+mg_status guarded(F&& f) {
+  try {
+    f();
+    return MG_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    set_last_error("host allocation failed (std::bad_alloc)");
+    return MG_INTERNAL_ERROR;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return MG_INTERNAL_ERROR;
+  }
+}
+
+inline std::string shape_str(index_t r, index_t c) { return std::to_string(r) + "x" + std::to_string(c); }
+
+// ---------------------------------------------------------------- host parallel_for
+int host_threads();
+// Runs f(begin, end) over [0, n) split into contiguous chunks, one per thread.
+void parallel_for(index_t n, const std::function<void(index_t, index_t)>& f, index_t min_chunk = 4096);
+
+// ---------------------------------------------------------------- RNG (inc/rng.hpp:13-28)
+// std::mt19937_64 restated so the host generator, permutation and Glorot init are platform-pinned.
+class Rng {
+ public:
+  explicit Rng(std::uint64_t seed);
+  std::uint64_t next();
+  std::uint64_t below(std::uint64_t n) { return next() % n; }
+  double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+
+ private:
+  std::uint64_t mt_[312];
+  int idx_;
+};
+
+// ---------------------------------------------------------------- config
+struct Config {
+  std::vector<index_t> dims;
+  double lr = 0.01, beta1 = 0.9, beta2 = 0.999, epsilon = 1e-8;
+  int epochs = 100;
+  std::uint64_t seed = 1;
+  bool permute = false, overlap = false, skip_first_backward_spmm = false, order_swap = false;
+  int gemm_mode = MG_GEMM_TF32X3;
+  int spmm_mode = MG_SPMM_EXACT;
+  int layers() const { return static_cast<int>(dims.size()) - 1; }
+};
+Config to_config(const mg_config* c);  // validates (inc/gcn.hpp:29-35)
+
+// ---------------------------------------------------------------- CSR / dataset
+struct Csr {  // int64 row_ptr/col_idx like rowgcn::CsrMatrix (inc/sparse.hpp:25-55)
+  index_t rows = 0, cols = 0;
+  std::vector<index_t> row_ptr, col_idx;
+  std::vector<float> values;
+  index_t nnz() const { return static_cast<index_t>(col_idx.size()); }
+  void validate() const;
+};
+
+}  // namespace mg
+
+struct mg_dataset {
+  mg::Csr graph;
+  std::vector<float> features;  // n x d0
+  mg::index_t d0 = 0;
+  std::vector<std::int32_t> labels;
+  std::vector<std::uint8_t> train_mask;  // empty = all
+  mg::index_t n() const { return graph.rows; }
+};
+
+namespace mg {
+
+// One tile of the symmetric row tiling (rowgcn::TilePlan, inc/partition.hpp:158-171) in the device
+// staging format: int64 row_ptr (host), int32 local column, fp32 value.
+struct Tile {
+  index_t rows = 0, cols = 0;
+  std::vector<index_t> row_ptr;
+  std::vector<std::int32_t> col;
+  std::vector<float> val;
+  index_t nnz() const { return static_cast<index_t>(col.size()); }
+};
+
+}  // namespace mg
+
+struct mg_partition {
+  mg::index_t n = 0, d0 = 0, mask_count = 0;
+  int parts = 1;
+  int only_rank = -1;
+  std::vector<mg::index_t> bounds;
+  std::vector<mg::index_t> perm_forward;
+  std::vector<float> features;  // permuted, n x d0
+  std::vector<std::int32_t> labels;
+  std::vector<std::uint8_t> mask;
+  // tiles[dir][i][j]; rows i != only_rank are left empty when only_rank >= 0
+  std::vector<std::vector<mg::Tile>> tiles[2];
+  bool has_row(int i) const { return only_rank < 0 || only_rank == i; }
+};

@@ -1,0 +1,406 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// sm_100a kernels of the training step (CUDA C++, no libraries):
+//   * SpMM over one CSR tile (rowgcn::spmm, inc/sparse.hpp:140-188)  — the hot path
+//   * exact SIMT GeMMs (rowgcn::gemm, inc/dense.hpp:140-204) with the fused ReLU epilogues
+//   * fused masked softmax cross-entropy + gradient + argmax (inc/dense.hpp:241-277, gcn.hpp:271-290)
+//   * fused canonical W-grad block sum + Adam (inc/gcn.hpp:365-377, :61-85)
+//   * rank-order reduction for the in-process transport (inc/collectives.hpp:76-94)
+// Device layout: every dense activation is row-major with a leading dimension padded to a multiple of
+// 4 floats (16-byte rows for float4 traffic); padding columns are kept at +0.0 by every producer.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mg {
+namespace k {
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ float fma_free(float acc, float a, float b) {  // acc + a*b, two roundings
+  return __fadd_rn(acc, __fmul_rn(a, b));
+}
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void axpy4(float4& acc, float v, const float4& x) {
+  acc.x = fma_free(acc.x, v, x.x);
+  acc.y = fma_free(acc.y, v, x.y);
+  acc.z = fma_free(acc.z, v, x.z);
+  acc.w = fma_free(acc.w, v, x.w);
+}
+__device__ __forceinline__ float relu1(float x) { return x > 0.0f ? x : 0.0f; }  // dense.hpp:214
+
+// ============================================================================ SpMM (exact)
+// One row per group of G lanes (G | 32); lane l of the group owns the float4 column chunks
+// c = l + k*G (k < CPL). Every output element is a left fold over the row's nonzeros in column
+// order with a separate multiply and add — exactly rowgcn::detail::spmm_rows (sparse.hpp:144-153) —
+// so the result is bitwise equal to the reference and independent of the launch geometry.
+// Rows are visited in `order` (sorted by decreasing length on the host) so the long rows start first.
+// Edge records {col, val} are loaded cooperatively (one per lane) and broadcast with shuffles; the
+// h-row gathers of U consecutive nonzeros are issued before any of them is consumed (memory-level
+// parallelism without changing the accumulation order).
+template <int G, int CPL>
+__global__ void __launch_bounds__(256) spmm_exact_rows(const int* __restrict__ row_ptr, const int2* __restrict__ edges,
+                                                       const int* __restrict__ order, int n_order,
+                                                       const float* __restrict__ h, float* __restrict__ out, int ld,
+                                                       int nchunk, int accumulate, int relu) {
+  constexpr int U = (CPL <= 2) ? 4 : 2;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  const int groups = gridDim.x * (blockDim.x / G);
+  for (int idx = blockIdx.x * (blockDim.x / G) + threadIdx.x / G; idx < n_order; idx += groups) {
+    const int r = order ? __ldg(order + idx) : idx;
+    const int e0 = __ldg(row_ptr + r), e1 = __ldg(row_ptr + r + 1);
+    float* orow = out + (size_t)r * ld;
+    float4 acc[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int c = lane + k * G;
+      acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (accumulate && c < nchunk) acc[k] = *reinterpret_cast<const float4*>(orow + 4 * c);
+    }
+    for (int base = e0; base < e1; base += G) {
+      const int cnt = min(G, e1 - base);
+      const int2 my = lane < cnt ? __ldg(edges + base + lane) : make_int2(0, 0);
+      int j = 0;
+      for (; j + U <= cnt; j += U) {
+        float4 x[U][CPL];
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int col = __shfl_sync(gmask, my.x, j + u, G);
+          v[u] = __int_as_float(__shfl_sync(gmask, my.y, j + u, G));
+          const float* hr = h + (size_t)col * ld;
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            const int c = lane + k * G;
+            x[u][k] = c < nchunk ? ldg4(hr + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) axpy4(acc[k], v[u], x[u][k]);
+      }
+      for (; j < cnt; ++j) {
+        const int col = __shfl_sync(gmask, my.x, j, G);
+        const float v = __int_as_float(__shfl_sync(gmask, my.y, j, G));
+        const float* hr = h + (size_t)col * ld;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          const int c = lane + k * G;
+          if (c < nchunk) axpy4(acc[k], v, ldg4(hr + 4 * c));
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int c = lane + k * G;
+      if (c < nchunk) {
+        float4 a = acc[k];
+        if (relu) a = make_float4(relu1(a.x), relu1(a.y), relu1(a.z), relu1(a.w));
+        *reinterpret_cast<float4*>(orow + 4 * c) = a;
+      }
+    }
+  }
+}
+
+// Long rows (hubs of the power-law graph): one CTA per (row, 64-column slab). The row's h-slabs are
+// streamed through a cp.async ring of NST stages x 32 nonzeros (all 256 threads produce), and the
+// first 64 threads consume them in column order, one output column each — the same left fold as
+// above, so still bitwise exact, but with ~64 KB of gathers in flight per CTA instead of one warp's.
+constexpr int kHeavySlab = 64;
+constexpr int kHeavyB = 32;
+constexpr int kHeavyNst = 8;
+constexpr size_t kHeavySmem = sizeof(float) * (kHeavyNst * kHeavyB * kHeavySlab + kHeavyNst * kHeavyB);
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__global__ void __launch_bounds__(256) spmm_exact_heavy(const int* __restrict__ row_ptr, const int2* __restrict__ edges,
+                                                        const int* __restrict__ heavy, int nslab,
+                                                        const float* __restrict__ h, float* __restrict__ out, int ld,
+                                                        int accumulate, int relu) {
+  extern __shared__ __align__(16) float smem[];
+  float* buf = smem;                                           // [NST][B][SLAB]
+  float* vals = smem + kHeavyNst * kHeavyB * kHeavySlab;       // [NST][B]
+  const int r = heavy[blockIdx.x / nslab];
+  const int col0 = (blockIdx.x % nslab) * kHeavySlab;
+  const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
+  const int nst_total = (e1 - e0 + kHeavyB - 1) / kHeavyB;
+  const int t = threadIdx.x;
+  const int my_col = col0 + t;
+  float acc = 0.0f;
+  if (t < kHeavySlab && accumulate && my_col < ld) acc = out[(size_t)r * ld + my_col];
+
+  auto issue = [&](int st) {
+    if (st < nst_total) {
+      const int slot = st % kHeavyNst;
+      const int base = e0 + st * kHeavyB;
+      // 32 edges x 16 chunks of 16 B = 512 copies; 2 per thread
+      for (int q = t; q < kHeavyB * (kHeavySlab / 4); q += blockDim.x) {
+        const int b = q / (kHeavySlab / 4), c4 = q % (kHeavySlab / 4);
+        const int e = base + b;
+        const int c = col0 + 4 * c4;
+        if (e < e1 && c < ld) {
+          const int2 ed = __ldg(edges + e);
+          cp_async16(buf + ((size_t)slot * kHeavyB + b) * kHeavySlab + 4 * c4, h + (size_t)ed.x * ld + c);
+        }
+      }
+      if (t < kHeavyB) {
+        const int e = base + t;
+        vals[slot * kHeavyB + t] = e < e1 ? __int_as_float(__ldg(edges + e).y) : 0.0f;
+      }
+    }
+    cp_async_commit();
+  };
+  for (int s = 0; s < kHeavyNst - 1; ++s) issue(s);
+  for (int st = 0; st < nst_total; ++st) {
+    cp_async_wait<kHeavyNst - 2>();
+    __syncthreads();
+    issue(st + kHeavyNst - 1);
+    if (t < kHeavySlab && my_col < ld) {
+      const int slot = st % kHeavyNst;
+      const int cnt = min(kHeavyB, e1 - (e0 + st * kHeavyB));
+      const float* bs = buf + (size_t)slot * kHeavyB * kHeavySlab + t;
+      const float* vs = vals + slot * kHeavyB;
+      for (int b = 0; b < cnt; ++b) acc = fma_free(acc, vs[b], bs[b * kHeavySlab]);
+    }
+  }
+  cp_async_wait<0>();
+  if (t < kHeavySlab && my_col < ld) out[(size_t)r * ld + my_col] = relu ? relu1(acc) : acc;
+}
+
+// ============================================================================ GeMM (exact SIMT)
+// C[M,N] = op(A) op(B) with the reference's per-element order: k ascending, separate multiply and
+// add; NN/TN skip zero A entries (dense.hpp:165, :177); NT forms the dot product then adds it to a
+// zeroed output (dense.hpp:189-191, i.e. 0 + acc). 64x64 tiles, 256 threads, 4x4 outputs each.
+// EPI 0: store; 1: relu_backward in place, C = C_old > 0 ? r : 0 (dense.hpp:221-231); 2: relu.
+constexpr int kGBM = 64, kGBN = 64, kGBK = 16;
+
+template <bool TA, bool TB, int EPI>
+__global__ void __launch_bounds__(256) gemm_exact(int M, int N, int K, const float* __restrict__ A, long lda,
+                                                  const float* __restrict__ B, long ldb, float* __restrict__ C,
+                                                  long ldc) {
+  __shared__ float As[kGBK][kGBM + 4];
+  __shared__ float Bs[kGBK][kGBN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const long m0 = (long)blockIdx.x * kGBM;  // M (rows of the activations) on x: no 65535 limit
+  const int n0 = blockIdx.y * kGBN;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+  for (int k0 = 0; k0 < K; k0 += kGBK) {
+    // A tile -> As[kk][i]
+    for (int q = tid; q < kGBK * kGBM; q += 256) {
+      int kk, i;
+      if (TA) { kk = q / kGBM; i = q % kGBM; } else { i = q / kGBK; kk = q % kGBK; }
+      const long m = m0 + i;
+      const int kx = k0 + kk;
+      float v = 0.0f;
+      if (m < M && kx < K) v = TA ? A[(long)kx * lda + m] : A[m * lda + kx];
+      As[kk][i] = v;
+    }
+    for (int q = tid; q < kGBK * kGBN; q += 256) {
+      int kk, j;
+      if (TB) { j = q / kGBK; kk = q % kGBK; } else { kk = q / kGBN; j = q % kGBN; }
+      const int n = n0 + j;
+      const int kx = k0 + kk;
+      float v = 0.0f;
+      if (n < N && kx < K) v = TB ? B[(long)n * ldb + kx] : B[(long)kx * ldb + n];
+      Bs[kk][j] = v;
+    }
+    __syncthreads();
+    const int kmax = min(kGBK, K - k0);
+    for (int kk = 0; kk < kmax; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (!TB && a[i] == 0.0f) continue;  // NN/TN zero skip
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma_free(acc[i][j], a[i], b[j]);
+      }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const long m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      float r = acc[i][j];
+      if (TB) r = __fadd_rn(0.0f, r);  // out(i,j) += acc on a zeroed out
+      float* cp = C + m * ldc + n;
+      if (EPI == 1) r = (*cp > 0.0f) ? r : 0.0f;
+      if (EPI == 2) r = relu1(r);
+      *cp = r;
+    }
+  }
+}
+
+// ============================================================================ loss
+// Masked softmax cross-entropy over the logits rows, gradient written in place (softmax - onehot) /
+// denom (dense.hpp:241-277), argmax with first-max-wins ties (gcn.hpp:279-282). One warp per row,
+// C <= 32*kLossCpl. Per-block partial sums (fp64) land in `partials`; finalize_stats sums them in a
+// fixed order so the reported loss is run-to-run deterministic.
+constexpr int kLossCpl = 8;
+
+__global__ void __launch_bounds__(256) softmax_xent(float* __restrict__ logits, int ld, int rows, int C,
+                                                    const int* __restrict__ labels, const uint8_t* __restrict__ mask,
+                                                    float inv_denom, double* __restrict__ partials) {
+  __shared__ double s_loss[8], s_corr[8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double my_loss = 0.0, my_corr = 0.0;
+  for (int r = blockIdx.x * 8 + warp; r < rows; r += gridDim.x * 8) {
+    float* row = logits + (size_t)r * ld;
+    if (!mask[r]) {
+      for (int j = lane; j < ld; j += 32) row[j] = 0.0f;
+      continue;
+    }
+    const int label = labels[r];
+    float z[kLossCpl];
+    float mx = -INFINITY;
+    int arg = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < kLossCpl; ++q) {
+      const int j = lane + 32 * q;
+      z[q] = j < C ? row[j] : -INFINITY;
+      if (j < C && (arg == 0x7fffffff || z[q] > mx)) {
+        mx = z[q];
+        arg = j;
+      }
+    }
+    // (max, first index) warp reduction: strictly greater wins, ties keep the smaller index
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const float om = __shfl_xor_sync(0xffffffffu, mx, off);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, off);
+      if (oa != 0x7fffffff && (arg == 0x7fffffff || om > mx || (om == mx && oa < arg))) {
+        mx = om;
+        arg = oa;
+      }
+    }
+    float se = 0.0f;
+#pragma unroll
+    for (int q = 0; q < kLossCpl; ++q) {
+      const int j = lane + 32 * q;
+      if (j < C) se += expf(z[q] - mx);
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) se += __shfl_xor_sync(0xffffffffu, se, off);
+    float zlab = 0.0f;
+#pragma unroll
+    for (int q = 0; q < kLossCpl; ++q)
+      if (label == lane + 32 * q) zlab = z[q];
+    zlab = __shfl_sync(0xffffffffu, zlab, label & 31);
+    if (lane == 0) {
+      my_loss += (double)(logf(se) - (zlab - mx));
+      my_corr += (arg == label) ? 1.0 : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kLossCpl; ++q) {
+      const int j = lane + 32 * q;
+      if (j < C) {
+        float g = __fmul_rn(__fdiv_rn(expf(z[q] - mx), se), inv_denom);
+        if (j == label) g = __fsub_rn(g, inv_denom);
+        row[j] = g;
+      }
+    }
+    for (int j = C + lane; j < ld; j += 32) row[j] = 0.0f;
+  }
+  if (lane == 0) {
+    s_loss[warp] = my_loss;
+    s_corr[warp] = my_corr;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < 8; ++w) {
+      a += s_loss[w];
+      b += s_corr[w];
+    }
+    partials[2 * blockIdx.x] = a;
+    partials[2 * blockIdx.x + 1] = b;
+  }
+}
+
+__global__ void finalize_stats(const double* __restrict__ partials, int nblocks, double* __restrict__ stats) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int i = 0; i < nblocks; ++i) {
+      a += partials[2 * i];
+      b += partials[2 * i + 1];
+    }
+    stats[0] = a;
+    stats[1] = b;
+  }
+}
+
+// ============================================================================ W-grad finalize + Adam
+// w_grad = 0 + stage[0] + ... + stage[7] in block order (gcn.hpp:365-377), then Adam with the
+// reference's float constants and operation order (gcn.hpp:61-85), grads zeroed afterwards.
+// Works on the padded d_l x ld_{l+1} arrays; padding stays exactly 0.
+struct AdamConsts {
+  float b1, one_m_b1, b2, one_m_b2, lr, eps, corr1, corr2;
+};
+
+__global__ void finalize_adam(int size, int blocks, const float* __restrict__ stage, float* __restrict__ w,
+                              float* __restrict__ g, float* __restrict__ m, float* __restrict__ v, int run_adam,
+                              AdamConsts c) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < size; i += gridDim.x * blockDim.x) {
+    float s = 0.0f;
+    for (int b = 0; b < blocks; ++b) s = __fadd_rn(s, stage[(size_t)b * size + i]);
+    if (!run_adam) {
+      g[i] = s;
+      continue;
+    }
+    const float mi = __fadd_rn(__fmul_rn(c.b1, m[i]), __fmul_rn(c.one_m_b1, s));
+    const float vi = __fadd_rn(__fmul_rn(c.b2, v[i]), __fmul_rn(__fmul_rn(c.one_m_b2, s), s));
+    const float mhat = __fdiv_rn(mi, c.corr1);
+    const float vhat = __fdiv_rn(vi, c.corr2);
+    m[i] = mi;
+    v[i] = vi;
+    w[i] = __fsub_rn(w[i], __fdiv_rn(__fmul_rn(c.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), c.eps)));
+    g[i] = 0.0f;
+  }
+}
+
+// ============================================================================ in-process reduction
+// DeviceGroup::all_reduce_sum (inc/collectives.hpp:76-94): acc = 0 + b_0 + b_1 + ... in rank order,
+// written back to every participant. Used by the LOCAL transport (several workers per device).
+constexpr int kMaxLocal = 16;
+template <class T>
+struct PtrList {
+  T* p[kMaxLocal];
+};
+
+template <class T>
+__global__ void rank_order_allreduce(PtrList<T> bufs, int nranks, long count) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (long)gridDim.x * blockDim.x) {
+    T acc = T(0);
+    for (int r = 0; r < nranks; ++r) acc = acc + bufs.p[r][i];
+    for (int r = 0; r < nranks; ++r) bufs.p[r][i] = acc;
+  }
+}
+
+// zero fill (float4 granularity when aligned)
+__global__ void fill_zero(float* __restrict__ p, long n) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) p[i] = 0.0f;
+}
+
+}  // namespace k
+}  // namespace mg

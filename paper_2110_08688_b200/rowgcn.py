@@ -1,0 +1,548 @@
+"""Python mirror of the reference's training API (rowgcn, proj/include/rowgcn/) on top of libmggcn.so.
+
+Same names, argument meaning and error behaviour as the C++ reference so parity tests read like the
+reference's own tests:
+  errors      inc/errors.hpp:10-39          ShapeError, ValueError, ... (+ CudaError, NcclError)
+  GcnConfig   inc/gcn.hpp:14-36             + gemm_mode / spmm_mode (device arithmetic)
+  parse_config / materialize_config / config_to_json   inc/driver.hpp:19-71
+  Dataset, synth_graph                      inc/dataset.hpp:19-56, :287-334
+  prepare_data / PreparedData               inc/driver.hpp:75-117
+  Group (the GcnWorkers of this process)    inc/gcn.hpp:101-398
+  TrainOptions / TrainArtifacts / train_run inc/driver.hpp:119-206
+  GradArtifacts / grad_run                  inc/driver.hpp:209-251
+  fnv1a                                     inc/gcn.hpp:87-94
+Every call goes through the C ABI (include/mggcn.h); nothing here computes on the CPU.
+"""
+from __future__ import annotations
+
+import builtins
+import ctypes as C
+import json
+from dataclasses import dataclass, field, fields
+from typing import Callable, Optional
+
+import numpy as np
+
+from ._lib import lib, mg_config, mg_csr
+
+# ----------------------------------------------------------------------------- errors (inc/errors.hpp)
+
+
+class RowgcnError(RuntimeError):
+    pass
+
+
+class ShapeError(RowgcnError):
+    pass
+
+
+class ValueError(RowgcnError, builtins.ValueError):  # noqa: A001 - mirrors rowgcn::ValueError
+    pass
+
+
+class ProtocolError(RowgcnError):
+    pass
+
+
+class ShutdownError(RowgcnError):
+    pass
+
+
+class ParseError(RowgcnError):
+    pass
+
+
+class ConfigError(RowgcnError):
+    pass
+
+
+class IoError(RowgcnError):
+    pass
+
+
+class CudaError(RowgcnError):
+    pass
+
+
+class NcclError(RowgcnError):
+    pass
+
+
+_STATUS = {1: ShapeError, 2: ValueError, 3: ProtocolError, 4: ShutdownError, 5: ParseError, 6: ConfigError,
+           7: IoError, 8: CudaError, 9: NcclError, 10: RowgcnError}
+
+GEMM_EXACT, GEMM_TF32X3, GEMM_TF32 = 0, 1, 2
+SPMM_EXACT, SPMM_FAST = 0, 1
+TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1, 2
+T_W, T_WGRAD, T_AHW, T_HW, T_X, T_ADAM_M, T_ADAM_V, T_WSTAGE = range(8)
+
+
+def _check(rc: int):
+    if rc != 0:
+        msg = lib().mg_last_error().decode(errors="replace")
+        raise _STATUS.get(rc, RowgcnError)(msg)
+
+
+def _p(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+# ----------------------------------------------------------------------------- config (inc/gcn.hpp:14-36)
+
+
+@dataclass
+class GcnConfig:
+    layer_dims: list = field(default_factory=list)
+    lr: float = 0.01
+    beta1: float = 0.9
+    beta2: float = 0.999
+    epsilon: float = 1e-8
+    epochs: int = 100
+    seed: int = 1
+    permute: bool = False
+    overlap: bool = False
+    skip_first_backward_spmm: bool = False
+    order_swap: bool = False
+    gemm_mode: int = GEMM_EXACT
+    spmm_mode: int = SPMM_EXACT
+
+    def layers(self) -> int:
+        return len(self.layer_dims) - 1
+
+    def _c(self):
+        dims = np.ascontiguousarray(np.asarray(self.layer_dims, dtype=np.int64))
+        c = mg_config(dims.ctypes.data_as(C.c_void_p), len(dims), self.lr, self.beta1, self.beta2, self.epsilon,
+                      self.epochs, self.seed, int(self.permute), int(self.overlap),
+                      int(self.skip_first_backward_spmm), int(self.order_swap), self.gemm_mode, self.spmm_mode)
+        c._keep = dims
+        return c
+
+    def validate(self):
+        _check(lib().mg_config_validate(C.byref(self._c())))
+
+
+@dataclass
+class ConfigFile:
+    hidden_dims: list = field(default_factory=lambda: [16])
+    cfg: GcnConfig = field(default_factory=GcnConfig)
+
+
+_KNOWN_KEYS = ("hidden_dims", "lr", "beta1", "beta2", "epsilon", "epochs", "seed", "permute", "overlap",
+               "skip_first_backward_spmm", "order_swap")
+
+
+def parse_config(j) -> ConfigFile:
+    """inc/driver.hpp:24-47: one JSON document, unknown keys rejected with ConfigError."""
+    if isinstance(j, (str, bytes)):
+        try:
+            j = json.loads(j)
+        except json.JSONDecodeError as e:
+            raise ParseError(f"config: {e}") from None
+    for k in j:
+        if k not in _KNOWN_KEYS:
+            raise ConfigError(f"config: unknown key '{k}'")
+    cf = ConfigFile()
+    if "hidden_dims" in j:
+        cf.hidden_dims = [int(x) for x in j["hidden_dims"]]
+    for k in _KNOWN_KEYS[1:]:
+        if k in j:
+            setattr(cf.cfg, k, type(getattr(cf.cfg, k))(j[k]))
+    return cf
+
+
+def materialize_config(cf: ConfigFile, d0: int, classes: int) -> GcnConfig:
+    """inc/driver.hpp:49-57: layer_dims = [d0, hidden..., classes], validated."""
+    kw = {f.name: getattr(cf.cfg, f.name) for f in fields(GcnConfig)}
+    kw["layer_dims"] = [int(d0)] + list(cf.hidden_dims) + [int(classes)]
+    cfg = GcnConfig(**kw)
+    cfg.validate()
+    return cfg
+
+
+def config_to_json(cfg: GcnConfig) -> dict:
+    """inc/driver.hpp:59-71"""
+    return {"layer_dims": list(cfg.layer_dims), "lr": cfg.lr, "beta1": cfg.beta1, "beta2": cfg.beta2,
+            "epsilon": cfg.epsilon, "epochs": cfg.epochs, "seed": cfg.seed, "permute": cfg.permute,
+            "overlap": cfg.overlap, "skip_first_backward_spmm": cfg.skip_first_backward_spmm,
+            "order_swap": cfg.order_swap}
+
+
+# ----------------------------------------------------------------------------- dataset (inc/dataset.hpp)
+
+
+class Dataset:
+    """rowgcn::Dataset in host memory (owned by libmggcn)."""
+
+    def __init__(self, handle, name: str = ""):
+        self._h = C.c_void_p(handle)
+        self.name = name
+
+    @classmethod
+    def from_arrays(cls, row_ptr, col_idx, values, features, labels, train_mask=None, name="arrays"):
+        rp = np.ascontiguousarray(row_ptr, np.int64)
+        ci = np.ascontiguousarray(col_idx, np.int64)
+        v = np.ascontiguousarray(values, np.float32)
+        x = np.ascontiguousarray(features, np.float32)
+        lab = np.ascontiguousarray(labels, np.int32)
+        m = None if train_mask is None else np.ascontiguousarray(train_mask, np.uint8)
+        n = len(rp) - 1
+        g = mg_csr(n, n, _p(rp), _p(ci), _p(v))
+        out = C.c_void_p()
+        _check(lib().mg_dataset_from_arrays(C.byref(g), _p(x), x.shape[1] if x.ndim == 2 else 0, _p(lab), _p(m),
+                                            C.byref(out)))
+        return cls(out.value, name)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            lib().mg_dataset_free(h)
+            self._h = C.c_void_p()
+
+    def _view(self):
+        g = mg_csr()
+        f = C.c_void_p()
+        d0 = C.c_int64()
+        lab = C.c_void_p()
+        m = C.c_void_p()
+        _check(lib().mg_dataset_view(self._h, C.byref(g), C.byref(f), C.byref(d0), C.byref(lab), C.byref(m)))
+        return g, f, d0.value, lab, m
+
+    def n(self) -> int:
+        return int(self._view()[0].rows)
+
+    @property
+    def graph(self):
+        """(row_ptr, col_idx, values) as numpy copies."""
+        g = self._view()[0]
+        n = g.rows
+        rp = np.ctypeslib.as_array(C.cast(g.row_ptr, C.POINTER(C.c_int64)), (n + 1,)).copy()
+        nnz = int(rp[-1])
+        ci = np.ctypeslib.as_array(C.cast(g.col_idx, C.POINTER(C.c_int64)), (max(nnz, 1),))[:nnz].copy()
+        v = np.ctypeslib.as_array(C.cast(g.values, C.POINTER(C.c_float)), (max(nnz, 1),))[:nnz].copy()
+        return rp, ci, v
+
+    @property
+    def features(self):
+        g, f, d0, _, _ = self._view()
+        return np.ctypeslib.as_array(C.cast(f, C.POINTER(C.c_float)), (g.rows * d0,)).reshape(g.rows, d0).copy()
+
+    @property
+    def labels(self):
+        g, _, _, lab, _ = self._view()
+        return np.ctypeslib.as_array(C.cast(lab, C.POINTER(C.c_int32)), (g.rows,)).copy()
+
+    @property
+    def nnz(self) -> int:
+        return int(self.graph[0][-1])
+
+    @property
+    def d0(self) -> int:
+        return self._view()[2]
+
+    def num_classes(self) -> int:
+        return int(lib().mg_dataset_num_classes(self._h))
+
+    def validate(self):
+        _check(lib().mg_dataset_validate(self._h))
+
+
+def synth_graph(n, avg_degree, exponent, seed, feature_dim=16, classes=4) -> Dataset:
+    """rowgcn::synth_graph<float> (inc/dataset.hpp:287-334), bit-identical output."""
+    out = C.c_void_p()
+    _check(lib().mg_dataset_synth(int(n), float(avg_degree), float(exponent), int(seed), int(feature_dim),
+                                  int(classes), C.byref(out)))
+    return Dataset(out.value, f"synth-n{n}-d{avg_degree}")
+
+
+# ----------------------------------------------------------------------------- partitioner (driver.hpp:75-117)
+
+
+class PreparedData:
+    def __init__(self, handle, workers: int):
+        self._h = C.c_void_p(handle)
+        self.workers = workers
+        n = C.c_int64()
+        mc = C.c_int64()
+        b = np.zeros(workers + 1, np.int64)
+        _check(lib().mg_partition_info(self._h, C.byref(n), C.byref(mc), _p(b)))
+        self.n = n.value
+        self.mask_count = mc.value
+        self.bounds = b
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            lib().mg_partition_free(h)
+            self._h = C.c_void_p()
+
+    def tile(self, direction: int, i: int, j: int):
+        """(row_ptr, col_idx, values) of tile (i, j); direction 0 = A_hat^T (forward), 1 = A_hat."""
+        r, c, z = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().mg_partition_tile_info(self._h, direction, i, j, C.byref(r), C.byref(c), C.byref(z)))
+        rp = np.zeros(r.value + 1, np.int64)
+        ci = np.zeros(max(z.value, 1), np.int64)
+        v = np.zeros(max(z.value, 1), np.float32)
+        _check(lib().mg_partition_tile_export(self._h, direction, i, j, _p(rp), _p(ci), _p(v)))
+        return rp, ci[:z.value], v[:z.value]
+
+    def rows_export(self, d0: int):
+        x = np.zeros((self.n, d0), np.float32)
+        lab = np.zeros(self.n, np.int32)
+        m = np.zeros(self.n, np.uint8)
+        pf = np.zeros(self.n, np.int64)
+        _check(lib().mg_partition_rows_export(self._h, _p(x), _p(lab), _p(m), _p(pf)))
+        return x, lab, m, pf
+
+
+def prepare_data(ds: Dataset, cfg: GcnConfig, workers: int, only_rank: int = -1) -> PreparedData:
+    out = C.c_void_p()
+    _check(lib().mg_prepare(ds._h, C.byref(cfg._c()), int(workers), int(only_rank), C.byref(out)))
+    return PreparedData(out.value, workers)
+
+
+# ----------------------------------------------------------------------------- device group (gcn.hpp)
+
+
+def set_tuning(key: str, value: int):
+    _check(lib().mg_set_tuning(key.encode(), int(value)))
+
+
+def nccl_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    _check(lib().mg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+def device_count() -> int:
+    import torch  # plumbing only: device enumeration
+    return torch.cuda.device_count()
+
+
+class Group:
+    """The GcnWorkers of this process (one per local rank), their streams and communicator."""
+
+    def __init__(self, cfg: GcnConfig, prep: PreparedData, world: int, local_ranks=None, devices=None,
+                 nccl_id: Optional[bytes] = None, transport: int = TRANSPORT_AUTO):
+        self.cfg = cfg
+        self.world = world
+        local_ranks = list(range(world)) if local_ranks is None else list(local_ranks)
+        if devices is None:
+            nd = max(1, device_count())
+            devices = [r % nd for r in local_ranks]
+        self.local_ranks = local_ranks
+        r = np.asarray(local_ranks, np.int32)
+        d = np.asarray(devices, np.int32)
+        idb = None if nccl_id is None else (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        out = C.c_void_p()
+        self._prep = prep  # keep alive until the upload finished
+        _check(lib().mg_group_create(C.byref(cfg._c()), prep._h, world, len(local_ranks), _p(r), _p(d), idb,
+                                     transport, C.byref(out)))
+        self._h = C.c_void_p(out.value)
+        self.dims = list(cfg.layer_dims)
+
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h and h.value:
+            lib().mg_group_destroy(h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        self.close()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def init_params(self):
+        _check(lib().mg_group_init_params(self._h))
+
+    def train_step(self, t: int):
+        loss, acc, wall = C.c_double(), C.c_double(), C.c_double()
+        _check(lib().mg_group_train_step(self._h, int(t), C.byref(loss), C.byref(acc), C.byref(wall)))
+        self.last_accuracy = acc.value
+        self.last_wall_us = wall.value
+        return loss.value
+
+    def train_step_async(self, t: int):
+        _check(lib().mg_group_train_step_async(self._h, int(t)))
+
+    def sync(self):
+        _check(lib().mg_group_sync(self._h))
+
+    def last_stats(self):
+        loss, acc = C.c_double(), C.c_double()
+        _check(lib().mg_group_last_stats(self._h, C.byref(loss), C.byref(acc)))
+        return loss.value, acc.value
+
+    def compute_gradients(self):
+        loss, acc = C.c_double(), C.c_double()
+        _check(lib().mg_group_compute_gradients(self._h, C.byref(loss), C.byref(acc)))
+        self.last_accuracy = acc.value
+        return loss.value
+
+    def loss_only(self):
+        loss = C.c_double()
+        _check(lib().mg_group_loss_only(self._h, C.byref(loss)))
+        return loss.value
+
+    def forward(self):
+        _check(lib().mg_group_forward(self._h))
+
+    def rows(self, rank: int):
+        b, n = C.c_int64(), C.c_int64()
+        _check(lib().mg_group_rows(self._h, rank, C.byref(b), C.byref(n)))
+        return b.value, n.value
+
+    def _shape(self, rank, which, layer):
+        d = self.dims
+        if which in (T_W, T_WGRAD, T_ADAM_M, T_ADAM_V):
+            return (d[layer], d[layer + 1])
+        if which == T_WSTAGE:
+            return (8 * d[layer], d[layer + 1])
+        rows = self.rows(rank)[1]
+        if which in (T_AHW, T_HW):
+            return (rows, d[layer + 1])
+        if which == T_X:
+            return (rows, d[0])
+        raise ValueError(f"tensor: unknown id {which}")
+
+    def read(self, which: int, layer: int = 0, rank: Optional[int] = None) -> np.ndarray:
+        rank = self.local_ranks[0] if rank is None else rank
+        shape = self._shape(rank, which, layer)
+        out = np.zeros(shape, np.float32)
+        _check(lib().mg_group_read(self._h, rank, which, layer, _p(out), out.size))
+        return out
+
+    def write(self, which: int, layer: int, data, rank: int = -1):
+        a = np.ascontiguousarray(data, np.float32)
+        _check(lib().mg_group_write(self._h, rank, which, layer, _p(a), a.size))
+
+    def params(self, rank: Optional[int] = None):
+        return [self.read(T_W, l, rank) for l in range(len(self.dims) - 1)]
+
+    def set_params(self, ws):
+        for l, w in enumerate(ws):
+            self.write(T_W, l, w)
+
+    def w_grads(self, rank: Optional[int] = None):
+        return [self.read(T_WGRAD, l, rank) for l in range(len(self.dims) - 1)]
+
+    def w_hash(self, rank: Optional[int] = None) -> int:
+        h = C.c_uint64()
+        _check(lib().mg_group_w_hash(self._h, self.local_ranks[0] if rank is None else rank, C.byref(h)))
+        return h.value
+
+    def buffer_audit(self):
+        lb, sa, by = C.c_int32(), C.c_int64(), C.c_int64()
+        _check(lib().mg_group_buffer_audit(self._h, C.byref(lb), C.byref(sa), C.byref(by)))
+        return lb.value, sa.value, by.value
+
+    def kernels_last_step(self) -> int:
+        a, b, c = C.c_double(), C.c_double(), C.c_double()
+        kk = C.c_int64()
+        _check(lib().mg_group_last_profile(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(kk)))
+        return kk.value
+
+    def logits(self, rank: Optional[int] = None):
+        return self.read(T_AHW, len(self.dims) - 2, rank)
+
+
+# ----------------------------------------------------------------------------- driver (driver.hpp:119-251)
+
+
+@dataclass
+class TrainOptions:
+    workers: int = 1
+    collect_logits: bool = False
+    on_epoch: Optional[Callable[[int, float, float, float], None]] = None
+    devices: Optional[list] = None
+    transport: int = TRANSPORT_AUTO
+
+
+@dataclass
+class TrainArtifacts:
+    epoch_loss: list = field(default_factory=list)
+    epoch_acc: list = field(default_factory=list)
+    epoch_wall_us: list = field(default_factory=list)
+    w_hashes: list = field(default_factory=list)  # [epoch][rank]
+    final_w: list = field(default_factory=list)   # rank 0's replicas
+    logits: Optional[np.ndarray] = None           # gathered post-training logits (permuted order)
+    workers: int = 1
+
+    def final_loss(self):
+        return self.epoch_loss[-1] if self.epoch_loss else 0.0
+
+    def final_acc(self):
+        return self.epoch_acc[-1] if self.epoch_acc else 0.0
+
+
+def train_run(ds: Dataset, cfg: GcnConfig, opts: TrainOptions = TrainOptions()) -> TrainArtifacts:
+    """inc/driver.hpp:140-206: prepare_data, init_params, `epochs` train steps, artifacts."""
+    cfg.validate()
+    if cfg.layer_dims[0] != ds.d0:
+        raise ConfigError(f"config: layer_dims[0]={cfg.layer_dims[0]} but dataset features have width {ds.d0}")
+    prep = prepare_data(ds, cfg, opts.workers)
+    art = TrainArtifacts(workers=opts.workers)
+    with Group(cfg, prep, opts.workers, devices=opts.devices, transport=opts.transport) as g:
+        g.init_params()
+        for e in range(1, cfg.epochs + 1):
+            loss = g.train_step(e)
+            art.epoch_loss.append(loss)
+            art.epoch_acc.append(g.last_accuracy)
+            art.epoch_wall_us.append(g.last_wall_us)
+            art.w_hashes.append([g.w_hash(r) for r in range(opts.workers)])
+            if opts.on_epoch:
+                opts.on_epoch(e, loss, g.last_accuracy, g.last_wall_us)
+        if opts.collect_logits:
+            g.loss_only()
+            art.logits = np.concatenate([g.logits(r) for r in range(opts.workers)], axis=0)
+        art.final_w = g.params(0)
+    return art
+
+
+@dataclass
+class GradArtifacts:
+    w_grad: list = field(default_factory=list)
+    grad_hash_per_rank: list = field(default_factory=list)
+    loss: float = 0.0
+
+
+def grad_run(ds: Dataset, cfg: GcnConfig, workers: int, devices=None, transport=TRANSPORT_AUTO) -> GradArtifacts:
+    """inc/driver.hpp:216-251: one forward/backward, W_G materialised, no update."""
+    cfg.validate()
+    prep = prepare_data(ds, cfg, workers)
+    art = GradArtifacts()
+    with Group(cfg, prep, workers, devices=devices, transport=transport) as g:
+        g.init_params()
+        art.loss = g.compute_gradients()
+        for r in range(workers):
+            art.grad_hash_per_rank.append(fnv1a(g.w_grads(r)))
+        art.w_grad = g.w_grads(0)
+    return art
+
+
+def fnv1a(arrays, h: int = 0xcbf29ce484222325) -> int:
+    """inc/gcn.hpp:87-94 over the raw bytes of each array in turn."""
+    for a in arrays:
+        b = np.frombuffer(np.ascontiguousarray(a).tobytes(), np.uint8)
+        for byte in b:
+            h ^= int(byte)
+            h = (h * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return h
+
+
+# ----------------------------------------------------------------------------- kernel-level entry points
+
+
+def dev_spmm(rows, row_ptr_ptr, edges_ptr, h_ptr, out_ptr, w, ld, accumulate=False, relu=False, mode=SPMM_EXACT,
+             stream=0):
+    """rowgcn::spmm on device pointers (see include/mggcn.h mg_dev_spmm)."""
+    _check(lib().mg_dev_spmm(rows, C.c_void_p(row_ptr_ptr), C.c_void_p(edges_ptr), C.c_void_p(h_ptr),
+                             C.c_void_p(out_ptr), w, ld, int(accumulate), int(relu), mode, C.c_void_p(stream)))
+
+
+def dev_gemm(ta, tb, M, N, K, a_ptr, lda, b_ptr, ldb, c_ptr, ldc, epilogue=0, mode=GEMM_EXACT, stream=0):
+    _check(lib().mg_dev_gemm(int(ta), int(tb), M, N, K, C.c_void_p(a_ptr), lda, C.c_void_p(b_ptr), ldb,
+                             C.c_void_p(c_ptr), ldc, epilogue, mode, C.c_void_p(stream)))

@@ -1,0 +1,124 @@
+"""GPU parity of the sm_100a kernels through the C ABI (mg_dev_spmm / mg_dev_gemm) against the CPU
+oracles: exact modes must be BITWISE equal to the reference's f32 arithmetic (inc/sparse.hpp:144-153,
+inc/dense.hpp:140-204)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+from gpu_util import bits_equal, dev_padded, dev_tile, pad4  # noqa: E402
+
+from paper_2110_08688_b200 import rowgcn as R  # noqa: E402
+
+
+def run_spmm(rp, ci, v, h, accumulate=False, out0=None, relu=False, mode=R.SPMM_EXACT):
+    rows = len(rp) - 1
+    w = h.shape[1]
+    ld = pad4(w)
+    rp_d, ed_d = dev_tile(rp, ci, v)
+    h_d = dev_padded(h, ld)
+    out_d = dev_padded(out0 if out0 is not None else np.zeros((rows, w), np.float32), ld)
+    R.dev_spmm(rows, rp_d.data_ptr(), ed_d.data_ptr(), h_d.data_ptr(), out_d.data_ptr(), w, ld, accumulate, relu, mode)
+    torch.cuda.synchronize()
+    out = out_d.cpu().numpy()
+    assert np.all(out[:, w:] == 0), "padding columns must stay zero"
+    return out[:, :w]
+
+
+@pytest.mark.parametrize("k", range(4))
+def test_spmm_exact_golden(golden, k):
+    rp, ci, v = golden[f"spmm{k}_f32_rp"], golden[f"spmm{k}_f32_ci"], golden[f"spmm{k}_f32_v"]
+    h = golden[f"spmm{k}_f32_h"]
+    assert bits_equal(run_spmm(rp, ci, v, h), golden[f"spmm{k}_f32_out"])
+    out = run_spmm(rp, ci, v, h, accumulate=True, out0=golden[f"spmm{k}_f32_o0"])
+    assert bits_equal(out, golden[f"spmm{k}_f32_acc"])
+
+
+def random_tile(rng, rows, cols, density, hub_rows=(), hub_len=0):
+    rp = [0]
+    ci, v = [], []
+    for r in range(rows):
+        if r in hub_rows:
+            cols_r = np.sort(rng.choice(cols, size=min(hub_len, cols), replace=False))
+        else:
+            cols_r = np.nonzero(rng.random(cols) < density)[0]
+        ci.extend(cols_r.tolist())
+        v.extend(rng.uniform(-1, 1, len(cols_r)).tolist())
+        rp.append(len(ci))
+    return np.array(rp, np.int64), np.array(ci, np.int64), np.array(v, np.float32)
+
+
+@pytest.mark.parametrize("w", [1, 3, 4, 7, 16, 40, 47, 64, 128, 256, 300, 602, 1100])
+def test_spmm_exact_widths(port32, w):
+    rng = np.random.default_rng(w)
+    rows, cols = 150, 90
+    rp, ci, v = random_tile(rng, rows, cols, 0.08)
+    h = rng.uniform(-1, 1, (cols, w)).astype(np.float32)
+    ref = port32.spmm(rows, cols, rp, ci, v, h)
+    assert bits_equal(run_spmm(rp, ci, v, h), ref)
+    o0 = rng.uniform(-1, 1, (rows, w)).astype(np.float32)
+    ref_acc = port32.spmm(rows, cols, rp, ci, v, h, True, o0)
+    assert bits_equal(run_spmm(rp, ci, v, h, True, o0), ref_acc)
+    relu = run_spmm(rp, ci, v, h, True, o0, relu=True)
+    assert bits_equal(relu, np.where(ref_acc > 0, ref_acc, np.float32(0)))
+
+
+@pytest.mark.parametrize("w", [8, 48, 256])
+def test_spmm_exact_hub_rows(port32, w):
+    """Rows above the heavy threshold take the cp.async hub kernel; still bitwise exact."""
+    rng = np.random.default_rng(7 + w)
+    rows, cols = 300, 5000
+    rp, ci, v = random_tile(rng, rows, cols, 0.002, hub_rows=(0, 17, 299), hub_len=4500)
+    h = rng.uniform(-1, 1, (cols, w)).astype(np.float32)
+    o0 = rng.uniform(-1, 1, (rows, w)).astype(np.float32)
+    ref = port32.spmm(rows, cols, rp, ci, v, h, True, o0)
+    R.set_tuning("heavy_row", 1000)
+    try:
+        out = run_spmm(rp, ci, v, h, True, o0)
+    finally:
+        R.set_tuning("heavy_row", 4096)
+    assert bits_equal(out, ref)
+
+
+def test_spmm_empty_rows_and_tile():
+    rp = np.zeros(6, np.int64)
+    out = run_spmm(rp, np.zeros(0, np.int64), np.zeros(0, np.float32), np.ones((4, 5), np.float32))
+    assert np.all(out == 0)
+
+
+def run_gemm(a, b, ta, tb, epi=0, c0=None, mode=R.GEMM_EXACT):
+    m = a.shape[1] if ta else a.shape[0]
+    k = a.shape[0] if ta else a.shape[1]
+    n = b.shape[0] if tb else b.shape[1]
+    a_d = dev_padded(a)
+    b_d = dev_padded(b)
+    c_d = dev_padded(c0 if c0 is not None else np.zeros((m, n), np.float32))
+    R.dev_gemm(ta, tb, m, n, k, a_d.data_ptr(), a_d.shape[1], b_d.data_ptr(), b_d.shape[1], c_d.data_ptr(),
+               c_d.shape[1], epi, mode)
+    torch.cuda.synchronize()
+    return c_d.cpu().numpy()[:, :n]
+
+
+@pytest.mark.parametrize("k,ta,tb", [(0, False, False), (1, True, False), (2, False, True)])
+def test_gemm_exact_golden(golden, k, ta, tb):
+    a, b = golden[f"gemm{k}_f32_a"], golden[f"gemm{k}_f32_b"]
+    assert bits_equal(run_gemm(a, b, ta, tb), golden[f"gemm{k}_f32_out"])
+
+
+@pytest.mark.parametrize("shape", [(1, 1, 1), (70, 33, 65), (300, 256, 100), (129, 47, 256), (5, 300, 17)])
+@pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True)])
+def test_gemm_exact_shapes(port32, shape, ta, tb):
+    m, n, k = shape
+    rng = np.random.default_rng(m * 7 + n * 3 + k)
+    a = rng.uniform(-1, 1, (k, m) if ta else (m, k)).astype(np.float32)
+    a[rng.random(a.shape) < 0.3] = 0
+    b = rng.uniform(-1, 1, (n, k) if tb else (k, n)).astype(np.float32)
+    ref = port32.gemm(a, b, ta, tb)
+    assert bits_equal(run_gemm(a, b, ta, tb), ref)
+    if not ta:
+        c0 = rng.normal(size=(m, n)).astype(np.float32)
+        got = run_gemm(a, b, ta, tb, epi=1, c0=c0)  # relu_backward mask (dense.hpp:221-231)
+        assert bits_equal(got, np.where(c0 > 0, ref, np.float32(0)))
+        got = run_gemm(a, b, ta, tb, epi=2)
+        assert bits_equal(got, np.where(ref > 0, ref, np.float32(0)))
