@@ -2,13 +2,16 @@
 // tcgen05 (5th-gen tensor core) GeMMs for the TF32X3 / TF32 modes — see mg_tc_gemm.cu.
 #pragma once
 #include <cuda_runtime.h>
+#include <cstddef>
 #include <cstdint>
 
 namespace mg {
 namespace tc {
 bool available();
 // C = op(A) op(B) (+ epilogue), row-major with leading dimensions; returns kernels launched.
+// TN (ta) needs a split-K workspace of tn_workspace_bytes(M, N, K) (one per concurrent stream).
 int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
-         int64_t ldb, float* C, int64_t ldc, int epi, cudaStream_t s);
+         int64_t ldb, float* C, int64_t ldc, int epi, float* ws, size_t ws_bytes, cudaStream_t s);
+size_t tn_workspace_bytes(int64_t M, int64_t N, int64_t K);
 }  // namespace tc
 }  // namespace mg
