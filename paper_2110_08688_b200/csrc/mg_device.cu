@@ -140,9 +140,10 @@ static int spmm_heavy(const SpmmLaunch& t, const float* h, float* out, index_t l
 
 // GeMM dispatch: exact SIMT or tcgen05 (mg_tc_gemm.cuh).
 static int gemm_launch(int mode, bool ta, bool tb, index_t M, index_t N, index_t K, const float* A, index_t lda,
-                       const float* B, index_t ldb, float* Cm, index_t ldc, int epi, cudaStream_t s) {
+                       const float* B, index_t ldb, float* Cm, index_t ldc, int epi, cudaStream_t s,
+                       float* ws = nullptr, size_t ws_bytes = 0) {
   if (M <= 0 || N <= 0) return 0;
-  if (mode != MG_GEMM_EXACT) return tc::gemm(mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, s);
+  if (mode != MG_GEMM_EXACT) return tc::gemm(mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, ws, ws_bytes, s);
   dim3 grid(ceil_div(M, k::kGBM), ceil_div(N, k::kGBN));
 #define MG_G(TA, TB, E) k::gemm_exact<TA, TB, E><<<grid, 256, 0, s>>>((int)M, (int)N, (int)K, A, lda, B, ldb, Cm, ldc)
   if (!ta && !tb) {
@@ -172,6 +173,8 @@ struct Worker {
   float *hw = nullptr, *bc1 = nullptr, *bc2 = nullptr;
   std::vector<float*> W, WG, M, V, stage;
   double* partials = nullptr;
+  float* ws = nullptr;  // tcgen05 TN split-K partials (W-grad), private to this worker's stream
+  size_t ws_bytes = 0;
   double* stats = nullptr;
   double* h_stats = nullptr;  // pinned
   int loss_blocks = 0;
@@ -413,7 +416,7 @@ class Step {
   void gemm(Worker& w, bool ta, bool tb, index_t M, index_t N, index_t K, const float* A, index_t lda, const float* B,
             index_t ldb, float* Cm, index_t ldc, int epi) {
     const int pi = prof_begin(w);
-    g_.kernels_last += gemm_launch(cfg_.gemm_mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, w.s0);
+    g_.kernels_last += gemm_launch(cfg_.gemm_mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, w.s0, w.ws, w.ws_bytes);
     prof_end(w, pi, 1);
   }
 
@@ -765,6 +768,16 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
         w.V.push_back(dalloc_t<float>(*g, w, sz));
         w.stage.push_back(dalloc_t<float>(*g, w, 8 * sz));
       }
+      if (cfg.gemm_mode != MG_GEMM_EXACT) {  // largest W-grad block this worker can own
+        index_t kmax = 1;
+        for (int b = 0; b < 8; ++b) {
+          const index_t a = std::max(g->wblocks[b], w.r0), e = std::min(g->wblocks[b + 1], w.r0 + w.rows);
+          kmax = std::max(kmax, e - a);
+        }
+        for (int l = 0; l < L; ++l)
+          w.ws_bytes = std::max(w.ws_bytes, tc::tn_workspace_bytes(g->ld[l], g->ld[l + 1], kmax));
+        w.ws = static_cast<float*>(dalloc(*g, w, w.ws_bytes));
+      }
       w.loss_blocks = std::max(1, std::min(ceil_div(w.rows, 8), num_sms() * 8));
       w.partials = dalloc_t<double>(*g, w, 2 * w.loss_blocks);
       w.stats = dalloc_t<double>(*g, w, 2);
@@ -1099,7 +1112,18 @@ mg_status mg_dev_gemm(int32_t ta, int32_t tb, int64_t M, int64_t N, int64_t K, c
                       void* stream) {
   return guarded([&] {
     if (epilogue < 0 || epilogue > 2) throw ValueError("gemm: unknown epilogue");
-    gemm_launch(mode, ta != 0, tb != 0, M, N, K, A, lda, B, ldb, Cm, ldc, epilogue, static_cast<cudaStream_t>(stream));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    float* ws = nullptr;
+    size_t wsb = 0;
+    if (ta && mode != MG_GEMM_EXACT) {
+      wsb = tc::tn_workspace_bytes(M, N, std::max<int64_t>(K, 1));
+      MG_CUDA(cudaMalloc(&ws, wsb));
+    }
+    gemm_launch(mode, ta != 0, tb != 0, M, N, K, A, lda, B, ldb, Cm, ldc, epilogue, st, ws, wsb);
+    if (ws) {
+      MG_CUDA(cudaStreamSynchronize(st));
+      MG_CUDA(cudaFree(ws));
+    }
   });
 }
 

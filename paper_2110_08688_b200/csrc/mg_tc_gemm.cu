@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(Params p) {
     chunk = blockIdx.x / p.m_tiles;
     m0 = static_cast<long>(mtile) * BM;
     k_begin = static_cast<long>(chunk) * kSplitRows;
-    k_end = std::min(p.K, k_begin + kSplitRows);
+    k_end = (p.K < k_begin + kSplitRows) ? p.K : k_begin + kSplitRows;
   } else {
     m0 = static_cast<long>(blockIdx.x) * BM;
     k_begin = 0;
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(Params p) {
   const int row = q * 32 + (threadIdx.x & 31);
   const long grow = m0 + row;
   const int cols_half = (((np + 31) / 32) + 1) / 2 * 32;
-  const int c_begin = half * cols_half, c_end = std::min(np, c_begin + cols_half);
+  const int c_begin = half * cols_half, c_end = min(np, c_begin + cols_half);
   for (int c0 = c_begin; c0 < c_end; c0 += 32) {
     float v[32];
     if (nk > 0) {

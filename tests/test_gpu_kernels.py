@@ -122,3 +122,42 @@ def test_gemm_exact_shapes(port32, shape, ta, tb):
         assert bits_equal(got, np.where(c0 > 0, ref, np.float32(0)))
         got = run_gemm(a, b, ta, tb, epi=2)
         assert bits_equal(got, np.where(ref > 0, ref, np.float32(0)))
+
+
+# ---------------------------------------------------------------------------- tcgen05 GeMMs
+# TF32X3 (3-term hi/lo split on kind::tf32): normwise error vs an fp64 product <= 1e-5 (measured ~1e-6);
+# TF32 (1 term) is the reduced-precision mode and only has to be within 5e-3.
+TC_SHAPES = [(1000, 256, 100), (777, 256, 256), (130, 48, 256), (300, 256, 47), (64, 16, 8), (513, 100, 602),
+             (2000, 256, 33)]
+
+
+@pytest.mark.parametrize("mode,tol", [(R.GEMM_TF32X3, 1e-5), (R.GEMM_TF32, 5e-3)])
+@pytest.mark.parametrize("shape", TC_SHAPES)
+@pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False)])
+def test_gemm_tcgen05(shape, ta, tb, mode, tol):
+    from gpu_util import normwise
+    m, n, k = shape
+    if ta:  # W-grad shape: M, N = layer widths, K = rows (exercise several 4096-row split-K chunks)
+        m, n, k = min(m, 256), n, k * 23
+    rng = np.random.default_rng(m + 3 * n + 7 * k + 11 * ta + 13 * tb)
+    a = rng.uniform(-1, 1, (k, m) if ta else (m, k)).astype(np.float32)
+    b = rng.uniform(-1, 1, (n, k) if tb else (k, n)).astype(np.float32)
+    ref = (a.astype(np.float64).T if ta else a.astype(np.float64)) @ (b.astype(np.float64).T if tb else b)
+    got = run_gemm(a, b, ta, tb, mode=mode)
+    assert normwise(got, ref) <= tol, normwise(got, ref)
+    if not ta:
+        c0 = rng.normal(size=(m, n)).astype(np.float32)
+        got1 = run_gemm(a, b, ta, tb, epi=1, c0=c0, mode=mode)
+        assert np.all(got1[c0 <= 0] == 0)
+        assert normwise(got1, np.where(c0 > 0, ref, 0)) <= tol
+        got2 = run_gemm(a, b, ta, tb, epi=2, mode=mode)
+        assert np.all(got2 >= 0) and normwise(got2, np.maximum(ref, 0)) <= tol
+
+
+def test_gemm_tcgen05_deterministic():
+    rng = np.random.default_rng(5)
+    a = rng.normal(size=(20000, 256)).astype(np.float32)
+    b = rng.normal(size=(20000, 47)).astype(np.float32)
+    r1 = run_gemm(a, b, True, False, mode=R.GEMM_TF32X3)
+    r2 = run_gemm(a, b, True, False, mode=R.GEMM_TF32X3)
+    assert bits_equal(r1, r2)

@@ -160,3 +160,47 @@ def test_loss_only_keeps_logits_and_matches_train_loss():
         assert bits_equal(gather(g, R.T_AHW, 1, 2), logits)
         l1 = g.compute_gradients()
         assert abs(l0 - l1) <= 1e-12 * abs(l1)
+
+
+@pytest.mark.parametrize("mode,tol", [(R.GEMM_TF32X3, 1e-4)])
+def test_step_dump_tcgen05(golden, mode, tol):
+    """The same teacher-forced step with the tcgen05 GeMMs: every tensor within the stated tolerance."""
+    ds, _ = small_ds(golden)
+    cfg = R.GcnConfig([12, 8, 6, 5], seed=5, permute=True, overlap=True, gemm_mode=mode)
+    with group(ds, cfg, 2) as g:
+        g.forward()
+        for l in range(3):
+            assert normwise(gather(g, R.T_AHW, l, 2), golden[f"dump300_ahw_fwd{l}"]) <= 1e-5
+    with group(ds, cfg, 2) as g:
+        g.compute_gradients()
+        for l in range(3):
+            assert normwise(g.read(R.T_WGRAD, l), golden[f"dump300_wgrad{l}"]) <= tol
+        for l in range(2):
+            assert normwise(gather(g, R.T_AHW, l, 2), golden[f"dump300_ahw_bwd{l}"]) <= tol
+    with group(ds, cfg, 2) as g:
+        loss = g.train_step(1)
+        assert abs(loss - golden["dump300_loss"][0]) <= tol * abs(golden["dump300_loss"][0])
+        for l in range(3):
+            assert normwise(g.read(R.T_W, l), golden[f"dump300_wafter{l}"]) <= tol
+
+
+def test_c1_trajectory_tcgen05(golden):
+    ds = R.synth_graph(2708, 3.9, 0.7, 1, 1433, 7)
+    cfg = R.GcnConfig([1433, 16, 7], epochs=5, seed=1, permute=True, gemm_mode=R.GEMM_TF32X3)
+    art = R.train_run(ds, cfg, R.TrainOptions(workers=1, devices=[0]))
+    ref64 = golden["c1_f64_perm1_loss"]
+    for e in range(5):
+        assert abs(art.epoch_loss[e] - ref64[e]) <= TOL * abs(ref64[e])
+
+
+def test_p_invariance_bitwise_tcgen05():
+    """The tcgen05 path is deterministic and row-local, and the W-grad split-K chunks are fixed relative to the
+    canonical blocks, so the W trajectory stays bitwise P-invariant in TF32X3 mode too."""
+    ds = R.synth_graph(9000, 8.0, 0.5, 44, 16, 4)
+    cfg = R.GcnConfig([16, 32, 4], epochs=3, seed=17, permute=True, overlap=True, gemm_mode=R.GEMM_TF32X3)
+    base = R.train_run(ds, cfg, R.TrainOptions(workers=1, devices=[0]))
+    for P in (2, 4):
+        dist = R.train_run(ds, cfg, R.TrainOptions(workers=P, devices=[0] * P, transport=R.TRANSPORT_LOCAL))
+        for e in range(cfg.epochs):
+            assert all(h == dist.w_hashes[e][0] for h in dist.w_hashes[e])
+            assert dist.w_hashes[e][0] == base.w_hashes[e][0]
