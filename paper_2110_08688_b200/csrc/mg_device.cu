@@ -648,6 +648,8 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
       g_heavy_row = static_cast<int>(std::min<int64_t>(value, 1 << 30));
     } else if (k == "profile") {
       g_profile = value != 0 ? 1 : 0;
+    } else if (k == "tn_chunk") {
+      tc::set_tn_chunk(static_cast<int>(value));
     } else {
       throw ValueError("tuning: unknown key '" + k + "'");
     }

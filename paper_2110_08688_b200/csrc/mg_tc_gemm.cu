@@ -36,7 +36,7 @@ namespace tc {
 constexpr int BM = 128;       // tile rows (TMEM lanes)
 constexpr int BK = 32;        // fp32 per 128-byte swizzle row
 constexpr int kThreads = 256;
-constexpr int kSplitRows = 4096;  // TN split-K chunk (rows), fixed relative to the block start
+static int g_split_rows = 4096;  // TN split-K chunk (rows), fixed relative to the block start (tuning "tn_chunk")
 
 __host__ __device__ constexpr int a_bytes() { return BM * BK * 4; }           // 16 KB
 __host__ __device__ constexpr int b_bytes(int np) { return np * BK * 4; }     // <= 32 KB
@@ -199,7 +199,7 @@ struct Params {
   int kpad;              // K padded to the source's 4-float granularity (direct operands)
   int epi;               // 0 store, 1 relu_backward mask in place, 2 relu
   float* partial;        // TN: [n_chunks][m_tiles][BM][np]
-  int n_chunks, m_tiles;
+  int n_chunks, m_tiles, k_chunk;
 };
 
 // MODE 0: NN (A direct, B transposed: W is K x N); 1: NT (A direct, B direct: W is N x K);
@@ -222,8 +222,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(Params p) {
     mtile = blockIdx.x % p.m_tiles;
     chunk = blockIdx.x / p.m_tiles;
     m0 = static_cast<long>(mtile) * BM;
-    k_begin = static_cast<long>(chunk) * kSplitRows;
-    k_end = (p.K < k_begin + kSplitRows) ? p.K : k_begin + kSplitRows;
+    k_begin = static_cast<long>(chunk) * p.k_chunk;
+    k_end = (p.K < k_begin + p.k_chunk) ? p.K : k_begin + p.k_chunk;
   } else {
     m0 = static_cast<long>(blockIdx.x) * BM;
     k_begin = 0;
@@ -315,7 +315,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(Params p) {
     if (MODE == 2) {
       float* dst = p.partial + ((static_cast<long>(chunk) * p.m_tiles + mtile) * BM + row) * np + c0;
 #pragma unroll
-      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      for (int i = 0; i < 32; i += 4)  // np % 16 == 0: a float4 is wholly inside or outside the row
+        if (c0 + i < np) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
     } else if (grow < p.M) {
       float* dst = p.C + grow * p.ldc;
 #pragma unroll
@@ -354,6 +355,11 @@ __global__ void reduce_partials(const float* __restrict__ partial, int n_chunks,
 
 bool available() { return true; }
 
+void set_tn_chunk(int rows) {
+  if (rows < BK || rows % BK) throw ValueError("tuning: tn_chunk must be a positive multiple of 32");
+  g_split_rows = rows;
+}
+
 namespace {
 template <int MODE, int TERMS>
 void launch(const Params& p, int grid, cudaStream_t s) {
@@ -372,7 +378,7 @@ void launch(const Params& p, int grid, cudaStream_t s) {
 size_t tn_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   const int np = static_cast<int>((N + 15) / 16 * 16);
   const long m_tiles = (M + BM - 1) / BM;
-  const long chunks = (K + kSplitRows - 1) / kSplitRows;
+  const long chunks = (K + g_split_rows - 1) / g_split_rows;
   return sizeof(float) * static_cast<size_t>(chunks * m_tiles * BM * np);
 }
 
@@ -409,7 +415,8 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
   // TN: split-K over fixed 4096-row chunks, then the fixed-order reduction (epilogue must be 0)
   if (epi != 0) throw ValueError("tc gemm: TN has no fused epilogue");
   p.m_tiles = static_cast<int>((M + BM - 1) / BM);
-  p.n_chunks = static_cast<int>(std::max<int64_t>(1, (K + kSplitRows - 1) / kSplitRows));
+  p.k_chunk = g_split_rows;
+  p.n_chunks = static_cast<int>(std::max<int64_t>(1, (K + p.k_chunk - 1) / p.k_chunk));
   if (!ws || ws_bytes < tn_workspace_bytes(M, N, std::max<int64_t>(K, 1)))
     throw ValueError("tc gemm: TN split-K workspace too small");
   p.partial = ws;

@@ -13,5 +13,6 @@ bool available();
 int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
          int64_t ldb, float* C, int64_t ldc, int epi, float* ws, size_t ws_bytes, cudaStream_t s);
 size_t tn_workspace_bytes(int64_t M, int64_t N, int64_t K);
+void set_tn_chunk(int rows);  // TN split-K chunk length (rows, multiple of 32); set before creating groups
 }  // namespace tc
 }  // namespace mg
