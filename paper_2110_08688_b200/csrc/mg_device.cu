@@ -70,8 +70,9 @@ void build_orders(const std::vector<index_t>& rp, std::vector<int>& light, std::
   light.clear();
   heavy.clear();
   for (index_t r = 0; r < rows; ++r) ((rp[r + 1] - rp[r]) >= ht ? heavy : light).push_back(static_cast<int>(r));
-  std::stable_sort(light.begin(), light.end(),
-                   [&](int a, int b) { return (rp[a + 1] - rp[a]) > (rp[b + 1] - rp[b]); });
+  auto longer = [&](int a, int b) { return (rp[a + 1] - rp[a]) > (rp[b + 1] - rp[b]); };
+  std::stable_sort(light.begin(), light.end(), longer);
+  std::stable_sort(heavy.begin(), heavy.end(), longer);
 }
 
 }  // namespace
@@ -132,7 +133,7 @@ static int spmm_heavy(const SpmmLaunch& t, const float* h, float* out, index_t l
     attr = true;
   }
   const int nslab = ceil_div(ld, k::kHeavySlab);
-  k::spmm_exact_heavy<<<t.n_heavy * nslab, 256, k::kHeavySmem, s>>>(t.row_ptr, t.edges, t.heavy, nslab, h, out,
+  k::spmm_exact_heavy<<<t.n_heavy * nslab, k::kHeavyThreads, k::kHeavySmem, s>>>(t.row_ptr, t.edges, t.heavy, nslab, h, out,
                                                                    static_cast<int>(ld), acc, relu);
   MG_LAUNCHED();
   return 1;
@@ -527,15 +528,28 @@ class Step {
         Worker& w = W(k);
         dev(w);
         const float* h_in = l == 0 ? w.x : w.ahw[l - 1];
-        for (int b = 0; b < 8; ++b) {
-          const index_t a = std::max(g_.wblocks[b], w.r0), e = std::min(g_.wblocks[b + 1], w.r0 + w.rows);
-          float* dst = w.stage[l] + b * bs;
-          if (a >= e) {
-            MG_CUDA(cudaMemsetAsync(dst, 0, sizeof(float) * bs, w.s0));
-            continue;
+        if (cfg_.gemm_mode != MG_GEMM_EXACT) {  // one tcgen05 launch for all 8 blocks (+ ordered reduction)
+          int64_t begin[8], len[8];
+          for (int b = 0; b < 8; ++b) {
+            const index_t a = std::max(g_.wblocks[b], w.r0), e = std::min(g_.wblocks[b + 1], w.r0 + w.rows);
+            begin[b] = std::max<index_t>(0, a - w.r0);
+            len[b] = std::max<index_t>(0, e - a);
           }
-          gemm(w, true, false, ldl, ldl1, e - a, h_in + (a - w.r0) * ldl, ldl, grad_rows[k] + (a - w.r0) * ldl1, ldl1,
-               dst, ldl1, 0);
+          const int pi = prof_begin(w);
+          g_.kernels_last += tc::gemm_tn_blocks(cfg_.gemm_mode, 8, begin, len, ldl, ldl1, h_in, ldl, grad_rows[k], ldl1,
+                                                w.stage[l], ldl1, bs, w.ws, w.ws_bytes, w.s0);
+          prof_end(w, pi, 1);
+        } else {
+          for (int b = 0; b < 8; ++b) {
+            const index_t a = std::max(g_.wblocks[b], w.r0), e = std::min(g_.wblocks[b + 1], w.r0 + w.rows);
+            float* dst = w.stage[l] + b * bs;
+            if (a >= e) {
+              MG_CUDA(cudaMemsetAsync(dst, 0, sizeof(float) * bs, w.s0));
+              continue;
+            }
+            gemm(w, true, false, ldl, ldl1, e - a, h_in + (a - w.r0) * ldl, ldl, grad_rows[k] + (a - w.r0) * ldl1,
+                 ldl1, dst, ldl1, 0);
+          }
         }
         MG_CUDA(cudaEventRecord(w.wg_done[l], w.s0));
         MG_CUDA(cudaStreamWaitEvent(w.s1, w.wg_done[l], 0));

@@ -104,75 +104,104 @@ __global__ void __launch_bounds__(256) spmm_exact_rows(const int* __restrict__ r
   }
 }
 
-// Long rows (hubs of the power-law graph): one CTA per (row, 64-column slab). The row's h-slabs are
-// streamed through a cp.async ring of NST stages x 32 nonzeros (all 256 threads produce), and the
-// first 64 threads consume them in column order, one output column each — the same left fold as
-// above, so still bitwise exact, but with ~64 KB of gathers in flight per CTA instead of one warp's.
+// Long rows (hubs of the power-law graph): one CTA per (row, 64-column slab), warp-specialised.
+// Warp 2 (producer) streams the row's h-slabs into an NST-deep ring of 32-nonzero stages with TMA
+// bulk copies (cp.async.bulk, one 256-byte copy per nonzero, completion counted in bytes on the
+// stage's mbarrier); warps 0-1 (consumers, one output column per thread) fold each stage in column
+// order with a separate multiply and add — the same left fold as above, so still bitwise exact — and
+// release the stage through a second mbarrier. ~56 KB of gathers stay in flight per CTA.
 constexpr int kHeavySlab = 64;
 constexpr int kHeavyB = 32;
 constexpr int kHeavyNst = 8;
-constexpr size_t kHeavySmem = sizeof(float) * (kHeavyNst * kHeavyB * kHeavySlab + kHeavyNst * kHeavyB);
+constexpr int kHeavyThreads = 96;
+constexpr size_t kHeavySmem = sizeof(float) * (kHeavyNst * kHeavyB * kHeavySlab + kHeavyNst * kHeavyB) + 16 * kHeavyNst + 128;
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
 
-__global__ void __launch_bounds__(256) spmm_exact_heavy(const int* __restrict__ row_ptr, const int2* __restrict__ edges,
-                                                        const int* __restrict__ heavy, int nslab,
-                                                        const float* __restrict__ h, float* __restrict__ out, int ld,
-                                                        int accumulate, int relu) {
-  extern __shared__ __align__(16) float smem[];
-  float* buf = smem;                                           // [NST][B][SLAB]
-  float* vals = smem + kHeavyNst * kHeavyB * kHeavySlab;       // [NST][B]
+__global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __restrict__ row_ptr,
+                                                                  const int2* __restrict__ edges,
+                                                                  const int* __restrict__ heavy, int nslab,
+                                                                  const float* __restrict__ h, float* __restrict__ out,
+                                                                  int ld, int accumulate, int relu) {
+  extern __shared__ __align__(128) float smem[];
+  float* buf = smem;                                       // [NST][B][SLAB]
+  float* vals = smem + kHeavyNst * kHeavyB * kHeavySlab;   // [NST][B]
+  uint64_t* full = reinterpret_cast<uint64_t*>(vals + kHeavyNst * kHeavyB);
+  uint64_t* empty = full + kHeavyNst;
   const int r = heavy[blockIdx.x / nslab];
   const int col0 = (blockIdx.x % nslab) * kHeavySlab;
   const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
   const int nst_total = (e1 - e0 + kHeavyB - 1) / kHeavyB;
-  const int t = threadIdx.x;
-  const int my_col = col0 + t;
-  float acc = 0.0f;
-  if (t < kHeavySlab && accumulate && my_col < ld) acc = out[(size_t)r * ld + my_col];
-
-  auto issue = [&](int st) {
-    if (st < nst_total) {
-      const int slot = st % kHeavyNst;
-      const int base = e0 + st * kHeavyB;
-      // 32 edges x 16 chunks of 16 B = 512 copies; 2 per thread
-      for (int q = t; q < kHeavyB * (kHeavySlab / 4); q += blockDim.x) {
-        const int b = q / (kHeavySlab / 4), c4 = q % (kHeavySlab / 4);
-        const int e = base + b;
-        const int c = col0 + 4 * c4;
-        if (e < e1 && c < ld) {
-          const int2 ed = __ldg(edges + e);
-          cp_async16(buf + ((size_t)slot * kHeavyB + b) * kHeavySlab + 4 * c4, h + (size_t)ed.x * ld + c);
-        }
-      }
-      if (t < kHeavyB) {
-        const int e = base + t;
-        vals[slot * kHeavyB + t] = e < e1 ? __int_as_float(__ldg(edges + e).y) : 0.0f;
-      }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t slab_bytes = static_cast<uint32_t>(min(kHeavySlab, ld - col0)) * 4u;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kHeavyNst; ++s) {
+      mbar_init(&full[s], 32);
+      mbar_init(&empty[s], 2);
     }
-    cp_async_commit();
-  };
-  for (int s = 0; s < kHeavyNst - 1; ++s) issue(s);
-  for (int st = 0; st < nst_total; ++st) {
-    cp_async_wait<kHeavyNst - 2>();
-    __syncthreads();
-    issue(st + kHeavyNst - 1);
-    if (t < kHeavySlab && my_col < ld) {
-      const int slot = st % kHeavyNst;
-      const int cnt = min(kHeavyB, e1 - (e0 + st * kHeavyB));
-      const float* bs = buf + (size_t)slot * kHeavyB * kHeavySlab + t;
-      const float* vs = vals + slot * kHeavyB;
-      for (int b = 0; b < cnt; ++b) acc = fma_free(acc, vs[b], bs[b * kHeavySlab]);
-    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  cp_async_wait<0>();
-  if (t < kHeavySlab && my_col < ld) out[(size_t)r * ld + my_col] = relu ? relu1(acc) : acc;
+  __syncthreads();
+  if (warp == 2) {  // producer
+    for (int st = 0; st < nst_total; ++st) {
+      const int s = st % kHeavyNst;
+      if (st >= kHeavyNst) mbar_wait(&empty[s], ((st / kHeavyNst) - 1) & 1);
+      const int base = e0 + st * kHeavyB;
+      const int cnt = min(kHeavyB, e1 - base);
+      if (lane == 0) mbar_arrive_tx(&full[s], slab_bytes * cnt);
+      __syncwarp();
+      if (lane < cnt) {
+        const int2 ed = __ldg(edges + base + lane);
+        vals[s * kHeavyB + lane] = __int_as_float(ed.y);
+        bulk_g2s(buf + ((size_t)s * kHeavyB + lane) * kHeavySlab, h + (size_t)ed.x * ld + col0, slab_bytes, &full[s]);
+      }
+      if (lane != 0) mbar_arrive(&full[s]);
+    }
+  } else {  // consumers: one column each
+    const int t = threadIdx.x;
+    const int my_col = col0 + t;
+    const bool active = my_col < ld;
+    float acc = 0.0f;
+    if (active && accumulate) acc = out[(size_t)r * ld + my_col];
+    for (int st = 0; st < nst_total; ++st) {
+      const int s = st % kHeavyNst;
+      mbar_wait(&full[s], (st / kHeavyNst) & 1);
+      const int cnt = min(kHeavyB, e1 - (e0 + st * kHeavyB));
+      const float* bs = buf + (size_t)s * kHeavyB * kHeavySlab + t;
+      const float* vs = vals + s * kHeavyB;
+      if (active)
+        for (int b = 0; b < cnt; ++b) acc = fma_free(acc, vs[b], bs[b * kHeavySlab]);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (active) out[(size_t)r * ld + my_col] = relu ? relu1(acc) : acc;
+  }
 }
 
 // ============================================================================ GeMM (exact SIMT)

@@ -1,21 +1,28 @@
 // SPDX-License-Identifier: Apache-2.0
 //
-// tcgen05 GeMMs of the training step (TF32X3 and TF32 modes), hand-written PTX for sm_100a.
+// tcgen05 GeMMs of the training step (TF32X3 and TF32 modes): TMA-fed, warp-specialised, persistent.
 //
-//   NN  C[M,N] = A[M,K] W[K,N]       forward HW = H W            (rowgcn gemm NN, dense.hpp:158-169)
-//   NT  C[M,N] = A[M,K] W[N,K]^T     H-grad, relu_backward fused (dense.hpp:182-193, :221-231)
-//   TN  C[M,N] = A[K,M]^T B[K,N]     W-grad per canonical block  (dense.hpp:170-181), deterministic split-K
+//   NN  C[M,N] = A[M,K] W[K,N]       forward HW = H W             (rowgcn gemm NN, dense.hpp:158-169)
+//   NT  C[M,N] = A[M,K] W[N,K]^T     H-grad with relu_backward fused (dense.hpp:182-193, :221-231)
+//   TN  stage[g] = H[rows_g]^T G[rows_g] for the 8 canonical row blocks g (W-grad, gcn.hpp:316-331)
 //
-// Operands are staged by SIMT producer threads: float4 global loads, split x = hi + lo with
-// hi = x & 0xffffe000 (exactly representable in TF32, so the tensor core reads it unchanged) and
-// lo = x - hi (exact in fp32), written into the canonical UMMA K-major SWIZZLE_128B layout (8-row x
-// 128-byte atoms, 16-byte chunk c of row r stored at chunk c ^ (r & 7)). One elected thread issues
-// tcgen05.mma.kind::tf32 (M = 128, N <= 256, K = 8 per instruction) accumulating
-//   D += A_hi B_hi + A_hi B_lo + A_lo B_hi        (TF32X3: fp32-level accuracy, ~2^-21 relative)
-//   D += A_hi B_hi                                (TF32:   the 1-term mode, reported separately)
-// into TMEM; tcgen05.commit arrives on an mbarrier per smem stage (double buffered, the next K block is
-// staged while the tensor core consumes the current one). The epilogue reads TMEM with tcgen05.ld
-// (warp w owns TMEM lanes 32*(w%4)..+31 = tile rows) and applies the fused epilogue on the way to HBM.
+// Per 16-deep K block, warp 0 (one lane) issues TMA tensor loads of the raw fp32 tiles straight into
+// the UMMA canonical smem layouts: K-major operands (A of NN/NT, B of NT) as SWIZZLE_64B boxes
+// {16 k, rows}; MN-major operands (B = W of NN, both operands of TN, which are K x M row-major in HBM)
+// as SWIZZLE_128B boxes {32 mn, 16 k} — no transposition anywhere. Warps 2-5 split each element
+// in place, x = hi + lo with hi = x & 0xffffe000 (exact in TF32) and lo = x - hi (exact in fp32), and
+// mask TN rows past the chunk end. Warp 1 (one lane) issues tcgen05.mma.kind::tf32 (M = 128,
+// N <= 256, K = 8) into one of two TMEM accumulators:
+//   TF32X3: D += A_lo B_hi + A_hi B_lo + A_hi B_hi      TF32: D += A_hi B_hi
+// Warps 6-9 drain TMEM with tcgen05.ld (warp w owns lanes 32*(w%4)) and apply the fused epilogue on
+// the way to HBM. The tensor core accumulates with truncation, so the long-K TN GeMM is "promoted":
+// every 256 rows the TMEM partial is drained and added in fp32 round-to-nearest into the work item's
+// partial tile (L2 resident); partials of fixed 4096-row chunks (relative to the block start) are then
+// summed in chunk order — deterministic and independent of the number of workers P.
+// mbarriers: full[s] (TMA bytes) -> conv[s] (split done) -> empty[s] (tcgen05.commit) for the smem
+// ring; tfull[b] (tcgen05.commit) / tempty[b] (epilogue) for the two TMEM accumulators.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,27 +40,49 @@ namespace tc {
     if (_e != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(_e));           \
   } while (0)
 
-constexpr int BM = 128;       // tile rows (TMEM lanes)
-constexpr int BK = 32;        // fp32 per 128-byte swizzle row
-constexpr int kThreads = 256;
-static int g_split_rows = 4096;  // TN split-K chunk (rows), fixed relative to the block start (tuning "tn_chunk")
+constexpr int BM = 128;            // tile rows = TMEM lanes
+constexpr int BK = 16;             // K per pipeline stage
+constexpr int kMaxStages = 8;
+constexpr int kThreads = 320;      // 10 warps: 0 TMA, 1 MMA, 2-5 split, 6-9 epilogue
+constexpr int kPromoteKb = 16;     // TN: drain TMEM every 16 K blocks (256 rows)
+constexpr int kSmemBudget = 200 * 1024;
+static int g_split_rows = 4096;    // TN chunk (rows), fixed relative to the block start ("tn_chunk")
 
-__host__ __device__ constexpr int a_bytes() { return BM * BK * 4; }           // 16 KB
-__host__ __device__ constexpr int b_bytes(int np) { return np * BK * 4; }     // <= 32 KB
-__host__ __device__ constexpr int stage_bytes(int np, int terms) {
-  return terms == 1 ? a_bytes() + b_bytes(np) : 2 * (a_bytes() + b_bytes(np));
-}
-inline int smem_bytes(int np, int terms) { return 2 * stage_bytes(np, terms) + 1024 + 64; }
+enum { NN = 0, NT = 1, TN = 2 };
+
+struct Params {
+  long M, N, K;          // NN/NT: C is M x N, reduction K. TN: M, N = output dims; rows given per block
+  int np;                // N padded to 16 (MMA N)
+  int npb;               // B rows held in smem per stage (np for K-major B, np rounded to 32 for MN-major)
+  int tstride;           // TMEM columns per accumulator (npb rounded to 32)
+  int nst;               // smem stages
+  int m_tiles;
+  int n_items;           // work items
+  int terms;             // 3 = TF32X3, 1 = TF32
+  float* C;
+  long ldc;
+  int epi;               // 0 store, 1 relu_backward mask in place, 2 relu
+  // TN
+  int chunk_rows;
+  int nblocks;
+  long blk_begin[8], blk_len[8];
+  int blk_first[9];      // first work item of each block (prefix over blocks)
+  float* partial;        // [n_items][BM][npb]
+};
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
 }
-
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
@@ -62,27 +91,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       "@!p bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity));
+      "r"(parity)
+      : "memory");
 }
-
-// SWIZZLE_128B K-major matrix descriptor (sm_100 "version 1"): start >> 4, LBO = 16 B (unused for
-// swizzled K-major), SBO = 1024 B between 8-row groups, layout type 2 = SWIZZLE_128B.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
-  d |= static_cast<uint64_t>(1) << 16;
-  d |= static_cast<uint64_t>(1024 >> 4) << 32;
-  d |= static_cast<uint64_t>(1) << 46;
-  d |= static_cast<uint64_t>(2) << 61;
-  return d;
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
 }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
 
-// kind::tf32 instruction descriptor: D f32, A/B tf32, both K-major, N >> 3 at bit 17, M >> 4 at bit 24.
-__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
-         (static_cast<uint32_t>(m >> 4) << 24);
+// K-major SWIZZLE_64B: 8-row x 64-byte atoms, SBO = 512 B between 8-row groups, LBO unused (16 B).
+__device__ __forceinline__ uint64_t desc_k64(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(512 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(4) << 61);
 }
-
+// MN-major SWIZZLE_128B: 8 k-rows x 128-byte (32 fp32 along M/N) atoms; LBO = 2048 B between atoms along
+// M/N (one 16-row TMA box each), SBO = 1024 B between the two 8-row atoms along K.
+__device__ __forceinline__ uint64_t desc_mn128(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(2048 >> 4) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
+}
+// kind::tf32 instruction descriptor: D f32 (bit 4), A/B tf32 (2 at bits 7, 10), majors (bits 15, 16),
+// N >> 3 at bit 17, M >> 4 at bit 24.
+__host__ __device__ constexpr uint32_t idesc_tf32(int m, int n, int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | (static_cast<uint32_t>(a_mn) << 15) | (static_cast<uint32_t>(b_mn) << 16) |
+         (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
   asm volatile(
       "{\n"
@@ -92,16 +131,10 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
       "}\n" ::"r"(tmem_d),
       "l"(a), "l"(b), "r"(idesc), "r"(acc));
 }
-
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
 }
-
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
   asm volatile(
@@ -116,317 +149,430 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
-
-// byte offset of (row, 16-byte chunk) inside a K-major SW128 tile of 128-byte rows
-__device__ __forceinline__ uint32_t sw128_off(int row, int chunk) {
-  return static_cast<uint32_t>((row >> 3) * 1024 + (row & 7) * 128 + ((chunk ^ (row & 7)) << 4));
+__device__ __forceinline__ float4 split4(float4 x, float4& lo) {
+  float4 h;
+  h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
+  h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
+  h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
+  h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
+  lo = make_float4(__fsub_rn(x.x, h.x), __fsub_rn(x.y, h.y), __fsub_rn(x.z, h.z), __fsub_rn(x.w, h.w));
+  return h;
 }
 
-__device__ __forceinline__ void split(float x, float& hi, float& lo) {
-  hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-  lo = __fsub_rn(x, hi);
-}
-
-// ---------------------------------------------------------------- operand staging
-// "direct": source row-major with K contiguous (rows = tile rows). Each 16-byte chunk is one float4.
-template <bool SPLIT>
-__device__ __forceinline__ void stage_direct(uint8_t* hi, uint8_t* lo, const float* __restrict__ src, long ld,
-                                             long row0, long rows_valid, int rows_tile, int k0, int kpad) {
-  const int nchunks = rows_tile * (BK / 4);
-  for (int q = threadIdx.x; q < nchunks; q += kThreads) {
-    const int r = q >> 3, c = q & 7;
-    const long gr = row0 + r;
-    const int k = k0 + 4 * c;
-    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (gr < rows_valid && k < kpad) x = __ldg(reinterpret_cast<const float4*>(src + gr * ld + k));
-    const uint32_t off = sw128_off(r, c);
-    if (SPLIT) {
-      float4 h, l;
-      split(x.x, h.x, l.x);
-      split(x.y, h.y, l.y);
-      split(x.z, h.z, l.z);
-      split(x.w, h.w, l.w);
-      *reinterpret_cast<float4*>(hi + off) = h;
-      *reinterpret_cast<float4*>(lo + off) = l;
-    } else {
-      *reinterpret_cast<float4*>(hi + off) = x;
-    }
-  }
-}
-
-// "transposed": source row-major K x R (K = rows of the source, R contiguous). Lanes cover 8 k x 4
-// float4 groups so the global reads are full 32-byte sectors and the scattered 4-byte smem writes
-// hit at most 2 ways of every bank.
-template <bool SPLIT>
-__device__ __forceinline__ void stage_trans(uint8_t* hi, uint8_t* lo, const float* __restrict__ src, long ld,
-                                            long k_row0, long k_rows_valid, int r0, int r_valid, int rows_tile) {
-  const int groups = rows_tile / 4;  // float4 groups along R
-  const int total = BK * groups;
-  for (int q = threadIdx.x; q < total; q += kThreads) {
-    const int lane = q & 31, wq = q >> 5;
-    const int kk = (lane & 7) + 8 * (wq % (BK / 8));
-    const int g4 = (lane >> 3) + 4 * (wq / (BK / 8));
-    if (g4 >= groups) continue;
-    const long gk = k_row0 + kk;
-    const int rr = 4 * g4;
-    float4 x = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (gk < k_rows_valid && r0 + rr < r_valid) x = __ldg(reinterpret_cast<const float4*>(src + gk * ld + r0 + rr));
-    const float xs[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t off = sw128_off(rr + i, kk >> 2) + ((kk & 3) << 2);
-      if (SPLIT) {
-        float h, l;
-        split(xs[i], h, l);
-        *reinterpret_cast<float*>(hi + off) = h;
-        *reinterpret_cast<float*>(lo + off) = l;
-      } else {
-        *reinterpret_cast<float*>(hi + off) = xs[i];
-      }
-    }
-  }
-}
-
-struct Params {
-  long M, N, K;          // logical sizes (K: reduction length; for TN the rows of A/B)
-  const float* A;
-  long lda;
-  const float* B;
-  long ldb;
-  float* C;
-  long ldc;
-  int np;                // padded N (multiple of 16, <= 256)
-  int kpad;              // K padded to the source's 4-float granularity (direct operands)
-  int epi;               // 0 store, 1 relu_backward mask in place, 2 relu
-  float* partial;        // TN: [n_chunks][m_tiles][BM][np]
-  int n_chunks, m_tiles, k_chunk;
+// ---------------------------------------------------------------- work decomposition
+struct Item {
+  long row0;    // NN/NT: first output row. TN: first K row (local)
+  long k_end;   // TN: one past the last K row of this item
+  int mt;       // TN: m tile
+  int nkb;      // K blocks of the item
 };
 
-// MODE 0: NN (A direct, B transposed: W is K x N); 1: NT (A direct, B direct: W is N x K);
-// 2: TN (A transposed: H is K x M, B transposed: G is K x N), split-K partials.
-template <int MODE, int TERMS>
-__global__ void __launch_bounds__(kThreads, 1) gemm_tc(Params p) {
+__device__ __forceinline__ Item item_of(const Params& p, int MODE_, int it) {
+  Item r{};
+  if (MODE_ != TN) {
+    r.row0 = static_cast<long>(it) * BM;
+    r.nkb = static_cast<int>((p.K + BK - 1) / BK);
+    return r;
+  }
+  int g = 0;
+  while (g + 1 < p.nblocks && it >= p.blk_first[g + 1]) ++g;
+  const int local = it - p.blk_first[g];
+  const int c = local / p.m_tiles;
+  r.mt = local % p.m_tiles;
+  r.row0 = p.blk_begin[g] + static_cast<long>(c) * p.chunk_rows;
+  const long end = p.blk_begin[g] + p.blk_len[g];
+  r.k_end = (r.row0 + p.chunk_rows < end) ? r.row0 + p.chunk_rows : end;
+  r.nkb = static_cast<int>((r.k_end - r.row0 + BK - 1) / BK);
+  return r;
+}
+
+// ---------------------------------------------------------------- the kernel
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc(const __grid_constant__ CUtensorMap map_a,
+                                                       const __grid_constant__ CUtensorMap map_b, Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t mbar[2];
+  __shared__ uint64_t full[kMaxStages], conv[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_s;
-  const int warp = threadIdx.x >> 5;
-  constexpr bool SPLIT = TERMS == 3;
-  const int np = p.np;
-  const int sb = stage_bytes(np, TERMS);
-
-  // work item
-  long m0, k_begin, k_end;
-  int chunk = 0, mtile = 0;
-  if (MODE == 2) {
-    mtile = blockIdx.x % p.m_tiles;
-    chunk = blockIdx.x / p.m_tiles;
-    m0 = static_cast<long>(mtile) * BM;
-    k_begin = static_cast<long>(chunk) * p.k_chunk;
-    k_end = (p.K < k_begin + p.k_chunk) ? p.K : k_begin + p.k_chunk;
-  } else {
-    m0 = static_cast<long>(blockIdx.x) * BM;
-    k_begin = 0;
-    k_end = p.K;
-  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr bool A_MN = MODE == TN;
+  constexpr bool B_MN = MODE != NT;
+  const int a_bytes = BM * BK * 4;          // 8 KB
+  const int b_bytes = p.npb * BK * 4;
+  const int half = a_bytes + b_bytes;       // hi (TMA target) part of a stage; lo part follows
+  const int stage = p.terms == 3 ? 2 * half : half;
+  const uint32_t tx_bytes = static_cast<uint32_t>(half);
+  const uint32_t tmem_cols = 2 * p.tstride <= 32 ? 32 : 2 * p.tstride <= 64 ? 64 : 2 * p.tstride <= 128 ? 128
+                             : 2 * p.tstride <= 256 ? 256 : 512;
 
   if (threadIdx.x == 0) {
-    mbar_init(&mbar[0], 1);
-    mbar_init(&mbar[1], 1);
+    for (int s = 0; s < p.nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 0) {
-    const uint32_t cols = np <= 32 ? 32 : np <= 64 ? 64 : np <= 128 ? 128 : 256;
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+  }
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_s)),
-                 "r"(cols));
+                 "r"(tmem_cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
-  const uint32_t idesc = idesc_tf32(BM, np);
 
-  const int nk = static_cast<int>((k_end - k_begin + BK - 1) / BK);
-  uint32_t phase[2] = {0, 0};
-  for (int it = 0; it < nk; ++it) {
-    const int s = it & 1;
-    if (it >= 2) {
-      mbar_wait(&mbar[s], phase[s]);
-      phase[s] ^= 1;
-    }
-    uint8_t* a_hi = smem + s * sb;
-    uint8_t* a_lo = a_hi + a_bytes();
-    uint8_t* b_hi = SPLIT ? a_lo + a_bytes() : a_hi + a_bytes();
-    uint8_t* b_lo = b_hi + b_bytes(np);
-    const long k0 = k_begin + static_cast<long>(it) * BK;
-    if (MODE == 2) {
-      stage_trans<SPLIT>(a_hi, a_lo, p.A, p.lda, k0, k_end, static_cast<int>(m0), static_cast<int>(p.M), BM);
-      stage_trans<SPLIT>(b_hi, b_lo, p.B, p.ldb, k0, k_end, 0, static_cast<int>(p.N), np);
-    } else {
-      stage_direct<SPLIT>(a_hi, a_lo, p.A, p.lda, m0, p.M, BM, static_cast<int>(k0), p.kpad);
-      if (MODE == 0)
-        stage_trans<SPLIT>(b_hi, b_lo, p.B, p.ldb, k0, p.K, 0, static_cast<int>(p.N), np);
-      else
-        stage_direct<SPLIT>(b_hi, b_lo, p.B, p.ldb, 0, p.N, np, static_cast<int>(k0), p.kpad);
-    }
-    fence_async_smem();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      tc_fence_after();
-      const uint32_t ah = smem_u32(a_hi), al = smem_u32(a_lo), bh = smem_u32(b_hi), bl = smem_u32(b_lo);
-#pragma unroll
-      for (int kk = 0; kk < BK / 8; ++kk) {
-        const uint32_t off = kk * 32;  // 8 tf32 = 32 bytes along the swizzled row
-        const uint32_t acc0 = (it > 0 || kk > 0) ? 1u : 0u;
-        if (SPLIT) {
-          mma_tf32(tmem, sw128_desc(al + off), sw128_desc(bh + off), idesc, acc0);
-          mma_tf32(tmem, sw128_desc(ah + off), sw128_desc(bl + off), idesc, 1u);
-          mma_tf32(tmem, sw128_desc(ah + off), sw128_desc(bh + off), idesc, 1u);
-        } else {
-          mma_tf32(tmem, sw128_desc(ah + off), sw128_desc(bh + off), idesc, acc0);
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t sc = 0;
+      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+        const Item I = item_of(p, MODE, it);
+        for (int kb = 0; kb < I.nkb; ++kb, ++sc) {
+          const int s = sc % p.nst;
+          if (sc >= static_cast<uint32_t>(p.nst)) mbar_wait(&empty[s], ((sc / p.nst) - 1) & 1);
+          uint8_t* a = smem + s * stage;
+          uint8_t* b = a + a_bytes;
+          mbar_arrive_tx(&full[s], tx_bytes);
+          if (MODE == TN) {
+            const int k0 = static_cast<int>(I.row0) + kb * BK;
+            for (int j = 0; j < BM / 32; ++j) tma_load_2d(a + j * 2048, &map_a, I.mt * BM + j * 32, k0, &full[s]);
+            for (int j = 0; j < p.npb / 32; ++j) tma_load_2d(b + j * 2048, &map_b, j * 32, k0, &full[s]);
+          } else {
+            const int k0 = kb * BK;
+            tma_load_2d(a, &map_a, k0, static_cast<int>(I.row0), &full[s]);
+            if (B_MN) {
+              for (int j = 0; j < p.npb / 32; ++j) tma_load_2d(b + j * 2048, &map_b, j * 32, k0, &full[s]);
+            } else {
+              tma_load_2d(b, &map_b, k0, 0, &full[s]);
+            }
+          }
         }
       }
-      mma_commit(&mbar[s]);
     }
-  }
-  // the last commit tracks every MMA issued before it
-  if (nk > 0) {
-    const int s = (nk - 1) & 1;
-    mbar_wait(&mbar[s], phase[s]);
-  }
-  tc_fence_after();
-
-  // epilogue: warps w and w+4 share TMEM lanes 32*(w%4) (tile rows), splitting the columns
-  const int q = warp & 3;
-  const int half = warp >> 2;
-  const int row = q * 32 + (threadIdx.x & 31);
-  const long grow = m0 + row;
-  const int cols_half = (((np + 31) / 32) + 1) / 2 * 32;
-  const int c_begin = half * cols_half, c_end = min(np, c_begin + cols_half);
-  for (int c0 = c_begin; c0 < c_end; c0 += 32) {
-    float v[32];
-    if (nk > 0) {
-      tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
-    } else {
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer
+    const uint32_t idesc = idesc_tf32(BM, p.np, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    uint32_t sc = 0, ac = 0;
+    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+      const Item I = item_of(p, MODE, it);
+      const int groups = MODE == TN ? (I.nkb + kPromoteKb - 1) / kPromoteKb : 1;
+      for (int gi = 0; gi < groups; ++gi, ++ac) {
+        const int kb0 = MODE == TN ? gi * kPromoteKb : 0;
+        const int kb1 = MODE == TN ? min(I.nkb, kb0 + kPromoteKb) : I.nkb;
+        const int buf = ac & 1;
+        if (ac >= 2) mbar_wait(&tempty[buf], ((ac >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + static_cast<uint32_t>(buf * p.tstride);
+        for (int kb = kb0; kb < kb1; ++kb, ++sc) {
+          const int s = sc % p.nst;
+          mbar_wait(&conv[s], (sc / p.nst) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t ah = smem_u32(smem + s * stage), bh = ah + a_bytes;
+            const uint32_t al = ah + half, bl = bh + half;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = 0.f;
-    }
-    if (MODE == 2) {
-      float* dst = p.partial + ((static_cast<long>(chunk) * p.m_tiles + mtile) * BM + row) * np + c0;
-#pragma unroll
-      for (int i = 0; i < 32; i += 4)  // np % 16 == 0: a float4 is wholly inside or outside the row
-        if (c0 + i < np) *reinterpret_cast<float4*>(dst + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-    } else if (grow < p.M) {
-      float* dst = p.C + grow * p.ldc;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const long c = c0 + i;
-        if (c < p.N) {
-          float r = v[i];
-          if (p.epi == 1) r = dst[c] > 0.0f ? r : 0.0f;
-          if (p.epi == 2) r = r > 0.0f ? r : 0.0f;
-          dst[c] = r;
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint32_t ao = A_MN ? kk * 1024 : kk * 32, bo = B_MN ? kk * 1024 : kk * 32;
+              const uint64_t dah = A_MN ? desc_mn128(ah + ao) : desc_k64(ah + ao);
+              const uint64_t dbh = B_MN ? desc_mn128(bh + bo) : desc_k64(bh + bo);
+              const uint32_t first = (kb == kb0 && kk == 0) ? 0u : 1u;
+              if (p.terms == 3) {
+                const uint64_t dal = A_MN ? desc_mn128(al + ao) : desc_k64(al + ao);
+                const uint64_t dbl = B_MN ? desc_mn128(bl + bo) : desc_k64(bl + bo);
+                mma_tf32(d, dal, dbh, idesc, first);
+                mma_tf32(d, dah, dbl, idesc, 1u);
+                mma_tf32(d, dah, dbh, idesc, 1u);
+              } else {
+                mma_tf32(d, dah, dbh, idesc, first);
+              }
+            }
+            mma_commit(&empty[s]);
+          }
+          __syncwarp();
         }
+        if (lane == 0) mma_commit(&tfull[buf]);
+        __syncwarp();
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ split (+ TN chunk-end mask)
+    const int t = threadIdx.x - 64;  // 0..127
+    uint32_t sc = 0;
+    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+      const Item I = item_of(p, MODE, it);
+      for (int kb = 0; kb < I.nkb; ++kb, ++sc) {
+        const int s = sc % p.nst;
+        mbar_wait(&full[s], (sc / p.nst) & 1);
+        uint8_t* hi = smem + s * stage;
+        uint8_t* lo = hi + half;
+        const int valid_rows = MODE == TN ? static_cast<int>(min(static_cast<long>(BK), I.k_end - (I.row0 + kb * BK))) : BK;
+        if (p.terms == 3 || valid_rows < BK) {
+          for (int q = t; q < half / 16; q += 128) {
+            float4 x = reinterpret_cast<float4*>(hi)[q];
+            if (MODE == TN && valid_rows < BK && q < a_bytes / 16) {
+              const int krow = ((q * 16) % 2048) >> 7;  // row of the MN-major box
+              if (krow >= valid_rows) x = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            if (p.terms == 3) {
+              float4 l;
+              const float4 h = split4(x, l);
+              reinterpret_cast<float4*>(hi)[q] = h;
+              reinterpret_cast<float4*>(lo)[q] = l;
+            } else {
+              reinterpret_cast<float4*>(hi)[q] = x;
+            }
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    uint32_t ac = 0;
+    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+      const Item I = item_of(p, MODE, it);
+      const int groups = MODE == TN ? (I.nkb + kPromoteKb - 1) / kPromoteKb : 1;
+      for (int gi = 0; gi < groups; ++gi, ++ac) {
+        const int buf = ac & 1;
+        mbar_wait(&tfull[buf], (ac >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf * p.tstride);
+        for (int c0 = 0; c0 < p.np; c0 += 32) {
+          float v[32];
+          tmem_ld32(tbase + c0, v);
+          if (MODE == TN) {
+            float* dst = p.partial + (static_cast<long>(it) * BM + row) * p.npb + c0;
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              if (c0 + i < p.npb) {
+                float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                if (gi > 0) {
+                  const float4 prev = *reinterpret_cast<const float4*>(dst + i);
+                  o = make_float4(__fadd_rn(prev.x, o.x), __fadd_rn(prev.y, o.y), __fadd_rn(prev.z, o.z),
+                                  __fadd_rn(prev.w, o.w));
+                }
+                *reinterpret_cast<float4*>(dst + i) = o;
+              }
+            }
+          } else {
+            const long grow = I.row0 + row;
+            if (grow < p.M) {
+              float* dst = p.C + grow * p.ldc;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const long c = c0 + i;
+                if (c < p.N) {
+                  float r = v[i];
+                  if (p.epi == 1) r = dst[c] > 0.0f ? r : 0.0f;
+                  if (p.epi == 2) r = r > 0.0f ? r : 0.0f;
+                  dst[c] = r;
+                }
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
       }
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) {
-    const uint32_t cols = np <= 32 ? 32 : np <= 64 ? 64 : np <= 128 ? 128 : 256;
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(cols));
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tmem_cols));
+}
+
+// Fixed-order sum of the TN partials of every block: stage[g][m][n] = 0 + p_0 + p_1 + ... (chunk order).
+__global__ void reduce_partials(Params p, float* __restrict__ stage, long block_stride) {
+  const long per = p.M * p.N;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < per * p.nblocks;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(i / per);
+    const long e = i % per;
+    const long m = e / p.N, n = e % p.N;
+    const long t = m / BM, r = m % BM;
+    float s = 0.0f;
+    for (int it = p.blk_first[g] + static_cast<int>(t); it < p.blk_first[g + 1]; it += p.m_tiles)
+      s = __fadd_rn(s, p.partial[(static_cast<long>(it) * BM + r) * p.npb + n]);
+    stage[g * block_stride + m * p.ldc + n] = s;
   }
 }
 
-// Fixed-order sum of the split-K partials: C[m][n] = 0 + p_0 + p_1 + ... (chunk order).
-__global__ void reduce_partials(const float* __restrict__ partial, int n_chunks, int m_tiles, int np, long M, long N,
-                                float* __restrict__ C, long ldc) {
-  const long total = M * N;
-  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-       i += static_cast<long>(gridDim.x) * blockDim.x) {
-    const long m = i / N, n = i % N;
-    const long t = m / BM, r = m % BM;
-    float s = 0.0f;
-    for (int c = 0; c < n_chunks; ++c) s = __fadd_rn(s, partial[((static_cast<long>(c) * m_tiles + t) * BM + r) * np + n]);
-    C[m * ldc + n] = s;
-  }
+// ---------------------------------------------------------------- host side
+namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    TC_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
 }
+
+// 2-D fp32 map over a row-major matrix [outer][inner] with row pitch ld floats.
+CUtensorMap make_map(const float* base, long inner, long outer, long ld, int box_inner, int box_outer,
+                     CUtensorMapSwizzle sw) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(std::max<long>(inner, 1)),
+                              static_cast<cuuint64_t>(std::max<long>(outer, 1))};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+                                 es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+  return m;
+}
+
+int num_sms() {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms;
+}
+
+void finish_params(Params& p, long N, bool b_mn, int terms) {
+  p.np = static_cast<int>((N + 15) / 16 * 16);
+  p.npb = b_mn ? (p.np + 31) / 32 * 32 : p.np;
+  p.tstride = (p.npb + 31) / 32 * 32;
+  p.terms = terms;
+  const int half = BM * BK * 4 + p.npb * BK * 4;
+  const int stage = terms == 3 ? 2 * half : half;
+  p.nst = std::max(2, std::min(kMaxStages, kSmemBudget / stage));
+}
+
+inline int smem_bytes(const Params& p) {
+  const int half = BM * BK * 4 + p.npb * BK * 4;
+  return p.nst * (p.terms == 3 ? 2 * half : half) + 1024;
+}
+
+template <int MODE>
+void launch(const CUtensorMap& a, const CUtensorMap& b, const Params& p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    TC_CUDA(cudaFuncSetAttribute(gemm_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024));
+    attr = true;
+  }
+  const int grid = std::max(1, std::min(p.n_items, num_sms()));
+  gemm_tc<MODE><<<grid, kThreads, smem_bytes(p), s>>>(a, b, p);
+  TC_CUDA(cudaGetLastError());
+}
+
+void check_ptr(const void* p, long ld, const char* what) {
+  if ((reinterpret_cast<uintptr_t>(p) & 15) || ld % 4)
+    throw ValueError(std::string("tc gemm: ") + what + " must be 16-byte aligned with ld % 4 == 0");
+}
+
+}  // namespace
 
 bool available() { return true; }
 
 void set_tn_chunk(int rows) {
-  if (rows < BK || rows % BK) throw ValueError("tuning: tn_chunk must be a positive multiple of 32");
+  if (rows < BK * kPromoteKb || rows % (BK * kPromoteKb))
+    throw ValueError("tuning: tn_chunk must be a positive multiple of 256");
   g_split_rows = rows;
 }
 
-namespace {
-template <int MODE, int TERMS>
-void launch(const Params& p, int grid, cudaStream_t s) {
-  const int sm = smem_bytes(p.np, TERMS);
-  static bool attr = false;
-  if (!attr) {
-    TC_CUDA(cudaFuncSetAttribute(gemm_tc<MODE, TERMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem_bytes(256, TERMS)));
-    attr = true;
-  }
-  gemm_tc<MODE, TERMS><<<grid, kThreads, sm, s>>>(p);
-  TC_CUDA(cudaGetLastError());
-}
-}  // namespace
-
 size_t tn_workspace_bytes(int64_t M, int64_t N, int64_t K) {
-  const int np = static_cast<int>((N + 15) / 16 * 16);
+  const long npb = ((N + 15) / 16 * 16 + 31) / 32 * 32;
   const long m_tiles = (M + BM - 1) / BM;
-  const long chunks = (K + g_split_rows - 1) / g_split_rows;
-  return sizeof(float) * static_cast<size_t>(chunks * m_tiles * BM * np);
+  const long chunks = (K + g_split_rows - 1) / g_split_rows + 8;  // + one partial chunk per block boundary
+  return sizeof(float) * static_cast<size_t>(chunks * m_tiles * BM * npb);
 }
 
 int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
          int64_t ldb, float* C, int64_t ldc, int epi, float* ws, size_t ws_bytes, cudaStream_t s) {
+  if (ta) {
+    const int64_t begin[1] = {0}, len[1] = {K};
+    return gemm_tn_blocks(mode, 1, begin, len, M, N, A, lda, B, ldb, C, ldc, 0, ws, ws_bytes, s);
+  }
   if (mode != MG_GEMM_TF32X3 && mode != MG_GEMM_TF32) throw ValueError("tc gemm: bad mode");
   if (N > 256) throw ValueError("tc gemm: N > 256 not supported (" + std::to_string(N) + ")");
-  if (ta && tb) throw ValueError("gemm: transposed A and B together is not on the training path");
-  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B)) & 15 || lda % 4 || ldb % 4)
-    throw ValueError("tc gemm: operands must be 16-byte aligned with ld % 4 == 0");
+  if (M <= 0 || N <= 0) return 0;
+  if (K <= 0) throw ValueError("tc gemm: K must be >= 1");
+  check_ptr(A, lda, "A");
+  check_ptr(B, ldb, "B");
   Params p{};
   p.M = M;
   p.N = N;
   p.K = K;
-  p.A = A;
-  p.lda = lda;
-  p.B = B;
-  p.ldb = ldb;
   p.C = C;
   p.ldc = ldc;
-  p.np = static_cast<int>((N + 15) / 16 * 16);
-  p.kpad = static_cast<int>((K + 3) / 4 * 4);
   p.epi = epi;
-  const bool x3 = mode == MG_GEMM_TF32X3;
-  if (!ta) {
-    const int grid = static_cast<int>((M + BM - 1) / BM);
-    if (!tb) {
-      x3 ? launch<0, 3>(p, grid, s) : launch<0, 1>(p, grid, s);
-    } else {
-      x3 ? launch<1, 3>(p, grid, s) : launch<1, 1>(p, grid, s);
-    }
-    return 1;
-  }
-  // TN: split-K over fixed 4096-row chunks, then the fixed-order reduction (epilogue must be 0)
-  if (epi != 0) throw ValueError("tc gemm: TN has no fused epilogue");
+  finish_params(p, N, !tb, mode == MG_GEMM_TF32X3 ? 3 : 1);
   p.m_tiles = static_cast<int>((M + BM - 1) / BM);
-  p.k_chunk = g_split_rows;
-  p.n_chunks = static_cast<int>(std::max<int64_t>(1, (K + p.k_chunk - 1) / p.k_chunk));
-  if (!ws || ws_bytes < tn_workspace_bytes(M, N, std::max<int64_t>(K, 1)))
-    throw ValueError("tc gemm: TN split-K workspace too small");
+  p.n_items = p.m_tiles;
+  const CUtensorMap ma = make_map(A, K, M, lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (!tb) {  // NN: W is K x N row-major -> MN-major boxes {32 n, 16 k}
+    const CUtensorMap mb = make_map(B, N, K, ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B);
+    launch<NN>(ma, mb, p, s);
+  } else {    // NT: W is N x K row-major -> K-major box {16 k, np rows}
+    const CUtensorMap mb = make_map(B, K, N, ldb, BK, p.np, CU_TENSOR_MAP_SWIZZLE_64B);
+    launch<NT>(ma, mb, p, s);
+  }
+  return 1;
+}
+
+int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* len, int64_t M, int64_t N,
+                   const float* H, int64_t ldh, const float* G, int64_t ldg, float* stage, int64_t ldc,
+                   int64_t block_stride, float* ws, size_t ws_bytes, cudaStream_t s) {
+  if (mode != MG_GEMM_TF32X3 && mode != MG_GEMM_TF32) throw ValueError("tc gemm: bad mode");
+  if (N > 256) throw ValueError("tc gemm: N > 256 not supported (" + std::to_string(N) + ")");
+  if (nblocks < 1 || nblocks > 8) throw ValueError("tc gemm: 1..8 blocks");
+  if (M <= 0 || N <= 0) return 0;
+  check_ptr(H, ldh, "H");
+  check_ptr(G, ldg, "G");
+  Params p{};
+  p.M = M;
+  p.N = N;
+  p.C = stage;
+  p.ldc = ldc;
+  finish_params(p, N, true, mode == MG_GEMM_TF32X3 ? 3 : 1);
+  p.m_tiles = static_cast<int>((M + BM - 1) / BM);
+  p.chunk_rows = g_split_rows;
+  p.nblocks = nblocks;
+  int64_t rows_hi = 0;
+  p.blk_first[0] = 0;
+  for (int g = 0; g < nblocks; ++g) {
+    p.blk_begin[g] = begin[g];
+    p.blk_len[g] = std::max<int64_t>(0, len[g]);
+    const long chunks = (p.blk_len[g] + p.chunk_rows - 1) / p.chunk_rows;
+    p.blk_first[g + 1] = p.blk_first[g] + static_cast<int>(chunks) * p.m_tiles;
+    rows_hi = std::max<int64_t>(rows_hi, begin[g] + len[g]);
+  }
+  p.n_items = p.blk_first[nblocks];
+  const size_t need = sizeof(float) * static_cast<size_t>(p.n_items) * BM * p.npb;
+  if (p.n_items > 0 && (!ws || ws_bytes < need)) throw ValueError("tc gemm: TN split-K workspace too small");
   p.partial = ws;
-  const int grid = p.m_tiles * p.n_chunks;
-  x3 ? launch<2, 3>(p, grid, s) : launch<2, 1>(p, grid, s);
-  const long total = M * N;
-  const int rb = static_cast<int>(std::min<long>(4096, (total + 255) / 256));
-  reduce_partials<<<rb, 256, 0, s>>>(p.partial, p.n_chunks, p.m_tiles, p.np, M, N, C, ldc);
+  int kernels = 0;
+  if (p.n_items > 0) {
+    const CUtensorMap ma = make_map(H, M, rows_hi, ldh, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap mb = make_map(G, N, rows_hi, ldg, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B);
+    launch<TN>(ma, mb, p, s);
+    ++kernels;
+  }
+  const long total = M * N * nblocks;
+  reduce_partials<<<static_cast<int>(std::min<long>(4096, (total + 255) / 256)), 256, 0, s>>>(p, stage, block_stride);
   TC_CUDA(cudaGetLastError());
-  return 2;
+  return kernels + 1;
 }
 
 }  // namespace tc

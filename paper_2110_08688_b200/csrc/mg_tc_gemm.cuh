@@ -13,6 +13,12 @@ bool available();
 int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
          int64_t ldb, float* C, int64_t ldc, int epi, float* ws, size_t ws_bytes, cudaStream_t s);
 size_t tn_workspace_bytes(int64_t M, int64_t N, int64_t K);
+// W-grad over up to 8 canonical row blocks in one launch: stage + g*block_stride (M x N, ld ldc) =
+// H[begin_g : begin_g + len_g]^T G[same rows]; empty blocks are written as zeros. Deterministic and
+// independent of how the rows are distributed over workers (chunks are relative to each block start).
+int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* len, int64_t M, int64_t N,
+                   const float* H, int64_t ldh, const float* G, int64_t ldg, float* stage, int64_t ldc,
+                   int64_t block_stride, float* ws, size_t ws_bytes, cudaStream_t s);
 void set_tn_chunk(int rows);  // TN split-K chunk length (rows, multiple of 32); set before creating groups
 }  // namespace tc
 }  // namespace mg
