@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "mg_internal.hpp"
@@ -68,6 +70,7 @@ struct Params {
   long blk_begin[8], blk_len[8];
   int blk_first[9];      // first work item of each block (prefix over blocks)
   float* partial;        // [n_items][BM][npb]
+  float* dbg;            // debugging aid (MGGCN_TC_DEBUG): first stage tiles + first TMEM rows, else null
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -315,6 +318,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(const __grid_constant__ C
         mbar_wait(&full[s], (sc / p.nst) & 1);
         uint8_t* hi = smem + s * stage;
         uint8_t* lo = hi + half;
+        if (p.dbg && sc == 0 && blockIdx.x == 0)
+          for (int q = t; q < half / 4; q += 128) p.dbg[q] = reinterpret_cast<float*>(hi)[q];
         const int valid_rows = MODE == TN ? static_cast<int>(min(static_cast<long>(BK), I.k_end - (I.row0 + kb * BK))) : BK;
         if (p.terms == 3 || valid_rows < BK) {
           for (int q = t; q < half / 16; q += 128) {
@@ -354,6 +359,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(const __grid_constant__ C
         for (int c0 = 0; c0 < p.np; c0 += 32) {
           float v[32];
           tmem_ld32(tbase + c0, v);
+          if (p.dbg && ac == 0 && blockIdx.x == 0 && c0 == 0)
+            for (int i = 0; i < 32; ++i) p.dbg[16384 + row * 32 + i] = v[i];
           if (MODE == TN) {
             float* dst = p.partial + (static_cast<long>(it) * BM + row) * p.npb + c0;
 #pragma unroll
@@ -520,6 +527,13 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
   finish_params(p, N, !tb, mode == MG_GEMM_TF32X3 ? 3 : 1);
   p.m_tiles = static_cast<int>((M + BM - 1) / BM);
   p.n_items = p.m_tiles;
+  static float* dbg = [] {
+    float* d = nullptr;
+    if (std::getenv("MGGCN_TC_DEBUG")) TC_CUDA(cudaMallocManaged(&d, sizeof(float) * 65536));
+    return d;
+  }();
+  p.dbg = dbg;
+  if (dbg) std::fill(dbg, dbg + 65536, -7.0f);
   const CUtensorMap ma = make_map(A, K, M, lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!tb) {  // NN: W is K x N row-major -> MN-major boxes {32 n, 16 k}
     const CUtensorMap mb = make_map(B, N, K, ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -527,6 +541,19 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
   } else {    // NT: W is N x K row-major -> K-major box {16 k, np rows}
     const CUtensorMap mb = make_map(B, K, N, ldb, BK, p.np, CU_TENSOR_MAP_SWIZZLE_64B);
     launch<NT>(ma, mb, p, s);
+  }
+  if (dbg) {
+    TC_CUDA(cudaDeviceSynchronize());
+    std::fprintf(stderr, "[tc dbg] M=%ld N=%ld K=%ld np=%d npb=%d nst=%d terms=%d\n  A tile:", static_cast<long>(M),
+                 static_cast<long>(N), static_cast<long>(K), p.np, p.npb, p.nst, p.terms);
+    for (int i = 0; i < 24; ++i) std::fprintf(stderr, " %.4g", dbg[i]);
+    std::fprintf(stderr, "\n  B tile:");
+    for (int i = 0; i < 24; ++i) std::fprintf(stderr, " %.4g", dbg[2048 + i]);
+    std::fprintf(stderr, "\n  TMEM row0:");
+    for (int i = 0; i < 8; ++i) std::fprintf(stderr, " %.4g", dbg[16384 + i]);
+    std::fprintf(stderr, "\n  TMEM row1:");
+    for (int i = 0; i < 8; ++i) std::fprintf(stderr, " %.4g", dbg[16384 + 32 + i]);
+    std::fprintf(stderr, "\n");
   }
   return 1;
 }
