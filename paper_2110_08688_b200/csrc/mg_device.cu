@@ -791,7 +791,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
           kmax = std::max(kmax, e - a);
         }
         for (int l = 0; l < L; ++l)
-          w.ws_bytes = std::max(w.ws_bytes, tc::tn_workspace_bytes(g->ld[l], g->ld[l + 1], kmax));
+          w.ws_bytes = std::max(w.ws_bytes, tc::tn_workspace_bytes(g->ld[l], g->ld[l + 1], std::max<index_t>(1, w.rows)));
         w.ws = static_cast<float*>(dalloc(*g, w, w.ws_bytes));
       }
       w.loss_blocks = std::max(1, std::min(ceil_div(w.rows, 8), num_sms() * 8));

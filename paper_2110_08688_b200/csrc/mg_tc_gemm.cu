@@ -113,11 +113,13 @@ __device__ __forceinline__ uint64_t desc_k64(uint32_t saddr) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
          (static_cast<uint64_t>(512 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(4) << 61);
 }
-// MN-major SWIZZLE_128B: 8 k-rows x 128-byte (32 fp32 along M/N) atoms; LBO = 2048 B between atoms along
-// M/N (one 16-row TMA box each), SBO = 1024 B between the two 8-row atoms along K.
+// MN-major 32-bit operands use the SWIZZLE_128B_BASE32B layout (UMMA layout type 1; TMA
+// CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 4 k-rows x 128-byte (32 fp32 along M/N) atoms, 32-byte chunks
+// XOR-swizzled by the row. LBO = 2048 B between atoms along M/N (one {32, 16} TMA box each),
+// SBO = 512 B between consecutive 4-row atoms along K; one K = 8 MMA spans two of them.
 __device__ __forceinline__ uint64_t desc_mn128(uint32_t saddr) {
   return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(2048 >> 4) << 16) |
-         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
+         (static_cast<uint64_t>(512 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(1) << 61);
 }
 // kind::tf32 instruction descriptor: D f32 (bit 4), A/B tf32 (2 at bits 7, 10), majors (bits 15, 16),
 // N >> 3 at bit 17, M >> 4 at bit 24.
@@ -536,7 +538,7 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
   if (dbg) std::fill(dbg, dbg + 65536, -7.0f);
   const CUtensorMap ma = make_map(A, K, M, lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_64B);
   if (!tb) {  // NN: W is K x N row-major -> MN-major boxes {32 n, 16 k}
-    const CUtensorMap mb = make_map(B, N, K, ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap mb = make_map(B, N, K, ldb, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     launch<NN>(ma, mb, p, s);
   } else {    // NT: W is N x K row-major -> K-major box {16 k, np rows}
     const CUtensorMap mb = make_map(B, K, N, ldb, BK, p.np, CU_TENSOR_MAP_SWIZZLE_64B);
@@ -591,8 +593,8 @@ int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* l
   p.partial = ws;
   int kernels = 0;
   if (p.n_items > 0) {
-    const CUtensorMap ma = make_map(H, M, rows_hi, ldh, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B);
-    const CUtensorMap mb = make_map(G, N, rows_hi, ldg, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B);
+    const CUtensorMap ma = make_map(H, M, rows_hi, ldh, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    const CUtensorMap mb = make_map(G, N, rows_hi, ldg, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     launch<TN>(ma, mb, p, s);
     ++kernels;
   }
