@@ -250,7 +250,7 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
   std::vector<int> light, heavy;
   build_orders(t.row_ptr, light, heavy);
   d.row_ptr = dalloc_t<int>(g, w, rp32.size());
-  d.edges = dalloc_t<int2>(g, w, std::max<index_t>(1, d.nnz));
+  d.edges = dalloc_t<int2>(g, w, d.nnz + k::kEdgePad);
   d.light = dalloc_t<int>(g, w, std::max<size_t>(1, light.size()));
   d.heavy = dalloc_t<int>(g, w, std::max<size_t>(1, heavy.size()));
   d.n_light = static_cast<int>(light.size());
@@ -1113,13 +1113,22 @@ mg_status mg_dev_spmm(int64_t rows, const int32_t* row_ptr, const void* edges, c
     MG_CUDA(cudaMalloc(&dh, sizeof(int) * std::max<size_t>(1, heavy.size())));
     if (!light.empty()) MG_CUDA(cudaMemcpy(dl, light.data(), sizeof(int) * light.size(), cudaMemcpyHostToDevice));
     if (!heavy.empty()) MG_CUDA(cudaMemcpy(dh, heavy.data(), sizeof(int) * heavy.size(), cudaMemcpyHostToDevice));
-    SpmmLaunch sl{row_ptr, static_cast<const int2*>(edges), dl, static_cast<int>(light.size()), dh,
+    // the hub-row kernel bulk-copies edge records from 16-byte aligned starts: give it a padded copy
+    int2* ep = nullptr;
+    if (!heavy.empty()) {
+      const index_t nnz = rp.back();
+      MG_CUDA(cudaMalloc(&ep, sizeof(int2) * (nnz + k::kEdgePad)));
+      MG_CUDA(cudaMemsetAsync(ep, 0, sizeof(int2) * (nnz + k::kEdgePad), s));
+      MG_CUDA(cudaMemcpyAsync(ep, edges, sizeof(int2) * nnz, cudaMemcpyDeviceToDevice, s));
+    }
+    SpmmLaunch sl{row_ptr, ep ? ep : static_cast<const int2*>(edges), dl, static_cast<int>(light.size()), dh,
                   static_cast<int>(heavy.size())};
     spmm_heavy(sl, h, out, ld, accumulate, relu, s);
     spmm_light(sl, h, out, ld, accumulate, relu, s);
     MG_CUDA(cudaStreamSynchronize(s));
     cudaFree(dl);
     cudaFree(dh);
+    if (ep) cudaFree(ep);
   });
 }
 

@@ -114,7 +114,10 @@ constexpr int kHeavySlab = 64;
 constexpr int kHeavyB = 32;
 constexpr int kHeavyNst = 8;
 constexpr int kHeavyThreads = 96;
-constexpr size_t kHeavySmem = sizeof(float) * (kHeavyNst * kHeavyB * kHeavySlab + kHeavyNst * kHeavyB) + 16 * kHeavyNst + 128;
+constexpr int kHeavyEslots = 16;  // edge-record ring (2 x the stage ring: reuse needs consumption)
+constexpr size_t kHeavySmem = sizeof(float) * kHeavyNst * kHeavyB * kHeavySlab + 8 * kHeavyEslots * (kHeavyB + 2) +
+                              8 * (2 * kHeavyNst + kHeavyEslots) + 128;
+constexpr int kEdgePad = 2;  // edge arrays carry 2 spare records so the aligned bulk copies stay in bounds
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -150,10 +153,11 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __r
                                                                   const float* __restrict__ h, float* __restrict__ out,
                                                                   int ld, int accumulate, int relu) {
   extern __shared__ __align__(128) float smem[];
-  float* buf = smem;                                       // [NST][B][SLAB]
-  float* vals = smem + kHeavyNst * kHeavyB * kHeavySlab;   // [NST][B]
-  uint64_t* full = reinterpret_cast<uint64_t*>(vals + kHeavyNst * kHeavyB);
+  float* buf = smem;                                                            // [NST][B][SLAB] h slabs
+  int2* ering = reinterpret_cast<int2*>(smem + kHeavyNst * kHeavyB * kHeavySlab);  // [ESLOTS][B + 2] edge records
+  uint64_t* full = reinterpret_cast<uint64_t*>(ering + kHeavyEslots * (kHeavyB + 2));
   uint64_t* empty = full + kHeavyNst;
+  uint64_t* efull = empty + kHeavyNst;
   const int r = heavy[blockIdx.x / nslab];
   const int col0 = (blockIdx.x % nslab) * kHeavySlab;
   const int e0 = row_ptr[r], e1 = row_ptr[r + 1];
@@ -165,22 +169,38 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __r
       mbar_init(&full[s], 32);
       mbar_init(&empty[s], 2);
     }
+    for (int s = 0; s < kHeavyEslots; ++s) mbar_init(&efull[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
+  // Edge records of stage q arrive by one bulk copy (16-byte aligned start, so the copy may begin one
+  // record early and end one late: the edge array is padded) into slot q % ESLOTS, kHeavyNst stages
+  // ahead of use; the slot's previous occupant (stage q - ESLOTS) is long consumed by then.
+  auto issue_edges = [&](int q) {
+    const int base = e0 + q * kHeavyB;
+    const int al = base & ~1;
+    const int n = (min(kHeavyB, e1 - base) + (base - al) + 1) & ~1;
+    const int slot = q % kHeavyEslots;
+    mbar_arrive_tx(&efull[slot], static_cast<uint32_t>(n) * 8u);
+    bulk_g2s(ering + slot * (kHeavyB + 2), edges + al, static_cast<uint32_t>(n) * 8u, &efull[slot]);
+  };
   if (warp == 2) {  // producer
+    if (lane == 0)
+      for (int q = 0; q < min(kHeavyNst, nst_total); ++q) issue_edges(q);
     for (int st = 0; st < nst_total; ++st) {
       const int s = st % kHeavyNst;
-      if (st >= kHeavyNst) mbar_wait(&empty[s], ((st / kHeavyNst) - 1) & 1);
+      if (st >= kHeavyNst) mbar_wait(&empty[s], ((st / kHeavyNst) - 1) & 1);  // consumer is done with st - NST
+      if (lane == 0 && st + kHeavyNst < nst_total) issue_edges(st + kHeavyNst);
+      const int slot = st % kHeavyEslots;
+      mbar_wait(&efull[slot], (st / kHeavyEslots) & 1);
       const int base = e0 + st * kHeavyB;
       const int cnt = min(kHeavyB, e1 - base);
+      const int2* er = ering + slot * (kHeavyB + 2) + (base & 1);
       if (lane == 0) mbar_arrive_tx(&full[s], slab_bytes * cnt);
       __syncwarp();
-      if (lane < cnt) {
-        const int2 ed = __ldg(edges + base + lane);
-        vals[s * kHeavyB + lane] = __int_as_float(ed.y);
-        bulk_g2s(buf + ((size_t)s * kHeavyB + lane) * kHeavySlab, h + (size_t)ed.x * ld + col0, slab_bytes, &full[s]);
-      }
+      if (lane < cnt)
+        bulk_g2s(buf + ((size_t)s * kHeavyB + lane) * kHeavySlab, h + (size_t)er[lane].x * ld + col0, slab_bytes,
+                 &full[s]);
       if (lane != 0) mbar_arrive(&full[s]);
     }
   } else {  // consumers: one column each
@@ -192,11 +212,12 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __r
     for (int st = 0; st < nst_total; ++st) {
       const int s = st % kHeavyNst;
       mbar_wait(&full[s], (st / kHeavyNst) & 1);
-      const int cnt = min(kHeavyB, e1 - (e0 + st * kHeavyB));
+      const int base = e0 + st * kHeavyB;
+      const int cnt = min(kHeavyB, e1 - base);
       const float* bs = buf + (size_t)s * kHeavyB * kHeavySlab + t;
-      const float* vs = vals + s * kHeavyB;
+      const int2* er = ering + (st % kHeavyEslots) * (kHeavyB + 2) + (base & 1);
       if (active)
-        for (int b = 0; b < cnt; ++b) acc = fma_free(acc, vs[b], bs[b * kHeavySlab]);
+        for (int b = 0; b < cnt; ++b) acc = fma_free(acc, __int_as_float(er[b].y), bs[b * kHeavySlab]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }

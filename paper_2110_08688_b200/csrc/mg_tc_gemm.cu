@@ -47,7 +47,8 @@ constexpr int BK = 16;             // K per pipeline stage
 constexpr int kMaxStages = 8;
 constexpr int kThreads = 320;      // 10 warps: 0 TMA, 1 MMA, 2-5 split, 6-9 epilogue
 constexpr int kPromoteKb = 16;     // TN: drain TMEM every 16 K blocks (256 rows)
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kSmemBudget = 200 * 1024;  // smem stage ring
+constexpr int kEpiSmem = 4 * 32 * 33 * 4;  // epilogue transpose, one 32 x 33 tile per epilogue warp
 static int g_split_rows = 4096;    // TN chunk (rows), fixed relative to the block start ("tn_chunk")
 
 enum { NN = 0, NT = 1, TN = 2 };
@@ -358,39 +359,40 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(const __grid_constant__ C
         mbar_wait(&tfull[buf], (ac >> 1) & 1);
         tc_fence_after();
         const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf * p.tstride);
+        // TMEM gives each lane one row; a 32 x 33 smem transpose per warp turns that into 128-byte
+        // row segments so every global load/store of the epilogue is fully coalesced.
+        float* stg = reinterpret_cast<float*>(smem + p.nst * stage) + q * (32 * 33);
         for (int c0 = 0; c0 < p.np; c0 += 32) {
           float v[32];
           tmem_ld32(tbase + c0, v);
           if (p.dbg && ac == 0 && blockIdx.x == 0 && c0 == 0)
             for (int i = 0; i < 32; ++i) p.dbg[16384 + row * 32 + i] = v[i];
-          if (MODE == TN) {
-            float* dst = p.partial + (static_cast<long>(it) * BM + row) * p.npb + c0;
+          __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              if (c0 + i < p.npb) {
-                float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                if (gi > 0) {
-                  const float4 prev = *reinterpret_cast<const float4*>(dst + i);
-                  o = make_float4(__fadd_rn(prev.x, o.x), __fadd_rn(prev.y, o.y), __fadd_rn(prev.z, o.z),
-                                  __fadd_rn(prev.w, o.w));
-                }
-                *reinterpret_cast<float4*>(dst + i) = o;
+          for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
+          __syncwarp();
+          const int c = c0 + lane;
+          if (MODE == TN) {
+            if (c < p.npb) {
+              float* dst = p.partial + (static_cast<long>(it) * BM + q * 32) * p.npb + c;
+#pragma unroll 4
+              for (int r = 0; r < 32; ++r) {
+                float x = stg[r * 33 + lane];
+                if (gi > 0) x = __fadd_rn(dst[static_cast<long>(r) * p.npb], x);
+                dst[static_cast<long>(r) * p.npb] = x;
               }
             }
-          } else {
-            const long grow = I.row0 + row;
-            if (grow < p.M) {
-              float* dst = p.C + grow * p.ldc;
-#pragma unroll
-              for (int i = 0; i < 32; ++i) {
-                const long c = c0 + i;
-                if (c < p.N) {
-                  float r = v[i];
-                  if (p.epi == 1) r = dst[c] > 0.0f ? r : 0.0f;
-                  if (p.epi == 2) r = r > 0.0f ? r : 0.0f;
-                  dst[c] = r;
-                }
-              }
+          } else if (c < p.N) {
+            const long g0 = I.row0 + q * 32;
+            float* dst = p.C + g0 * p.ldc + c;
+#pragma unroll 4
+            for (int r = 0; r < 32; ++r) {
+              if (g0 + r >= p.M) break;
+              float x = stg[r * 33 + lane];
+              float* d = dst + static_cast<long>(r) * p.ldc;
+              if (p.epi == 1) x = *d > 0.0f ? x : 0.0f;
+              if (p.epi == 2) x = x > 0.0f ? x : 0.0f;
+              *d = x;
             }
           }
         }
@@ -470,14 +472,15 @@ void finish_params(Params& p, long N, bool b_mn, int terms) {
 
 inline int smem_bytes(const Params& p) {
   const int half = BM * BK * 4 + p.npb * BK * 4;
-  return p.nst * (p.terms == 3 ? 2 * half : half) + 1024;
+  return p.nst * (p.terms == 3 ? 2 * half : half) + kEpiSmem + 1024;
 }
 
 template <int MODE>
 void launch(const CUtensorMap& a, const CUtensorMap& b, const Params& p, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    TC_CUDA(cudaFuncSetAttribute(gemm_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBudget + 1024));
+    TC_CUDA(cudaFuncSetAttribute(gemm_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemBudget + kEpiSmem + 1024));
     attr = true;
   }
   const int grid = std::max(1, std::min(p.n_items, num_sms()));
