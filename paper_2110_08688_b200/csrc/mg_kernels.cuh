@@ -105,21 +105,25 @@ __global__ void __launch_bounds__(256) spmm_exact_rows(const int* __restrict__ r
 }
 
 // Long rows (hubs of the power-law graph): one CTA per (row, 64-column slab), warp-specialised.
-// Warp 2 (producer) streams the row's h-slabs into an NST-deep ring of 32-nonzero stages with TMA
-// bulk copies (cp.async.bulk, one 256-byte copy per nonzero, completion counted in bytes on the
-// stage's mbarrier); warps 0-1 (consumers, one output column per thread) fold each stage in column
-// order with a separate multiply and add — the same left fold as above, so still bitwise exact — and
-// release the stage through a second mbarrier. ~56 KB of gathers stay in flight per CTA.
+// Warps 2-3 (producers) stream the row's h-slabs into an NST-deep ring of 32-nonzero stages with
+// 16-byte cp.async (completion tracked per stage by cp.async.mbarrier.arrive); the stage's edge
+// records arrive ahead of time in a second ring by one TMA bulk copy per stage (per-nonzero bulk copies
+// were measured to be issue-bound on the TMA unit). Warps 0-1 (consumers, one output column per
+// thread) fold each stage in column order with a separate multiply and add — the same left fold as
+// above, so still bitwise exact — and release the stage through a second mbarrier.
 constexpr int kHeavySlab = 64;
 constexpr int kHeavyB = 32;
 constexpr int kHeavyNst = 8;
-constexpr int kHeavyThreads = 96;
+constexpr int kHeavyThreads = 128;  // warps 0-1 consume (one column each), warps 2-3 produce
 constexpr int kHeavyEslots = 16;  // edge-record ring (2 x the stage ring: reuse needs consumption)
 constexpr size_t kHeavySmem = sizeof(float) * kHeavyNst * kHeavyB * kHeavySlab + 8 * kHeavyEslots * (kHeavyB + 2) +
                               8 * (2 * kHeavyNst + kHeavyEslots) + 128;
 constexpr int kEdgePad = 2;  // edge arrays carry 2 spare records so the aligned bulk copies stay in bounds
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr(smem)), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(bar)), "r"(count));
 }
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __r
   const uint32_t slab_bytes = static_cast<uint32_t>(min(kHeavySlab, ld - col0)) * 4u;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kHeavyNst; ++s) {
-      mbar_init(&full[s], 32);
+      mbar_init(&full[s], 64);  // one cp.async.mbarrier.arrive.noinc per producer thread
       mbar_init(&empty[s], 2);
     }
     for (int s = 0; s < kHeavyEslots; ++s) mbar_init(&efull[s], 1);
@@ -184,24 +188,26 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __r
     mbar_arrive_tx(&efull[slot], static_cast<uint32_t>(n) * 8u);
     bulk_g2s(ering + slot * (kHeavyB + 2), edges + al, static_cast<uint32_t>(n) * 8u, &efull[slot]);
   };
-  if (warp == 2) {  // producer
-    if (lane == 0)
+  if (warp >= 2) {  // producers (warps 2-3): 16-byte cp.async per thread, completion tracked per stage
+    const int pt = threadIdx.x - 64;  // 0..63
+    const int nchunk = static_cast<int>(slab_bytes / 16);
+    if (pt == 0)
       for (int q = 0; q < min(kHeavyNst, nst_total); ++q) issue_edges(q);
     for (int st = 0; st < nst_total; ++st) {
       const int s = st % kHeavyNst;
       if (st >= kHeavyNst) mbar_wait(&empty[s], ((st / kHeavyNst) - 1) & 1);  // consumer is done with st - NST
-      if (lane == 0 && st + kHeavyNst < nst_total) issue_edges(st + kHeavyNst);
+      if (pt == 0 && st + kHeavyNst < nst_total) issue_edges(st + kHeavyNst);
       const int slot = st % kHeavyEslots;
       mbar_wait(&efull[slot], (st / kHeavyEslots) & 1);
       const int base = e0 + st * kHeavyB;
       const int cnt = min(kHeavyB, e1 - base);
       const int2* er = ering + slot * (kHeavyB + 2) + (base & 1);
-      if (lane == 0) mbar_arrive_tx(&full[s], slab_bytes * cnt);
-      __syncwarp();
-      if (lane < cnt)
-        bulk_g2s(buf + ((size_t)s * kHeavyB + lane) * kHeavySlab, h + (size_t)er[lane].x * ld + col0, slab_bytes,
-                 &full[s]);
-      if (lane != 0) mbar_arrive(&full[s]);
+      float* dst = buf + (size_t)s * kHeavyB * kHeavySlab;
+      for (int q = pt; q < cnt * (kHeavySlab / 4); q += 64) {
+        const int b = q / (kHeavySlab / 4), c = q % (kHeavySlab / 4);
+        if (c < nchunk) cp_async16(dst + b * kHeavySlab + 4 * c, h + (size_t)er[b].x * ld + col0 + 4 * c);
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_addr(&full[s])) : "memory");
     }
   } else {  // consumers: one column each
     const int t = threadIdx.x;

@@ -375,24 +375,35 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(const __grid_constant__ C
           if (MODE == TN) {
             if (c < p.npb) {
               float* dst = p.partial + (static_cast<long>(it) * BM + q * 32) * p.npb + c;
-#pragma unroll 4
+              float prev[32];
+              if (gi > 0) {  // all 32 row loads in flight before the first add
+#pragma unroll
+                for (int r = 0; r < 32; ++r) prev[r] = dst[static_cast<long>(r) * p.npb];
+              }
+#pragma unroll
               for (int r = 0; r < 32; ++r) {
                 float x = stg[r * 33 + lane];
-                if (gi > 0) x = __fadd_rn(dst[static_cast<long>(r) * p.npb], x);
+                if (gi > 0) x = __fadd_rn(prev[r], x);
                 dst[static_cast<long>(r) * p.npb] = x;
               }
             }
           } else if (c < p.N) {
             const long g0 = I.row0 + q * 32;
+            const int nrows = static_cast<int>(min(32L, p.M - g0));
             float* dst = p.C + g0 * p.ldc + c;
-#pragma unroll 4
+            float old[32];
+            if (p.epi == 1) {  // relu_backward mask: issue every row load before the first store
+#pragma unroll
+              for (int r = 0; r < 32; ++r) old[r] = r < nrows ? dst[static_cast<long>(r) * p.ldc] : 0.0f;
+            }
+#pragma unroll
             for (int r = 0; r < 32; ++r) {
-              if (g0 + r >= p.M) break;
-              float x = stg[r * 33 + lane];
-              float* d = dst + static_cast<long>(r) * p.ldc;
-              if (p.epi == 1) x = *d > 0.0f ? x : 0.0f;
-              if (p.epi == 2) x = x > 0.0f ? x : 0.0f;
-              *d = x;
+              if (r < nrows) {
+                float x = stg[r * 33 + lane];
+                if (p.epi == 1) x = old[r] > 0.0f ? x : 0.0f;
+                if (p.epi == 2) x = x > 0.0f ? x : 0.0f;
+                dst[static_cast<long>(r) * p.ldc] = x;
+              }
             }
           }
         }
