@@ -222,8 +222,20 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __r
       const int cnt = min(kHeavyB, e1 - base);
       const float* bs = buf + (size_t)s * kHeavyB * kHeavySlab + t;
       const int2* er = ering + (st % kHeavyEslots) * (kHeavyB + 2) + (base & 1);
-      if (active)
-        for (int b = 0; b < cnt; ++b) acc = fma_free(acc, __int_as_float(er[b].y), bs[b * kHeavySlab]);
+      if (active) {
+        if (cnt == kHeavyB) {  // full stage: all 64 smem loads in flight, then the 32-long add chain
+          float x[kHeavyB], v[kHeavyB];
+#pragma unroll
+          for (int b = 0; b < kHeavyB; ++b) {
+            v[b] = __int_as_float(er[b].y);
+            x[b] = bs[b * kHeavySlab];
+          }
+#pragma unroll
+          for (int b = 0; b < kHeavyB; ++b) acc = fma_free(acc, v[b], x[b]);
+        } else {
+          for (int b = 0; b < cnt; ++b) acc = fma_free(acc, __int_as_float(er[b].y), bs[b * kHeavySlab]);
+        }
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
