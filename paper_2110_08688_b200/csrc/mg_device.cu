@@ -61,7 +61,42 @@ struct DevTile {
   int n_light = 0;
   int* heavy = nullptr;     // rows with nnz >= heavy threshold
   int n_heavy = 0;
+  // MG_SPMM_FAST work lists: items {e0, e1, dst, 0} (dst < 0: scratch segment), hubs {row, seg0, nseg, 0}
+  int4* items = nullptr;
+  int n_items = 0;
+  int4* hubs = nullptr;
+  int n_hubs = 0;
+  int n_segments = 0;
 };
+
+std::atomic<int> g_fast_segment{2048};
+
+// Fast-mode work lists: every hub row (>= heavy threshold) is cut into fixed segments of g_fast_segment
+// nonzeros (gathered in parallel, summed in order afterwards); segments first, then the ordinary rows
+// by decreasing length.
+void build_fast_items(const std::vector<index_t>& rp, std::vector<int4>& items, std::vector<int4>& hubs, int& nseg) {
+  const index_t rows = static_cast<index_t>(rp.size()) - 1;
+  const int ht = heavy_threshold(), seg = g_fast_segment.load();
+  std::vector<int> light;
+  items.clear();
+  hubs.clear();
+  nseg = 0;
+  for (index_t r = 0; r < rows; ++r) {
+    const index_t len = rp[r + 1] - rp[r];
+    if (len < ht) {
+      light.push_back(static_cast<int>(r));
+      continue;
+    }
+    const int first = nseg;
+    for (index_t e = rp[r]; e < rp[r + 1]; e += seg, ++nseg)
+      items.push_back(make_int4(static_cast<int>(e), static_cast<int>(std::min<index_t>(e + seg, rp[r + 1])),
+                                -(nseg + 1), 0));
+    hubs.push_back(make_int4(static_cast<int>(r), first, nseg - first, 0));
+  }
+  std::stable_sort(light.begin(), light.end(),
+                   [&](int a, int b) { return (rp[a + 1] - rp[a]) > (rp[b + 1] - rp[b]); });
+  for (int r : light) items.push_back(make_int4(static_cast<int>(rp[r]), static_cast<int>(rp[r + 1]), r, 0));
+}
 
 // Host-side construction of the launch lists for a tile (row order by decreasing length).
 void build_orders(const std::vector<index_t>& rp, std::vector<int>& light, std::vector<int>& heavy) {
@@ -124,6 +159,58 @@ static int spmm_light(const SpmmLaunch& t, const float* h, float* out, index_t l
   return launches;
 }
 
+struct FastLaunch {
+  const int4* items;
+  int n_items;
+  const int4* hubs;
+  int n_hubs;
+  const int2* edges;
+  float* scratch;  // n_segments x ld
+};
+
+template <int G, int CPL>
+static void launch_fast(const FastLaunch& t, const float* h, float* out, float* scratch, int ld, int nchunk, int acc,
+                        int relu, cudaStream_t s) {
+  const int gpb = 256 / G;
+  const int blocks = std::min(ceil_div(t.n_items, gpb), num_sms() * 16);
+  k::spmm_fast_items<G, CPL><<<blocks, 256, 0, s>>>(t.items, t.n_items, t.edges, h, out, scratch, ld, nchunk, acc,
+                                                    relu);
+  MG_LAUNCHED();
+}
+
+// MG_SPMM_FAST: one gather pass over rows + hub segments, then the ordered hub-segment sum.
+static int spmm_fast(const FastLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, cudaStream_t s) {
+  int launches = 0;
+  const int nchunk_all = static_cast<int>(ld / 4);
+  if (t.n_items > 0) {
+    for (int c0 = 0; c0 < nchunk_all; c0 += 256) {
+      const int nchunk = std::min(256, nchunk_all - c0);
+      const float* hs = h + 4 * c0;
+      float* os = out + 4 * c0;
+      float* ss = t.scratch ? t.scratch + 4 * c0 : nullptr;
+      const int L = static_cast<int>(ld);
+      if (nchunk <= 1) launch_fast<1, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      else if (nchunk <= 2) launch_fast<2, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      else if (nchunk <= 4) launch_fast<4, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      else if (nchunk <= 8) launch_fast<8, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      else if (nchunk <= 16) launch_fast<16, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      else if (nchunk <= 32) launch_fast<32, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      else if (nchunk <= 64) launch_fast<32, 2>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      else if (nchunk <= 96) launch_fast<32, 3>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      else if (nchunk <= 128) launch_fast<32, 4>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      else if (nchunk <= 192) launch_fast<32, 6>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      else launch_fast<32, 8>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      ++launches;
+    }
+  }
+  if (t.n_hubs > 0) {
+    k::spmm_fast_hubs<<<t.n_hubs, 256, 0, s>>>(t.hubs, t.scratch, out, static_cast<int>(ld), acc, relu);
+    MG_LAUNCHED();
+    ++launches;
+  }
+  return launches;
+}
+
 static int spmm_heavy(const SpmmLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, cudaStream_t s) {
   if (t.n_heavy <= 0) return 0;
   static bool attr = false;
@@ -174,6 +261,7 @@ struct Worker {
   float *hw = nullptr, *bc1 = nullptr, *bc2 = nullptr;
   std::vector<float*> W, WG, M, V, stage;
   double* partials = nullptr;
+  float* seg_scratch = nullptr;  // MG_SPMM_FAST hub-row segment partials (max segments x ld_max)
   float* ws = nullptr;  // tcgen05 TN split-K partials (W-grad), private to this worker's stream
   size_t ws_bytes = 0;
   double* stats = nullptr;
@@ -247,16 +335,27 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
       ed[i] = make_int2(t.col[i], bits);
     }
   });
-  std::vector<int> light, heavy;
-  build_orders(t.row_ptr, light, heavy);
   d.row_ptr = dalloc_t<int>(g, w, rp32.size());
   d.edges = dalloc_t<int2>(g, w, d.nnz + k::kEdgePad);
+  MG_CUDA(cudaMemcpy(d.row_ptr, rp32.data(), sizeof(int) * rp32.size(), cudaMemcpyHostToDevice));
+  if (d.nnz) MG_CUDA(cudaMemcpy(d.edges, ed.data(), sizeof(int2) * d.nnz, cudaMemcpyHostToDevice));
+  if (g.cfg.spmm_mode == MG_SPMM_FAST) {
+    std::vector<int4> items, hubs;
+    build_fast_items(t.row_ptr, items, hubs, d.n_segments);
+    d.items = dalloc_t<int4>(g, w, std::max<size_t>(1, items.size()));
+    d.hubs = dalloc_t<int4>(g, w, std::max<size_t>(1, hubs.size()));
+    d.n_items = static_cast<int>(items.size());
+    d.n_hubs = static_cast<int>(hubs.size());
+    if (!items.empty()) MG_CUDA(cudaMemcpy(d.items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
+    if (!hubs.empty()) MG_CUDA(cudaMemcpy(d.hubs, hubs.data(), sizeof(int4) * hubs.size(), cudaMemcpyHostToDevice));
+    return;
+  }
+  std::vector<int> light, heavy;
+  build_orders(t.row_ptr, light, heavy);
   d.light = dalloc_t<int>(g, w, std::max<size_t>(1, light.size()));
   d.heavy = dalloc_t<int>(g, w, std::max<size_t>(1, heavy.size()));
   d.n_light = static_cast<int>(light.size());
   d.n_heavy = static_cast<int>(heavy.size());
-  MG_CUDA(cudaMemcpy(d.row_ptr, rp32.data(), sizeof(int) * rp32.size(), cudaMemcpyHostToDevice));
-  if (d.nnz) MG_CUDA(cudaMemcpy(d.edges, ed.data(), sizeof(int2) * d.nnz, cudaMemcpyHostToDevice));
   if (!light.empty()) MG_CUDA(cudaMemcpy(d.light, light.data(), sizeof(int) * light.size(), cudaMemcpyHostToDevice));
   if (!heavy.empty()) MG_CUDA(cudaMemcpy(d.heavy, heavy.data(), sizeof(int) * heavy.size(), cudaMemcpyHostToDevice));
 }
@@ -400,6 +499,13 @@ class Step {
         SpmmLaunch sl{t.row_ptr, t.edges, t.light, t.n_light, t.heavy, t.n_heavy};
         const int acc = j > 0, relu = relu_last && j == P_ - 1;
         const int pi = prof_begin(w);
+        if (cfg_.spmm_mode == MG_SPMM_FAST) {
+          FastLaunch fl{t.items, t.n_items, t.hubs, t.n_hubs, t.edges, w.seg_scratch};
+          g_.kernels_last += spmm_fast(fl, recv[k], out[k], ld, acc, relu, w.s0);
+          prof_end(w, pi, 0);
+          MG_CUDA(cudaEventRecord(w.mult[j], w.s0));
+          continue;
+        }
         if (t.n_heavy > 0) {  // hub rows run beside the light rows on the side stream
           MG_CUDA(cudaEventRecord(w.heavy_fork, w.s0));
           MG_CUDA(cudaStreamWaitEvent(w.s2, w.heavy_fork, 0));
@@ -662,6 +768,9 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
       g_heavy_row = static_cast<int>(std::min<int64_t>(value, 1 << 30));
     } else if (k == "profile") {
       g_profile = value != 0 ? 1 : 0;
+    } else if (k == "fast_segment") {
+      if (value < 32) throw ValueError("tuning: fast_segment must be >= 32");
+      g_fast_segment = static_cast<int>(std::min<int64_t>(value, 1 << 24));
     } else if (k == "tn_chunk") {
       tc::set_tn_chunk(static_cast<int>(value));
     } else {
@@ -757,10 +866,15 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       w.t_start = mk_event(true);
       w.t_end = mk_event(true);
       // tiles
+      int max_segments = 0;
       for (int d = 0; d < 2; ++d) {
         w.tiles[d].resize(world);
-        for (int j = 0; j < world; ++j) upload_tile(*g, w, p->tiles[d][w.rank][j], w.tiles[d][j]);
+        for (int j = 0; j < world; ++j) {
+          upload_tile(*g, w, p->tiles[d][w.rank][j], w.tiles[d][j]);
+          max_segments = std::max(max_segments, w.tiles[d][j].n_segments);
+        }
       }
+      if (max_segments > 0) w.seg_scratch = dalloc_t<float>(*g, w, static_cast<size_t>(max_segments) * g->ld_max);
       // rows: x_local, labels, mask (gcn.hpp:127-132)
       w.x = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));
       upload_padded(w.x, p->features.data() + w.r0 * p->d0, w.rows, p->d0, g->ld[0]);
@@ -1106,6 +1220,26 @@ mg_status mg_dev_spmm(int64_t rows, const int32_t* row_ptr, const void* edges, c
     std::vector<int> rp32(rows + 1);
     MG_CUDA(cudaMemcpy(rp32.data(), row_ptr, sizeof(int) * (rows + 1), cudaMemcpyDeviceToHost));
     std::vector<index_t> rp(rp32.begin(), rp32.end());
+    if (mode == MG_SPMM_FAST) {
+      std::vector<int4> items, hubs;
+      int nseg = 0;
+      build_fast_items(rp, items, hubs, nseg);
+      int4 *di = nullptr, *dh = nullptr;
+      float* sc = nullptr;
+      MG_CUDA(cudaMalloc(&di, sizeof(int4) * std::max<size_t>(1, items.size())));
+      MG_CUDA(cudaMalloc(&dh, sizeof(int4) * std::max<size_t>(1, hubs.size())));
+      MG_CUDA(cudaMalloc(&sc, sizeof(float) * std::max<size_t>(1, static_cast<size_t>(nseg) * ld)));
+      if (!items.empty()) MG_CUDA(cudaMemcpy(di, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
+      if (!hubs.empty()) MG_CUDA(cudaMemcpy(dh, hubs.data(), sizeof(int4) * hubs.size(), cudaMemcpyHostToDevice));
+      FastLaunch fl{di, static_cast<int>(items.size()), dh, static_cast<int>(hubs.size()),
+                    static_cast<const int2*>(edges), sc};
+      spmm_fast(fl, h, out, ld, accumulate, relu, s);
+      MG_CUDA(cudaStreamSynchronize(s));
+      cudaFree(di);
+      cudaFree(dh);
+      cudaFree(sc);
+      return;
+    }
     std::vector<int> light, heavy;
     build_orders(rp, light, heavy);
     int *dl = nullptr, *dh = nullptr;

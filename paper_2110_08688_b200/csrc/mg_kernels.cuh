@@ -104,6 +104,109 @@ __global__ void __launch_bounds__(256) spmm_exact_rows(const int* __restrict__ r
   }
 }
 
+// ============================================================================ SpMM (fast)
+// MG_SPMM_FAST: the same lane-group gather, with two differences that trade bitwise parity with the
+// reference for speed (the result stays deterministic and within fp32 rounding of it):
+//   * fused multiply-add per nonzero;
+//   * rows with >= heavy_row nonzeros are cut into fixed segments of `seg` nonzeros that are gathered
+//     in parallel like ordinary rows into a scratch buffer, then summed in segment order by
+//     spmm_fast_hubs — the hub rows no longer serialise on one CTA.
+// Work items are int4 {e_begin, e_end, dst, 0}: dst >= 0 is an output row (accumulate / relu apply),
+// dst < 0 is scratch segment -dst-1 (plain store).
+__device__ __forceinline__ void fma4(float4& acc, float v, const float4& x) {
+  acc.x = fmaf(v, x.x, acc.x);
+  acc.y = fmaf(v, x.y, acc.y);
+  acc.z = fmaf(v, x.z, acc.z);
+  acc.w = fmaf(v, x.w, acc.w);
+}
+
+template <int G, int CPL>
+__global__ void __launch_bounds__(256) spmm_fast_items(const int4* __restrict__ items, int n_items,
+                                                       const int2* __restrict__ edges, const float* __restrict__ h,
+                                                       float* __restrict__ out, float* __restrict__ scratch, int ld,
+                                                       int nchunk, int accumulate, int relu) {
+  constexpr int U = (CPL <= 2) ? 4 : 2;
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  const int groups = gridDim.x * (blockDim.x / G);
+  for (int idx = blockIdx.x * (blockDim.x / G) + threadIdx.x / G; idx < n_items; idx += groups) {
+    const int4 it = __ldg(items + idx);
+    const int e0 = it.x, e1 = it.y;
+    const bool seg = it.z < 0;
+    float* orow = seg ? scratch + (size_t)(-it.z - 1) * ld : out + (size_t)it.z * ld;
+    float4 acc[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int c = lane + k * G;
+      acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!seg && accumulate && c < nchunk) acc[k] = *reinterpret_cast<const float4*>(orow + 4 * c);
+    }
+    for (int base = e0; base < e1; base += G) {
+      const int cnt = min(G, e1 - base);
+      const int2 my = lane < cnt ? __ldg(edges + base + lane) : make_int2(0, 0);
+      int j = 0;
+      for (; j + U <= cnt; j += U) {
+        float4 x[U][CPL];
+        float v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int col = __shfl_sync(gmask, my.x, j + u, G);
+          v[u] = __int_as_float(__shfl_sync(gmask, my.y, j + u, G));
+          const float* hr = h + (size_t)col * ld;
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            const int c = lane + k * G;
+            x[u][k] = c < nchunk ? ldg4(hr + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) fma4(acc[k], v[u], x[u][k]);
+      }
+      for (; j < cnt; ++j) {
+        const int col = __shfl_sync(gmask, my.x, j, G);
+        const float v = __int_as_float(__shfl_sync(gmask, my.y, j, G));
+        const float* hr = h + (size_t)col * ld;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) {
+          const int c = lane + k * G;
+          if (c < nchunk) fma4(acc[k], v, ldg4(hr + 4 * c));
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int c = lane + k * G;
+      if (c < nchunk) {
+        float4 a = acc[k];
+        if (relu && !seg) a = make_float4(relu1(a.x), relu1(a.y), relu1(a.z), relu1(a.w));
+        *reinterpret_cast<float4*>(orow + 4 * c) = a;
+      }
+    }
+  }
+}
+
+// hubs[i] = {row, first segment, segment count}: out[row] = (acc ? out[row] : 0) + sum of its segments in
+// order, then relu. One CTA per hub row, threads over float4 chunks.
+__global__ void __launch_bounds__(256) spmm_fast_hubs(const int4* __restrict__ hubs, const float* __restrict__ scratch,
+                                                      float* __restrict__ out, int ld, int accumulate, int relu) {
+  const int4 hb = hubs[blockIdx.x];
+  float* orow = out + (size_t)hb.x * ld;
+  for (int c = threadIdx.x; c < ld / 4; c += blockDim.x) {
+    float4 s = accumulate ? *reinterpret_cast<const float4*>(orow + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int q = 0; q < hb.z; ++q) {
+      const float4 p = *reinterpret_cast<const float4*>(scratch + (size_t)(hb.y + q) * ld + 4 * c);
+      s.x += p.x;
+      s.y += p.y;
+      s.z += p.z;
+      s.w += p.w;
+    }
+    if (relu) s = make_float4(relu1(s.x), relu1(s.y), relu1(s.z), relu1(s.w));
+    *reinterpret_cast<float4*>(orow + 4 * c) = s;
+  }
+}
+
 // Long rows (hubs of the power-law graph): one CTA per (row, 64-column slab), warp-specialised.
 // Warps 2-3 (producers) stream the row's h-slabs into an NST-deep ring of 32-nonzero stages with
 // 16-byte cp.async (completion tracked per stage by cp.async.mbarrier.arrive); the stage's edge

@@ -161,3 +161,30 @@ def test_gemm_tcgen05_deterministic():
     r1 = run_gemm(a, b, True, False, mode=R.GEMM_TF32X3)
     r2 = run_gemm(a, b, True, False, mode=R.GEMM_TF32X3)
     assert bits_equal(r1, r2)
+
+
+# ---------------------------------------------------------------------------- MG_SPMM_FAST
+# FMA and hub rows cut into fixed segments summed in order: deterministic, within fp32 rounding of the
+# reference (normwise <= 1e-6 here; the model-level tolerance is 1e-4).
+@pytest.mark.parametrize("w", [4, 48, 256, 300])
+@pytest.mark.parametrize("seg", [64, 2048])
+def test_spmm_fast_with_hubs(port32, w, seg):
+    from gpu_util import normwise
+    rng = np.random.default_rng(11 + w + seg)
+    rows, cols = 300, 5000
+    rp, ci, v = random_tile(rng, rows, cols, 0.003, hub_rows=(0, 5, 299), hub_len=4800)
+    h = rng.uniform(-1, 1, (cols, w)).astype(np.float32)
+    o0 = rng.uniform(-1, 1, (rows, w)).astype(np.float32)
+    ref = port32.spmm(rows, cols, rp, ci, v, h, True, o0)
+    R.set_tuning("heavy_row", 1000)
+    R.set_tuning("fast_segment", seg)
+    try:
+        out = run_spmm(rp, ci, v, h, True, o0, mode=R.SPMM_FAST)
+        out2 = run_spmm(rp, ci, v, h, True, o0, mode=R.SPMM_FAST)
+        relu = run_spmm(rp, ci, v, h, True, o0, relu=True, mode=R.SPMM_FAST)
+    finally:
+        R.set_tuning("heavy_row", 4096)
+        R.set_tuning("fast_segment", 2048)
+    assert normwise(out, ref) <= 1e-6
+    assert bits_equal(out, out2)  # deterministic
+    assert np.all(relu >= 0) and normwise(relu, np.maximum(ref, 0)) <= 1e-6

@@ -204,3 +204,39 @@ def test_p_invariance_bitwise_tcgen05():
         for e in range(cfg.epochs):
             assert all(h == dist.w_hashes[e][0] for h in dist.w_hashes[e])
             assert dist.w_hashes[e][0] == base.w_hashes[e][0]
+
+
+def test_fast_modes_trajectory_and_determinism(golden):
+    """TF32X3 GeMMs + fast SpMM (the benchmark configuration): C1 losses within 1e-4 of the f64 reference,
+    run-to-run bitwise deterministic, and W bitwise P-invariant when no row is split (P-invariance with
+    hub segments holds up to the segment boundaries, which depend on the tile)."""
+    ds = R.synth_graph(2708, 3.9, 0.7, 1, 1433, 7)
+    cfg = R.GcnConfig([1433, 16, 7], epochs=5, seed=1, permute=True, gemm_mode=R.GEMM_TF32X3,
+                      spmm_mode=R.SPMM_FAST)
+    a = R.train_run(ds, cfg, R.TrainOptions(workers=1, devices=[0]))
+    b = R.train_run(ds, cfg, R.TrainOptions(workers=1, devices=[0]))
+    ref64 = golden["c1_f64_perm1_loss"]
+    for e in range(5):
+        assert abs(a.epoch_loss[e] - ref64[e]) <= TOL * abs(ref64[e])
+    assert a.epoch_loss == b.epoch_loss and a.w_hashes == b.w_hashes
+    d = R.train_run(ds, cfg, R.TrainOptions(workers=2, devices=[0, 0], transport=R.TRANSPORT_LOCAL))
+    for e in range(5):
+        assert abs(d.epoch_loss[e] - a.epoch_loss[e]) <= 1e-6 * abs(a.epoch_loss[e])
+
+
+def test_step_dump_fast_spmm(golden):
+    ds, _ = small_ds(golden)
+    cfg = R.GcnConfig([12, 8, 6, 5], seed=5, permute=True, overlap=True, gemm_mode=R.GEMM_TF32X3,
+                      spmm_mode=R.SPMM_FAST)
+    R.set_tuning("heavy_row", 8)  # force hub segments on this small graph
+    R.set_tuning("fast_segment", 32)
+    try:
+        with group(ds, cfg, 2) as g:
+            g.compute_gradients()
+            for l in range(3):
+                assert normwise(g.read(R.T_WGRAD, l), golden[f"dump300_wgrad{l}"]) <= TOL
+            for l in range(2):
+                assert normwise(gather(g, R.T_AHW, l, 2), golden[f"dump300_ahw_bwd{l}"]) <= TOL
+    finally:
+        R.set_tuning("heavy_row", 4096)
+        R.set_tuning("fast_segment", 2048)
