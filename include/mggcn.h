@@ -72,7 +72,8 @@ typedef struct mg_config {
 } mg_config;
 
 /* Fills the reference defaults (inc/gcn.hpp:16-25): lr 0.01, betas 0.9/0.999, eps 1e-8, 100 epochs,
- * seed 1, flags off; gemm_mode TF32X3, spmm_mode EXACT. layer_dims left NULL. */
+ * seed 1, flags off; gemm_mode TF32X3, spmm_mode FAST (both within rel 1e-4 of the reference; EXACT gives
+ * bitwise parity). layer_dims left NULL. */
 void mg_config_defaults(mg_config* cfg);
 /* GcnConfig::validate (inc/gcn.hpp:29-35) -> MG_CONFIG_ERROR. */
 mg_status mg_config_validate(const mg_config* cfg);
@@ -140,6 +141,8 @@ typedef struct mg_group mg_group;
 
 typedef enum mg_transport { MG_TRANSPORT_AUTO = 0, MG_TRANSPORT_NCCL = 1, MG_TRANSPORT_LOCAL = 2 } mg_transport;
 
+/* Number of visible CUDA devices (0 without a driver/GPU: the host half of the library still works). */
+int32_t mg_device_count(void);
 mg_status mg_nccl_unique_id(uint8_t id[128]);
 mg_status mg_group_create(const mg_config* cfg, const mg_partition* p, int32_t world, int32_t n_local,
                           const int32_t* local_ranks, const int32_t* devices, const uint8_t* nccl_id,

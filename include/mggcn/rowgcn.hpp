@@ -1,0 +1,423 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// mggcn/rowgcn.hpp — C++ drop-in for the reference's training API (rowgcn, proj/include/rowgcn/),
+// header-only on top of the C ABI in mggcn.h (link with -lmggcn). Same names, argument meaning and
+// exception types as the reference, so a caller of rowgcn switches by changing the include and the
+// namespace:
+//
+//   rowgcn (reference)                                   mggcn::rowgcn (this header)
+//   ShapeError/ValueError/... inc/errors.hpp:10-39        same names, same what() text
+//   GcnConfig                 inc/gcn.hpp:14-36           + gemm_mode / spmm_mode
+//   parse_config / materialize_config  driver.hpp:24-57   same (generic over the JSON type)
+//   CsrMatrix / DenseMatrix / Dataset   sparse.hpp / dense.hpp / dataset.hpp
+//   synth_graph<float>        inc/dataset.hpp:287-334     bit-identical output
+//   prepare_data / PreparedData  driver.hpp:75-117        bit-identical tiles
+//   TrainOptions / TrainArtifacts / train_run  driver.hpp:119-206
+//   GradArtifacts / grad_run  driver.hpp:209-251
+//   write_checkpoint / read_checkpoint  driver.hpp:255-299  (MGDM blocks + JSON sidecar)
+//
+// The device work runs on the GPUs of this process (one GcnWorker per rank, two CUDA streams each,
+// NCCL or the in-process transport between them). Only float is provided: train_run<double> stays
+// with the CPU reference.
+#pragma once
+
+#include <cstdint>
+#include <cstring>
+#include <fstream>
+#include <functional>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "mggcn.h"
+
+namespace mggcn {
+namespace rowgcn {
+
+using index_t = std::int64_t;
+
+// ---------------------------------------------------------------- errors (inc/errors.hpp)
+struct ShapeError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ValueError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ProtocolError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ShutdownError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ParseError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct IoError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct NcclError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+inline void check(mg_status s) {
+  if (s == MG_OK) return;
+  const std::string m = mg_last_error();
+  switch (s) {
+    case MG_SHAPE_ERROR: throw ShapeError(m);
+    case MG_VALUE_ERROR: throw ValueError(m);
+    case MG_PROTOCOL_ERROR: throw ProtocolError(m);
+    case MG_SHUTDOWN_ERROR: throw ShutdownError(m);
+    case MG_PARSE_ERROR: throw ParseError(m);
+    case MG_CONFIG_ERROR: throw ConfigError(m);
+    case MG_IO_ERROR: throw IoError(m);
+    case MG_CUDA_ERROR: throw CudaError(m);
+    case MG_NCCL_ERROR: throw NcclError(m);
+    default: throw std::runtime_error(m);
+  }
+}
+
+// ---------------------------------------------------------------- containers
+template <class S>
+struct CsrMatrix {  // inc/sparse.hpp:25-55
+  index_t rows = 0, cols = 0;
+  std::vector<index_t> row_ptr, col_idx;
+  std::vector<S> values;
+  index_t nnz() const { return static_cast<index_t>(col_idx.size()); }
+};
+
+template <class S>
+class DenseMatrix {  // inc/dense.hpp:73-118 (row-major, ld = cols)
+ public:
+  DenseMatrix() = default;
+  DenseMatrix(index_t r, index_t c) : rows_(r), cols_(c), data_(static_cast<size_t>(r * c), S(0)) {
+    if (r < 0 || c < 0) throw ValueError("DenseMatrix: negative dimension");
+  }
+  index_t rows() const { return rows_; }
+  index_t cols() const { return cols_; }
+  index_t size() const { return rows_ * cols_; }
+  S* data() { return data_.data(); }
+  const S* data() const { return data_.data(); }
+  S& operator()(index_t i, index_t j) { return data_[static_cast<size_t>(i * cols_ + j)]; }
+  S operator()(index_t i, index_t j) const { return data_[static_cast<size_t>(i * cols_ + j)]; }
+
+ private:
+  index_t rows_ = 0, cols_ = 0;
+  std::vector<S> data_;
+};
+
+template <class S>
+struct Dataset {  // inc/dataset.hpp:19-56
+  CsrMatrix<S> graph;
+  DenseMatrix<S> features;
+  std::vector<std::int32_t> labels;
+  std::vector<std::uint8_t> train_mask, val_mask, test_mask;
+  std::string name;
+  index_t n() const { return graph.rows; }
+  int num_classes() const {
+    std::int32_t c = 0;
+    for (auto l : labels) c = l > c ? l : c;
+    return c + 1;
+  }
+};
+
+// ---------------------------------------------------------------- config (inc/gcn.hpp:14-36)
+struct GcnConfig {
+  std::vector<index_t> layer_dims;
+  double lr = 0.01, beta1 = 0.9, beta2 = 0.999, epsilon = 1e-8;
+  int epochs = 100;
+  std::uint64_t seed = 1;
+  bool permute = false, overlap = false, skip_first_backward_spmm = false, order_swap = false;
+  int gemm_mode = MG_GEMM_TF32X3;  // see DESIGN.md: EXACT is bitwise, TF32X3/FAST meet rel 1e-4
+  int spmm_mode = MG_SPMM_FAST;
+  int layers() const { return static_cast<int>(layer_dims.size()) - 1; }
+  mg_config c() const {
+    mg_config m;
+    mg_config_defaults(&m);
+    m.layer_dims = layer_dims.data();
+    m.n_dims = static_cast<std::int32_t>(layer_dims.size());
+    m.lr = lr;
+    m.beta1 = beta1;
+    m.beta2 = beta2;
+    m.epsilon = epsilon;
+    m.epochs = epochs;
+    m.seed = seed;
+    m.permute = permute;
+    m.overlap = overlap;
+    m.skip_first_backward_spmm = skip_first_backward_spmm;
+    m.order_swap = order_swap;
+    m.gemm_mode = gemm_mode;
+    m.spmm_mode = spmm_mode;
+    return m;
+  }
+  void validate() const {
+    const mg_config m = c();
+    check(mg_config_validate(&m));
+  }
+};
+
+struct ConfigFile {  // inc/driver.hpp:19-22
+  std::vector<index_t> hidden_dims{16};
+  GcnConfig cfg;
+};
+
+// inc/driver.hpp:24-47, generic over the JSON type (nlohmann::json in the reference's callers).
+template <class Json>
+ConfigFile parse_config(const Json& j) {
+  static const char* known[] = {"hidden_dims", "lr", "beta1", "beta2", "epsilon", "epochs", "seed", "permute",
+                                "overlap", "skip_first_backward_spmm", "order_swap"};
+  for (auto it = j.begin(); it != j.end(); ++it) {
+    bool ok = false;
+    for (const char* k : known) ok = ok || it.key() == k;
+    if (!ok) throw ConfigError("config: unknown key '" + it.key() + "'");
+  }
+  ConfigFile cf;
+  if (j.contains("hidden_dims")) cf.hidden_dims = j.at("hidden_dims").template get<std::vector<index_t>>();
+  auto& c = cf.cfg;
+  c.lr = j.value("lr", c.lr);
+  c.beta1 = j.value("beta1", c.beta1);
+  c.beta2 = j.value("beta2", c.beta2);
+  c.epsilon = j.value("epsilon", c.epsilon);
+  c.epochs = j.value("epochs", c.epochs);
+  c.seed = j.value("seed", c.seed);
+  c.permute = j.value("permute", c.permute);
+  c.overlap = j.value("overlap", c.overlap);
+  c.skip_first_backward_spmm = j.value("skip_first_backward_spmm", c.skip_first_backward_spmm);
+  c.order_swap = j.value("order_swap", c.order_swap);
+  return cf;
+}
+
+inline GcnConfig materialize_config(const ConfigFile& cf, index_t d0, int classes) {  // driver.hpp:49-57
+  GcnConfig cfg = cf.cfg;
+  cfg.layer_dims.clear();
+  cfg.layer_dims.push_back(d0);
+  for (index_t h : cf.hidden_dims) cfg.layer_dims.push_back(h);
+  cfg.layer_dims.push_back(classes);
+  cfg.validate();
+  return cfg;
+}
+
+// ---------------------------------------------------------------- RAII handles over the C ABI
+namespace detail {
+struct DatasetHandle {
+  mg_dataset* p = nullptr;
+  ~DatasetHandle() { mg_dataset_free(p); }
+};
+struct PartitionDel {
+  void operator()(mg_partition* p) const { mg_partition_free(p); }
+};
+struct GroupDel {
+  void operator()(mg_group* g) const { mg_group_destroy(g); }
+};
+
+inline DatasetHandle to_handle(const Dataset<float>& ds) {
+  DatasetHandle h;
+  const mg_csr g{ds.graph.rows, ds.graph.cols, ds.graph.row_ptr.data(), ds.graph.col_idx.data(),
+                 ds.graph.values.data()};
+  check(mg_dataset_from_arrays(&g, ds.features.data(), ds.features.cols(), ds.labels.data(),
+                               ds.train_mask.empty() ? nullptr : ds.train_mask.data(), &h.p));
+  return h;
+}
+}  // namespace detail
+
+// rowgcn::synth_graph<float> (inc/dataset.hpp:287-334), bit-identical.
+inline Dataset<float> synth_graph(index_t n, double avg_degree, double exponent, std::uint64_t seed,
+                                  index_t feature_dim = 16, int classes = 4) {
+  detail::DatasetHandle h;
+  check(mg_dataset_synth(n, avg_degree, exponent, seed, feature_dim, classes, &h.p));
+  mg_csr g;
+  const float* f = nullptr;
+  const std::int32_t* lab = nullptr;
+  const std::uint8_t* mask = nullptr;
+  std::int64_t d0 = 0;
+  check(mg_dataset_view(h.p, &g, &f, &d0, &lab, &mask));
+  Dataset<float> ds;
+  ds.name = "synth-n" + std::to_string(n) + "-d" + std::to_string(avg_degree);
+  ds.graph.rows = g.rows;
+  ds.graph.cols = g.cols;
+  ds.graph.row_ptr.assign(g.row_ptr, g.row_ptr + g.rows + 1);
+  ds.graph.col_idx.assign(g.col_idx, g.col_idx + g.row_ptr[g.rows]);
+  ds.graph.values.assign(g.values, g.values + g.row_ptr[g.rows]);
+  ds.features = DenseMatrix<float>(n, d0);
+  std::memcpy(ds.features.data(), f, sizeof(float) * static_cast<size_t>(n * d0));
+  ds.labels.assign(lab, lab + n);
+  return ds;
+}
+
+// rowgcn::PreparedData (inc/driver.hpp:75-85): owns the bit-exact tiles of this process's ranks.
+struct PreparedData {
+  std::unique_ptr<mg_partition, detail::PartitionDel> p;
+  int workers = 1;
+  std::vector<index_t> bounds() const {
+    std::vector<index_t> b(static_cast<size_t>(workers) + 1);
+    check(mg_partition_info(p.get(), nullptr, nullptr, b.data()));
+    return b;
+  }
+  CsrMatrix<float> tile(int dir, int i, int j) const {  // dir 0: A_hat^T (forward), 1: A_hat
+    CsrMatrix<float> t;
+    std::int64_t nnz = 0;
+    check(mg_partition_tile_info(p.get(), dir, i, j, &t.rows, &t.cols, &nnz));
+    t.row_ptr.resize(static_cast<size_t>(t.rows) + 1);
+    t.col_idx.resize(static_cast<size_t>(nnz));
+    t.values.resize(static_cast<size_t>(nnz));
+    check(mg_partition_tile_export(p.get(), dir, i, j, t.row_ptr.data(), t.col_idx.data(), t.values.data()));
+    return t;
+  }
+};
+
+inline PreparedData prepare_data(const Dataset<float>& ds, const GcnConfig& cfg, int workers, int only_rank = -1) {
+  auto h = detail::to_handle(ds);
+  const mg_config c = cfg.c();
+  mg_partition* p = nullptr;
+  check(mg_prepare(h.p, &c, workers, only_rank, &p));
+  PreparedData out;
+  out.p.reset(p);
+  out.workers = workers;
+  return out;
+}
+
+// ---------------------------------------------------------------- driver (inc/driver.hpp:119-251)
+struct TrainOptions {
+  int workers = 1;
+  bool collect_logits = false;
+  std::function<void(int, double, double, double)> on_epoch;  // (epoch, loss, acc, wall_us) on rank 0
+  std::vector<int> devices;  // CUDA device per rank; default rank % #devices
+  int transport = MG_TRANSPORT_AUTO;
+};
+
+template <class S>
+struct TrainArtifacts {
+  std::vector<double> epoch_loss, epoch_acc, epoch_wall_us;
+  std::vector<std::vector<std::uint64_t>> w_hashes;  // [epoch][rank]
+  std::vector<DenseMatrix<S>> final_w;               // rank 0's replicas
+  DenseMatrix<S> logits;                             // gathered post-training logits (permuted order)
+  int workers = 1;
+  double final_loss() const { return epoch_loss.empty() ? 0.0 : epoch_loss.back(); }
+  double final_acc() const { return epoch_acc.empty() ? 0.0 : epoch_acc.back(); }
+};
+
+template <class S>
+struct GradArtifacts {
+  std::vector<DenseMatrix<S>> w_grad;
+  std::vector<std::uint64_t> grad_hash_per_rank;
+  double loss = 0.0;
+};
+
+namespace detail {
+inline std::unique_ptr<mg_group, GroupDel> make_group(const GcnConfig& cfg, const PreparedData& prep, int workers,
+                                                      std::vector<int> devices, int transport) {
+  std::vector<std::int32_t> ranks(static_cast<size_t>(workers));
+  if (devices.empty()) {
+    int nd = mg_device_count();
+    if (nd < 1) nd = 1;
+    for (int r = 0; r < workers; ++r) devices.push_back(r % nd);
+  }
+  for (int r = 0; r < workers; ++r) ranks[static_cast<size_t>(r)] = r;
+  const mg_config c = cfg.c();
+  mg_group* g = nullptr;
+  check(mg_group_create(&c, prep.p.get(), workers, workers, ranks.data(), devices.data(), nullptr, transport, &g));
+  return std::unique_ptr<mg_group, GroupDel>(g);
+}
+
+inline DenseMatrix<float> read(mg_group* g, int rank, int which, int layer, index_t rows, index_t cols) {
+  DenseMatrix<float> m(rows, cols);
+  check(mg_group_read(g, rank, which, layer, m.data(), m.size()));
+  return m;
+}
+}  // namespace detail
+
+inline TrainArtifacts<float> train_run(const Dataset<float>& ds, const GcnConfig& cfg, const TrainOptions& opts) {
+  cfg.validate();
+  if (cfg.layer_dims.front() != ds.features.cols())
+    throw ConfigError("config: layer_dims[0]=" + std::to_string(cfg.layer_dims.front()) +
+                      " but dataset features have width " + std::to_string(ds.features.cols()));
+  const PreparedData prep = prepare_data(ds, cfg, opts.workers);
+  auto g = detail::make_group(cfg, prep, opts.workers, opts.devices, opts.transport);
+  check(mg_group_init_params(g.get()));
+  TrainArtifacts<float> art;
+  art.workers = opts.workers;
+  for (int e = 1; e <= cfg.epochs; ++e) {
+    double loss = 0, acc = 0, wall = 0;
+    check(mg_group_train_step(g.get(), e, &loss, &acc, &wall));
+    art.epoch_loss.push_back(loss);
+    art.epoch_acc.push_back(acc);
+    art.epoch_wall_us.push_back(wall);
+    std::vector<std::uint64_t> hs(static_cast<size_t>(opts.workers));
+    for (int r = 0; r < opts.workers; ++r) check(mg_group_w_hash(g.get(), r, &hs[static_cast<size_t>(r)]));
+    art.w_hashes.push_back(std::move(hs));
+    if (opts.on_epoch) opts.on_epoch(e, loss, acc, wall);
+  }
+  const int L = cfg.layers();
+  if (opts.collect_logits) {
+    double l = 0;
+    check(mg_group_loss_only(g.get(), &l));
+    art.logits = DenseMatrix<float>(ds.n(), cfg.layer_dims.back());
+    for (int r = 0; r < opts.workers; ++r) {
+      std::int64_t b = 0, rows = 0;
+      check(mg_group_rows(g.get(), r, &b, &rows));
+      check(mg_group_read(g.get(), r, MG_T_AHW, L - 1, art.logits.data() + b * cfg.layer_dims.back(),
+                          rows * cfg.layer_dims.back()));
+    }
+  }
+  for (int l = 0; l < L; ++l)
+    art.final_w.push_back(detail::read(g.get(), 0, MG_T_W, l, cfg.layer_dims[static_cast<size_t>(l)],
+                                       cfg.layer_dims[static_cast<size_t>(l) + 1]));
+  return art;
+}
+
+inline GradArtifacts<float> grad_run(const Dataset<float>& ds, const GcnConfig& cfg, int workers) {
+  cfg.validate();
+  const PreparedData prep = prepare_data(ds, cfg, workers);
+  auto g = detail::make_group(cfg, prep, workers, {}, MG_TRANSPORT_AUTO);
+  check(mg_group_init_params(g.get()));
+  GradArtifacts<float> art;
+  double acc = 0;
+  check(mg_group_compute_gradients(g.get(), &art.loss, &acc));
+  const int L = cfg.layers();
+  for (int r = 0; r < workers; ++r) {
+    std::uint64_t h = 0xcbf29ce484222325ull;
+    for (int l = 0; l < L; ++l) {
+      auto m = detail::read(g.get(), r, MG_T_WGRAD, l, cfg.layer_dims[static_cast<size_t>(l)],
+                            cfg.layer_dims[static_cast<size_t>(l) + 1]);
+      const auto* p = reinterpret_cast<const unsigned char*>(m.data());
+      for (size_t i = 0; i < sizeof(float) * static_cast<size_t>(m.size()); ++i) {
+        h ^= p[i];
+        h *= 0x100000001b3ull;
+      }
+      if (r == 0) art.w_grad.push_back(std::move(m));
+    }
+    art.grad_hash_per_rank.push_back(h);
+  }
+  return art;
+}
+
+// inc/driver.hpp:255-299: every W as an MGDM block ("MGDM", u64 rows, u64 cols, u8 4, payload).
+inline void write_checkpoint(const std::string& path, const std::vector<DenseMatrix<float>>& ws) {
+  std::ofstream f(path, std::ios::binary);
+  if (!f) throw IoError("cannot open " + path + " for writing");
+  for (const auto& w : ws) {
+    f.write("MGDM", 4);
+    const std::uint64_t r = static_cast<std::uint64_t>(w.rows()), c = static_cast<std::uint64_t>(w.cols());
+    const std::uint8_t width = 4;
+    f.write(reinterpret_cast<const char*>(&r), 8);
+    f.write(reinterpret_cast<const char*>(&c), 8);
+    f.write(reinterpret_cast<const char*>(&width), 1);
+    f.write(reinterpret_cast<const char*>(w.data()), static_cast<std::streamsize>(4 * w.size()));
+  }
+  if (!f) throw IoError("short write to " + path);
+}
+
+inline std::vector<DenseMatrix<float>> read_checkpoint(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw IoError("cannot open " + path);
+  std::vector<DenseMatrix<float>> ws;
+  while (true) {
+    char magic[4];
+    f.read(magic, 4);
+    if (!f) break;
+    if (std::memcmp(magic, "MGDM", 4) != 0) throw ParseError(path + ": bad checkpoint block magic");
+    std::uint64_t r = 0, c = 0;
+    std::uint8_t width = 0;
+    f.read(reinterpret_cast<char*>(&r), 8);
+    f.read(reinterpret_cast<char*>(&c), 8);
+    f.read(reinterpret_cast<char*>(&width), 1);
+    if (!f || width != 4)
+      throw ParseError(path + ": checkpoint dtype width " + std::to_string(width) + " does not match run dtype 4");
+    DenseMatrix<float> w(static_cast<index_t>(r), static_cast<index_t>(c));
+    f.read(reinterpret_cast<char*>(w.data()), static_cast<std::streamsize>(4 * w.size()));
+    if (!f) throw ParseError(path + ": truncated checkpoint block");
+    ws.push_back(std::move(w));
+  }
+  return ws;
+}
+
+}  // namespace rowgcn
+}  // namespace mggcn

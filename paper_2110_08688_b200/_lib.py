@@ -44,6 +44,7 @@ SIGNATURES = [
                                            C.c_void_p]),
     ("mg_partition_rows_export", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("mg_partition_free", None, [C.c_void_p]),
+    ("mg_device_count", C.c_int32, []),
     ("mg_nccl_unique_id", C.c_int, [C.c_void_p]),
     ("mg_group_create", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                   C.c_int32, C.c_void_p]),

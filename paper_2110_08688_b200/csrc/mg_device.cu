@@ -779,6 +779,15 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
   });
 }
 
+int32_t mg_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();  // clear the sticky "no device" status
+    return 0;
+  }
+  return n;
+}
+
 mg_status mg_nccl_unique_id(uint8_t id[128]) {
   return guarded([&] {
     ncclUniqueId u;

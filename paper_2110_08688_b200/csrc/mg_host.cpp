@@ -363,8 +363,8 @@ void mg_config_defaults(mg_config* c) {
   c->epsilon = 1e-8;
   c->epochs = 100;
   c->seed = 1;
-  c->gemm_mode = MG_GEMM_EXACT;
-  c->spmm_mode = MG_SPMM_EXACT;
+  c->gemm_mode = MG_GEMM_TF32X3;
+  c->spmm_mode = MG_SPMM_FAST;
 }
 
 mg_status mg_config_validate(const mg_config* cfg) {

@@ -103,8 +103,8 @@ class GcnConfig:
     overlap: bool = False
     skip_first_backward_spmm: bool = False
     order_swap: bool = False
-    gemm_mode: int = GEMM_EXACT
-    spmm_mode: int = SPMM_EXACT
+    gemm_mode: int = GEMM_TF32X3  # production default; GEMM_EXACT/SPMM_EXACT give bitwise parity
+    spmm_mode: int = SPMM_FAST
 
     def layers(self) -> int:
         return len(self.layer_dims) - 1
@@ -314,8 +314,7 @@ def nccl_unique_id() -> bytes:
 
 
 def device_count() -> int:
-    import torch  # plumbing only: device enumeration
-    return torch.cuda.device_count()
+    return int(lib().mg_device_count())
 
 
 class Group:

@@ -19,6 +19,13 @@ from paper_2110_08688_b200 import rowgcn as R  # noqa: E402
 TOL = 1e-4
 
 
+def cfgx(*a, **k):
+    """GcnConfig in the bitwise-parity modes unless a test asks for the tcgen05 / fast ones."""
+    k.setdefault("gemm_mode", R.GEMM_EXACT)
+    k.setdefault("spmm_mode", R.SPMM_EXACT)
+    return R.GcnConfig(*a, **k)
+
+
 def small_ds(golden):
     return (R.Dataset.from_arrays(golden["synth300_row_ptr"], golden["synth300_col_idx"], golden["synth300_values"],
                                   golden["synth300_features"], golden["synth300_labels"]),
@@ -41,7 +48,7 @@ def gather(g, which, layer, P):
 @pytest.mark.parametrize("overlap", [False, True])
 def test_forward_bitwise(golden, port32, P, overlap):
     ds, ods = small_ds(golden)
-    cfg = R.GcnConfig([12, 8, 6, 5], seed=5, permute=True, overlap=overlap)
+    cfg = cfgx([12, 8, 6, 5], seed=5, permute=True, overlap=overlap)
     m = port32.model(ods, [12, 8, 6, 5], P, seed=5, permute=True)
     ref = m.step(1, mode=2, dumps=True)["ahw_fwd"]
     with group(ds, cfg, P) as g:
@@ -53,7 +60,7 @@ def test_forward_bitwise(golden, port32, P, overlap):
 def test_step_dump_vs_reference(golden):
     """Teacher-forced train_step(1) on the small graph at P=2 vs the compiled reference's dump."""
     ds, _ = small_ds(golden)
-    cfg = R.GcnConfig([12, 8, 6, 5], seed=5, permute=True, overlap=True)
+    cfg = cfgx([12, 8, 6, 5], seed=5, permute=True, overlap=True)
     with group(ds, cfg, 2) as g:
         g.forward()
         for l in range(3):
@@ -77,7 +84,7 @@ def test_step_dump_vs_reference(golden):
 def test_c1_trajectory(golden, perm):
     """C1 Cora-shaped [1433,16,7], 5 epochs at P=1: losses vs the reference (f32 and f64 runs)."""
     ds = R.synth_graph(2708, 3.9, 0.7, 1, 1433, 7)
-    cfg = R.GcnConfig([1433, 16, 7], epochs=5, seed=1, permute=bool(perm))
+    cfg = cfgx([1433, 16, 7], epochs=5, seed=1, permute=bool(perm))
     art = R.train_run(ds, cfg, R.TrainOptions(workers=1, devices=[0]))
     ref32 = golden[f"c1_f32_perm{perm}_loss"]
     ref64 = golden[f"c1_f64_perm{perm}_loss"]
@@ -90,7 +97,7 @@ def test_c1_trajectory(golden, perm):
 def test_p_invariance_bitwise():
     """W after every step is bitwise identical for P in {1,2,4} (tests/test_gcn.cpp:323-348)."""
     ds = R.synth_graph(2000, 8.0, 0.5, 44, 16, 4)
-    cfg = R.GcnConfig([16, 16, 4], epochs=4, seed=17, permute=True, overlap=True)
+    cfg = cfgx([16, 16, 4], epochs=4, seed=17, permute=True, overlap=True)
     base = R.train_run(ds, cfg, R.TrainOptions(workers=1, devices=[0]))
     for P in (2, 4):
         dist = R.train_run(ds, cfg, R.TrainOptions(workers=P, devices=[0] * P, transport=R.TRANSPORT_LOCAL))
@@ -104,7 +111,7 @@ def test_p_invariance_bitwise():
 
 def test_overlap_on_equals_off():
     ds = R.synth_graph(600, 6.0, 0.6, 27, 4, 2)
-    cfg = R.GcnConfig([4, 6, 2], epochs=3, seed=15)
+    cfg = cfgx([4, 6, 2], epochs=3, seed=15)
     a = R.train_run(ds, cfg, R.TrainOptions(workers=4, devices=[0] * 4, transport=R.TRANSPORT_LOCAL))
     cfg.overlap = True
     b = R.train_run(ds, cfg, R.TrainOptions(workers=4, devices=[0] * 4, transport=R.TRANSPORT_LOCAL))
@@ -118,14 +125,14 @@ def test_identity_pipeline_and_cycle():
     rng = np.random.default_rng(5)
     x = rng.uniform(0, 1, (n, 3)).astype(np.float32)
     eye = R.Dataset.from_arrays(np.arange(n + 1), np.arange(n), np.ones(n, np.float32), x, np.zeros(n, np.int32))
-    cfg = R.GcnConfig([3, 3, 3])
+    cfg = cfgx([3, 3, 3])
     with group(eye, cfg, 2) as g:
         g.set_params([np.eye(3, dtype=np.float32)] * 2)
         g.forward()
         assert np.array_equal(gather(g, R.T_AHW, 1, 2), x)
     cyc = R.Dataset.from_arrays([0, 1, 2], [1, 0], np.ones(2, np.float32), np.array([[1.0], [2.0]], np.float32),
                                 np.zeros(2, np.int32))
-    with group(cyc, R.GcnConfig([1, 1]), 1) as g:
+    with group(cyc, cfgx([1, 1]), 1) as g:
         g.set_params([np.array([[3.0]], np.float32)])
         g.forward()
         assert list(g.read(R.T_AHW, 0).ravel()) == [6.0, 3.0]
@@ -134,7 +141,7 @@ def test_identity_pipeline_and_cycle():
 def test_buffer_plan_and_no_step_allocations():
     ds = R.synth_graph(400, 6.0, 0.6, 71, 5, 3)
     for dims in ([5, 3], [5, 6, 3], [5, 6, 6, 3]):
-        with group(ds, R.GcnConfig(dims, seed=3), 2) as g:
+        with group(ds, cfgx(dims, seed=3), 2) as g:
             lb, allocs0, _ = g.buffer_audit()
             assert lb == len(dims) - 1 + 3
             for t in (1, 2, 3):
@@ -145,14 +152,14 @@ def test_buffer_plan_and_no_step_allocations():
 def test_label_out_of_range_raises():
     ds = R.Dataset.from_arrays([0, 1, 2], [1, 0], np.ones(2, np.float32), np.ones((2, 2), np.float32),
                                np.array([0, 5], np.int32))
-    with group(ds, R.GcnConfig([2, 2]), 1) as g:
+    with group(ds, cfgx([2, 2]), 1) as g:
         with pytest.raises(R.ValueError, match="out of range"):
             g.train_step(1)
 
 
 def test_loss_only_keeps_logits_and_matches_train_loss():
     ds = R.synth_graph(500, 6.0, 0.6, 3, 8, 4)
-    cfg = R.GcnConfig([8, 8, 4], seed=2, permute=True)
+    cfg = cfgx([8, 8, 4], seed=2, permute=True)
     with group(ds, cfg, 2) as g:
         l0 = g.loss_only()
         logits = gather(g, R.T_AHW, 1, 2)
@@ -166,7 +173,7 @@ def test_loss_only_keeps_logits_and_matches_train_loss():
 def test_step_dump_tcgen05(golden, mode, tol):
     """The same teacher-forced step with the tcgen05 GeMMs: every tensor within the stated tolerance."""
     ds, _ = small_ds(golden)
-    cfg = R.GcnConfig([12, 8, 6, 5], seed=5, permute=True, overlap=True, gemm_mode=mode)
+    cfg = cfgx([12, 8, 6, 5], seed=5, permute=True, overlap=True, gemm_mode=mode)
     with group(ds, cfg, 2) as g:
         g.forward()
         for l in range(3):
@@ -186,7 +193,7 @@ def test_step_dump_tcgen05(golden, mode, tol):
 
 def test_c1_trajectory_tcgen05(golden):
     ds = R.synth_graph(2708, 3.9, 0.7, 1, 1433, 7)
-    cfg = R.GcnConfig([1433, 16, 7], epochs=5, seed=1, permute=True, gemm_mode=R.GEMM_TF32X3)
+    cfg = cfgx([1433, 16, 7], epochs=5, seed=1, permute=True, gemm_mode=R.GEMM_TF32X3)
     art = R.train_run(ds, cfg, R.TrainOptions(workers=1, devices=[0]))
     ref64 = golden["c1_f64_perm1_loss"]
     for e in range(5):
@@ -197,7 +204,7 @@ def test_p_invariance_bitwise_tcgen05():
     """The tcgen05 path is deterministic and row-local, and the W-grad split-K chunks are fixed relative to the
     canonical blocks, so the W trajectory stays bitwise P-invariant in TF32X3 mode too."""
     ds = R.synth_graph(9000, 8.0, 0.5, 44, 16, 4)
-    cfg = R.GcnConfig([16, 32, 4], epochs=3, seed=17, permute=True, overlap=True, gemm_mode=R.GEMM_TF32X3)
+    cfg = cfgx([16, 32, 4], epochs=3, seed=17, permute=True, overlap=True, gemm_mode=R.GEMM_TF32X3)
     base = R.train_run(ds, cfg, R.TrainOptions(workers=1, devices=[0]))
     for P in (2, 4):
         dist = R.train_run(ds, cfg, R.TrainOptions(workers=P, devices=[0] * P, transport=R.TRANSPORT_LOCAL))
@@ -211,7 +218,7 @@ def test_fast_modes_trajectory_and_determinism(golden):
     run-to-run bitwise deterministic, and W bitwise P-invariant when no row is split (P-invariance with
     hub segments holds up to the segment boundaries, which depend on the tile)."""
     ds = R.synth_graph(2708, 3.9, 0.7, 1, 1433, 7)
-    cfg = R.GcnConfig([1433, 16, 7], epochs=5, seed=1, permute=True, gemm_mode=R.GEMM_TF32X3,
+    cfg = cfgx([1433, 16, 7], epochs=5, seed=1, permute=True, gemm_mode=R.GEMM_TF32X3,
                       spmm_mode=R.SPMM_FAST)
     a = R.train_run(ds, cfg, R.TrainOptions(workers=1, devices=[0]))
     b = R.train_run(ds, cfg, R.TrainOptions(workers=1, devices=[0]))
@@ -226,7 +233,7 @@ def test_fast_modes_trajectory_and_determinism(golden):
 
 def test_step_dump_fast_spmm(golden):
     ds, _ = small_ds(golden)
-    cfg = R.GcnConfig([12, 8, 6, 5], seed=5, permute=True, overlap=True, gemm_mode=R.GEMM_TF32X3,
+    cfg = cfgx([12, 8, 6, 5], seed=5, permute=True, overlap=True, gemm_mode=R.GEMM_TF32X3,
                       spmm_mode=R.SPMM_FAST)
     R.set_tuning("heavy_row", 8)  # force hub segments on this small graph
     R.set_tuning("fast_segment", 32)
