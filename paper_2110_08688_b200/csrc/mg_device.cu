@@ -43,7 +43,14 @@ inline int ceil_div(index_t a, index_t b) { return static_cast<int>((a + b - 1) 
 
 std::atomic<int> g_heavy_row{4096};
 std::atomic<int> g_profile{0};
+std::atomic<int> g_spmm_slab{0};  // floats per column-slab pass of the SpMM (0 = the whole width, <= 1024)
 int heavy_threshold() { return g_heavy_row.load(); }
+// float4 chunks per SpMM launch: each launch walks every row's nonzeros for one column slab, so a slab of
+// the gathered matrix (rows x slab x 4 B) can stay L2-resident while the edge stream passes through.
+int slab_chunks() {
+  const int s = g_spmm_slab.load();
+  return s > 0 ? std::max(1, std::min(256, s / 4)) : 256;
+}
 
 int num_sms() {
   int dev = 0, sms = 148;
@@ -138,8 +145,9 @@ static void launch_rows(const SpmmLaunch& t, const float* h, float* out, int ld,
 static int spmm_light(const SpmmLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, cudaStream_t s) {
   const int nchunk_all = static_cast<int>(ld / 4);
   int launches = 0;
-  for (int c0 = 0; c0 < nchunk_all; c0 += 256) {
-    const int nchunk = std::min(256, nchunk_all - c0);
+  const int step = slab_chunks();
+  for (int c0 = 0; c0 < nchunk_all; c0 += step) {
+    const int nchunk = std::min(step, nchunk_all - c0);
     const float* hs = h + 4 * c0;
     float* os = out + 4 * c0;
     const int L = static_cast<int>(ld);
@@ -183,8 +191,9 @@ static int spmm_fast(const FastLaunch& t, const float* h, float* out, index_t ld
   int launches = 0;
   const int nchunk_all = static_cast<int>(ld / 4);
   if (t.n_items > 0) {
-    for (int c0 = 0; c0 < nchunk_all; c0 += 256) {
-      const int nchunk = std::min(256, nchunk_all - c0);
+    const int step = slab_chunks();
+    for (int c0 = 0; c0 < nchunk_all; c0 += step) {
+      const int nchunk = std::min(step, nchunk_all - c0);
       const float* hs = h + 4 * c0;
       float* os = out + 4 * c0;
       float* ss = t.scratch ? t.scratch + 4 * c0 : nullptr;
@@ -768,6 +777,9 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
       g_heavy_row = static_cast<int>(std::min<int64_t>(value, 1 << 30));
     } else if (k == "profile") {
       g_profile = value != 0 ? 1 : 0;
+    } else if (k == "spmm_slab") {
+      if (value < 0 || value % 4) throw ValueError("tuning: spmm_slab must be 0 or a multiple of 4 floats");
+      g_spmm_slab = static_cast<int>(std::min<int64_t>(value, 1024));
     } else if (k == "fast_segment") {
       if (value < 32) throw ValueError("tuning: fast_segment must be >= 32");
       g_fast_segment = static_cast<int>(std::min<int64_t>(value, 1 << 24));

@@ -29,6 +29,21 @@ __device__ __forceinline__ void axpy4(float4& acc, float v, const float4& x) {
 }
 __device__ __forceinline__ float relu1(float x) { return x > 0.0f ? x : 0.0f; }  // dense.hpp:214
 
+// Edge records are streamed once per (column-slab) pass: mark them evict-first in L2 so they do not
+// displace the h rows being gathered (which are what L2 reuse is for).
+__device__ __forceinline__ int2 ld_edge(const int2* p) {
+  int2 v;
+  asm volatile(
+      "{\n"
+      ".reg .b64 pol;\n"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v2.s32 {%0, %1}, [%2], pol;\n"
+      "}\n"
+      : "=r"(v.x), "=r"(v.y)
+      : "l"(p));
+  return v;
+}
+
 // ============================================================================ SpMM (exact)
 // One row per group of G lanes (G | 32); lane l of the group owns the float4 column chunks
 // c = l + k*G (k < CPL). Every output element is a left fold over the row's nonzeros in column
@@ -60,7 +75,7 @@ __global__ void __launch_bounds__(256) spmm_exact_rows(const int* __restrict__ r
     }
     for (int base = e0; base < e1; base += G) {
       const int cnt = min(G, e1 - base);
-      const int2 my = lane < cnt ? __ldg(edges + base + lane) : make_int2(0, 0);
+      const int2 my = lane < cnt ? ld_edge(edges + base + lane) : make_int2(0, 0);
       int j = 0;
       for (; j + U <= cnt; j += U) {
         float4 x[U][CPL];
@@ -143,7 +158,7 @@ __global__ void __launch_bounds__(256) spmm_fast_items(const int4* __restrict__ 
     }
     for (int base = e0; base < e1; base += G) {
       const int cnt = min(G, e1 - base);
-      const int2 my = lane < cnt ? __ldg(edges + base + lane) : make_int2(0, 0);
+      const int2 my = lane < cnt ? ld_edge(edges + base + lane) : make_int2(0, 0);
       int j = 0;
       for (; j + U <= cnt; j += U) {
         float4 x[U][CPL];

@@ -1,0 +1,43 @@
+"""Launch-geometry knobs must not change results: the column-slab SpMM keeps every output element's
+fold order, so exact mode stays bitwise and fast mode stays identical to its unslabbed self."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+from test_gpu_kernels import random_tile, run_spmm  # noqa: E402
+from gpu_util import bits_equal  # noqa: E402
+
+from paper_2110_08688_b200 import rowgcn as R  # noqa: E402
+
+
+@pytest.mark.parametrize("slab", [4, 8, 16, 64])
+@pytest.mark.parametrize("w", [8, 47, 256])
+def test_spmm_slab_exact_bitwise(port32, slab, w):
+    rng = np.random.default_rng(slab * 7 + w)
+    rows, cols = 200, 400
+    rp, ci, v = random_tile(rng, rows, cols, 0.03)
+    h = rng.uniform(-1, 1, (cols, w)).astype(np.float32)
+    o0 = rng.uniform(-1, 1, (rows, w)).astype(np.float32)
+    ref = port32.spmm(rows, cols, rp, ci, v, h, True, o0)
+    R.set_tuning("spmm_slab", slab)
+    try:
+        exact = run_spmm(rp, ci, v, h, True, o0)
+        fast = run_spmm(rp, ci, v, h, True, o0, mode=R.SPMM_FAST)
+    finally:
+        R.set_tuning("spmm_slab", 0)
+    assert bits_equal(exact, ref)
+    assert bits_equal(fast, run_spmm(rp, ci, v, h, True, o0, mode=R.SPMM_FAST))
+
+
+def test_slab_training_equals_default():
+    ds = R.synth_graph(3000, 10.0, 0.7, 2, 12, 5)
+    cfg = R.GcnConfig([12, 40, 5], epochs=3, seed=2, permute=True)
+    a = R.train_run(ds, cfg, R.TrainOptions(devices=[0]))
+    R.set_tuning("spmm_slab", 8)
+    try:
+        b = R.train_run(ds, cfg, R.TrainOptions(devices=[0]))
+    finally:
+        R.set_tuning("spmm_slab", 0)
+    assert a.epoch_loss == b.epoch_loss and a.w_hashes == b.w_hashes
