@@ -44,6 +44,8 @@ inline int ceil_div(index_t a, index_t b) { return static_cast<int>((a + b - 1) 
 std::atomic<int> g_heavy_row{4096};
 std::atomic<int> g_profile{0};
 std::atomic<int> g_spmm_slab{0};  // floats per column-slab pass of the SpMM (0 = the whole width, <= 1024)
+std::atomic<int> g_narrow_group{0};  // lanes per row for widths of 33..64 floats (0 = 16, or 4 / 8)
+int narrow_group() { return g_narrow_group.load(); }
 int heavy_threshold() { return g_heavy_row.load(); }
 // float4 chunks per SpMM launch: each launch walks every row's nonzeros for one column slab, so a slab of
 // the gathered matrix (rows x slab x 4 B) can stay L2-resident while the edge stream passes through.
@@ -155,6 +157,8 @@ static int spmm_light(const SpmmLaunch& t, const float* h, float* out, index_t l
     else if (nchunk <= 2) launch_rows<2, 1>(t, hs, os, L, nchunk, acc, relu, s);
     else if (nchunk <= 4) launch_rows<4, 1>(t, hs, os, L, nchunk, acc, relu, s);
     else if (nchunk <= 8) launch_rows<8, 1>(t, hs, os, L, nchunk, acc, relu, s);
+    else if (nchunk <= 16 && narrow_group() == 4 && nchunk <= 12) launch_rows<4, 3>(t, hs, os, L, nchunk, acc, relu, s);
+    else if (nchunk <= 16 && narrow_group() == 8) launch_rows<8, 2>(t, hs, os, L, nchunk, acc, relu, s);
     else if (nchunk <= 16) launch_rows<16, 1>(t, hs, os, L, nchunk, acc, relu, s);
     else if (nchunk <= 32) launch_rows<32, 1>(t, hs, os, L, nchunk, acc, relu, s);
     else if (nchunk <= 64) launch_rows<32, 2>(t, hs, os, L, nchunk, acc, relu, s);
@@ -202,6 +206,8 @@ static int spmm_fast(const FastLaunch& t, const float* h, float* out, index_t ld
       else if (nchunk <= 2) launch_fast<2, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
       else if (nchunk <= 4) launch_fast<4, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
       else if (nchunk <= 8) launch_fast<8, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      else if (nchunk <= 12 && narrow_group() == 4) launch_fast<4, 3>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      else if (nchunk <= 16 && narrow_group() == 8) launch_fast<8, 2>(t, hs, os, ss, L, nchunk, acc, relu, s);
       else if (nchunk <= 16) launch_fast<16, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
       else if (nchunk <= 32) launch_fast<32, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
       else if (nchunk <= 64) launch_fast<32, 2>(t, hs, os, ss, L, nchunk, acc, relu, s);
@@ -777,6 +783,9 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
       g_heavy_row = static_cast<int>(std::min<int64_t>(value, 1 << 30));
     } else if (k == "profile") {
       g_profile = value != 0 ? 1 : 0;
+    } else if (k == "spmm_narrow_group") {
+      if (value != 0 && value != 4 && value != 8) throw ValueError("tuning: spmm_narrow_group must be 0, 4 or 8");
+      g_narrow_group = static_cast<int>(value);
     } else if (k == "spmm_slab") {
       if (value < 0 || value % 4) throw ValueError("tuning: spmm_slab must be 0 or a multiple of 4 floats");
       g_spmm_slab = static_cast<int>(std::min<int64_t>(value, 1024));

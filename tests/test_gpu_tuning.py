@@ -31,6 +31,26 @@ def test_spmm_slab_exact_bitwise(port32, slab, w):
     assert bits_equal(fast, run_spmm(rp, ci, v, h, True, o0, mode=R.SPMM_FAST))
 
 
+@pytest.mark.parametrize("group", [4, 8])
+@pytest.mark.parametrize("w", [36, 47, 48, 64])
+def test_spmm_narrow_group_variants(port32, group, w):
+    rng = np.random.default_rng(group + w)
+    rows, cols = 300, 500
+    rp, ci, v = random_tile(rng, rows, cols, 0.02)
+    h = rng.uniform(-1, 1, (cols, w)).astype(np.float32)
+    o0 = rng.uniform(-1, 1, (rows, w)).astype(np.float32)
+    ref = port32.spmm(rows, cols, rp, ci, v, h, True, o0)
+    base_fast = run_spmm(rp, ci, v, h, True, o0, mode=R.SPMM_FAST)
+    R.set_tuning("spmm_narrow_group", group)
+    try:
+        exact = run_spmm(rp, ci, v, h, True, o0)
+        fast = run_spmm(rp, ci, v, h, True, o0, mode=R.SPMM_FAST)
+    finally:
+        R.set_tuning("spmm_narrow_group", 0)
+    assert bits_equal(exact, ref)
+    assert bits_equal(fast, base_fast)
+
+
 def test_slab_training_equals_default():
     ds = R.synth_graph(3000, 10.0, 0.7, 2, 12, 5)
     cfg = R.GcnConfig([12, 40, 5], epochs=3, seed=2, permute=True)
