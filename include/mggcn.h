@@ -82,7 +82,11 @@ const char* mg_last_error(void);
 int32_t mg_abi_version(void);
 /* Process-wide tuning knobs (no reference analogue; defaults in DESIGN.md):
  *   "heavy_row"  nonzeros from which a tile row takes the cp.async hub-row SpMM path (default 4096)
- *   "profile"    1 = record per-kernel CUDA events during steps (mg_group_last_profile). */
+ *   "profile"    1 = record per-kernel CUDA events during steps (mg_group_last_profile)
+ *   "tn_chunk"   W-grad split-K chunk in rows (multiple of 256, default 4096)
+ *   "fast_segment"  hub-row segment length of MG_SPMM_FAST (default 2048)
+ *   "spmm_slab" / "spmm_narrow_group"  SpMM launch-geometry experiments (default 0 = off)
+ *   "gemm_kernel"  tcgen05 GeMM variant: 1 = both split operands in smem, 2 = A split into TMEM (default). */
 mg_status mg_set_tuning(const char* key, int64_t value);
 
 /* ---------------------------------------------------------------- host datasets

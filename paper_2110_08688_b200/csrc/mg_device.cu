@@ -794,6 +794,8 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
       g_fast_segment = static_cast<int>(std::min<int64_t>(value, 1 << 24));
     } else if (k == "tn_chunk") {
       tc::set_tn_chunk(static_cast<int>(value));
+    } else if (k == "gemm_kernel") {
+      tc::set_gemm_version(static_cast<int>(value));
     } else {
       throw ValueError("tuning: unknown key '" + k + "'");
     }
@@ -935,7 +937,8 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
           kmax = std::max(kmax, e - a);
         }
         for (int l = 0; l < L; ++l)
-          w.ws_bytes = std::max(w.ws_bytes, tc::tn_workspace_bytes(g->ld[l], g->ld[l + 1], std::max<index_t>(1, w.rows)));
+          w.ws_bytes = std::max({w.ws_bytes, tc::tn_workspace_bytes(g->ld[l], g->ld[l + 1], std::max<index_t>(1, w.rows)),
+                                 tc::nn_workspace_bytes(g->ld[l + 1], g->ld[l])});
         w.ws = static_cast<float*>(dalloc(*g, w, w.ws_bytes));
       }
       w.loss_blocks = std::max(1, std::min(ceil_div(w.rows, 8), num_sms() * 8));
@@ -1304,8 +1307,8 @@ mg_status mg_dev_gemm(int32_t ta, int32_t tb, int64_t M, int64_t N, int64_t K, c
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     float* ws = nullptr;
     size_t wsb = 0;
-    if (ta && mode != MG_GEMM_EXACT) {
-      wsb = tc::tn_workspace_bytes(M, N, std::max<int64_t>(K, 1));
+    if (mode != MG_GEMM_EXACT) {
+      wsb = ta ? tc::tn_workspace_bytes(M, N, std::max<int64_t>(K, 1)) : tc::nn_workspace_bytes(N, K);
       MG_CUDA(cudaMalloc(&ws, wsb));
     }
     gemm_launch(mode, ta != 0, tb != 0, M, N, K, A, lda, B, ldb, Cm, ldc, epilogue, st, ws, wsb);

@@ -418,6 +418,282 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(const __grid_constant__ C
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tmem_cols));
 }
 
+// ================================================================ v2: A operand in TMEM ("TS" MMAs)
+// Same pipeline, but the split A operand never goes back to shared memory: the four split warps own
+// the 128 TMEM lanes (= tile rows) and write A_hi / A_lo of each 16-deep K block straight into a TMEM
+// stage with tcgen05.st; the MMA reads A from TMEM and only B from smem. For NN / NT the B operand (W)
+// is split and laid out K-major once per call (split_b), so its hi / lo tiles arrive by TMA ready to use.
+// Shared-memory traffic per K block drops from ~168 KB to ~96 KB (N = 256), below the tensor-core time.
+// TMEM: accumulators in columns [0, 256) (two of 128 when N <= 128, else one of 256), A stages in
+// [256, 256 + 32 * nst).
+constexpr int kAcol = 256;
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};\n" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
+
+// W (padded ld) -> B_hi / B_lo, K-major (np x kp): NN reads W as K x N (transpose), NT as N x K.
+__global__ void split_b(const float* __restrict__ W, long ldw, int trans, int np, int kp, long nvalid, long kvalid,
+                        int terms, float* __restrict__ hi, float* __restrict__ lo) {
+  const long total = static_cast<long>(np) * kp;
+  for (long i = static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<long>(gridDim.x) * blockDim.x) {
+    const long n = i / kp, k = i % kp;
+    float x = 0.0f;
+    if (n < nvalid && k < kvalid) x = trans ? W[k * ldw + n] : W[n * ldw + k];
+    const float h = terms == 3 ? __uint_as_float(__float_as_uint(x) & 0xFFFFE000u) : x;
+    hi[i] = h;
+    lo[i] = terms == 3 ? __fsub_rn(x, h) : 0.0f;
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ CUtensorMap map_a,
+                                                        const __grid_constant__ CUtensorMap map_bh,
+                                                        const __grid_constant__ CUtensorMap map_bl, Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t full[kMaxStages], conv[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr bool B_MN = MODE == TN;  // NN/NT read the pre-split K-major B
+  const int a_bytes = BM * BK * 4;    // raw A tile (no swizzle): NN/NT [128 rows][16 k], TN [16 k][128 m]
+  const int b_bytes = p.npb * BK * 4;
+  const int stage = a_bytes + 2 * b_bytes;  // A raw | B hi | B lo
+  const int nacc = p.np <= 128 ? 2 : 1;
+  const int tstride = nacc == 2 ? 128 : 256;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < p.nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&conv[s], 4);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_bh)) : "memory");
+    if (MODE != TN) asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_bl)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      uint32_t sc = 0;
+      const uint32_t tx = static_cast<uint32_t>(MODE == TN ? a_bytes + b_bytes : stage);
+      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+        const Item I = item_of(p, MODE, it);
+        for (int kb = 0; kb < I.nkb; ++kb, ++sc) {
+          const int s = sc % p.nst;
+          if (sc >= static_cast<uint32_t>(p.nst)) mbar_wait(&empty[s], ((sc / p.nst) - 1) & 1);
+          uint8_t* a = smem + s * stage;
+          uint8_t* b = a + a_bytes;
+          mbar_arrive_tx(&full[s], tx);
+          if (MODE == TN) {
+            const int k0 = static_cast<int>(I.row0) + kb * BK;
+            tma_load_2d(a, &map_a, I.mt * BM, k0, &full[s]);
+            for (int j = 0; j < p.npb / 32; ++j) tma_load_2d(b + j * 2048, &map_bh, j * 32, k0, &full[s]);
+          } else {
+            const int k0 = kb * BK;
+            tma_load_2d(a, &map_a, k0, static_cast<int>(I.row0), &full[s]);
+            tma_load_2d(b, &map_bh, k0, 0, &full[s]);
+            tma_load_2d(b + b_bytes, &map_bl, k0, 0, &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (A from TMEM)
+    const uint32_t idesc = idesc_tf32(BM, p.np, 0, B_MN ? 1 : 0);
+    uint32_t sc = 0, ac = 0;
+    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+      const Item I = item_of(p, MODE, it);
+      const int groups = MODE == TN ? (I.nkb + kPromoteKb - 1) / kPromoteKb : 1;
+      for (int gi = 0; gi < groups; ++gi, ++ac) {
+        const int kb0 = MODE == TN ? gi * kPromoteKb : 0;
+        const int kb1 = MODE == TN ? min(I.nkb, kb0 + kPromoteKb) : I.nkb;
+        const int buf = static_cast<int>(ac % nacc);
+        if (ac >= static_cast<uint32_t>(nacc)) mbar_wait(&tempty[buf], ((ac / nacc) - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + static_cast<uint32_t>(buf * tstride);
+        for (int kb = kb0; kb < kb1; ++kb, ++sc) {
+          const int s = sc % p.nst;
+          mbar_wait(&conv[s], (sc / p.nst) & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t bh = smem_u32(smem + s * stage + a_bytes), bl = bh + b_bytes;
+            const uint32_t ah = tmem + static_cast<uint32_t>(kAcol + s * 32), al = ah + 16;
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk) {
+              const uint32_t bo = B_MN ? kk * 1024 : kk * 32;
+              const uint64_t dbh = B_MN ? desc_mn128(bh + bo) : desc_k64(bh + bo);
+              const uint32_t first = (kb == kb0 && kk == 0) ? 0u : 1u;
+              if (p.terms == 3) {
+                const uint64_t dbl = B_MN ? desc_mn128(bl + bo) : desc_k64(bl + bo);
+                mma_tf32_ts(d, al + kk * 8, dbh, idesc, first);
+                mma_tf32_ts(d, ah + kk * 8, dbl, idesc, 1u);
+                mma_tf32_ts(d, ah + kk * 8, dbh, idesc, 1u);
+              } else {
+                mma_tf32_ts(d, ah + kk * 8, dbh, idesc, first);
+              }
+            }
+            mma_commit(&empty[s]);
+          }
+          __syncwarp();
+        }
+        if (lane == 0) mma_commit(&tfull[buf]);
+        __syncwarp();
+      }
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ split A into TMEM (+ split B for TN)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int t = threadIdx.x - 64;
+    uint32_t sc = 0;
+    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+      const Item I = item_of(p, MODE, it);
+      for (int kb = 0; kb < I.nkb; ++kb, ++sc) {
+        const int s = sc % p.nst;
+        mbar_wait(&full[s], (sc / p.nst) & 1);  // also implies the MMAs of this stage's last use are done
+        const float* araw = reinterpret_cast<const float*>(smem + s * stage);
+        float x[BK];
+        if (MODE == TN) {
+          const int valid = static_cast<int>(min(static_cast<long>(BK), I.k_end - (I.row0 + kb * BK)));
+#pragma unroll
+          for (int k = 0; k < BK; ++k) x[k] = k < valid ? araw[k * BM + row] : 0.0f;
+        } else {
+#pragma unroll
+          for (int k4 = 0; k4 < BK / 4; ++k4) {
+            const float4 v = reinterpret_cast<const float4*>(araw + row * BK)[k4];
+            x[4 * k4] = v.x;
+            x[4 * k4 + 1] = v.y;
+            x[4 * k4 + 2] = v.z;
+            x[4 * k4 + 3] = v.w;
+          }
+        }
+        uint32_t hi[BK], lo[BK];
+#pragma unroll
+        for (int k = 0; k < BK; ++k) {
+          const float h = p.terms == 3 ? __uint_as_float(__float_as_uint(x[k]) & 0xFFFFE000u) : x[k];
+          hi[k] = __float_as_uint(h);
+          lo[k] = __float_as_uint(__fsub_rn(x[k], h));
+        }
+        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(kAcol + s * 32);
+        tmem_st16(ta, hi);
+        if (p.terms == 3) tmem_st16(ta + 16, lo);
+        if (MODE == TN && p.terms == 3) {  // B = G rows: split in place in smem (hi) + lo copy
+          uint8_t* bh = smem + s * stage + a_bytes;
+          uint8_t* bl = bh + b_bytes;
+          for (int q4 = t; q4 < b_bytes / 16; q4 += 128) {
+            float4 l;
+            const float4 h = split4(reinterpret_cast<float4*>(bh)[q4], l);
+            reinterpret_cast<float4*>(bh)[q4] = h;
+            reinterpret_cast<float4*>(bl)[q4] = l;
+          }
+          fence_async_smem();
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (as v1)
+    const int q = warp & 3;
+    uint32_t ac = 0;
+    float* stg = reinterpret_cast<float*>(smem + p.nst * stage) + q * (32 * 33);
+    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+      const Item I = item_of(p, MODE, it);
+      const int groups = MODE == TN ? (I.nkb + kPromoteKb - 1) / kPromoteKb : 1;
+      for (int gi = 0; gi < groups; ++gi, ++ac) {
+        const int buf = static_cast<int>(ac % nacc);
+        mbar_wait(&tfull[buf], (ac / nacc) & 1);
+        tc_fence_after();
+        const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf * tstride);
+        for (int c0 = 0; c0 < p.np; c0 += 32) {
+          float v[32];
+          tmem_ld32(tbase + c0, v);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
+          __syncwarp();
+          const int c = c0 + lane;
+          if (MODE == TN) {
+            if (c < p.npb) {
+              float* dst = p.partial + (static_cast<long>(it) * BM + q * 32) * p.npb + c;
+              float prev[32];
+              if (gi > 0) {
+#pragma unroll
+                for (int r = 0; r < 32; ++r) prev[r] = dst[static_cast<long>(r) * p.npb];
+              }
+#pragma unroll
+              for (int r = 0; r < 32; ++r) {
+                float xv = stg[r * 33 + lane];
+                if (gi > 0) xv = __fadd_rn(prev[r], xv);
+                dst[static_cast<long>(r) * p.npb] = xv;
+              }
+            }
+          } else if (c < p.N) {
+            const long g0 = I.row0 + q * 32;
+            const int nrows = static_cast<int>(min(32L, p.M - g0));
+            float* dst = p.C + g0 * p.ldc + c;
+            float old[32];
+            if (p.epi == 1) {
+#pragma unroll
+              for (int r = 0; r < 32; ++r) old[r] = r < nrows ? dst[static_cast<long>(r) * p.ldc] : 0.0f;
+            }
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+              if (r < nrows) {
+                float xv = stg[r * 33 + lane];
+                if (p.epi == 1) xv = old[r] > 0.0f ? xv : 0.0f;
+                if (p.epi == 2) xv = xv > 0.0f ? xv : 0.0f;
+                dst[static_cast<long>(r) * p.ldc] = xv;
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[buf]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
 // Fixed-order sum of the TN partials of every block: stage[g][m][n] = 0 + p_0 + p_1 + ... (chunk order).
 __global__ void reduce_partials(Params p, float* __restrict__ stage, long block_stride) {
   const long per = p.M * p.N;
@@ -504,7 +780,43 @@ void check_ptr(const void* p, long ld, const char* what) {
     throw ValueError(std::string("tc gemm: ") + what + " must be 16-byte aligned with ld % 4 == 0");
 }
 
+// ---- v2 (A in TMEM) host side
+int g_gemm_version = 2;
+
+void finish_params2(Params& p, long N, bool tn, int terms) {
+  p.np = static_cast<int>((N + 15) / 16 * 16);
+  p.npb = tn ? (p.np + 31) / 32 * 32 : p.np;
+  p.tstride = 0;
+  p.terms = terms;
+  const int stage = BM * BK * 4 + 2 * p.npb * BK * 4;
+  p.nst = std::max(2, std::min(kMaxStages, kSmemBudget / stage));
+}
+
+inline int smem_bytes2(const Params& p) { return p.nst * (BM * BK * 4 + 2 * p.npb * BK * 4) + kEpiSmem + 1024; }
+
+template <int MODE>
+void launch2(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const Params& p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    TC_CUDA(cudaFuncSetAttribute(gemm_tc2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemBudget + kEpiSmem + 1024));
+    attr = true;
+  }
+  const int grid = std::max(1, std::min(p.n_items, num_sms()));
+  gemm_tc2<MODE><<<grid, kThreads, smem_bytes2(p), s>>>(a, bh, bl, p);
+  TC_CUDA(cudaGetLastError());
+}
+
 }  // namespace
+
+size_t nn_workspace_bytes(int64_t N, int64_t K) {
+  return 2 * sizeof(float) * static_cast<size_t>((N + 15) / 16 * 16) * static_cast<size_t>((K + 3) / 4 * 4);
+}
+
+void set_gemm_version(int v) {
+  if (v != 1 && v != 2) throw ValueError("tuning: gemm_kernel must be 1 (SS) or 2 (A in TMEM)");
+  g_gemm_version = v;
+}
 
 bool available() { return true; }
 
@@ -540,6 +852,27 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
   p.C = C;
   p.ldc = ldc;
   p.epi = epi;
+  if (g_gemm_version == 2) {
+    finish_params2(p, N, false, mode == MG_GEMM_TF32X3 ? 3 : 1);
+    p.m_tiles = static_cast<int>((M + BM - 1) / BM);
+    p.n_items = p.m_tiles;
+    const int kp = static_cast<int>((K + 3) / 4 * 4);
+    if (!ws || ws_bytes < nn_workspace_bytes(N, K)) throw ValueError("tc gemm: B split workspace too small");
+    float* bh = ws;
+    float* bl = ws + static_cast<size_t>(p.np) * kp;
+    const long tot = static_cast<long>(p.np) * kp;
+    split_b<<<static_cast<int>(std::min<long>(1024, (tot + 255) / 256)), 256, 0, s>>>(B, ldb, tb ? 0 : 1, p.np, kp, N, K,
+                                                                                       p.terms, bh, bl);
+    TC_CUDA(cudaGetLastError());
+    const CUtensorMap ma = make_map(A, K, M, lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const CUtensorMap mbh = make_map(bh, kp, p.np, kp, BK, p.np, CU_TENSOR_MAP_SWIZZLE_64B);
+    const CUtensorMap mbl = make_map(bl, kp, p.np, kp, BK, p.np, CU_TENSOR_MAP_SWIZZLE_64B);
+    if (!tb)
+      launch2<NN>(ma, mbh, mbl, p, s);
+    else
+      launch2<NT>(ma, mbh, mbl, p, s);
+    return 2;
+  }
   finish_params(p, N, !tb, mode == MG_GEMM_TF32X3 ? 3 : 1);
   p.m_tiles = static_cast<int>((M + BM - 1) / BM);
   p.n_items = p.m_tiles;
@@ -588,7 +921,10 @@ int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* l
   p.N = N;
   p.C = stage;
   p.ldc = ldc;
-  finish_params(p, N, true, mode == MG_GEMM_TF32X3 ? 3 : 1);
+  if (g_gemm_version == 2)
+    finish_params2(p, N, true, mode == MG_GEMM_TF32X3 ? 3 : 1);
+  else
+    finish_params(p, N, true, mode == MG_GEMM_TF32X3 ? 3 : 1);
   p.m_tiles = static_cast<int>((M + BM - 1) / BM);
   p.chunk_rows = g_split_rows;
   p.nblocks = nblocks;
@@ -607,9 +943,14 @@ int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* l
   p.partial = ws;
   int kernels = 0;
   if (p.n_items > 0) {
-    const CUtensorMap ma = make_map(H, M, rows_hi, ldh, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     const CUtensorMap mb = make_map(G, N, rows_hi, ldg, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    launch<TN>(ma, mb, p, s);
+    if (g_gemm_version == 2) {  // A = H rows land raw ([16 k][128 m]) and go to TMEM transposed per lane
+      const CUtensorMap ma = make_map(H, M, rows_hi, ldh, BM, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
+      launch2<TN>(ma, mb, mb, p, s);
+    } else {
+      const CUtensorMap ma = make_map(H, M, rows_hi, ldh, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+      launch<TN>(ma, mb, p, s);
+    }
     ++kernels;
   }
   const long total = M * N * nblocks;

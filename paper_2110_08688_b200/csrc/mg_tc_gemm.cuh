@@ -19,6 +19,9 @@ size_t tn_workspace_bytes(int64_t M, int64_t N, int64_t K);
 int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* len, int64_t M, int64_t N,
                    const float* H, int64_t ldh, const float* G, int64_t ldg, float* stage, int64_t ldc,
                    int64_t block_stride, float* ws, size_t ws_bytes, cudaStream_t s);
-void set_tn_chunk(int rows);  // TN split-K chunk length (rows, multiple of 32); set before creating groups
+// NN / NT (v2 kernel) pre-split W into K-major hi/lo planes: nn_workspace_bytes(N, K).
+size_t nn_workspace_bytes(int64_t N, int64_t K);
+void set_tn_chunk(int rows);
+void set_gemm_version(int v);  // 1 = both operands in smem (SS), 2 = A split into TMEM (TS, default)  // TN split-K chunk length (rows, multiple of 32); set before creating groups
 }  // namespace tc
 }  // namespace mg

@@ -134,7 +134,8 @@ TC_SHAPES = [(1000, 256, 100), (777, 256, 256), (130, 48, 256), (300, 256, 47), 
 @pytest.mark.parametrize("mode,tol", [(R.GEMM_TF32X3, 1e-5), (R.GEMM_TF32, 5e-3)])
 @pytest.mark.parametrize("shape", TC_SHAPES)
 @pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False)])
-def test_gemm_tcgen05(shape, ta, tb, mode, tol):
+@pytest.mark.parametrize("kernel", [1, 2])  # 1: both operands split in smem (SS); 2: A split into TMEM (TS)
+def test_gemm_tcgen05(gemm_kernel, shape, ta, tb, mode, tol):
     from gpu_util import normwise
     m, n, k = shape
     if ta:  # W-grad shape: M, N = layer widths, K = rows (exercise several 4096-row split-K chunks)
@@ -154,7 +155,15 @@ def test_gemm_tcgen05(shape, ta, tb, mode, tol):
         assert np.all(got2 >= 0) and normwise(got2, np.maximum(ref, 0)) <= tol
 
 
-def test_gemm_tcgen05_deterministic():
+@pytest.fixture
+def gemm_kernel(kernel):
+    R.set_tuning("gemm_kernel", kernel)
+    yield kernel
+    R.set_tuning("gemm_kernel", 2)
+
+
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_gemm_tcgen05_deterministic(gemm_kernel):
     rng = np.random.default_rng(5)
     a = rng.normal(size=(20000, 256)).astype(np.float32)
     b = rng.normal(size=(20000, 47)).astype(np.float32)
