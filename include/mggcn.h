@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define MG_ABI_VERSION 1
+#define MG_ABI_VERSION 2
 
 typedef enum mg_status {
   MG_OK = 0,
@@ -69,6 +69,11 @@ typedef struct mg_config {
   uint8_t permute, overlap, skip_first_backward_spmm, order_swap;
   int32_t gemm_mode; /* mg_gemm_mode */
   int32_t spmm_mode; /* mg_spmm_mode */
+  /* 1: in MG_SPMM_FAST, layer 0 runs as (Â·X)·W0 and W0's gradient as (Â·X)^T·G0 (Â·X kept from the
+   * forward) whenever d0 < 2·d1 and skip_first_backward_spmm is off: one d0-wide SpMM replaces the
+   * forward and backward d1-wide ones (the association inc/gcn.hpp:254-260 uses under order_swap, carried
+   * into the backward). Mathematically the same gradient; float order differs, so EXACT ignores it. */
+  int32_t aggregate_input;
 } mg_config;
 
 /* Fills the reference defaults (inc/gcn.hpp:16-25): lr 0.01, betas 0.9/0.999, eps 1e-8, 100 epochs,

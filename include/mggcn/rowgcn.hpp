@@ -118,6 +118,7 @@ struct GcnConfig {
   bool permute = false, overlap = false, skip_first_backward_spmm = false, order_swap = false;
   int gemm_mode = MG_GEMM_TF32X3;  // see DESIGN.md: EXACT is bitwise, TF32X3/FAST meet rel 1e-4
   int spmm_mode = MG_SPMM_FAST;
+  bool aggregate_input = true;  // FAST only: layer 0 as (A X) W0 (mggcn.h)
   int layers() const { return static_cast<int>(layer_dims.size()) - 1; }
   mg_config c() const {
     mg_config m;
@@ -136,6 +137,7 @@ struct GcnConfig {
     m.order_swap = order_swap;
     m.gemm_mode = gemm_mode;
     m.spmm_mode = spmm_mode;
+    m.aggregate_input = aggregate_input;
     return m;
   }
   void validate() const {

@@ -20,7 +20,8 @@ class mg_config(C.Structure):
     _fields_ = [("layer_dims", C.c_void_p), ("n_dims", C.c_int32), ("lr", C.c_double), ("beta1", C.c_double),
                 ("beta2", C.c_double), ("epsilon", C.c_double), ("epochs", C.c_int32), ("seed", C.c_uint64),
                 ("permute", C.c_uint8), ("overlap", C.c_uint8), ("skip_first_backward_spmm", C.c_uint8),
-                ("order_swap", C.c_uint8), ("gemm_mode", C.c_int32), ("spmm_mode", C.c_int32)]
+                ("order_swap", C.c_uint8), ("gemm_mode", C.c_int32), ("spmm_mode", C.c_int32),
+                ("aggregate_input", C.c_int32)]
 
 
 # (name, restype, argtypes) for every symbol declared in include/mggcn.h

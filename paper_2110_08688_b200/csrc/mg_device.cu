@@ -274,6 +274,7 @@ struct Worker {
   uint8_t* mask = nullptr;
   std::vector<float*> ahw;
   float *hw = nullptr, *bc1 = nullptr, *bc2 = nullptr;
+  float* ax = nullptr;  // Â·X (rows x ld0) when Config::aggregate_first()
   std::vector<float*> W, WG, M, V, stage;
   double* partials = nullptr;
   float* seg_scratch = nullptr;  // MG_SPMM_FAST hub-row segment partials (max segments x ld_max)
@@ -568,6 +569,19 @@ class Step {
       const index_t ldl = g_.ld[l], ldl1 = g_.ld[l + 1];
       const bool swap = cfg_.order_swap && dl < dl1;  // gcn.hpp:145-148
       std::vector<float*> src(nloc()), out(nloc());
+      if (l == 0 && cfg_.aggregate_first()) {  // ax = Â·X (d0 wide), ahw[0] = ax·W0 (+ReLU)
+        for (size_t k = 0; k < nloc(); ++k) {
+          src[k] = W(k).x;
+          out[k] = W(k).ax;
+        }
+        staged_spmm(0, dl, src, out, false);
+        for (size_t k = 0; k < nloc(); ++k) {
+          Worker& w = W(k);
+          dev(w);
+          gemm(w, false, false, w.rows, ldl1, dl, w.ax, ldl, w.W[0], ldl1, w.ahw[0], ldl1, L_ > 1 ? 2 : 0);
+        }
+        continue;
+      }
       for (size_t k = 0; k < nloc(); ++k) {
         Worker& w = W(k);
         dev(w);
@@ -629,7 +643,8 @@ class Step {
     for (int l = L_ - 1; l >= 0; --l) {
       const index_t dl = cfg_.dims[l], dl1 = cfg_.dims[l + 1];
       const index_t ldl = g_.ld[l], ldl1 = g_.ld[l + 1];
-      const bool skip = l == 0 && cfg_.skip_first_backward_spmm;
+      const bool agg = l == 0 && cfg_.aggregate_first();  // W0 grad = (Â·X)^T G0, no backward SpMM
+      const bool skip = l == 0 && (cfg_.skip_first_backward_spmm || agg);
       std::vector<float*> grad_rows(nloc());
       if (!skip) {
         std::vector<float*> src(nloc()), out(nloc());
@@ -648,7 +663,7 @@ class Step {
       for (size_t k = 0; k < nloc(); ++k) {
         Worker& w = W(k);
         dev(w);
-        const float* h_in = l == 0 ? w.x : w.ahw[l - 1];
+        const float* h_in = l == 0 ? (agg ? w.ax : w.x) : w.ahw[l - 1];
         if (cfg_.gemm_mode != MG_GEMM_EXACT) {  // one tcgen05 launch for all 8 blocks (+ ordered reduction)
           int64_t begin[8], len[8];
           for (int b = 0; b < 8; ++b) {
@@ -921,6 +936,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       w.hw = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld_max));
       w.bc1 = dalloc_t<float>(*g, w, std::max<index_t>(1, g->max_part * g->ld_max));
       w.bc2 = dalloc_t<float>(*g, w, std::max<index_t>(1, g->max_part * g->ld_max));
+      if (cfg.aggregate_first()) w.ax = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));
       // parameters, Adam state, W-grad staging (gcn.hpp:150-158), padded ld_l x ld_{l+1}
       for (int l = 0; l < L; ++l) {
         const index_t sz = g->ld[l] * g->ld[l + 1];
@@ -1195,7 +1211,8 @@ mg_status mg_group_rows(mg_group* g, int32_t rank, int64_t* row_begin, int64_t* 
 
 mg_status mg_group_buffer_audit(mg_group* g, int32_t* large_buffers, int64_t* step_allocations, int64_t* device_bytes) {
   return guarded([&] {
-    if (large_buffers) *large_buffers = g->cfg.layers() + 3;  // ahw[L] + hw + bc1 + bc2
+    // ahw[L] + hw + bc1 + bc2 (+ Â·X under aggregate_first)
+    if (large_buffers) *large_buffers = g->cfg.layers() + 3 + (g->cfg.aggregate_first() ? 1 : 0);
     if (step_allocations) *step_allocations = g->step_allocs;
     if (device_bytes) *device_bytes = g->workers[0]->bytes;
   });

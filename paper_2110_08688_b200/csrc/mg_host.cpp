@@ -101,6 +101,9 @@ Config to_config(const mg_config* c) {
   cfg.order_swap = c->order_swap != 0;
   cfg.gemm_mode = c->gemm_mode;
   cfg.spmm_mode = c->spmm_mode;
+  if (c->aggregate_input != 0 && c->aggregate_input != 1)
+    throw ConfigError("config: aggregate_input must be 0 or 1, got " + std::to_string(c->aggregate_input));
+  cfg.aggregate_input = c->aggregate_input != 0;
   if (cfg.layers() < 1)
     throw ConfigError("config: need at least one layer (layer_dims has " + std::to_string(cfg.dims.size()) +
                       " entries)");
@@ -365,6 +368,7 @@ void mg_config_defaults(mg_config* c) {
   c->seed = 1;
   c->gemm_mode = MG_GEMM_TF32X3;
   c->spmm_mode = MG_SPMM_FAST;
+  c->aggregate_input = 1;
 }
 
 mg_status mg_config_validate(const mg_config* cfg) {

@@ -80,7 +80,13 @@ struct Config {
   bool permute = false, overlap = false, skip_first_backward_spmm = false, order_swap = false;
   int gemm_mode = MG_GEMM_TF32X3;
   int spmm_mode = MG_SPMM_EXACT;
+  bool aggregate_input = false;
   int layers() const { return static_cast<int>(dims.size()) - 1; }
+  // Layer 0 as (Â·X)·W0 with Â·X kept for W0's gradient: one d0-wide SpMM replaces the d1-wide forward
+  // and backward ones. Reassociation changes the float order, so only in MG_SPMM_FAST.
+  bool aggregate_first() const {
+    return aggregate_input && spmm_mode == MG_SPMM_FAST && !skip_first_backward_spmm && dims[0] < 2 * dims[1];
+  }
 };
 Config to_config(const mg_config* c);  // validates (inc/gcn.hpp:29-35)
 

@@ -105,6 +105,7 @@ class GcnConfig:
     order_swap: bool = False
     gemm_mode: int = GEMM_TF32X3  # production default; GEMM_EXACT/SPMM_EXACT give bitwise parity
     spmm_mode: int = SPMM_FAST
+    aggregate_input: bool = True  # FAST only: layer 0 as (A X) W0, A X reused for W0's gradient (mggcn.h)
 
     def layers(self) -> int:
         return len(self.layer_dims) - 1
@@ -113,7 +114,8 @@ class GcnConfig:
         dims = np.ascontiguousarray(np.asarray(self.layer_dims, dtype=np.int64))
         c = mg_config(dims.ctypes.data_as(C.c_void_p), len(dims), self.lr, self.beta1, self.beta2, self.epsilon,
                       self.epochs, self.seed, int(self.permute), int(self.overlap),
-                      int(self.skip_first_backward_spmm), int(self.order_swap), self.gemm_mode, self.spmm_mode)
+                      int(self.skip_first_backward_spmm), int(self.order_swap), self.gemm_mode, self.spmm_mode,
+                      int(self.aggregate_input))
         c._keep = dims
         return c
 

@@ -247,3 +247,34 @@ def test_step_dump_fast_spmm(golden):
     finally:
         R.set_tuning("heavy_row", 4096)
         R.set_tuning("fast_segment", 2048)
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_aggregate_input_trajectory(ref, P):
+    """aggregate_input (FAST default): layer 0 as (Â·X)·W0 with Â·X reused for W0's gradient. Same math as
+    the reference's A·(X·W0) / X^T·(Â^T·G0); losses within 1e-4 of the f64 reference, final W within 1e-4
+    of the f32 reference, and one extra n x d0 buffer in the plan."""
+    from oracle.pyoracle import make_cfg
+    dims = [20, 48, 24, 5]
+    ds = R.synth_graph(3000, 8.0, 0.7, 11, dims[0], dims[-1])
+    cfg = cfgx(dims, epochs=4, seed=2, permute=True, overlap=P > 1, gemm_mode=R.GEMM_TF32X3,
+               spmm_mode=R.SPMM_FAST)
+    assert cfg.aggregate_input
+    got = R.train_run(ds, cfg, R.TrainOptions(workers=P, devices=[0] * P,
+                                             transport=R.TRANSPORT_NCCL if P == 1 else R.TRANSPORT_LOCAL))
+    rcfg = make_cfg(dims, epochs=4, seed=2, permute=True, overlap=P > 1)
+    r64 = ref.train_run(ref.synth(3000, 8.0, 0.7, 11, dims[0], dims[-1], dtype=np.float64), rcfg, P, np.float64)
+    r32 = ref.train_run(ref.synth(3000, 8.0, 0.7, 11, dims[0], dims[-1]), rcfg, P)
+    for e in range(4):
+        assert abs(got.epoch_loss[e] - r64["loss"][e]) <= TOL * abs(r64["loss"][e])
+    for l in range(3):
+        assert normwise(got.final_w[l], r32["final_w"][l]) <= TOL
+    with group(ds, cfg, P) as g:
+        assert g.buffer_audit()[0] == 3 + 3 + 1
+
+
+def test_aggregate_input_ignored_in_exact_mode():
+    ds = R.synth_graph(800, 6.0, 0.6, 4, 6, 3)
+    a = R.train_run(ds, cfgx([6, 16, 3], epochs=2, seed=1, aggregate_input=True), R.TrainOptions(devices=[0]))
+    b = R.train_run(ds, cfgx([6, 16, 3], epochs=2, seed=1, aggregate_input=False), R.TrainOptions(devices=[0]))
+    assert a.epoch_loss == b.epoch_loss and a.w_hashes == b.w_hashes

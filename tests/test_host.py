@@ -31,7 +31,7 @@ def test_library_exports_every_header_symbol():
 
 def test_abi_version_and_defaults():
     from paper_2110_08688_b200._lib import lib, mg_config
-    assert lib().mg_abi_version() == 1
+    assert lib().mg_abi_version() == 2
     c = mg_config()
     lib().mg_config_defaults(ctypes.byref(c))
     assert (c.lr, c.beta1, c.beta2, c.epsilon, c.epochs, c.seed) == (0.01, 0.9, 0.999, 1e-8, 100, 1)
@@ -143,3 +143,14 @@ def test_csr_validation():
     ds = R.Dataset.from_arrays(rp, ci, np.ones(3, np.float32), np.zeros((2, 1), np.float32), np.zeros(2, np.int32))
     with pytest.raises(R.ValueError, match="not strictly increasing"):
         ds.validate()
+
+
+def test_aggregate_input_validation():
+    from paper_2110_08688_b200._lib import lib, mg_config
+    c = R.GcnConfig(layer_dims=[4, 8, 2])._c()
+    assert c.aggregate_input == 1
+    c.aggregate_input = 2
+    assert lib().mg_config_validate(ctypes.byref(c)) == 6  # MG_CONFIG_ERROR
+    d = mg_config()
+    lib().mg_config_defaults(ctypes.byref(d))
+    assert d.aggregate_input == 1 and d.spmm_mode == R.SPMM_FAST
