@@ -25,9 +25,11 @@ namespace mg {
 #define MG_CUDA(x)                                                                                     \
   do {                                                                                                 \
     cudaError_t _e = (x);                                                                              \
-    if (_e != cudaSuccess)                                                                             \
+    if (_e != cudaSuccess) {                                                                           \
+      (void)cudaGetLastError(); /* non-sticky errors must not leak into the next launch check */       \
       throw CudaError(std::string(#x) + ": " + cudaGetErrorString(_e) + " (" + __FILE__ + ":" +        \
                       std::to_string(__LINE__) + ")");                                                 \
+    }                                                                                                  \
   } while (0)
 #define MG_NCCL(x)                                                                                     \
   do {                                                                                                 \
@@ -859,7 +861,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
     g->bounds = p->bounds;
     for (index_t d : cfg.dims) g->ld.push_back(pad4(d));
     for (size_t i = 1; i < g->ld.size(); ++i) g->ld_max = std::max(g->ld_max, g->ld[i]);
-    if (cfg.order_swap) g->ld_max = std::max(g->ld_max, g->ld[0]);
+    if (cfg.order_swap || cfg.aggregate_first()) g->ld_max = std::max(g->ld_max, g->ld[0]);
     for (int i = 0; i < world; ++i) g->max_part = std::max(g->max_part, p->bounds[i + 1] - p->bounds[i]);
     for (int b = 0; b <= 8; ++b) g->wblocks[b] = static_cast<index_t>(b) * p->n / 8;  // driver.hpp:156
     // transport
@@ -954,7 +956,8 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
         }
         for (int l = 0; l < L; ++l)
           w.ws_bytes = std::max({w.ws_bytes, tc::tn_workspace_bytes(g->ld[l], g->ld[l + 1], std::max<index_t>(1, w.rows)),
-                                 tc::nn_workspace_bytes(g->ld[l + 1], g->ld[l])});
+                                 tc::nn_workspace_bytes(g->ld[l + 1], g->ld[l]),
+                                 tc::nn_workspace_bytes(g->ld[l], g->ld[l + 1])});
         w.ws = static_cast<float*>(dalloc(*g, w, w.ws_bytes));
       }
       w.loss_blocks = std::max(1, std::min(ceil_div(w.rows, 8), num_sms() * 8));

@@ -39,7 +39,10 @@ namespace tc {
 #define TC_CUDA(x)                                                                                     \
   do {                                                                                                 \
     cudaError_t _e = (x);                                                                              \
-    if (_e != cudaSuccess) throw CudaError(std::string(#x) + ": " + cudaGetErrorString(_e));           \
+    if (_e != cudaSuccess) {                                                                           \
+      (void)cudaGetLastError();                                                                        \
+      throw CudaError(std::string(#x) + ": " + cudaGetErrorString(_e));                                \
+    }                                                                                                  \
   } while (0)
 
 constexpr int BM = 128;            // tile rows = TMEM lanes
@@ -72,6 +75,9 @@ struct Params {
   int blk_first[9];      // first work item of each block (prefix over blocks)
   float* partial;        // [n_items][BM][npb]
   float* dbg;            // debugging aid (MGGCN_TC_DEBUG): first stage tiles + first TMEM rows, else null
+  // v2
+  int n_tiles;           // output column tiles of <= 128
+  int bnr;               // B rows (tile columns) loaded per stage: min(np, 128) (TN: rounded to 32)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -423,10 +429,17 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(const __grid_constant__ C
 // the 128 TMEM lanes (= tile rows) and write A_hi / A_lo of each 16-deep K block straight into a TMEM
 // stage with tcgen05.st; the MMA reads A from TMEM and only B from smem. For NN / NT the B operand (W)
 // is split and laid out K-major once per call (split_b), so its hi / lo tiles arrive by TMA ready to use.
-// Shared-memory traffic per K block drops from ~168 KB to ~96 KB (N = 256), below the tensor-core time.
-// TMEM: accumulators in columns [0, 256) (two of 128 when N <= 128, else one of 256), A stages in
-// [256, 256 + 32 * nst).
+// Output tiles are 128 x (<= 128) columns, so the two TMEM accumulators always double-buffer (wider N
+// runs as adjacent column tiles of the same row tile, issued back to back so A comes from L2 the
+// second time). TMEM: accumulators in columns [0, 256), A stages in [256, 256 + 32 * nst).
+// Epilogue: each epilogue warp owns 32 rows and up to four 32 x 32 fp32 smem buffers (SWIZZLE_128B,
+// the TMA layout). NN / NT: the relu_backward mask source (epi 1) is TMA-prefetched into the buffers
+// before the accumulator is ready, results are written back in place and leave with TMA bulk stores.
+// TN: the buffers hold the running fp32 sum of the promoted partials of the work item (no global
+// read-modify-write), stored once per item.
 constexpr int kAcol = 256;
+constexpr int kTileN = 128;
+constexpr int kEpiBuf = 4 * 4 * 4096;  // 4 warps x 4 chunks x (32 x 32 fp32)
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
   asm volatile(
@@ -446,6 +459,19 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       "}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
 }
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(x), "r"(y), "r"(smem_u32(src))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+// Row r's 16-byte chunk j of a 32 x 32 fp32 SWIZZLE_128B box.
+__device__ __forceinline__ float4* sw128(float* buf, int r, int j) {
+  return reinterpret_cast<float4*>(buf + r * 32 + ((j ^ (r & 7)) << 2));
+}
 
 // W (padded ld) -> B_hi / B_lo, K-major (np x kp): NN reads W as K x N (transpose), NT as N x K.
 __global__ void split_b(const float* __restrict__ W, long ldw, int trans, int np, int kp, long nvalid, long kvalid,
@@ -462,21 +488,36 @@ __global__ void split_b(const float* __restrict__ W, long ldw, int trans, int np
   }
 }
 
+struct Item2 {
+  Item k;   // rows / K range (TN: of the m-item)
+  int mi;   // TN: m-item (index into the partial tiles); NN/NT: row tile
+  int n0;   // first output column of the tile
+  int nw;   // tile columns (multiple of 16, <= 128)
+};
+__device__ __forceinline__ Item2 item2_of(const Params& p, int MODE_, int it) {
+  Item2 r;
+  r.mi = it / p.n_tiles;
+  const int nt = it - r.mi * p.n_tiles;
+  r.n0 = nt * kTileN;
+  r.nw = min(kTileN, p.np - r.n0);
+  r.k = item_of(p, MODE_, r.mi);
+  return r;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ CUtensorMap map_a,
                                                         const __grid_constant__ CUtensorMap map_bh,
-                                                        const __grid_constant__ CUtensorMap map_bl, Params p) {
+                                                        const __grid_constant__ CUtensorMap map_bl,
+                                                        const __grid_constant__ CUtensorMap map_c, Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t full[kMaxStages], conv[kMaxStages], empty[kMaxStages], tfull[2], tempty[2];
+  __shared__ uint64_t full[kMaxStages], conv[kMaxStages], empty[kMaxStages], tfull[2], tempty[2], oldbar[4];
   __shared__ uint32_t tmem_base_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr bool B_MN = MODE == TN;  // NN/NT read the pre-split K-major B
   const int a_bytes = BM * BK * 4;    // raw A tile (no swizzle): NN/NT [128 rows][16 k], TN [16 k][128 m]
-  const int b_bytes = p.npb * BK * 4;
+  const int b_bytes = p.bnr * BK * 4;  // one B tile (bnr = tile columns held per stage)
   const int stage = a_bytes + 2 * b_bytes;  // A raw | B hi | B lo
-  const int nacc = p.np <= 128 ? 2 : 1;
-  const int tstride = nacc == 2 ? 128 : 256;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nst; ++s) {
@@ -488,6 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 4);
     }
+    for (int q = 0; q < 4; ++q) mbar_init(&oldbar[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -510,40 +552,40 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
       uint32_t sc = 0;
       const uint32_t tx = static_cast<uint32_t>(MODE == TN ? a_bytes + b_bytes : stage);
       for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
-        const Item I = item_of(p, MODE, it);
-        for (int kb = 0; kb < I.nkb; ++kb, ++sc) {
+        const Item2 I = item2_of(p, MODE, it);
+        for (int kb = 0; kb < I.k.nkb; ++kb, ++sc) {
           const int s = sc % p.nst;
           if (sc >= static_cast<uint32_t>(p.nst)) mbar_wait(&empty[s], ((sc / p.nst) - 1) & 1);
           uint8_t* a = smem + s * stage;
           uint8_t* b = a + a_bytes;
           mbar_arrive_tx(&full[s], tx);
           if (MODE == TN) {
-            const int k0 = static_cast<int>(I.row0) + kb * BK;
-            tma_load_2d(a, &map_a, I.mt * BM, k0, &full[s]);
-            for (int j = 0; j < p.npb / 32; ++j) tma_load_2d(b + j * 2048, &map_bh, j * 32, k0, &full[s]);
+            const int k0 = static_cast<int>(I.k.row0) + kb * BK;
+            tma_load_2d(a, &map_a, I.k.mt * BM, k0, &full[s]);
+            for (int j = 0; j < p.bnr / 32; ++j) tma_load_2d(b + j * 2048, &map_bh, I.n0 + j * 32, k0, &full[s]);
           } else {
             const int k0 = kb * BK;
-            tma_load_2d(a, &map_a, k0, static_cast<int>(I.row0), &full[s]);
-            tma_load_2d(b, &map_bh, k0, 0, &full[s]);
-            tma_load_2d(b + b_bytes, &map_bl, k0, 0, &full[s]);
+            tma_load_2d(a, &map_a, k0, static_cast<int>(I.k.row0), &full[s]);
+            tma_load_2d(b, &map_bh, k0, I.n0, &full[s]);
+            tma_load_2d(b + b_bytes, &map_bl, k0, I.n0, &full[s]);
           }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (A from TMEM)
-    const uint32_t idesc = idesc_tf32(BM, p.np, 0, B_MN ? 1 : 0);
     uint32_t sc = 0, ac = 0;
     for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
-      const Item I = item_of(p, MODE, it);
-      const int groups = MODE == TN ? (I.nkb + kPromoteKb - 1) / kPromoteKb : 1;
+      const Item2 I = item2_of(p, MODE, it);
+      const uint32_t idesc = idesc_tf32(BM, I.nw, 0, B_MN ? 1 : 0);
+      const int groups = MODE == TN ? (I.k.nkb + kPromoteKb - 1) / kPromoteKb : 1;
       for (int gi = 0; gi < groups; ++gi, ++ac) {
         const int kb0 = MODE == TN ? gi * kPromoteKb : 0;
-        const int kb1 = MODE == TN ? min(I.nkb, kb0 + kPromoteKb) : I.nkb;
-        const int buf = static_cast<int>(ac % nacc);
-        if (ac >= static_cast<uint32_t>(nacc)) mbar_wait(&tempty[buf], ((ac / nacc) - 1) & 1);
+        const int kb1 = MODE == TN ? min(I.k.nkb, kb0 + kPromoteKb) : I.k.nkb;
+        const int buf = static_cast<int>(ac & 1);
+        if (ac >= 2u) mbar_wait(&tempty[buf], ((ac >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t d = tmem + static_cast<uint32_t>(buf * tstride);
+        const uint32_t d = tmem + static_cast<uint32_t>(buf * kTileN);
         for (int kb = kb0; kb < kb1; ++kb, ++sc) {
           const int s = sc % p.nst;
           mbar_wait(&conv[s], (sc / p.nst) & 1);
@@ -580,14 +622,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
     const int t = threadIdx.x - 64;
     uint32_t sc = 0;
     for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
-      const Item I = item_of(p, MODE, it);
-      for (int kb = 0; kb < I.nkb; ++kb, ++sc) {
+      const Item2 I = item2_of(p, MODE, it);
+      for (int kb = 0; kb < I.k.nkb; ++kb, ++sc) {
         const int s = sc % p.nst;
         mbar_wait(&full[s], (sc / p.nst) & 1);  // also implies the MMAs of this stage's last use are done
         const float* araw = reinterpret_cast<const float*>(smem + s * stage);
         float x[BK];
         if (MODE == TN) {
-          const int valid = static_cast<int>(min(static_cast<long>(BK), I.k_end - (I.row0 + kb * BK)));
+          const int valid = static_cast<int>(min(static_cast<long>(BK), I.k.k_end - (I.k.row0 + kb * BK)));
 #pragma unroll
           for (int k = 0; k < BK; ++k) x[k] = k < valid ? araw[k * BM + row] : 0.0f;
         } else {
@@ -628,66 +670,65 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (as v1)
+    // ------------------------------------------------------------ epilogue
     const int q = warp & 3;
-    uint32_t ac = 0;
-    float* stg = reinterpret_cast<float*>(smem + p.nst * stage) + q * (32 * 33);
-    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
-      const Item I = item_of(p, MODE, it);
-      const int groups = MODE == TN ? (I.nkb + kPromoteKb - 1) / kPromoteKb : 1;
+    uint32_t ac = 0, tiles = 0;
+    float* bufs = reinterpret_cast<float*>(smem + p.nst * stage) + q * (4 * 1024);  // 4 chunks of 32 x 32
+    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++tiles) {
+      const Item2 I = item2_of(p, MODE, it);
+      const int nch = (I.nw + 31) / 32;
+      // buffers are free once the previous tile's bulk stores have read them
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+      const long grow0 = (MODE == TN ? static_cast<long>(I.mi) * BM : I.k.row0) + q * 32;
+      if (MODE != TN && p.epi == 1 && lane == 0) {  // prefetch the relu_backward mask source
+        mbar_arrive_tx(&oldbar[q], static_cast<uint32_t>(nch * 4096));
+        for (int c = 0; c < nch; ++c)
+          tma_load_2d(bufs + c * 1024, &map_c, I.n0 + c * 32, static_cast<int>(grow0), &oldbar[q]);
+      }
+      const int groups = MODE == TN ? (I.k.nkb + kPromoteKb - 1) / kPromoteKb : 1;
       for (int gi = 0; gi < groups; ++gi, ++ac) {
-        const int buf = static_cast<int>(ac % nacc);
-        mbar_wait(&tfull[buf], (ac / nacc) & 1);
+        const int buf = static_cast<int>(ac & 1);
+        mbar_wait(&tfull[buf], (ac >> 1) & 1);
         tc_fence_after();
-        const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf * tstride);
-        for (int c0 = 0; c0 < p.np; c0 += 32) {
+        if (MODE != TN && p.epi == 1) mbar_wait(&oldbar[q], tiles & 1);
+        const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf * kTileN);
+        for (int c = 0; c < nch; ++c) {
           float v[32];
-          tmem_ld32(tbase + c0, v);
-          __syncwarp();
+          tmem_ld32(tbase + c * 32, v);
+          float* b = bufs + c * 1024;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) stg[lane * 33 + i] = v[i];
-          __syncwarp();
-          const int c = c0 + lane;
-          if (MODE == TN) {
-            if (c < p.npb) {
-              float* dst = p.partial + (static_cast<long>(it) * BM + q * 32) * p.npb + c;
-              float prev[32];
+          for (int j = 0; j < 8; ++j) {
+            float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            float4* dst = sw128(b, lane, j);
+            if (MODE == TN) {
               if (gi > 0) {
-#pragma unroll
-                for (int r = 0; r < 32; ++r) prev[r] = dst[static_cast<long>(r) * p.npb];
+                const float4 pv = *dst;
+                o = make_float4(__fadd_rn(pv.x, o.x), __fadd_rn(pv.y, o.y), __fadd_rn(pv.z, o.z), __fadd_rn(pv.w, o.w));
               }
-#pragma unroll
-              for (int r = 0; r < 32; ++r) {
-                float xv = stg[r * 33 + lane];
-                if (gi > 0) xv = __fadd_rn(prev[r], xv);
-                dst[static_cast<long>(r) * p.npb] = xv;
-              }
+            } else if (p.epi == 1) {
+              const float4 old = *dst;
+              o = make_float4(old.x > 0.0f ? o.x : 0.0f, old.y > 0.0f ? o.y : 0.0f, old.z > 0.0f ? o.z : 0.0f,
+                              old.w > 0.0f ? o.w : 0.0f);
+            } else if (p.epi == 2) {
+              o = make_float4(fmaxf(o.x, 0.0f), fmaxf(o.y, 0.0f), fmaxf(o.z, 0.0f), fmaxf(o.w, 0.0f));
             }
-          } else if (c < p.N) {
-            const long g0 = I.row0 + q * 32;
-            const int nrows = static_cast<int>(min(32L, p.M - g0));
-            float* dst = p.C + g0 * p.ldc + c;
-            float old[32];
-            if (p.epi == 1) {
-#pragma unroll
-              for (int r = 0; r < 32; ++r) old[r] = r < nrows ? dst[static_cast<long>(r) * p.ldc] : 0.0f;
-            }
-#pragma unroll
-            for (int r = 0; r < 32; ++r) {
-              if (r < nrows) {
-                float xv = stg[r * 33 + lane];
-                if (p.epi == 1) xv = old[r] > 0.0f ? xv : 0.0f;
-                if (p.epi == 2) xv = xv > 0.0f ? xv : 0.0f;
-                dst[static_cast<long>(r) * p.ldc] = xv;
-              }
-            }
+            *dst = o;
           }
         }
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
       }
+      // the finished 32-row slab leaves with bulk tensor stores (rows / columns past the end are clipped)
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        for (int c = 0; c < nch; ++c) tma_store_2d(&map_c, I.n0 + c * 32, static_cast<int>(grow0), bufs + c * 1024);
+        bulk_commit();
+      }
     }
+    if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
@@ -783,27 +824,33 @@ void check_ptr(const void* p, long ld, const char* what) {
 // ---- v2 (A in TMEM) host side
 int g_gemm_version = 2;
 
+constexpr int kSmemBudget2 = 160 * 1024;  // v2 stage ring (+ kEpiBuf epilogue buffers)
+
 void finish_params2(Params& p, long N, bool tn, int terms) {
   p.np = static_cast<int>((N + 15) / 16 * 16);
-  p.npb = tn ? (p.np + 31) / 32 * 32 : p.np;
+  p.npb = tn ? (p.np + 31) / 32 * 32 : p.np;  // TN partial row stride
   p.tstride = 0;
   p.terms = terms;
-  const int stage = BM * BK * 4 + 2 * p.npb * BK * 4;
-  p.nst = std::max(2, std::min(kMaxStages, kSmemBudget / stage));
+  p.n_tiles = (p.np + kTileN - 1) / kTileN;
+  p.bnr = std::min(p.np, kTileN);
+  if (tn) p.bnr = (p.bnr + 31) / 32 * 32;
+  const int stage = BM * BK * 4 + 2 * p.bnr * BK * 4;
+  p.nst = std::max(2, std::min(kMaxStages, kSmemBudget2 / stage));
 }
 
-inline int smem_bytes2(const Params& p) { return p.nst * (BM * BK * 4 + 2 * p.npb * BK * 4) + kEpiSmem + 1024; }
+inline int smem_bytes2(const Params& p) { return p.nst * (BM * BK * 4 + 2 * p.bnr * BK * 4) + kEpiBuf + 1024; }
 
 template <int MODE>
-void launch2(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const Params& p, cudaStream_t s) {
+void launch2(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
+             cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     TC_CUDA(cudaFuncSetAttribute(gemm_tc2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSmemBudget + kEpiSmem + 1024));
+                                 kSmemBudget2 + kEpiBuf + 1024));
     attr = true;
   }
   const int grid = std::max(1, std::min(p.n_items, num_sms()));
-  gemm_tc2<MODE><<<grid, kThreads, smem_bytes2(p), s>>>(a, bh, bl, p);
+  gemm_tc2<MODE><<<grid, kThreads, smem_bytes2(p), s>>>(a, bh, bl, c, p);
   TC_CUDA(cudaGetLastError());
 }
 
@@ -854,8 +901,9 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
   p.epi = epi;
   if (g_gemm_version == 2) {
     finish_params2(p, N, false, mode == MG_GEMM_TF32X3 ? 3 : 1);
+    check_ptr(C, ldc, "C");
     p.m_tiles = static_cast<int>((M + BM - 1) / BM);
-    p.n_items = p.m_tiles;
+    p.n_items = p.m_tiles * p.n_tiles;
     const int kp = static_cast<int>((K + 3) / 4 * 4);
     if (!ws || ws_bytes < nn_workspace_bytes(N, K)) throw ValueError("tc gemm: B split workspace too small");
     float* bh = ws;
@@ -865,12 +913,13 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
                                                                                        p.terms, bh, bl);
     TC_CUDA(cudaGetLastError());
     const CUtensorMap ma = make_map(A, K, M, lda, BK, BM, CU_TENSOR_MAP_SWIZZLE_NONE);
-    const CUtensorMap mbh = make_map(bh, kp, p.np, kp, BK, p.np, CU_TENSOR_MAP_SWIZZLE_64B);
-    const CUtensorMap mbl = make_map(bl, kp, p.np, kp, BK, p.np, CU_TENSOR_MAP_SWIZZLE_64B);
+    const CUtensorMap mbh = make_map(bh, kp, p.np, kp, BK, p.bnr, CU_TENSOR_MAP_SWIZZLE_64B);
+    const CUtensorMap mbl = make_map(bl, kp, p.np, kp, BK, p.bnr, CU_TENSOR_MAP_SWIZZLE_64B);
+    const CUtensorMap mc = make_map(C, N, M, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     if (!tb)
-      launch2<NN>(ma, mbh, mbl, p, s);
+      launch2<NN>(ma, mbh, mbl, mc, p, s);
     else
-      launch2<NT>(ma, mbh, mbl, p, s);
+      launch2<NT>(ma, mbh, mbl, mc, p, s);
     return 2;
   }
   finish_params(p, N, !tb, mode == MG_GEMM_TF32X3 ? 3 : 1);
@@ -937,8 +986,8 @@ int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* l
     p.blk_first[g + 1] = p.blk_first[g] + static_cast<int>(chunks) * p.m_tiles;
     rows_hi = std::max<int64_t>(rows_hi, begin[g] + len[g]);
   }
-  p.n_items = p.blk_first[nblocks];
-  const size_t need = sizeof(float) * static_cast<size_t>(p.n_items) * BM * p.npb;
+  p.n_items = p.blk_first[nblocks] * (g_gemm_version == 2 ? p.n_tiles : 1);
+  const size_t need = sizeof(float) * static_cast<size_t>(p.blk_first[nblocks]) * BM * p.npb;
   if (p.n_items > 0 && (!ws || ws_bytes < need)) throw ValueError("tc gemm: TN split-K workspace too small");
   p.partial = ws;
   int kernels = 0;
@@ -946,7 +995,9 @@ int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* l
     const CUtensorMap mb = make_map(G, N, rows_hi, ldg, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     if (g_gemm_version == 2) {  // A = H rows land raw ([16 k][128 m]) and go to TMEM transposed per lane
       const CUtensorMap ma = make_map(H, M, rows_hi, ldh, BM, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
-      launch2<TN>(ma, mb, mb, p, s);
+      const CUtensorMap mc = make_map(ws, p.npb, static_cast<long>(p.blk_first[nblocks]) * BM, p.npb, 32, 32,
+                                      CU_TENSOR_MAP_SWIZZLE_128B);
+      launch2<TN>(ma, mb, mb, mc, p, s);
     } else {
       const CUtensorMap ma = make_map(H, M, rows_hi, ldh, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
       launch<TN>(ma, mb, p, s);
