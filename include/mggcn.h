@@ -112,6 +112,40 @@ int32_t mg_dataset_num_classes(const mg_dataset* ds);
 /* Dataset::validate (inc/dataset.hpp:30-44) + CsrMatrix::validate (inc/sparse.hpp:37-54). */
 mg_status mg_dataset_validate(const mg_dataset* ds);
 void mg_dataset_free(mg_dataset* ds);
+/* Borrowed val / test / train masks (NULL when the dataset has none); Dataset::{train,val,test}_mask. */
+mg_status mg_dataset_masks(const mg_dataset* ds, const uint8_t** train, const uint8_t** val, const uint8_t** test);
+
+/* ---------------------------------------------------------------- on-disk formats
+ * rowgcn loaders (inc/dataset.hpp:84-280, inc/dense.hpp:290-335), multi-threaded, same accepted syntax,
+ * same exception types (MG_IO_ERROR: cannot open / short write; MG_PARSE_ERROR: "path:line: ..." for
+ * malformed text) and messages. Graphs are built like from_coo (inc/sparse.hpp:59-90): rows sorted,
+ * duplicate (u, v) weights summed (in file order). */
+typedef struct mg_graph mg_graph;  /* owned CSR */
+typedef struct mg_dense mg_dense;  /* owned row-major float matrix */
+
+/* load_dataset<float>(graph, features, labels, masks) (dataset.hpp:264-276); masks_path NULL or "" = none.
+ * The graph format is sniffed like load_graph; validates like Dataset::validate (name = graph_path). */
+mg_status mg_dataset_load(const char* graph_path, const char* features_path, const char* labels_path,
+                          const char* masks_path, mg_dataset** out);
+/* format 0 = load_graph (sniff "%%MatrixMarket", dataset.hpp:170-180), 1 = load_matrix_market
+ * (:87-143), 2 = load_edge_list (:147-168). */
+mg_status mg_graph_load(const char* path, int32_t format, mg_graph** out);
+mg_status mg_graph_view(const mg_graph* g, mg_csr* out); /* borrowed, valid until mg_graph_free */
+void mg_graph_free(mg_graph* g);
+/* load_features<float> (dataset.hpp:184-216): MGDM binary (by magic) or CSV rows. */
+mg_status mg_dense_load(const char* path, mg_dense** out);
+/* read_dense<float> (dense.hpp:311-335): MGDM only; f64 payloads are converted. */
+mg_status mg_dense_read(const char* path, mg_dense** out);
+mg_status mg_dense_view(const mg_dense* d, int64_t* rows, int64_t* cols, const float** data);
+void mg_dense_free(mg_dense* d);
+/* write_dense<float> (dense.hpp:293-307): "MGDM", u64 rows, u64 cols, u8 4, payload. */
+mg_status mg_dense_write(const char* path, int64_t rows, int64_t cols, const float* data);
+/* load_labels (dataset.hpp:218-234). *count = number of labels; dst (capacity entries) may be NULL to
+ * query the count first. */
+mg_status mg_labels_load(const char* path, int32_t* dst, int64_t capacity, int64_t* count);
+/* load_masks (dataset.hpp:237-262) for n vertices; each non-NULL output gets n bytes when its key is
+ * present. *present: bit 0 train, bit 1 val, bit 2 test. */
+mg_status mg_masks_load(const char* path, int64_t n, uint8_t* train, uint8_t* val, uint8_t* test, int32_t* present);
 
 /* ---------------------------------------------------------------- partitioner
  * rowgcn::prepare_data (inc/driver.hpp:87-117): random_permutation (partition.hpp:69-79), permute

@@ -11,6 +11,8 @@
 //   parse_config / materialize_config  driver.hpp:24-57   same (generic over the JSON type)
 //   CsrMatrix / DenseMatrix / Dataset   sparse.hpp / dense.hpp / dataset.hpp
 //   synth_graph<float>        inc/dataset.hpp:287-334     bit-identical output
+//   load_dataset / load_graph / load_features / load_labels / load_masks / read_dense / write_dense
+//                             inc/dataset.hpp:84-280, dense.hpp:290-335
 //   prepare_data / PreparedData  driver.hpp:75-117        bit-identical tiles
 //   TrainOptions / TrainArtifacts / train_run  driver.hpp:119-206
 //   GradArtifacts / grad_run  driver.hpp:209-251
@@ -210,28 +212,99 @@ inline DatasetHandle to_handle(const Dataset<float>& ds) {
 }
 }  // namespace detail
 
-// rowgcn::synth_graph<float> (inc/dataset.hpp:287-334), bit-identical.
-inline Dataset<float> synth_graph(index_t n, double avg_degree, double exponent, std::uint64_t seed,
-                                  index_t feature_dim = 16, int classes = 4) {
-  detail::DatasetHandle h;
-  check(mg_dataset_synth(n, avg_degree, exponent, seed, feature_dim, classes, &h.p));
+namespace detail {
+inline Dataset<float> from_handle(mg_dataset* p, const std::string& name) {
   mg_csr g;
   const float* f = nullptr;
   const std::int32_t* lab = nullptr;
   const std::uint8_t* mask = nullptr;
   std::int64_t d0 = 0;
-  check(mg_dataset_view(h.p, &g, &f, &d0, &lab, &mask));
+  check(mg_dataset_view(p, &g, &f, &d0, &lab, &mask));
+  const std::uint8_t *tr = nullptr, *va = nullptr, *te = nullptr;
+  check(mg_dataset_masks(p, &tr, &va, &te));
+  const index_t n = g.rows;
   Dataset<float> ds;
-  ds.name = "synth-n" + std::to_string(n) + "-d" + std::to_string(avg_degree);
+  ds.name = name;
   ds.graph.rows = g.rows;
   ds.graph.cols = g.cols;
-  ds.graph.row_ptr.assign(g.row_ptr, g.row_ptr + g.rows + 1);
-  ds.graph.col_idx.assign(g.col_idx, g.col_idx + g.row_ptr[g.rows]);
-  ds.graph.values.assign(g.values, g.values + g.row_ptr[g.rows]);
+  ds.graph.row_ptr.assign(g.row_ptr, g.row_ptr + n + 1);
+  ds.graph.col_idx.assign(g.col_idx, g.col_idx + g.row_ptr[n]);
+  ds.graph.values.assign(g.values, g.values + g.row_ptr[n]);
   ds.features = DenseMatrix<float>(n, d0);
-  std::memcpy(ds.features.data(), f, sizeof(float) * static_cast<size_t>(n * d0));
+  if (n * d0 > 0) std::memcpy(ds.features.data(), f, sizeof(float) * static_cast<size_t>(n * d0));
   ds.labels.assign(lab, lab + n);
+  if (tr) ds.train_mask.assign(tr, tr + n);
+  if (va) ds.val_mask.assign(va, va + n);
+  if (te) ds.test_mask.assign(te, te + n);
   return ds;
+}
+inline CsrMatrix<float> graph_from(int32_t format, const std::string& path) {
+  mg_graph* h = nullptr;
+  check(mg_graph_load(path.c_str(), format, &h));
+  std::unique_ptr<mg_graph, void (*)(mg_graph*)> guard(h, mg_graph_free);
+  mg_csr g;
+  check(mg_graph_view(h, &g));
+  CsrMatrix<float> m;
+  m.rows = g.rows;
+  m.cols = g.cols;
+  m.row_ptr.assign(g.row_ptr, g.row_ptr + g.rows + 1);
+  m.col_idx.assign(g.col_idx, g.col_idx + g.row_ptr[g.rows]);
+  m.values.assign(g.values, g.values + g.row_ptr[g.rows]);
+  return m;
+}
+inline DenseMatrix<float> dense_from(mg_status (*fn)(const char*, mg_dense**), const std::string& path) {
+  mg_dense* h = nullptr;
+  check(fn(path.c_str(), &h));
+  std::unique_ptr<mg_dense, void (*)(mg_dense*)> guard(h, mg_dense_free);
+  std::int64_t r = 0, c = 0;
+  const float* d = nullptr;
+  check(mg_dense_view(h, &r, &c, &d));
+  DenseMatrix<float> m(r, c);
+  if (r * c > 0) std::memcpy(m.data(), d, sizeof(float) * static_cast<size_t>(r * c));
+  return m;
+}
+}  // namespace detail
+
+// rowgcn::synth_graph<float> (inc/dataset.hpp:287-334), bit-identical.
+inline Dataset<float> synth_graph(index_t n, double avg_degree, double exponent, std::uint64_t seed,
+                                  index_t feature_dim = 16, int classes = 4) {
+  detail::DatasetHandle h;
+  check(mg_dataset_synth(n, avg_degree, exponent, seed, feature_dim, classes, &h.p));
+  return detail::from_handle(h.p, "synth-n" + std::to_string(n) + "-d" + std::to_string(avg_degree));
+}
+
+// On-disk formats (inc/dataset.hpp:84-280, inc/dense.hpp:290-335): native multi-threaded loaders,
+// same syntax, messages and exception types as the reference.
+inline CsrMatrix<float> load_matrix_market(const std::string& path) { return detail::graph_from(1, path); }
+inline CsrMatrix<float> load_edge_list(const std::string& path) { return detail::graph_from(2, path); }
+inline CsrMatrix<float> load_graph(const std::string& path) { return detail::graph_from(0, path); }
+inline DenseMatrix<float> load_features(const std::string& path) { return detail::dense_from(mg_dense_load, path); }
+inline DenseMatrix<float> read_dense(const std::string& path) { return detail::dense_from(mg_dense_read, path); }
+inline void write_dense(const std::string& path, const DenseMatrix<float>& m) {
+  check(mg_dense_write(path.c_str(), m.rows(), m.cols(), m.data()));
+}
+inline std::vector<std::int32_t> load_labels(const std::string& path) {
+  std::int64_t n = 0;
+  check(mg_labels_load(path.c_str(), nullptr, 0, &n));
+  std::vector<std::int32_t> out(static_cast<size_t>(n));
+  check(mg_labels_load(path.c_str(), out.data(), n, &n));
+  return out;
+}
+inline void load_masks(const std::string& path, index_t n, std::vector<std::uint8_t>& train,
+                       std::vector<std::uint8_t>& val, std::vector<std::uint8_t>& test) {
+  std::vector<std::uint8_t> a(static_cast<size_t>(n)), b(static_cast<size_t>(n)), c(static_cast<size_t>(n));
+  std::int32_t present = 0;
+  check(mg_masks_load(path.c_str(), n, a.data(), b.data(), c.data(), &present));
+  if (present & 1) train = std::move(a);
+  if (present & 2) val = std::move(b);
+  if (present & 4) test = std::move(c);
+}
+inline Dataset<float> load_dataset(const std::string& graph_path, const std::string& features_path,
+                                   const std::string& labels_path, const std::string& masks_path = "") {
+  detail::DatasetHandle h;
+  check(mg_dataset_load(graph_path.c_str(), features_path.c_str(), labels_path.c_str(),
+                        masks_path.empty() ? nullptr : masks_path.c_str(), &h.p));
+  return detail::from_handle(h.p, graph_path);
 }
 
 // rowgcn::PreparedData (inc/driver.hpp:75-85): owns the bit-exact tiles of this process's ranks.

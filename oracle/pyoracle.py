@@ -109,7 +109,91 @@ class Ref:
 
     def _check(self, rc):
         if rc != 0:
-            raise OracleError(f"reference error {rc}: {self.lib.ref_last_error().decode()}")
+            e = OracleError(f"reference error {rc}: {self.lib.ref_last_error().decode()}")
+            e.code = rc  # 1 ShapeError, 2 ValueError, ..., 5 ParseError, 7 IoError (ref_shim.cpp guarded)
+            e.message = self.lib.ref_last_error().decode()
+            raise e
+
+    # ------------------------------------------------------------ on-disk formats (dataset.hpp:84-280)
+    def _partial_graph(self, h):
+        try:
+            nn, nnz, d0 = C.c_int64(), C.c_int64(), C.c_int64()
+            self.lib.ref_ds_info_f32(C.c_void_p(h), C.byref(nn), C.byref(nnz), C.byref(d0))
+            rp = np.zeros(nn.value + 1, np.int64)
+            ci = np.empty(nnz.value, np.int64)
+            v = np.empty(nnz.value, np.float32)
+            if nn.value or nnz.value:
+                self.lib.ref_ds_export_f32(C.c_void_p(h), _ptr(rp), _ptr(ci), _ptr(v), None, None)
+            return rp, ci, v
+        finally:
+            self.lib.ref_ds_free_f32(C.c_void_p(h))
+
+    def load_graph(self, path, fmt=0):
+        """load_graph / load_matrix_market (fmt 1) / load_edge_list (fmt 2) -> (row_ptr, col_idx, values)."""
+        h = C.c_void_p()
+        self._check(self.lib.ref_load_graph_f32(str(path).encode(), C.c_int32(fmt), C.byref(h)))
+        return self._partial_graph(h.value)
+
+    def _partial_features(self, h):
+        try:
+            r, c = C.c_int64(), C.c_int64()
+            self.lib.ref_ds_feat_shape_f32(C.c_void_p(h), C.byref(r), C.byref(c))
+            x = np.zeros((r.value, c.value), np.float32)
+            if x.size:
+                self.lib.ref_ds_export_f32(C.c_void_p(h), None, None, None, _ptr(x), None)
+            return x
+        finally:
+            self.lib.ref_ds_free_f32(C.c_void_p(h))
+
+    def load_features(self, path):
+        h = C.c_void_p()
+        self._check(self.lib.ref_load_features_f32(str(path).encode(), C.byref(h)))
+        return self._partial_features(h.value)
+
+    def read_dense(self, path):
+        h = C.c_void_p()
+        self._check(self.lib.ref_read_dense_f32(str(path).encode(), C.byref(h)))
+        return self._partial_features(h.value)
+
+    def write_dense(self, path, m):
+        a = np.ascontiguousarray(m, np.float32)
+        self._check(self.lib.ref_write_dense_f32(str(path).encode(), C.c_int64(a.shape[0]), C.c_int64(a.shape[1]),
+                                                 _ptr(a)))
+
+    def load_labels(self, path):
+        cnt = C.c_int64()
+        self._check(self.lib.ref_load_labels(str(path).encode(), None, C.c_int64(0), C.byref(cnt)))
+        out = np.zeros(cnt.value, np.int32)
+        self._check(self.lib.ref_load_labels(str(path).encode(), _ptr(out), C.c_int64(cnt.value), C.byref(cnt)))
+        return out
+
+    def load_masks(self, path, n):
+        arrs = [np.zeros(n, np.uint8) for _ in range(3)]
+        pr = C.c_int32()
+        self._check(self.lib.ref_load_masks(str(path).encode(), C.c_int64(n), *[_ptr(a) for a in arrs], C.byref(pr)))
+        return tuple(a if pr.value & (1 << i) else np.zeros(0, np.uint8) for i, a in enumerate(arrs))
+
+    def load_dataset(self, g, f, l, m=""):
+        """load_dataset<float> -> (Dataset, (train, val, test))."""
+        h = C.c_void_p()
+        self._check(self.lib.ref_load_dataset_f32(str(g).encode(), str(f).encode(), str(l).encode(),
+                                                  str(m).encode() if m else None, C.byref(h)))
+        try:
+            nn, nnz, d0 = C.c_int64(), C.c_int64(), C.c_int64()
+            self.lib.ref_ds_info_f32(h, C.byref(nn), C.byref(nnz), C.byref(d0))
+            rp = np.empty(nn.value + 1, np.int64)
+            ci = np.empty(nnz.value, np.int64)
+            v = np.empty(nnz.value, np.float32)
+            x = np.empty((nn.value, d0.value), np.float32)
+            lab = np.empty(nn.value, np.int32)
+            self.lib.ref_ds_export_f32(h, _ptr(rp), _ptr(ci), _ptr(v), _ptr(x), _ptr(lab))
+            arrs = [np.zeros(nn.value, np.uint8) for _ in range(3)]
+            pr = C.c_int32()
+            self.lib.ref_ds_masks_f32(h, *[_ptr(a) for a in arrs], C.byref(pr))
+            masks = tuple(a if pr.value & (1 << i) else np.zeros(0, np.uint8) for i, a in enumerate(arrs))
+        finally:
+            self.lib.ref_ds_free_f32(h)
+        return Dataset(nn.value, rp, ci, v, x, lab), masks
 
     def set_spmm_threads(self, t: int):
         self.lib.ref_set_spmm_threads(C.c_int(t))

@@ -19,6 +19,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -402,5 +403,70 @@ MODEL_FUNCS(float, f32)
 MODEL_FUNCS(double, f64)
 
 uint64_t ref_fnv1a(const void* data, uint64_t len, uint64_t h) { return fnv1a(data, len, h); }
+
+// ---------------------------------------------------------------- on-disk formats (dataset.hpp:84-280)
+// Datasets returned here may be partial (graph only / features only); ref_ds_info / ref_ds_export and
+// ref_ds_feat_shape read them.
+int ref_load_graph_f32(const char* path, int32_t fmt, void** out) {
+  return guarded([&] {
+    auto ds = std::make_unique<Dataset<float>>();
+    ds->graph = fmt == 1 ? load_matrix_market<float>(path) : fmt == 2 ? load_edge_list<float>(path)
+                                                                       : load_graph<float>(path);
+    *out = ds.release();
+  });
+}
+int ref_load_features_f32(const char* path, void** out) {
+  return guarded([&] {
+    auto ds = std::make_unique<Dataset<float>>();
+    ds->features = load_features<float>(path);
+    *out = ds.release();
+  });
+}
+int ref_read_dense_f32(const char* path, void** out) {
+  return guarded([&] {
+    auto ds = std::make_unique<Dataset<float>>();
+    ds->features = read_dense<float>(path);
+    *out = ds.release();
+  });
+}
+void ref_ds_feat_shape_f32(void* h, int64_t* rows, int64_t* cols) {
+  auto* ds = static_cast<Dataset<float>*>(h);
+  *rows = ds->features.rows();
+  *cols = ds->features.cols();
+}
+int ref_write_dense_f32(const char* path, int64_t rows, int64_t cols, const float* data) {
+  return guarded([&] {
+    DenseMatrix<float> m(rows, cols);
+    if (rows * cols) std::memcpy(m.data(), data, sizeof(float) * static_cast<size_t>(rows * cols));
+    write_dense<float>(path, m.view());
+  });
+}
+int ref_load_labels(const char* path, int32_t* dst, int64_t cap, int64_t* count) {
+  return guarded([&] {
+    const auto l = load_labels(path);
+    *count = static_cast<int64_t>(l.size());
+    if (dst) std::memcpy(dst, l.data(), 4 * std::min<size_t>(l.size(), static_cast<size_t>(cap)));
+  });
+}
+int ref_load_masks(const char* path, int64_t n, uint8_t* train, uint8_t* val, uint8_t* test, int32_t* present) {
+  return guarded([&] {
+    std::vector<uint8_t> tr, va, te;
+    load_masks(path, n, tr, va, te);
+    *present = (tr.empty() ? 0 : 1) | (va.empty() ? 0 : 2) | (te.empty() ? 0 : 4);
+    if (!tr.empty()) std::memcpy(train, tr.data(), tr.size());
+    if (!va.empty()) std::memcpy(val, va.data(), va.size());
+    if (!te.empty()) std::memcpy(test, te.data(), te.size());
+  });
+}
+int ref_load_dataset_f32(const char* g, const char* f, const char* l, const char* m, void** out) {
+  return guarded([&] { *out = new Dataset<float>(load_dataset<float>(g, f, l, m ? m : "")); });
+}
+void ref_ds_masks_f32(void* h, uint8_t* train, uint8_t* val, uint8_t* test, int32_t* present) {
+  auto* ds = static_cast<Dataset<float>*>(h);
+  *present = (ds->train_mask.empty() ? 0 : 1) | (ds->val_mask.empty() ? 0 : 2) | (ds->test_mask.empty() ? 0 : 4);
+  if (!ds->train_mask.empty()) std::memcpy(train, ds->train_mask.data(), ds->train_mask.size());
+  if (!ds->val_mask.empty()) std::memcpy(val, ds->val_mask.data(), ds->val_mask.size());
+  if (!ds->test_mask.empty()) std::memcpy(test, ds->test_mask.data(), ds->test_mask.size());
+}
 
 }  // extern "C"

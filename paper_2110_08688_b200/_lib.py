@@ -37,6 +37,18 @@ SIGNATURES = [
     ("mg_dataset_num_classes", C.c_int32, [C.c_void_p]),
     ("mg_dataset_validate", C.c_int, [C.c_void_p]),
     ("mg_dataset_free", None, [C.c_void_p]),
+    ("mg_dataset_masks", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("mg_dataset_load", C.c_int, [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_void_p]),
+    ("mg_graph_load", C.c_int, [C.c_char_p, C.c_int32, C.c_void_p]),
+    ("mg_graph_view", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("mg_graph_free", None, [C.c_void_p]),
+    ("mg_dense_load", C.c_int, [C.c_char_p, C.c_void_p]),
+    ("mg_dense_read", C.c_int, [C.c_char_p, C.c_void_p]),
+    ("mg_dense_view", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("mg_dense_free", None, [C.c_void_p]),
+    ("mg_dense_write", C.c_int, [C.c_char_p, C.c_int64, C.c_int64, C.c_void_p]),
+    ("mg_labels_load", C.c_int, [C.c_char_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    ("mg_masks_load", C.c_int, [C.c_char_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("mg_prepare", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     ("mg_partition_info", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("mg_partition_tile_info", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,

@@ -352,6 +352,22 @@ void random_permutation(index_t n, std::uint64_t seed, std::vector<index_t>& for
 using namespace mg;
 
 // ======================================================================== C ABI (host half)
+// Dataset::validate (inc/dataset.hpp:30-44)
+void mg::validate_dataset_named(const mg_dataset& ds) {
+  ds.graph.validate();
+  const std::string who = "dataset " + ds.name + ": ";
+  if (ds.graph.rows != ds.graph.cols)
+    throw ShapeError(who + "adjacency is " + shape_str(ds.graph.rows, ds.graph.cols) + ", expected square");
+  if (ds.feature_rows != ds.graph.rows)
+    throw ShapeError(who + "features have " + std::to_string(ds.feature_rows) + " rows but graph has " +
+                     std::to_string(ds.graph.rows) + " vertices");
+  if (static_cast<index_t>(ds.labels.size()) != ds.graph.rows)
+    throw ShapeError(who + std::to_string(ds.labels.size()) + " labels but graph has " +
+                     std::to_string(ds.graph.rows) + " vertices");
+  if (!ds.train_mask.empty() && static_cast<index_t>(ds.train_mask.size()) != ds.graph.rows)
+    throw ShapeError(who + "train mask length " + std::to_string(ds.train_mask.size()) + " != n " +
+                     std::to_string(ds.graph.rows));
+}
 extern "C" {
 
 const char* mg_last_error(void) { return g_last_error.c_str(); }
@@ -455,6 +471,8 @@ mg_status mg_dataset_synth(int64_t n, double avg_degree, double exponent, uint64
         for (index_t i = 0; i < uniq[u + 1] - uniq[u]; ++i) ds->graph.col_idx[uniq[u] + i] = adj[start[u] + i];
     });
     ds->d0 = feature_dim;
+    ds->feature_rows = n;
+    ds->name = "synth-n" + std::to_string(n) + "-d" + std::to_string(avg_degree);  // dataset.hpp:326
     ds->features.resize(static_cast<size_t>(n * feature_dim));
     for (auto& x : ds->features) x = static_cast<float>(rng.uniform(-1.0, 1.0));
     ds->labels.resize(n);
@@ -478,6 +496,7 @@ mg_status mg_dataset_from_arrays(const mg_csr* graph, const float* features, int
     ds->graph.col_idx.assign(graph->col_idx, graph->col_idx + nnz);
     ds->graph.values.assign(graph->values, graph->values + nnz);
     ds->d0 = d0;
+    ds->feature_rows = n;
     ds->features.assign(features, features + n * d0);
     ds->labels.assign(labels, labels + n);
     if (train_mask) ds->train_mask.assign(train_mask, train_mask + n);
@@ -509,21 +528,7 @@ int32_t mg_dataset_num_classes(const mg_dataset* ds) {
   return c + 1;
 }
 
-// Dataset::validate (inc/dataset.hpp:30-44)
-static void validate_dataset(const mg_dataset& ds) {
-  ds.graph.validate();
-  if (ds.graph.rows != ds.graph.cols)
-    throw ShapeError("dataset : adjacency is " + shape_str(ds.graph.rows, ds.graph.cols) + ", expected square");
-  if (static_cast<index_t>(ds.features.size()) != ds.graph.rows * ds.d0)
-    throw ShapeError("dataset : features have " + std::to_string(ds.d0 ? ds.features.size() / ds.d0 : 0) +
-                     " rows but graph has " + std::to_string(ds.graph.rows) + " vertices");
-  if (static_cast<index_t>(ds.labels.size()) != ds.graph.rows)
-    throw ShapeError("dataset : " + std::to_string(ds.labels.size()) + " labels but graph has " +
-                     std::to_string(ds.graph.rows) + " vertices");
-  if (!ds.train_mask.empty() && static_cast<index_t>(ds.train_mask.size()) != ds.graph.rows)
-    throw ShapeError("dataset : train mask length " + std::to_string(ds.train_mask.size()) + " != n " +
-                     std::to_string(ds.graph.rows));
-}
+static void validate_dataset(const mg_dataset& ds) { mg::validate_dataset_named(ds); }
 
 mg_status mg_dataset_validate(const mg_dataset* ds) {
   return guarded([&] {

@@ -103,14 +103,19 @@ struct Csr {  // int64 row_ptr/col_idx like rowgcn::CsrMatrix (inc/sparse.hpp:25
 
 struct mg_dataset {
   mg::Csr graph;
-  std::vector<float> features;  // n x d0
+  std::vector<float> features;  // feature_rows x d0 (feature_rows == n once validated)
   mg::index_t d0 = 0;
+  mg::index_t feature_rows = 0;
   std::vector<std::int32_t> labels;
   std::vector<std::uint8_t> train_mask;  // empty = all
+  std::vector<std::uint8_t> val_mask, test_mask;
+  std::string name;
   mg::index_t n() const { return graph.rows; }
 };
 
 namespace mg {
+
+void validate_dataset_named(const mg_dataset& ds);  // Dataset::validate (inc/dataset.hpp:30-44)
 
 // One tile of the symmetric row tiling (rowgcn::TilePlan, inc/partition.hpp:158-171) in the device
 // staging format: int64 row_ptr (host), int32 local column, fp32 value.

@@ -6,6 +6,8 @@ reference's own tests:
   GcnConfig   inc/gcn.hpp:14-36             + gemm_mode / spmm_mode (device arithmetic)
   parse_config / materialize_config / config_to_json   inc/driver.hpp:19-71
   Dataset, synth_graph                      inc/dataset.hpp:19-56, :287-334
+  load_dataset / load_graph / load_matrix_market / load_edge_list / load_features / load_labels /
+  load_masks, read_dense / write_dense      inc/dataset.hpp:84-280, inc/dense.hpp:290-335
   prepare_data / PreparedData               inc/driver.hpp:75-117
   Group (the GcnWorkers of this process)    inc/gcn.hpp:101-398
   TrainOptions / TrainArtifacts / train_run inc/driver.hpp:119-206
@@ -246,6 +248,122 @@ class Dataset:
 
     def validate(self):
         _check(lib().mg_dataset_validate(self._h))
+
+
+def _masks(ds_handle):
+    tr, va, te = C.c_void_p(), C.c_void_p(), C.c_void_p()
+    _check(lib().mg_dataset_masks(ds_handle, C.byref(tr), C.byref(va), C.byref(te)))
+    return tr.value, va.value, te.value
+
+
+def _mask_array(ptr, n):
+    if not ptr:
+        return np.zeros(0, np.uint8)
+    return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint8)), (n,)).copy()
+
+
+Dataset.train_mask = property(lambda self: _mask_array(_masks(self._h)[0], self.n()),
+                              doc="Dataset::train_mask (empty = all vertices)")
+Dataset.val_mask = property(lambda self: _mask_array(_masks(self._h)[1], self.n()), doc="Dataset::val_mask")
+Dataset.test_mask = property(lambda self: _mask_array(_masks(self._h)[2], self.n()), doc="Dataset::test_mask")
+
+
+# ----------------------------------------------------------------------------- on-disk formats
+# (inc/dataset.hpp:84-280, inc/dense.hpp:290-335) — native multi-threaded loaders in libmggcn.
+
+
+def _enc(path) -> bytes:
+    return str(path).encode()
+
+
+def _graph(fmt: int, path) -> tuple:
+    h = C.c_void_p()
+    _check(lib().mg_graph_load(_enc(path), fmt, C.byref(h)))
+    try:
+        g = mg_csr()
+        _check(lib().mg_graph_view(h, C.byref(g)))
+        n = g.rows
+        rp = np.ctypeslib.as_array(C.cast(g.row_ptr, C.POINTER(C.c_int64)), (n + 1,)).copy()
+        nnz = int(rp[-1])
+        if nnz == 0:
+            return rp, np.zeros(0, np.int64), np.zeros(0, np.float32)
+        ci = np.ctypeslib.as_array(C.cast(g.col_idx, C.POINTER(C.c_int64)), (nnz,)).copy()
+        v = np.ctypeslib.as_array(C.cast(g.values, C.POINTER(C.c_float)), (nnz,)).copy()
+        return rp, ci, v
+    finally:
+        lib().mg_graph_free(h)
+
+
+def load_graph(path):
+    """load_graph<float> (dataset.hpp:170-180): (row_ptr, col_idx, values) of the sorted, deduplicated CSR."""
+    return _graph(0, path)
+
+
+def load_matrix_market(path):
+    """load_matrix_market<float> (dataset.hpp:87-143)."""
+    return _graph(1, path)
+
+
+def load_edge_list(path):
+    """load_edge_list<float> (dataset.hpp:147-168)."""
+    return _graph(2, path)
+
+
+def _dense(fn, path) -> np.ndarray:
+    h = C.c_void_p()
+    _check(fn(_enc(path), C.byref(h)))
+    try:
+        r, c, d = C.c_int64(), C.c_int64(), C.c_void_p()
+        _check(lib().mg_dense_view(h, C.byref(r), C.byref(c), C.byref(d)))
+        n = r.value * c.value
+        if n == 0:
+            return np.zeros((r.value, c.value), np.float32)
+        return np.ctypeslib.as_array(C.cast(d, C.POINTER(C.c_float)), (n,)).reshape(r.value, c.value).copy()
+    finally:
+        lib().mg_dense_free(h)
+
+
+def load_features(path) -> np.ndarray:
+    """load_features<float> (dataset.hpp:184-216): MGDM binary or CSV."""
+    return _dense(lib().mg_dense_load, path)
+
+
+def read_dense(path) -> np.ndarray:
+    """read_dense<float> (dense.hpp:311-335)."""
+    return _dense(lib().mg_dense_read, path)
+
+
+def write_dense(path, m):
+    """write_dense<float> (dense.hpp:293-307)."""
+    a = np.ascontiguousarray(m, np.float32)
+    if a.ndim != 2:
+        raise ShapeError(f"write_dense: expected a matrix, got shape {a.shape}")
+    _check(lib().mg_dense_write(_enc(path), a.shape[0], a.shape[1], _p(a)))
+
+
+def load_labels(path) -> np.ndarray:
+    """load_labels (dataset.hpp:218-234)."""
+    cnt = C.c_int64()
+    _check(lib().mg_labels_load(_enc(path), None, 0, C.byref(cnt)))
+    out = np.zeros(cnt.value, np.int32)
+    _check(lib().mg_labels_load(_enc(path), _p(out), cnt.value, C.byref(cnt)))
+    return out[: cnt.value]
+
+
+def load_masks(path, n: int):
+    """load_masks (dataset.hpp:237-262) -> (train, val, test); an absent key gives an empty array."""
+    arrs = [np.zeros(n, np.uint8) for _ in range(3)]
+    present = C.c_int32()
+    _check(lib().mg_masks_load(_enc(path), int(n), *[_p(a) for a in arrs], C.byref(present)))
+    return tuple(a if present.value & (1 << i) else np.zeros(0, np.uint8) for i, a in enumerate(arrs))
+
+
+def load_dataset(graph_path, features_path, labels_path, masks_path="") -> Dataset:
+    """load_dataset<float> (dataset.hpp:264-276); validates like Dataset::validate."""
+    out = C.c_void_p()
+    _check(lib().mg_dataset_load(_enc(graph_path), _enc(features_path), _enc(labels_path),
+                                 _enc(masks_path) if masks_path else None, C.byref(out)))
+    return Dataset(out.value, str(graph_path))
 
 
 def synth_graph(n, avg_degree, exponent, seed, feature_dim=16, classes=4) -> Dataset:
