@@ -238,6 +238,43 @@ mg_status mg_group_last_profile(mg_group* g, double* spmm_us, double* gemm_us, d
                                 int64_t* kernels);
 void mg_group_destroy(mg_group* g);
 
+/* ---------------------------------------------------------------- timeline
+ * rowgcn::TimelineEvent (inc/collectives.hpp:24-34): one record per task the reference submits to a
+ * worker lane — lane 0 compute ("gemm" hw|wgrad|hgrad, "spmm" stage, "other" loss|adam|wgrad_final),
+ * lane 1 comm ("broadcast" h_stage, "reduce" loss|wgrad) — timed by CUDA events on the lane's stream
+ * (lane 0 = compute stream, lane 1 = comm stream), microseconds from the worker's base event. stage is
+ * the staged-SpMM stage (or the layer for gemm / wgrad reduce, -1 otherwise), as in the reference.
+ * The forward ReLU and relu_backward are fused into the SpMM / hgrad epilogues and have no own task. */
+typedef struct mg_timeline_event {
+  int32_t worker, lane, stage, n_deps;
+  char kind[16];
+  char op[16];
+  double t_start_us, t_end_us;
+  uint64_t task;         /* > 0, unique within the group */
+  const uint64_t* deps;  /* n_deps task ids this task waited for */
+} mg_timeline_event;
+
+/* on != 0: clear and start recording every subsequent step (and mg_group_bench_spmm); 0: stop. */
+mg_status mg_group_set_timeline(mg_group* g, int32_t on);
+/* Synchronises and returns the recorded events (borrowed, valid until the next timeline call on g):
+ * *count = number of events; the first min(count, capacity) are copied to out (out may be NULL). */
+mg_status mg_group_timeline(mg_group* g, mg_timeline_event* out, int64_t capacity, int64_t* count);
+/* export_timeline (inc/timeline.hpp:31-36): JSON array, one object per event, reference schema. */
+mg_status mg_timeline_export(const char* path, const mg_timeline_event* ev, int64_t count);
+/* audit_timeline (timeline.hpp:64-94): well formed, per-(worker, lane) non-overlapping, every dependency
+ * finished before its dependent started. MG_VALUE_ERROR with the reference's message on violation. */
+mg_status mg_timeline_audit(const mg_timeline_event* ev, int64_t count);
+/* audit_staged_run (timeline.hpp:96-126) on the events of ONE staged SpMM. */
+mg_status mg_timeline_audit_staged(const mg_timeline_event* ev, int64_t count, int32_t world, int32_t overlapped);
+/* runtime_breakdown (inc/breakdown.hpp:63-82): totals_us = {spmm, gemm, activation, loss, adam, comm}. */
+mg_status mg_timeline_breakdown(const mg_timeline_event* ev, int64_t count, double totals_us[6]);
+
+/* bench-spmm (proj/tools/main.cpp:120-178): one staged SpMM of this group's local feature rows X
+ * (width d0) over the dir tiles (0 forward Â^T, 1 backward Â) into the HW buffer (read with MG_T_HW),
+ * synchronously. Recorded in the timeline when it is on. *wall_us = device time of the run on rank 0's
+ * compute stream. */
+mg_status mg_group_bench_spmm(mg_group* g, int32_t dir, double* wall_us);
+
 /* ---------------------------------------------------------------- kernel-level entry points
  * Device pointers, caller's stream (cudaStream_t passed as void*, NULL = legacy default stream).
  * Used by the parity tests and the micro-benchmarks (the reference's bench-spmm, proj/tools/main.cpp:120-178). */

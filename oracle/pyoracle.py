@@ -173,6 +173,24 @@ class Ref:
         self._check(self.lib.ref_load_masks(str(path).encode(), C.c_int64(n), *[_ptr(a) for a in arrs], C.byref(pr)))
         return tuple(a if pr.value & (1 << i) else np.zeros(0, np.uint8) for i, a in enumerate(arrs))
 
+    def timeline_check(self, path, world=0, overlapped=False):
+        """The reference's load_timeline + audit_timeline (+ audit_staged_run when world > 0) on a JSON
+        file; returns (event count, runtime_breakdown totals dict). Raises OracleError on violation."""
+        t = np.zeros(6, np.float64)
+        cnt = C.c_int64()
+        self._check(self.lib.ref_timeline_check(str(path).encode(), C.c_int32(world), C.c_int32(int(overlapped)),
+                                                _ptr(t), C.byref(cnt)))
+        return cnt.value, dict(zip(("spmm", "gemm", "activation", "loss", "adam", "comm"), t.tolist()))
+
+    def train_timeline(self, ds: Dataset, cfg, workers: int, path):
+        """Exports the reference trainer's own timeline (train_run<float>) to path."""
+        h = self._ds_handle(ds, np.float32)
+        try:
+            self._check(self.lib.ref_train_timeline_f32(C.c_void_p(h), C.byref(cfg), C.c_int32(workers),
+                                                        str(path).encode()))
+        finally:
+            self._ds_free(h, np.float32)
+
     def load_dataset(self, g, f, l, m=""):
         """load_dataset<float> -> (Dataset, (train, val, test))."""
         h = C.c_void_p()

@@ -23,7 +23,9 @@
 #include <string>
 #include <vector>
 
+#include "rowgcn/breakdown.hpp"
 #include "rowgcn/driver.hpp"
+#include "rowgcn/timeline.hpp"
 
 using namespace rowgcn;
 
@@ -461,6 +463,32 @@ int ref_load_masks(const char* path, int64_t n, uint8_t* train, uint8_t* val, ui
 int ref_load_dataset_f32(const char* g, const char* f, const char* l, const char* m, void** out) {
   return guarded([&] { *out = new Dataset<float>(load_dataset<float>(g, f, l, m ? m : "")); });
 }
+// ---------------------------------------------------------------- timeline (timeline.hpp, breakdown.hpp)
+// Loads a timeline JSON with the reference's own load_timeline, runs audit_timeline, optionally
+// audit_staged_run (world > 0), and returns runtime_breakdown totals {spmm, gemm, activation, loss, adam,
+// comm} and the event count.
+int ref_timeline_check(const char* path, int32_t world, int32_t overlapped, double* totals, int64_t* count) {
+  return guarded([&] {
+    const auto ev = load_timeline(path);
+    *count = static_cast<int64_t>(ev.size());
+    audit_timeline(ev);
+    if (world > 0) audit_staged_run(ev, world, overlapped != 0);
+    const auto rep = runtime_breakdown(ev);
+    const double t[6] = {rep.spmm_us, rep.gemm_us, rep.activation_us, rep.loss_us, rep.adam_us, rep.comm_us};
+    std::memcpy(totals, t, sizeof(t));
+  });
+}
+// The reference's own training-run timeline (DeviceGroup, threads as GPUs) exported to path: the
+// structural template the device timeline mirrors (kinds, ops, stages, lanes, dependency shape).
+int ref_train_timeline_f32(void* dsh, const RefCfg* c, int32_t workers, const char* path) {
+  return guarded([&] {
+    TrainOptions opts;
+    opts.workers = workers;
+    const auto art = train_run<float>(*static_cast<Dataset<float>*>(dsh), to_cfg(c), opts);
+    export_timeline(path, art.timeline);
+  });
+}
+
 void ref_ds_masks_f32(void* h, uint8_t* train, uint8_t* val, uint8_t* test, int32_t* present) {
   auto* ds = static_cast<Dataset<float>*>(h);
   *present = (ds->train_mask.empty() ? 0 : 1) | (ds->val_mask.empty() ? 0 : 2) | (ds->test_mask.empty() ? 0 : 4);

@@ -24,6 +24,12 @@ class mg_config(C.Structure):
                 ("aggregate_input", C.c_int32)]
 
 
+class mg_timeline_event(C.Structure):
+    _fields_ = [("worker", C.c_int32), ("lane", C.c_int32), ("stage", C.c_int32), ("n_deps", C.c_int32),
+                ("kind", C.c_char * 16), ("op", C.c_char * 16), ("t_start_us", C.c_double),
+                ("t_end_us", C.c_double), ("task", C.c_uint64), ("deps", C.POINTER(C.c_uint64))]
+
+
 # (name, restype, argtypes) for every symbol declared in include/mggcn.h
 SIGNATURES = [
     ("mg_config_defaults", None, [C.c_void_p]),
@@ -76,6 +82,13 @@ SIGNATURES = [
     ("mg_group_buffer_audit", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("mg_group_last_profile", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("mg_group_destroy", None, [C.c_void_p]),
+    ("mg_group_set_timeline", C.c_int, [C.c_void_p, C.c_int32]),
+    ("mg_group_timeline", C.c_int, [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]),
+    ("mg_timeline_export", C.c_int, [C.c_char_p, C.c_void_p, C.c_int64]),
+    ("mg_timeline_audit", C.c_int, [C.c_void_p, C.c_int64]),
+    ("mg_timeline_audit_staged", C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32]),
+    ("mg_timeline_breakdown", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
+    ("mg_group_bench_spmm", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     ("mg_dev_spmm", C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                               C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     ("mg_dev_gemm", C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,

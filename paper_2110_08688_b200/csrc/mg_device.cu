@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -192,6 +193,40 @@ static void launch_fast(const FastLaunch& t, const float* h, float* out, float* 
   MG_LAUNCHED();
 }
 
+std::atomic<int> g_spmm_async{1};  // MG_SPMM_FAST gathers through the cp.async ring (spmm_fast_async)
+
+template <int G, int CPL, int E, int D>
+static void launch_fast_async(const FastLaunch& t, const float* h, float* out, float* scratch, int ld, int nchunk,
+                              int acc, int relu, cudaStream_t s) {
+  constexpr int kThreads = 128;
+  constexpr size_t smem = sizeof(float4) * kThreads * D * E * CPL;
+  static int blocks_per_sm = 0;
+  if (!blocks_per_sm) {
+    MG_CUDA(cudaFuncSetAttribute(k::spmm_fast_async<G, CPL, E, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k::spmm_fast_async<G, CPL, E, D>, kThreads,
+                                                          smem));
+    blocks_per_sm = std::max(1, blocks_per_sm);
+  }
+  const int gpb = kThreads / G;
+  const int blocks = std::min(ceil_div(t.n_items, gpb), num_sms() * blocks_per_sm);
+  k::spmm_fast_async<G, CPL, E, D><<<blocks, kThreads, smem, s>>>(t.items, t.n_items, t.edges, h, out, scratch, ld,
+                                                                  nchunk, acc, relu);
+  MG_LAUNCHED();
+}
+
+// cp.async-pipelined variants for rows of >= 32 floats; false = use the register-gather kernel.
+static bool launch_fast_pipelined(const FastLaunch& t, const float* hs, float* os, float* ss, int L, int nchunk,
+                                  int acc, int relu, cudaStream_t s) {
+  if (!g_spmm_async.load() || nchunk < 8) return false;
+  if (nchunk <= 16) launch_fast_async<16, 1, 4, 4>(t, hs, os, ss, L, nchunk, acc, relu, s);
+  else if (nchunk <= 32) launch_fast_async<32, 1, 4, 4>(t, hs, os, ss, L, nchunk, acc, relu, s);
+  else if (nchunk <= 64) launch_fast_async<32, 2, 4, 4>(t, hs, os, ss, L, nchunk, acc, relu, s);
+  else if (nchunk <= 128) launch_fast_async<32, 4, 2, 4>(t, hs, os, ss, L, nchunk, acc, relu, s);
+  else return false;
+  return true;
+}
+
 // MG_SPMM_FAST: one gather pass over rows + hub segments, then the ordered hub-segment sum.
 static int spmm_fast(const FastLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, cudaStream_t s) {
   int launches = 0;
@@ -204,7 +239,8 @@ static int spmm_fast(const FastLaunch& t, const float* h, float* out, index_t ld
       float* os = out + 4 * c0;
       float* ss = t.scratch ? t.scratch + 4 * c0 : nullptr;
       const int L = static_cast<int>(ld);
-      if (nchunk <= 1) launch_fast<1, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      if (launch_fast_pipelined(t, hs, os, ss, L, nchunk, acc, relu, s)) {
+      } else if (nchunk <= 1) launch_fast<1, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
       else if (nchunk <= 2) launch_fast<2, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
       else if (nchunk <= 4) launch_fast<4, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
       else if (nchunk <= 8) launch_fast<8, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
@@ -290,6 +326,11 @@ struct Worker {
   cudaEvent_t prior, heavy_fork, heavy_join, loss_done, stats_done, src_ready, copy_done, ar_ready, ar_done;
   std::vector<cudaEvent_t> bc_done, mult, wg_done, red_done;
   cudaEvent_t t_start, t_end;
+  // timeline recorder (mg_group_set_timeline): timing events on the task's lane stream, base on s0
+  std::vector<cudaEvent_t> tl_pool;
+  size_t tl_used = 0;
+  cudaEvent_t tl_base = nullptr;
+  uint64_t last_task[2] = {0, 0};  // last recorded task per lane (WorkerCtx::last, collectives.hpp)
   std::vector<void*> allocs;
   index_t bytes = 0;
 };
@@ -317,6 +358,19 @@ struct mg_group {
   std::vector<std::pair<int, int>> prof_pending;  // (kind, index of the start event)
   double last_loss = 0, last_acc = 0;
   bool stats_pending = false;
+  // timeline (rowgcn::TimelineEvent, collectives.hpp:24-34): one record per task, times resolved on drain
+  struct TlRec {
+    int worker_k, lane, stage;
+    const char* kind;
+    const char* op;
+    uint64_t task;
+    std::vector<uint64_t> deps;
+    size_t ev;  // start event index in the worker's pool (end = ev + 1)
+  };
+  bool tl_on = false;
+  uint64_t tl_next = 1;
+  std::vector<TlRec> tl;
+  std::vector<mg_timeline_event> tl_out;  // last drained events (deps point into tl)
 };
 
 namespace mg {
@@ -493,17 +547,24 @@ class Step {
                    bool relu_last) {
     const index_t ld = pad4(width);
     const bool ov = cfg_.overlap;
+    std::vector<uint64_t> prior_task(nloc());
+    std::vector<std::vector<uint64_t>> mult_task(nloc(), std::vector<uint64_t>(P_, 0));
     for (size_t k = 0; k < nloc(); ++k) {
       dev(W(k));
       MG_CUDA(cudaEventRecord(W(k).prior, W(k).s0));
+      prior_task[k] = W(k).last_task[0];
     }
     for (int j = 0; j < P_; ++j) {
       std::vector<float*> recv(nloc());
+      std::vector<int> tb(nloc(), -1);
       for (size_t k = 0; k < nloc(); ++k) {
         Worker& w = W(k);
         dev(w);
         cudaEvent_t dep = ov ? (j >= 2 ? w.mult[j - 2] : w.prior) : (j >= 1 ? w.mult[j - 1] : w.prior);
         MG_CUDA(cudaStreamWaitEvent(w.s1, dep, 0));
+        const uint64_t dep_task = ov ? (j >= 2 ? mult_task[k][j - 2] : prior_task[k])
+                                     : (j >= 1 ? mult_task[k][j - 1] : prior_task[k]);
+        tb[k] = tl_begin(k, 1, "broadcast", "h_stage", j, {dep_task});
         recv[k] = (w.rank == j) ? src[k] : ((!ov || j % 2 == 0) ? w.bc1 : w.bc2);
       }
       const size_t count = static_cast<size_t>((g_.bounds[j + 1] - g_.bounds[j]) * ld);
@@ -511,8 +572,10 @@ class Step {
       for (size_t k = 0; k < nloc(); ++k) {
         Worker& w = W(k);
         dev(w);
+        const uint64_t bc_task = tl_end(k, tb[k]);
         MG_CUDA(cudaEventRecord(w.bc_done[j], w.s1));
         MG_CUDA(cudaStreamWaitEvent(w.s0, w.bc_done[j], 0));
+        const int ts = tl_begin(k, 0, "spmm", "stage", j, {bc_task});
         const DevTile& t = w.tiles[dir][j];
         SpmmLaunch sl{t.row_ptr, t.edges, t.light, t.n_light, t.heavy, t.n_heavy};
         const int acc = j > 0, relu = relu_last && j == P_ - 1;
@@ -521,6 +584,7 @@ class Step {
           FastLaunch fl{t.items, t.n_items, t.hubs, t.n_hubs, t.edges, w.seg_scratch};
           g_.kernels_last += spmm_fast(fl, recv[k], out[k], ld, acc, relu, w.s0);
           prof_end(w, pi, 0);
+          mult_task[k][j] = tl_end(k, ts);
           MG_CUDA(cudaEventRecord(w.mult[j], w.s0));
           continue;
         }
@@ -533,17 +597,47 @@ class Step {
         g_.kernels_last += spmm_light(sl, recv[k], out[k], ld, acc, relu, w.s0);
         if (t.n_heavy > 0) MG_CUDA(cudaStreamWaitEvent(w.s0, w.heavy_join, 0));
         prof_end(w, pi, 0);
+        mult_task[k][j] = tl_end(k, ts);
         MG_CUDA(cudaEventRecord(w.mult[j], w.s0));
       }
     }
   }
 
-  void gemm(Worker& w, bool ta, bool tb, index_t M, index_t N, index_t K, const float* A, index_t lda, const float* B,
-            index_t ldb, float* Cm, index_t ldc, int epi) {
+  // one GeMM task ("gemm", op, layer) on the compute lane, depending on the lane's previous task
+  void gemm(size_t k, const char* op, int layer, bool ta, bool tb, index_t M, index_t N, index_t K, const float* A,
+            index_t lda, const float* B, index_t ldb, float* Cm, index_t ldc, int epi) {
+    Worker& w = W(k);
+    const int th = tl_begin(k, 0, "gemm", op, layer, {w.last_task[0]});
     const int pi = prof_begin(w);
     g_.kernels_last += gemm_launch(cfg_.gemm_mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, w.s0, w.ws, w.ws_bytes);
     prof_end(w, pi, 1);
+    tl_end(k, th);
   }
+
+  // -------------------------------------------------------------- timeline (collectives.hpp:119-140)
+  // Every task the reference submits to a lane (WorkerCtx::submit) is bracketed by a timing-event pair
+  // on the matching stream: lane 0 = compute stream, lane 1 = comm stream. Returns a handle for tl_end.
+  int tl_begin(size_t k, int lane, const char* kind, const char* op, int stage, std::vector<uint64_t> deps) {
+    if (!g_.tl_on) return -1;
+    Worker& w = W(k);
+    if (w.tl_used + 2 > w.tl_pool.size())
+      for (int i = 0; i < 256; ++i) w.tl_pool.push_back(mk_event(true));
+    const size_t ev = w.tl_used;
+    w.tl_used += 2;
+    MG_CUDA(cudaEventRecord(w.tl_pool[ev], lane == 0 ? w.s0 : w.s1));
+    deps.erase(std::remove(deps.begin(), deps.end(), uint64_t{0}), deps.end());
+    g_.tl.push_back({static_cast<int>(k), lane, stage, kind, op, g_.tl_next++, std::move(deps), ev});
+    return static_cast<int>(g_.tl.size() - 1);
+  }
+  uint64_t tl_end(size_t k, int h) {
+    if (h < 0) return 0;
+    Worker& w = W(k);
+    auto& r = g_.tl[static_cast<size_t>(h)];
+    MG_CUDA(cudaEventRecord(w.tl_pool[r.ev + 1], r.lane == 0 ? w.s0 : w.s1));
+    w.last_task[r.lane] = r.task;
+    return r.task;
+  }
+  uint64_t tl_task(int h) const { return h < 0 ? 0 : g_.tl[static_cast<size_t>(h)].task; }
 
   // -------------------------------------------------------------- optional per-kernel timing
   // Event pairs on the launching (compute) stream of the first local worker; enabled with
@@ -580,7 +674,7 @@ class Step {
         for (size_t k = 0; k < nloc(); ++k) {
           Worker& w = W(k);
           dev(w);
-          gemm(w, false, false, w.rows, ldl1, dl, w.ax, ldl, w.W[0], ldl1, w.ahw[0], ldl1, L_ > 1 ? 2 : 0);
+          gemm(k, "hw", 0, false, false, w.rows, ldl1, dl, w.ax, ldl, w.W[0], ldl1, w.ahw[0], ldl1, L_ > 1 ? 2 : 0);
         }
         continue;
       }
@@ -589,7 +683,7 @@ class Step {
         dev(w);
         const float* h_in = l == 0 ? w.x : w.ahw[l - 1];
         if (!swap) {
-          gemm(w, false, false, w.rows, ldl1, dl, h_in, ldl, w.W[l], ldl1, w.hw, ldl1, 0);
+          gemm(k, "hw", l, false, false, w.rows, ldl1, dl, h_in, ldl, w.W[l], ldl1, w.hw, ldl1, 0);
           src[k] = w.hw;
         } else {
           src[k] = const_cast<float*>(h_in);
@@ -601,7 +695,7 @@ class Step {
         for (size_t k = 0; k < nloc(); ++k) {
           Worker& w = W(k);
           dev(w);
-          gemm(w, false, false, w.rows, ldl1, dl, w.hw, ldl, w.W[l], ldl1, w.ahw[l], ldl1, l < L_ - 1 ? 2 : 0);
+          gemm(k, "hw", l, false, false, w.rows, ldl1, dl, w.hw, ldl, w.W[l], ldl1, w.ahw[l], ldl1, l < L_ - 1 ? 2 : 0);
         }
       }
     }
@@ -612,9 +706,11 @@ class Step {
     const index_t C = cfg_.dims[L_];
     const float inv_denom = 1.0f / static_cast<float>(g_.mask_count);
     std::vector<double*> st(nloc());
+    std::vector<int> tr(nloc(), -1);
     for (size_t k = 0; k < nloc(); ++k) {
       Worker& w = W(k);
       dev(w);
+      const int th = tl_begin(k, 0, "other", "loss", -1, {w.last_task[0]});
       const int pi = prof_begin(w);
       if (w.rows > 0) {
         k::softmax_xent<<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
@@ -627,8 +723,10 @@ class Step {
       MG_LAUNCHED();
       ++g_.kernels_last;
       prof_end(w, pi, 2);
+      const uint64_t loss_task = tl_end(k, th);
       MG_CUDA(cudaEventRecord(w.loss_done, w.s0));
       MG_CUDA(cudaStreamWaitEvent(w.s1, w.loss_done, 0));
+      tr[k] = tl_begin(k, 1, "reduce", "loss", -1, {loss_task});
       st[k] = w.stats;
     }
     allreduce<double>(2, st);
@@ -636,6 +734,7 @@ class Step {
       Worker& w = W(k);
       dev(w);
       MG_CUDA(cudaMemcpyAsync(w.h_stats, w.stats, 2 * sizeof(double), cudaMemcpyDeviceToHost, w.s1));
+      tl_end(k, tr[k]);
       MG_CUDA(cudaEventRecord(w.stats_done, w.s1));
     }
   }
@@ -661,11 +760,13 @@ class Step {
       }
       // W_G staging over the 8 canonical row blocks (gcn.hpp:309-331), then one all-reduce.
       std::vector<float*> stg(nloc());
+      std::vector<int> trd(nloc(), -1);
       const index_t bs = ldl * ldl1;
       for (size_t k = 0; k < nloc(); ++k) {
         Worker& w = W(k);
         dev(w);
         const float* h_in = l == 0 ? (agg ? w.ax : w.x) : w.ahw[l - 1];
+        const int tw = tl_begin(k, 0, "gemm", "wgrad", l, {w.last_task[0]});
         if (cfg_.gemm_mode != MG_GEMM_EXACT) {  // one tcgen05 launch for all 8 blocks (+ ordered reduction)
           int64_t begin[8], len[8];
           for (int b = 0; b < 8; ++b) {
@@ -685,25 +786,30 @@ class Step {
               MG_CUDA(cudaMemsetAsync(dst, 0, sizeof(float) * bs, w.s0));
               continue;
             }
-            gemm(w, true, false, ldl, ldl1, e - a, h_in + (a - w.r0) * ldl, ldl, grad_rows[k] + (a - w.r0) * ldl1,
-                 ldl1, dst, ldl1, 0);
+            const int pi = prof_begin(w);
+            g_.kernels_last += gemm_launch(cfg_.gemm_mode, true, false, ldl, ldl1, e - a, h_in + (a - w.r0) * ldl, ldl,
+                                           grad_rows[k] + (a - w.r0) * ldl1, ldl1, dst, ldl1, 0, w.s0, w.ws, w.ws_bytes);
+            prof_end(w, pi, 1);
           }
         }
+        const uint64_t wg_task = tl_end(k, tw);
         MG_CUDA(cudaEventRecord(w.wg_done[l], w.s0));
         MG_CUDA(cudaStreamWaitEvent(w.s1, w.wg_done[l], 0));
+        trd[k] = tl_begin(k, 1, "reduce", "wgrad", l, {wg_task});
         stg[k] = w.stage[l];
       }
       allreduce<float>(static_cast<size_t>(8 * bs), stg);
       for (size_t k = 0; k < nloc(); ++k) {
         Worker& w = W(k);
         dev(w);
+        red_task_[k].push_back(tl_end(k, trd[k]));
         MG_CUDA(cudaEventRecord(w.red_done[l], w.s1));
       }
       if (l > 0) {  // H_G = HW_G W^T fused with relu_backward into ahw[l-1] (gcn.hpp:337-348)
         for (size_t k = 0; k < nloc(); ++k) {
           Worker& w = W(k);
           dev(w);
-          gemm(w, false, true, w.rows, ldl, dl1, grad_rows[k], ldl1, w.W[l], ldl1, w.ahw[l - 1], ldl, 1);
+          gemm(k, "hgrad", l, false, true, w.rows, ldl, dl1, grad_rows[k], ldl1, w.W[l], ldl1, w.ahw[l - 1], ldl, 1);
         }
       }
       (void)dl;
@@ -728,6 +834,9 @@ class Step {
       Worker& w = W(k);
       dev(w);
       for (int l = 0; l < L_; ++l) MG_CUDA(cudaStreamWaitEvent(w.s0, w.red_done[l], 0));
+      std::vector<uint64_t> deps = red_task_[k];
+      deps.push_back(w.last_task[0]);
+      const int th = tl_begin(k, 0, "other", adam ? "adam" : "wgrad_final", -1, std::move(deps));
       const int pi = prof_begin(w);
       for (int l = 0; l < L_; ++l) {
         const int size = static_cast<int>(g_.ld[l] * g_.ld[l + 1]);
@@ -737,6 +846,7 @@ class Step {
         ++g_.kernels_last;
       }
       prof_end(w, pi, 2);
+      tl_end(k, th);
     }
   }
 
@@ -765,6 +875,7 @@ class Step {
   mg_group& g_;
   const Config& cfg_;
   int L_, P_;
+  std::vector<std::vector<uint64_t>> red_task_ = std::vector<std::vector<uint64_t>>(g_.workers.size());
 };
 
 void sync_all(mg_group& g) {
@@ -806,6 +917,8 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
     } else if (k == "spmm_slab") {
       if (value < 0 || value % 4) throw ValueError("tuning: spmm_slab must be 0 or a multiple of 4 floats");
       g_spmm_slab = static_cast<int>(std::min<int64_t>(value, 1024));
+    } else if (k == "spmm_async") {
+      g_spmm_async = value != 0 ? 1 : 0;
     } else if (k == "fast_segment") {
       if (value < 32) throw ValueError("tuning: fast_segment must be >= 32");
       g_fast_segment = static_cast<int>(std::min<int64_t>(value, 1 << 24));
@@ -1252,8 +1365,9 @@ void mg_group_destroy(mg_group* g) {
     for (cudaEvent_t e : {w.prior, w.heavy_fork, w.heavy_join, w.loss_done, w.stats_done, w.src_ready, w.copy_done,
                           w.ar_ready, w.ar_done, w.t_start, w.t_end})
       cudaEventDestroy(e);
-    for (auto* vec : {&w.bc_done, &w.mult, &w.wg_done, &w.red_done})
+    for (auto* vec : {&w.bc_done, &w.mult, &w.wg_done, &w.red_done, &w.tl_pool})
       for (cudaEvent_t e : *vec) cudaEventDestroy(e);
+    if (w.tl_base) cudaEventDestroy(w.tl_base);
     cudaStreamDestroy(w.s0);
     cudaStreamDestroy(w.s1);
     cudaStreamDestroy(w.s2);
@@ -1261,6 +1375,81 @@ void mg_group_destroy(mg_group* g) {
   if (!g->workers.empty()) cudaSetDevice(g->workers[0]->device);
   for (cudaEvent_t e : g->prof_pool) cudaEventDestroy(e);
   delete g;
+}
+
+// ---------------------------------------------------------------- timeline / bench-spmm
+mg_status mg_group_set_timeline(mg_group* g, int32_t on) {
+  return guarded([&] {
+    if (!g) throw ValueError("group: null");
+    sync_all(*g);
+    if (on) {
+      g->tl.clear();
+      g->tl_out.clear();
+      g->tl_next = 1;
+      for (auto& wp : g->workers) {
+        Worker& w = *wp;
+        MG_CUDA(cudaSetDevice(w.device));
+        if (!w.tl_base) w.tl_base = mk_event(true);
+        MG_CUDA(cudaEventRecord(w.tl_base, w.s0));
+        w.tl_used = 0;
+        w.last_task[0] = w.last_task[1] = 0;
+      }
+    }
+    g->tl_on = on != 0;
+  });
+}
+
+mg_status mg_group_timeline(mg_group* g, mg_timeline_event* out, int64_t capacity, int64_t* count) {
+  return guarded([&] {
+    if (!g || !count) throw ValueError("timeline: null argument");
+    sync_all(*g);
+    g->tl_out.clear();
+    for (const auto& r : g->tl) {
+      Worker& w = *g->workers[static_cast<size_t>(r.worker_k)];
+      MG_CUDA(cudaSetDevice(w.device));
+      float a = 0.f, b = 0.f;
+      MG_CUDA(cudaEventElapsedTime(&a, w.tl_base, w.tl_pool[r.ev]));
+      MG_CUDA(cudaEventElapsedTime(&b, w.tl_base, w.tl_pool[r.ev + 1]));
+      mg_timeline_event e{};
+      e.worker = w.rank;
+      e.lane = r.lane;
+      e.stage = r.stage;
+      e.n_deps = static_cast<int32_t>(r.deps.size());
+      std::snprintf(e.kind, sizeof(e.kind), "%s", r.kind);
+      std::snprintf(e.op, sizeof(e.op), "%s", r.op);
+      e.t_start_us = 1000.0 * a;
+      e.t_end_us = 1000.0 * b;
+      e.task = r.task;
+      e.deps = r.deps.empty() ? nullptr : r.deps.data();
+      g->tl_out.push_back(e);
+    }
+    *count = static_cast<int64_t>(g->tl_out.size());
+    if (out)
+      std::copy(g->tl_out.begin(), g->tl_out.begin() + std::min<int64_t>(capacity, *count), out);
+  });
+}
+
+mg_status mg_group_bench_spmm(mg_group* g, int32_t dir, double* wall_us) {
+  return guarded([&] {
+    if (!g) throw ValueError("group: null");
+    if (dir != 0 && dir != 1) throw ValueError("bench_spmm: dir must be 0 (forward) or 1 (backward)");
+    Step st(*g);
+    std::vector<float*> src, out;
+    for (auto& wp : g->workers) {
+      src.push_back(wp->x);
+      out.push_back(wp->hw);
+    }
+    Worker& w0 = *g->workers[0];
+    MG_CUDA(cudaSetDevice(w0.device));
+    MG_CUDA(cudaEventRecord(w0.t_start, w0.s0));
+    st.staged_spmm(dir, g->cfg.dims[0], src, out, false);
+    MG_CUDA(cudaSetDevice(w0.device));
+    MG_CUDA(cudaEventRecord(w0.t_end, w0.s0));
+    sync_all(*g);
+    float ms = 0.f;
+    MG_CUDA(cudaEventElapsedTime(&ms, w0.t_start, w0.t_end));
+    if (wall_us) *wall_us = 1000.0 * ms;
+  });
 }
 
 // ---------------------------------------------------------------- kernel-level entry points

@@ -202,6 +202,109 @@ __global__ void __launch_bounds__(256) spmm_fast_items(const int4* __restrict__ 
   }
 }
 
+// MG_SPMM_FAST, cp.async-pipelined: the same per-lane FMA chain as spmm_fast_items (bitwise identical
+// results), but the h-row gathers land in a per-group shared-memory ring (LDGSTS, no registers held while
+// in flight), so D-1 stages of E nonzeros stay in flight per group instead of U. The gather addresses come
+// from edge records held in three rotating G-record register windows (current, next, prefetched), so no
+// gather waits on its own edge-record load. Requires E | G and (D - 1) * E <= G.
+__device__ __forceinline__ void cp_async16_cg(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int G, int CPL, int E, int D>
+__global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ items, int n_items,
+                                                       const int2* __restrict__ edges, const float* __restrict__ h,
+                                                       float* __restrict__ out, float* __restrict__ scratch, int ld,
+                                                       int nchunk, int accumulate, int relu) {
+  static_assert(G % E == 0 && (D - 1) * E <= G, "pipeline depth must stay within one record window");
+  extern __shared__ float4 ring_all[];
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  float4* ring = ring_all + (size_t)(threadIdx.x / G) * (D * E * CPL * G);  // [D][E][CPL][G]
+  const int groups = gridDim.x * (blockDim.x / G);
+  for (int idx = blockIdx.x * (blockDim.x / G) + threadIdx.x / G; idx < n_items; idx += groups) {
+    const int4 it = __ldg(items + idx);
+    const int e0 = it.x, n = it.y - it.x;
+    const bool seg = it.z < 0;
+    float* orow = seg ? scratch + (size_t)(-it.z - 1) * ld : out + (size_t)it.z * ld;
+    float4 acc[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int c = lane + k * G;
+      acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (!seg && accumulate && c < nchunk) acc[k] = *reinterpret_cast<const float4*>(orow + 4 * c);
+    }
+    auto win = [&](int w) {
+      const int i = w * G + lane;
+      return i < n ? ld_edge(edges + e0 + i) : make_int2(0, 0);
+    };
+    int2 wa = win(0), wb = win(1), wc = win(2);  // records of windows wi, wi + 1, wi + 2
+    int wi = 0;
+    const int nst = (n + E - 1) / E;
+    auto issue = [&](int t) {  // gathers of stage t (edges t*E .. t*E+E-1) into slot t % D
+      float4* slot = ring + (t % D) * (E * CPL * G);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = t * E + e;
+        const int src = (i / G == wi) ? wa.x : wb.x;
+        const int col = __shfl_sync(gmask, src, i & (G - 1), G);
+        if (i < n) {
+          const float* hr = h + (size_t)col * ld;
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) {
+            const int c = lane + k * G;
+            if (c < nchunk) cp_async16_cg(slot + (e * CPL + k) * G + lane, hr + 4 * c);
+          }
+        }
+      }
+    };
+#pragma unroll
+    for (int t = 0; t < D - 1; ++t) {
+      if (t < nst) issue(t);
+      cp_async_commit();
+    }
+    for (int t = 0; t < nst; ++t) {
+      if (t > 0 && (t * E) % G == 0) {  // consumption enters window wi + 1
+        wa = wb;
+        wb = wc;
+        ++wi;
+        wc = win(wi + 2);
+      }
+      if (t + D - 1 < nst) issue(t + D - 1);
+      cp_async_commit();
+      cp_async_wait<D - 1>();
+      const float4* slot = ring + (t % D) * (E * CPL * G);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = t * E + e;
+        const float v = __int_as_float(__shfl_sync(gmask, wa.y, i & (G - 1), G));
+        if (i < n) {
+#pragma unroll
+          for (int k = 0; k < CPL; ++k)
+            if (lane + k * G < nchunk) fma4(acc[k], v, slot[(e * CPL + k) * G + lane]);
+        }
+      }
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int c = lane + k * G;
+      if (c < nchunk) {
+        float4 a = acc[k];
+        if (relu && !seg) a = make_float4(relu1(a.x), relu1(a.y), relu1(a.z), relu1(a.w));
+        *reinterpret_cast<float4*>(orow + 4 * c) = a;
+      }
+    }
+  }
+}
+
 // hubs[i] = {row, first segment, segment count}: out[row] = (acc ? out[row] : 0) + sum of its segments in
 // order, then relu. One CTA per hub row, threads over float4 chunks.
 __global__ void __launch_bounds__(256) spmm_fast_hubs(const int4* __restrict__ hubs, const float* __restrict__ scratch,

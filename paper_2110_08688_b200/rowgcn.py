@@ -25,7 +25,7 @@ from typing import Callable, Optional
 
 import numpy as np
 
-from ._lib import lib, mg_config, mg_csr
+from ._lib import lib, mg_config, mg_csr, mg_timeline_event
 
 # ----------------------------------------------------------------------------- errors (inc/errors.hpp)
 
@@ -509,6 +509,24 @@ class Group:
     def forward(self):
         _check(lib().mg_group_forward(self._h))
 
+    def set_timeline(self, on: bool):
+        """Start (clearing) / stop recording TimelineEvents from CUDA events (mg_group_set_timeline)."""
+        _check(lib().mg_group_set_timeline(self._h, int(bool(on))))
+
+    def timeline(self) -> list:
+        """The recorded events (rowgcn::DeviceGroup::timeline)."""
+        cnt = C.c_int64()
+        _check(lib().mg_group_timeline(self._h, None, 0, C.byref(cnt)))
+        buf = (mg_timeline_event * max(1, cnt.value))()
+        _check(lib().mg_group_timeline(self._h, buf, cnt.value, C.byref(cnt)))
+        return [_from_c_event(buf[i]) for i in range(cnt.value)]
+
+    def bench_spmm(self, direction: int = 0) -> float:
+        """One staged SpMM of the local X rows (mg_group_bench_spmm); returns its device time in us."""
+        us = C.c_double()
+        _check(lib().mg_group_bench_spmm(self._h, direction, C.byref(us)))
+        return us.value
+
     def rows(self, rank: int):
         b, n = C.c_int64(), C.c_int64()
         _check(lib().mg_group_rows(self._h, rank, C.byref(b), C.byref(n)))
@@ -589,6 +607,7 @@ class TrainArtifacts:
     final_w: list = field(default_factory=list)   # rank 0's replicas
     logits: Optional[np.ndarray] = None           # gathered post-training logits (permuted order)
     workers: int = 1
+    timeline: list = field(default_factory=list)  # TimelineEvent per task, every epoch (CUDA events)
 
     def final_loss(self):
         return self.epoch_loss[-1] if self.epoch_loss else 0.0
@@ -606,6 +625,7 @@ def train_run(ds: Dataset, cfg: GcnConfig, opts: TrainOptions = TrainOptions()) 
     art = TrainArtifacts(workers=opts.workers)
     with Group(cfg, prep, opts.workers, devices=opts.devices, transport=opts.transport) as g:
         g.init_params()
+        g.set_timeline(True)
         for e in range(1, cfg.epochs + 1):
             loss = g.train_step(e)
             art.epoch_loss.append(loss)
@@ -614,6 +634,8 @@ def train_run(ds: Dataset, cfg: GcnConfig, opts: TrainOptions = TrainOptions()) 
             art.w_hashes.append([g.w_hash(r) for r in range(opts.workers)])
             if opts.on_epoch:
                 opts.on_epoch(e, loss, g.last_accuracy, g.last_wall_us)
+        art.timeline = g.timeline()
+        g.set_timeline(False)
         if opts.collect_logits:
             g.loss_only()
             art.logits = np.concatenate([g.logits(r) for r in range(opts.workers)], axis=0)
@@ -650,6 +672,165 @@ def fnv1a(arrays, h: int = 0xcbf29ce484222325) -> int:
             h ^= int(byte)
             h = (h * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
     return h
+
+
+# ----------------------------------------------------------------------------- timeline (inc/timeline.hpp)
+
+
+@dataclass
+class TimelineEvent:
+    """rowgcn::TimelineEvent (inc/collectives.hpp:24-34)."""
+    worker: int = 0
+    lane: int = 0
+    stage: int = -1
+    kind: str = ""
+    op: str = ""
+    t_start_us: float = 0.0
+    t_end_us: float = 0.0
+    task: int = 0
+    deps: list = field(default_factory=list)
+
+
+def _from_c_event(e) -> TimelineEvent:
+    return TimelineEvent(e.worker, e.lane, e.stage, e.kind.decode(), e.op.decode(), e.t_start_us, e.t_end_us,
+                         int(e.task), [int(e.deps[i]) for i in range(e.n_deps)])
+
+
+def _to_c_events(events):
+    arr = (mg_timeline_event * max(1, len(events)))()
+    keep = []
+    for i, e in enumerate(events):
+        d = (C.c_uint64 * max(1, len(e.deps)))(*e.deps)
+        keep.append(d)
+        arr[i] = mg_timeline_event(e.worker, e.lane, e.stage, len(e.deps), e.kind.encode()[:15], e.op.encode()[:15],
+                                   e.t_start_us, e.t_end_us, e.task, C.cast(d, C.POINTER(C.c_uint64)))
+    return arr, keep
+
+
+def timeline_to_json(events) -> list:
+    """inc/timeline.hpp:15-28."""
+    return [{"worker": e.worker, "lane": e.lane, "stage": e.stage, "kind": e.kind, "op": e.op,
+             "t_start_us": e.t_start_us, "t_end_us": e.t_end_us, "task": e.task, "deps": list(e.deps)}
+            for e in events]
+
+
+def export_timeline(path, events):
+    """inc/timeline.hpp:31-36 (native writer, mg_timeline_export)."""
+    arr, _keep = _to_c_events(events)
+    _check(lib().mg_timeline_export(_enc(path), arr, len(events)))
+
+
+def parse_timeline(arr) -> list:
+    """inc/timeline.hpp:38-55."""
+    out = []
+    for j in arr:
+        out.append(TimelineEvent(int(j["worker"]), int(j["lane"]), int(j["stage"]), str(j["kind"]),
+                                 str(j.get("op", "")), float(j["t_start_us"]), float(j["t_end_us"]),
+                                 int(j.get("task", 0)), [int(d) for d in j.get("deps", [])]))
+    return out
+
+
+def load_timeline(path) -> list:
+    """inc/timeline.hpp:57-63."""
+    try:
+        with open(path) as f:
+            return parse_timeline(json.load(f))
+    except OSError as ex:
+        raise IoError(f"cannot open {path}") from ex
+
+
+def audit_timeline(events):
+    """inc/timeline.hpp:64-94 (native, mg_timeline_audit): raises ValueError on violation."""
+    arr, _keep = _to_c_events(events)
+    _check(lib().mg_timeline_audit(arr, len(events)))
+
+
+def audit_staged_run(events, world: int, overlapped: bool):
+    """inc/timeline.hpp:96-126 (native, mg_timeline_audit_staged) on one staged SpMM's events."""
+    arr, _keep = _to_c_events(events)
+    _check(lib().mg_timeline_audit_staged(arr, len(events), int(world), int(bool(overlapped))))
+
+
+def timeline_span_us(events) -> float:
+    """inc/timeline.hpp:128-137."""
+    if not events:
+        return 0.0
+    return max(e.t_end_us for e in events) - min(e.t_start_us for e in events)
+
+
+@dataclass
+class BreakdownReport:
+    """rowgcn::BreakdownReport (inc/breakdown.hpp:14-61)."""
+    spmm_us: float = 0.0
+    gemm_us: float = 0.0
+    activation_us: float = 0.0
+    loss_us: float = 0.0
+    adam_us: float = 0.0
+    comm_us: float = 0.0
+    _KEYS = ("spmm", "gemm", "activation", "loss", "adam", "comm")
+
+    def total_us(self) -> float:
+        return self.spmm_us + self.gemm_us + self.activation_us + self.loss_us + self.adam_us + self.comm_us
+
+    def frac(self, v: float) -> float:
+        t = self.total_us()
+        return v / t if t > 0 else 0.0
+
+    def to_json(self) -> dict:
+        vals = [getattr(self, k + "_us") for k in self._KEYS]
+        return {"totals_us": dict(zip(self._KEYS, vals)), "fractions": {k: self.frac(v) for k, v in zip(self._KEYS, vals)}}
+
+    def text_table(self) -> str:
+        s = "kernel               time_us fraction\n"
+        for k in self._KEYS:
+            v = getattr(self, k + "_us")
+            s += f"{k:<12} {v:14.1f} {self.frac(v):8.3f}\n"
+        return s + f"{'total':<12} {self.total_us():14.1f} {self.frac(self.total_us()):8.3f}\n"
+
+
+def runtime_breakdown(events) -> BreakdownReport:
+    """inc/breakdown.hpp:63-82 (native, mg_timeline_breakdown)."""
+    arr, _keep = _to_c_events(events)
+    t = (C.c_double * 6)()
+    _check(lib().mg_timeline_breakdown(arr, len(events), t))
+    return BreakdownReport(*list(t))
+
+
+def bench_spmm(ds: Dataset, workers: int = 1, permute: bool = True, overlap: bool = True, seed: int = 1,
+               timeline_path: str = "", stage_csv: str = "", devices=None, transport=TRANSPORT_AUTO,
+               spmm_mode: int = SPMM_FAST) -> dict:
+    """`bench-spmm` (proj/tools/main.cpp:120-178): one staged SpMM of the dataset's features (width = d0)
+    over the forward tiles on `workers` GPUs; audits the staged-run rules, optionally exports the timeline
+    and the per-stage CSV (stage, worker, comm_us, comp_us); returns the summary (plus the output rows)."""
+    width = ds.d0
+    cfg = GcnConfig([width, width], epochs=1, seed=seed, permute=permute, overlap=overlap and workers > 1,
+                    spmm_mode=spmm_mode)
+    prep = prepare_data(ds, cfg, workers)
+    with Group(cfg, prep, workers, devices=devices, transport=transport) as g:
+        g.set_timeline(True)
+        device_us = g.bench_spmm(0)
+        events = g.timeline()
+        g.set_timeline(False)
+        out = np.concatenate([g.read(T_HW, 0, r) for r in range(workers)], axis=0)
+    audit_staged_run(events, workers, cfg.overlap)
+    if timeline_path:
+        export_timeline(timeline_path, events)
+    if stage_csv:
+        with open(stage_csv, "w") as f:
+            f.write("stage,worker,comm_us,comp_us\n")
+            for stage in range(workers):
+                for w in range(workers):
+                    comm = sum(e.t_end_us - e.t_start_us for e in events
+                               if e.worker == w and e.stage == stage and e.kind == "broadcast")
+                    comp = sum(e.t_end_us - e.t_start_us for e in events
+                               if e.worker == w and e.stage == stage and e.kind == "spmm")
+                    f.write(f"{stage},{w},{comm:g},{comp:g}\n")
+    nnz = sum(int(prep.tile(0, i, j)[0][-1]) for i in range(workers) for j in range(workers))
+    # DeviceGroup::total_bytes_sent (collectives.hpp:127): each root counts its stage message once
+    bytes_bc = sum((prep.bounds[j + 1] - prep.bounds[j]) * width * 4 for j in range(workers)) if workers > 1 else 0
+    return {"n": ds.n(), "nnz": nnz, "width": width, "workers": workers, "overlap": cfg.overlap, "permute": permute,
+            "wall_us": timeline_span_us(events), "device_us": device_us, "bytes_broadcast": int(bytes_bc),
+            "out": out, "events": events}
 
 
 # ----------------------------------------------------------------------------- kernel-level entry points

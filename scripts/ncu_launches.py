@@ -18,7 +18,8 @@ for r in rows:
         continue
     v = float(d["Metric Value"].replace(",", ""))
     unit = d["Metric Unit"]
-    scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}.get(unit, 1.0)
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6,
+             "s": 1e6}.get(unit, 1.0)
     name = d["Kernel Name"].split("(")[0][:70]
     agg[name][0] += 1
     agg[name][1] += v * scale

@@ -61,3 +61,32 @@ def test_slab_training_equals_default():
     finally:
         R.set_tuning("spmm_slab", 0)
     assert a.epoch_loss == b.epoch_loss and a.w_hashes == b.w_hashes
+
+
+@pytest.mark.parametrize("w", [32, 40, 47, 64, 100, 128, 256, 300, 512])
+def test_spmm_async_pipeline_bitwise(w):
+    """The cp.async-pipelined FAST gather keeps each lane's FMA chain: bitwise equal to the register
+    gather, with hub segments, accumulate and relu, rows shorter and longer than the record windows."""
+    rng = np.random.default_rng(w + 11)
+    rows, cols = 400, 700
+    rp, ci, v = random_tile(rng, rows, cols, 0.05, hub_rows=(3, 17, 200), hub_len=650)
+    h = rng.uniform(-1, 1, (cols, w)).astype(np.float32)
+    o0 = rng.uniform(-1, 1, (rows, w)).astype(np.float32)
+    R.set_tuning("heavy_row", 128)
+    try:
+        outs = {}
+        for on in (0, 1):
+            R.set_tuning("spmm_async", on)
+            outs[on] = (run_spmm(rp, ci, v, h, mode=R.SPMM_FAST),
+                        run_spmm(rp, ci, v, h, True, o0, relu=True, mode=R.SPMM_FAST))
+    finally:
+        R.set_tuning("spmm_async", 1)
+        R.set_tuning("heavy_row", 4096)
+    for a, b in zip(outs[0], outs[1]):
+        assert bits_equal(a, b)
+    ref = (rp, ci, v)
+    dense = np.zeros((rows, cols), np.float64)
+    for r in range(rows):
+        dense[r, ci[rp[r]:rp[r + 1]]] = v[rp[r]:rp[r + 1]]
+    assert np.max(np.abs(outs[1][0] - dense @ h.astype(np.float64))) <= 1e-4 * max(1.0, np.max(np.abs(dense @ h)))
+    del ref
