@@ -9,10 +9,14 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -83,6 +87,19 @@ struct DevTile {
 
 std::atomic<int> g_fast_segment{2048};
 
+// MGGCN_TIMING=1: host-side phase timings of group creation on stderr.
+struct Stopwatch {
+  bool on = std::getenv("MGGCN_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[mggcn] %-12s %9.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 // Fast-mode work lists: every hub row (>= heavy threshold) is cut into fixed segments of g_fast_segment
 // nonzeros (gathered in parallel, summed in order afterwards); segments first, then the ordinary rows
 // by decreasing length.
@@ -105,9 +122,17 @@ void build_fast_items(const std::vector<index_t>& rp, std::vector<int4>& items, 
                                 -(nseg + 1), 0));
     hubs.push_back(make_int4(static_cast<int>(r), first, nseg - first, 0));
   }
-  std::stable_sort(light.begin(), light.end(),
-                   [&](int a, int b) { return (rp[a + 1] - rp[a]) > (rp[b + 1] - rp[b]); });
-  for (int r : light) items.push_back(make_int4(static_cast<int>(rp[r]), static_cast<int>(rp[r + 1]), r, 0));
+  // light rows by decreasing length, ties in row order: a counting sort (stable), O(rows + max length)
+  index_t maxlen = 0;
+  for (int r : light) maxlen = std::max(maxlen, rp[r + 1] - rp[r]);
+  std::vector<index_t> cnt(static_cast<size_t>(maxlen) + 2, 0);
+  for (int r : light) cnt[maxlen - (rp[r + 1] - rp[r]) + 1]++;
+  for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+  const size_t base = items.size();
+  items.resize(base + light.size());
+  for (int r : light)
+    items[base + static_cast<size_t>(cnt[maxlen - (rp[r + 1] - rp[r])]++)] =
+        make_int4(static_cast<int>(rp[r]), static_cast<int>(rp[r + 1]), r, 0);
 }
 
 // Host-side construction of the launch lists for a tile (row order by decreasing length).
@@ -392,25 +417,79 @@ T* dalloc_t(mg_group& g, Worker& w, size_t count) {
   return static_cast<T*>(dalloc(g, w, sizeof(T) * count));
 }
 
+// Host -> device uploads go through a process-wide pair of pinned staging buffers: each chunk is produced
+// straight into pinned memory by the host threads (packing / narrowing / copying) while the previous
+// chunk's DMA is in flight, so no pageable copy and no full-size host temporary is needed.
+class Stager {
+ public:
+  static constexpr size_t kChunk = size_t(64) << 20;
+  // fill(dst, first_byte, bytes) writes bytes [first_byte, first_byte + bytes) of the payload into dst
+  void upload(void* dev, size_t bytes, const std::function<void(char*, size_t, size_t)>& fill, cudaStream_t s) {
+    std::lock_guard<std::mutex> lk(mu_);
+    init();
+    for (size_t off = 0, b = 0; off < bytes; off += kChunk, b ^= 1) {
+      const size_t len = std::min(kChunk, bytes - off);
+      MG_CUDA(cudaEventSynchronize(done_[b]));  // the previous DMA out of this buffer has finished
+      fill(buf_[b], off, len);
+      MG_CUDA(cudaMemcpyAsync(static_cast<char*>(dev) + off, buf_[b], len, cudaMemcpyHostToDevice, s));
+      MG_CUDA(cudaEventRecord(done_[b], s));
+    }
+    MG_CUDA(cudaStreamSynchronize(s));
+  }
+  template <class T>
+  void upload_array(T* dev, const T* src, size_t count, cudaStream_t s) {
+    upload(dev, count * sizeof(T), [&](char* dst, size_t off, size_t len) {
+      parallel_for(static_cast<index_t>(len), [&](index_t b, index_t e) {
+        std::memcpy(dst + b, reinterpret_cast<const char*>(src) + off + b, static_cast<size_t>(e - b));
+      }, index_t(1) << 20);
+    }, s);
+  }
+
+ private:
+  void init() {
+    if (buf_[0]) return;
+    for (int i = 0; i < 2; ++i) {
+      MG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&buf_[i]), kChunk));
+      MG_CUDA(cudaEventCreateWithFlags(&done_[i], cudaEventDisableTiming));
+      MG_CUDA(cudaEventRecord(done_[i], 0));
+    }
+  }
+  std::mutex mu_;
+  char* buf_[2] = {nullptr, nullptr};
+  cudaEvent_t done_[2] = {nullptr, nullptr};
+};
+Stager& stager() {
+  static Stager* s = new Stager();  // process lifetime (pinned memory is released at exit)
+  return *s;
+}
+
 void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
   d.rows = t.rows;
   d.cols = t.cols;
   d.nnz = t.nnz();
   if (d.nnz >= (index_t(1) << 31)) throw ValueError("tile has >= 2^31 nonzeros; split the graph over more workers");
-  std::vector<int> rp32(t.rows + 1);
-  for (index_t r = 0; r <= t.rows; ++r) rp32[r] = static_cast<int>(t.row_ptr[r]);
-  std::vector<int2> ed(d.nnz);
-  parallel_for(d.nnz, [&](index_t b, index_t e) {
-    for (index_t i = b; i < e; ++i) {
-      int bits;
-      std::memcpy(&bits, &t.val[i], 4);
-      ed[i] = make_int2(t.col[i], bits);
-    }
-  });
-  d.row_ptr = dalloc_t<int>(g, w, rp32.size());
+  d.row_ptr = dalloc_t<int>(g, w, t.rows + 1);
   d.edges = dalloc_t<int2>(g, w, d.nnz + k::kEdgePad);
-  MG_CUDA(cudaMemcpy(d.row_ptr, rp32.data(), sizeof(int) * rp32.size(), cudaMemcpyHostToDevice));
-  if (d.nnz) MG_CUDA(cudaMemcpy(d.edges, ed.data(), sizeof(int2) * d.nnz, cudaMemcpyHostToDevice));
+  Stager& st = stager();
+  st.upload(d.row_ptr, sizeof(int) * (t.rows + 1), [&](char* dst, size_t off, size_t len) {
+    int* o = reinterpret_cast<int*>(dst);
+    const index_t r0 = static_cast<index_t>(off / sizeof(int));
+    parallel_for(static_cast<index_t>(len / sizeof(int)), [&](index_t b, index_t e) {
+      for (index_t i = b; i < e; ++i) o[i] = static_cast<int>(t.row_ptr[r0 + i]);
+    }, index_t(1) << 18);
+  }, w.s0);
+  if (d.nnz)  // {col, value bits} records
+    st.upload(d.edges, sizeof(int2) * d.nnz, [&](char* dst, size_t off, size_t len) {
+      int2* o = reinterpret_cast<int2*>(dst);
+      const index_t e0 = static_cast<index_t>(off / sizeof(int2));
+      parallel_for(static_cast<index_t>(len / sizeof(int2)), [&](index_t b, index_t e) {
+        for (index_t i = b; i < e; ++i) {
+          int bits;
+          std::memcpy(&bits, &t.val[e0 + i], 4);
+          o[i] = make_int2(t.col[e0 + i], bits);
+        }
+      }, index_t(1) << 18);
+    }, w.s0);
   if (g.cfg.spmm_mode == MG_SPMM_FAST) {
     std::vector<int4> items, hubs;
     build_fast_items(t.row_ptr, items, hubs, d.n_segments);
@@ -418,7 +497,7 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
     d.hubs = dalloc_t<int4>(g, w, std::max<size_t>(1, hubs.size()));
     d.n_items = static_cast<int>(items.size());
     d.n_hubs = static_cast<int>(hubs.size());
-    if (!items.empty()) MG_CUDA(cudaMemcpy(d.items, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
+    if (!items.empty()) st.upload_array(d.items, items.data(), items.size(), w.s0);
     if (!hubs.empty()) MG_CUDA(cudaMemcpy(d.hubs, hubs.data(), sizeof(int4) * hubs.size(), cudaMemcpyHostToDevice));
     return;
   }
@@ -433,7 +512,11 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
 }
 
 // Copies rows x cols (host, dense) into a device buffer with leading dimension ld (padding = 0).
-void upload_padded(float* dst, const float* src, index_t rows, index_t cols, index_t ld) {
+void upload_padded(float* dst, const float* src, index_t rows, index_t cols, index_t ld, cudaStream_t s = 0) {
+  if (cols == ld && rows * cols > 0) {
+    stager().upload_array(dst, src, static_cast<size_t>(rows * cols), s);
+    return;
+  }
   if (cols == ld) {
     MG_CUDA(cudaMemcpy(dst, src, sizeof(float) * rows * cols, cudaMemcpyHostToDevice));
     return;
@@ -1001,6 +1084,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
                          std::to_string(C) + ") at row " + std::to_string(v);
       }
     const int L = cfg.layers();
+    Stopwatch sw;
     for (int k = 0; k < n_local; ++k) {
       auto wp = std::make_unique<Worker>();
       Worker& w = *wp;
@@ -1037,15 +1121,17 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
         }
       }
       if (max_segments > 0) w.seg_scratch = dalloc_t<float>(*g, w, static_cast<size_t>(max_segments) * g->ld_max);
+      sw.lap("tiles");
       // rows: x_local, labels, mask (gcn.hpp:127-132)
       w.x = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));
-      upload_padded(w.x, p->features.data() + w.r0 * p->d0, w.rows, p->d0, g->ld[0]);
+      upload_padded(w.x, p->features.data() + w.r0 * p->d0, w.rows, p->d0, g->ld[0], w.s0);
       w.labels = dalloc_t<int>(*g, w, std::max<index_t>(1, w.rows));
       w.mask = dalloc_t<uint8_t>(*g, w, std::max<index_t>(1, w.rows));
       if (w.rows) {
         MG_CUDA(cudaMemcpy(w.labels, p->labels.data() + w.r0, sizeof(int) * w.rows, cudaMemcpyHostToDevice));
         MG_CUDA(cudaMemcpy(w.mask, p->mask.data() + w.r0, w.rows, cudaMemcpyHostToDevice));
       }
+      sw.lap("rows");
       // the L + 3 buffer plan (gcn.hpp:134-140)
       for (int l = 0; l < L; ++l) w.ahw.push_back(dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[l + 1])));
       w.hw = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld_max));
@@ -1078,6 +1164,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       w.stats = dalloc_t<double>(*g, w, 2);
       MG_CUDA(cudaMallocHost(&w.h_stats, 2 * sizeof(double)));
       g->workers.push_back(std::move(wp));
+      sw.lap("buffers");
     }
     if (transport == MG_TRANSPORT_NCCL && world > 1) {
       if (n_local == world && !nccl_id) {
@@ -1095,10 +1182,12 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
         MG_NCCL(ncclGroupEnd());
       }
     }
+    sw.lap("nccl");
     for (auto& wp : g->workers) {
       MG_CUDA(cudaSetDevice(wp->device));
       MG_CUDA(cudaDeviceSynchronize());
     }
+    sw.lap("sync");
     g->sealed = true;
     *out = g.release();
   });

@@ -1,0 +1,31 @@
+"""Phase timings of the end-to-end path (group create / init / K synchronous steps / W read-back)."""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.environ.setdefault("MGGCN_TIMING", "1")
+from paper_2110_08688_b200 import rowgcn as R  # noqa: E402
+
+t0 = time.time()
+ds = R.synth_graph(2449029, 50.6, 0.7, 1, 100, 47)
+t1 = time.time()
+cfg = R.GcnConfig([100, 256, 256, 47], epochs=10, seed=1, permute=True)
+prep = R.prepare_data(ds, cfg, 1)
+t2 = time.time()
+print(f"synth {t1 - t0:.2f} s, prepare {t2 - t1:.2f} s", flush=True)
+for rep in range(2):
+    a = time.time()
+    g = R.Group(cfg, prep, 1, devices=[0])
+    b = time.time()
+    g.init_params()
+    c = time.time()
+    for t in range(1, 11):
+        g.train_step(t)
+    d = time.time()
+    ws = g.params(0)
+    e = time.time()
+    g.close()
+    f = time.time()
+    print(f"create {1e3 * (b - a):.1f} ms, init {1e3 * (c - b):.1f} ms, 10 steps {1e3 * (d - c):.1f} ms, "
+          f"params {1e3 * (e - d):.1f} ms, close {1e3 * (f - e):.1f} ms", flush=True)
