@@ -83,6 +83,7 @@ struct DevTile {
   int4* hubs = nullptr;
   int n_hubs = 0;
   int n_segments = 0;
+  bool hubs_classed = false;  // FAST: column hub classes in the top 4 bits of each edge record
 };
 
 std::atomic<int> g_fast_segment{2048};
@@ -206,6 +207,7 @@ struct FastLaunch {
   int n_hubs;
   const int2* edges;
   float* scratch;  // n_segments x ld
+  bool hubs_classed = false;  // edge records carry hub classes (upload_tile, FAST mode)
 };
 
 template <int G, int CPL>
@@ -219,6 +221,16 @@ static void launch_fast(const FastLaunch& t, const float* h, float* out, float* 
 }
 
 std::atomic<int> g_spmm_async{1};  // MG_SPMM_FAST gathers through the cp.async ring (spmm_fast_async)
+std::atomic<long long> g_hub_bytes{96ll << 20};  // L2 footprint of evict_last hub rows per gather (0 = no hints)
+
+// Largest hub class whose rows (10000 * 2^(k-1) of them, ld floats each) fit the hub footprint; -1 = no hints.
+int hub_class_max(int ld) {
+  const long long budget = g_hub_bytes.load();
+  if (budget <= 0) return -1;
+  int k = 0;
+  while (k < 7 && 10000ll * (1ll << k) * ld * 4 <= budget) ++k;
+  return k;
+}
 
 template <int G, int CPL, int E, int D>
 static void launch_fast_async(const FastLaunch& t, const float* h, float* out, float* scratch, int ld, int nchunk,
@@ -236,7 +248,7 @@ static void launch_fast_async(const FastLaunch& t, const float* h, float* out, f
   const int gpb = kThreads / G;
   const int blocks = std::min(ceil_div(t.n_items, gpb), num_sms() * blocks_per_sm);
   k::spmm_fast_async<G, CPL, E, D><<<blocks, kThreads, smem, s>>>(t.items, t.n_items, t.edges, h, out, scratch, ld,
-                                                                  nchunk, acc, relu);
+                                                                  nchunk, acc, relu, t.hubs_classed ? hub_class_max(ld) : -1);
   MG_LAUNCHED();
 }
 
@@ -419,13 +431,16 @@ T* dalloc_t(mg_group& g, Worker& w, size_t count) {
 
 // Host -> device uploads go through a process-wide pair of pinned staging buffers: each chunk is produced
 // straight into pinned memory by the host threads (packing / narrowing / copying) while the previous
-// chunk's DMA is in flight, so no pageable copy and no full-size host temporary is needed.
+// chunk's DMA is in flight, so no pageable copy and no full-size host temporary is needed. The copies
+// run on the legacy default stream, after dalloc's zero-fill (cudaMemset, also the legacy stream), and
+// upload() returns only when they are complete.
 class Stager {
  public:
   static constexpr size_t kChunk = size_t(64) << 20;
   // fill(dst, first_byte, bytes) writes bytes [first_byte, first_byte + bytes) of the payload into dst
-  void upload(void* dev, size_t bytes, const std::function<void(char*, size_t, size_t)>& fill, cudaStream_t s) {
+  void upload(void* dev, size_t bytes, const std::function<void(char*, size_t, size_t)>& fill) {
     std::lock_guard<std::mutex> lk(mu_);
+    const cudaStream_t s = cudaStreamLegacy;
     init();
     for (size_t off = 0, b = 0; off < bytes; off += kChunk, b ^= 1) {
       const size_t len = std::min(kChunk, bytes - off);
@@ -437,12 +452,12 @@ class Stager {
     MG_CUDA(cudaStreamSynchronize(s));
   }
   template <class T>
-  void upload_array(T* dev, const T* src, size_t count, cudaStream_t s) {
+  void upload_array(T* dev, const T* src, size_t count) {
     upload(dev, count * sizeof(T), [&](char* dst, size_t off, size_t len) {
       parallel_for(static_cast<index_t>(len), [&](index_t b, index_t e) {
         std::memcpy(dst + b, reinterpret_cast<const char*>(src) + off + b, static_cast<size_t>(e - b));
       }, index_t(1) << 20);
-    }, s);
+    });
   }
 
  private:
@@ -451,7 +466,7 @@ class Stager {
     for (int i = 0; i < 2; ++i) {
       MG_CUDA(cudaMallocHost(reinterpret_cast<void**>(&buf_[i]), kChunk));
       MG_CUDA(cudaEventCreateWithFlags(&done_[i], cudaEventDisableTiming));
-      MG_CUDA(cudaEventRecord(done_[i], 0));
+      MG_CUDA(cudaEventRecord(done_[i], cudaStreamLegacy));
     }
   }
   std::mutex mu_;
@@ -477,8 +492,28 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
     parallel_for(static_cast<index_t>(len / sizeof(int)), [&](index_t b, index_t e) {
       for (index_t i = b; i < e; ++i) o[i] = static_cast<int>(t.row_ptr[r0 + i]);
     }, index_t(1) << 18);
-  }, w.s0);
-  if (d.nnz)  // {col, value bits} records
+  });
+  // FAST mode: rank the tile's columns by how often they are gathered and tag each record with the
+  // column's hub class (top 4 bits), so the gather can keep the hottest rows resident in L2.
+  std::vector<uint8_t> cls;
+  if (g.cfg.spmm_mode == MG_SPMM_FAST && g_hub_bytes.load() > 0 && d.nnz && t.cols < (index_t(1) << 28)) {
+    std::vector<index_t> cnt(static_cast<size_t>(t.cols), 0);
+    for (index_t i = 0; i < d.nnz; ++i) cnt[t.col[i]]++;
+    index_t maxc = 0;
+    for (index_t c : cnt) maxc = std::max(maxc, c);
+    std::vector<index_t> hist(static_cast<size_t>(maxc) + 2, 0);  // columns per count, most gathered first
+    for (index_t c : cnt) hist[maxc - c + 1]++;
+    for (size_t i = 1; i < hist.size(); ++i) hist[i] += hist[i - 1];
+    cls.assign(static_cast<size_t>(t.cols), 0);
+    for (index_t c = 0; c < t.cols; ++c) {
+      const index_t rank = hist[maxc - cnt[c]]++;
+      int k = 1;
+      while (k <= 7 && rank >= 10000 * (index_t(1) << (k - 1))) ++k;
+      cls[c] = static_cast<uint8_t>(k <= 7 ? k : 0);
+    }
+    d.hubs_classed = true;
+  }
+  if (d.nnz)  // {col (| hub class << 28), value bits} records
     st.upload(d.edges, sizeof(int2) * d.nnz, [&](char* dst, size_t off, size_t len) {
       int2* o = reinterpret_cast<int2*>(dst);
       const index_t e0 = static_cast<index_t>(off / sizeof(int2));
@@ -486,10 +521,11 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
         for (index_t i = b; i < e; ++i) {
           int bits;
           std::memcpy(&bits, &t.val[e0 + i], 4);
-          o[i] = make_int2(t.col[e0 + i], bits);
+          const int c = t.col[e0 + i];
+          o[i] = make_int2(cls.empty() ? c : (c | (static_cast<int>(cls[c]) << 28)), bits);
         }
       }, index_t(1) << 18);
-    }, w.s0);
+    });
   if (g.cfg.spmm_mode == MG_SPMM_FAST) {
     std::vector<int4> items, hubs;
     build_fast_items(t.row_ptr, items, hubs, d.n_segments);
@@ -497,7 +533,7 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
     d.hubs = dalloc_t<int4>(g, w, std::max<size_t>(1, hubs.size()));
     d.n_items = static_cast<int>(items.size());
     d.n_hubs = static_cast<int>(hubs.size());
-    if (!items.empty()) st.upload_array(d.items, items.data(), items.size(), w.s0);
+    if (!items.empty()) st.upload_array(d.items, items.data(), items.size());
     if (!hubs.empty()) MG_CUDA(cudaMemcpy(d.hubs, hubs.data(), sizeof(int4) * hubs.size(), cudaMemcpyHostToDevice));
     return;
   }
@@ -512,9 +548,9 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
 }
 
 // Copies rows x cols (host, dense) into a device buffer with leading dimension ld (padding = 0).
-void upload_padded(float* dst, const float* src, index_t rows, index_t cols, index_t ld, cudaStream_t s = 0) {
+void upload_padded(float* dst, const float* src, index_t rows, index_t cols, index_t ld) {
   if (cols == ld && rows * cols > 0) {
-    stager().upload_array(dst, src, static_cast<size_t>(rows * cols), s);
+    stager().upload_array(dst, src, static_cast<size_t>(rows * cols));
     return;
   }
   if (cols == ld) {
@@ -664,7 +700,7 @@ class Step {
         const int acc = j > 0, relu = relu_last && j == P_ - 1;
         const int pi = prof_begin(w);
         if (cfg_.spmm_mode == MG_SPMM_FAST) {
-          FastLaunch fl{t.items, t.n_items, t.hubs, t.n_hubs, t.edges, w.seg_scratch};
+          FastLaunch fl{t.items, t.n_items, t.hubs, t.n_hubs, t.edges, w.seg_scratch, t.hubs_classed};
           g_.kernels_last += spmm_fast(fl, recv[k], out[k], ld, acc, relu, w.s0);
           prof_end(w, pi, 0);
           mult_task[k][j] = tl_end(k, ts);
@@ -1000,6 +1036,9 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
     } else if (k == "spmm_slab") {
       if (value < 0 || value % 4) throw ValueError("tuning: spmm_slab must be 0 or a multiple of 4 floats");
       g_spmm_slab = static_cast<int>(std::min<int64_t>(value, 1024));
+    } else if (k == "spmm_hub_bytes") {
+      if (value < 0) throw ValueError("tuning: spmm_hub_bytes must be >= 0");
+      g_hub_bytes = value;
     } else if (k == "spmm_async") {
       g_spmm_async = value != 0 ? 1 : 0;
     } else if (k == "fast_segment") {
@@ -1124,7 +1163,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       sw.lap("tiles");
       // rows: x_local, labels, mask (gcn.hpp:127-132)
       w.x = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));
-      upload_padded(w.x, p->features.data() + w.r0 * p->d0, w.rows, p->d0, g->ld[0], w.s0);
+      upload_padded(w.x, p->features.data() + w.r0 * p->d0, w.rows, p->d0, g->ld[0]);
       w.labels = dalloc_t<int>(*g, w, std::max<index_t>(1, w.rows));
       w.mask = dalloc_t<uint8_t>(*g, w, std::max<index_t>(1, w.rows));
       if (w.rows) {

@@ -29,6 +29,10 @@ __device__ __forceinline__ void axpy4(float4& acc, float v, const float4& x) {
 }
 __device__ __forceinline__ float relu1(float x) { return x > 0.0f ? x : 0.0f; }  // dense.hpp:214
 
+// FAST-mode edge records carry a hub class in the top 4 bits of the column (mg_device.cu upload_tile):
+// class k in 1..7 = the column is among the 10000 * 2^(k-1) most gathered of its tile, 0 = no class.
+constexpr int kColMask = 0x0FFFFFFF;
+
 // Edge records are streamed once per (column-slab) pass: mark them evict-first in L2 so they do not
 // displace the h rows being gathered (which are what L2 reuse is for).
 __device__ __forceinline__ int2 ld_edge(const int2* p) {
@@ -165,7 +169,7 @@ __global__ void __launch_bounds__(256) spmm_fast_items(const int4* __restrict__ 
         float v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          const int col = __shfl_sync(gmask, my.x, j + u, G);
+          const int col = __shfl_sync(gmask, my.x, j + u, G) & kColMask;
           v[u] = __int_as_float(__shfl_sync(gmask, my.y, j + u, G));
           const float* hr = h + (size_t)col * ld;
 #pragma unroll
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(256) spmm_fast_items(const int4* __restrict__ 
           for (int k = 0; k < CPL; ++k) fma4(acc[k], v[u], x[u][k]);
       }
       for (; j < cnt; ++j) {
-        const int col = __shfl_sync(gmask, my.x, j, G);
+        const int col = __shfl_sync(gmask, my.x, j, G) & kColMask;
         const float v = __int_as_float(__shfl_sync(gmask, my.y, j, G));
         const float* hr = h + (size_t)col * ld;
 #pragma unroll
@@ -218,12 +222,24 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, uint64_t pol) {
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem), "l"(pol)
+               : "memory");
+}
+
+// hub_max >= 0: gathers of columns of class 1..hub_max are marked L2 evict_last (they stay resident:
+// the hub rows of the power-law graph are re-gathered by many rows), every other gather evict_first.
 template <int G, int CPL, int E, int D>
 __global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ items, int n_items,
                                                        const int2* __restrict__ edges, const float* __restrict__ h,
                                                        float* __restrict__ out, float* __restrict__ scratch, int ld,
-                                                       int nchunk, int accumulate, int relu) {
+                                                       int nchunk, int accumulate, int relu, int hub_max) {
   static_assert(G % E == 0 && (D - 1) * E <= G, "pipeline depth must stay within one record window");
+  uint64_t pol_last, pol_first;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_last));
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_first));
   extern __shared__ float4 ring_all[];
   const int lane = threadIdx.x & (G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
@@ -254,13 +270,18 @@ __global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ 
       for (int e = 0; e < E; ++e) {
         const int i = t * E + e;
         const int src = (i / G == wi) ? wa.x : wb.x;
-        const int col = __shfl_sync(gmask, src, i & (G - 1), G);
+        const int rec = __shfl_sync(gmask, src, i & (G - 1), G);
         if (i < n) {
-          const float* hr = h + (size_t)col * ld;
+          const float* hr = h + (size_t)(rec & kColMask) * ld;
+          const int cls = static_cast<int>(static_cast<unsigned>(rec) >> 28);
+          const uint64_t pol = (cls != 0 && cls <= hub_max) ? pol_last : pol_first;
 #pragma unroll
           for (int k = 0; k < CPL; ++k) {
             const int c = lane + k * G;
-            if (c < nchunk) cp_async16_cg(slot + (e * CPL + k) * G + lane, hr + 4 * c);
+            if (c < nchunk) {
+              if (hub_max >= 0) cp_async16_hint(slot + (e * CPL + k) * G + lane, hr + 4 * c, pol);
+              else cp_async16_cg(slot + (e * CPL + k) * G + lane, hr + 4 * c);
+            }
           }
         }
       }

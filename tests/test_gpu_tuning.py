@@ -90,3 +90,18 @@ def test_spmm_async_pipeline_bitwise(w):
         dense[r, ci[rp[r]:rp[r + 1]]] = v[rp[r]:rp[r + 1]]
     assert np.max(np.abs(outs[1][0] - dense @ h.astype(np.float64))) <= 1e-4 * max(1.0, np.max(np.abs(dense @ h)))
     del ref
+
+
+@pytest.mark.parametrize("hub_bytes", [0, 1 << 20, 96 << 20])
+def test_hub_l2_hints_do_not_change_results(hub_bytes):
+    """FAST edge records carry a hub class in the column's top bits; the L2 evict_last / evict_first hints
+    they select change caching only: training is bitwise identical with and without them."""
+    ds = R.synth_graph(30000, 20.0, 0.7, 8, 24, 5)
+    cfg = R.GcnConfig([24, 64, 5], epochs=2, seed=1, permute=True, spmm_mode=R.SPMM_FAST)
+    a = R.train_run(ds, cfg, R.TrainOptions(devices=[0]))
+    R.set_tuning("spmm_hub_bytes", hub_bytes)
+    try:
+        b = R.train_run(ds, cfg, R.TrainOptions(devices=[0]))
+    finally:
+        R.set_tuning("spmm_hub_bytes", 96 << 20)
+    assert a.epoch_loss == b.epoch_loss and a.w_hashes == b.w_hashes
