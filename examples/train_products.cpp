@@ -29,6 +29,9 @@ int main(int argc, char** argv) {
     const auto art = R::train_run(ds, cfg, opts);
     std::printf("final loss %.7f over %zu epochs, %zu W matrices\n", art.final_loss(), art.epoch_loss.size(),
                 art.final_w.size());
+    R::audit_timeline(art.timeline);  // the CUDA-event timeline obeys the reference's audit rules
+    R::export_timeline("/tmp/mggcn_products.timeline.json", art.timeline);
+    std::printf("timeline: %zu events\n", art.timeline.size());
     R::write_checkpoint("/tmp/mggcn_products.ckpt", art.final_w);
     const auto back = R::read_checkpoint("/tmp/mggcn_products.ckpt");
     return back.size() == art.final_w.size() ? 0 : 1;

@@ -24,6 +24,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <fstream>
 #include <functional>
@@ -348,9 +349,65 @@ struct TrainOptions {
   int transport = MG_TRANSPORT_AUTO;
 };
 
+// rowgcn::TimelineEvent (inc/collectives.hpp:24-34), recorded from CUDA events (mggcn.h timeline).
+struct TimelineEvent {
+  int worker = 0, lane = 0, stage = -1;
+  std::string kind, op;
+  double t_start_us = 0, t_end_us = 0;
+  std::uint64_t task = 0;
+  std::vector<std::uint64_t> deps;
+};
+
+namespace detail {
+inline std::vector<TimelineEvent> timeline(mg_group* g) {
+  std::int64_t n = 0;
+  check(mg_group_timeline(g, nullptr, 0, &n));
+  std::vector<mg_timeline_event> raw(static_cast<size_t>(n));
+  check(mg_group_timeline(g, raw.data(), n, &n));
+  std::vector<TimelineEvent> out;
+  out.reserve(raw.size());
+  for (const auto& e : raw)
+    out.push_back({e.worker, e.lane, e.stage, e.kind, e.op, e.t_start_us, e.t_end_us, e.task,
+                   std::vector<std::uint64_t>(e.deps, e.deps + e.n_deps)});
+  return out;
+}
+inline std::vector<mg_timeline_event> to_c(const std::vector<TimelineEvent>& ev) {
+  std::vector<mg_timeline_event> out(ev.size());
+  for (size_t i = 0; i < ev.size(); ++i) {
+    auto& o = out[i];
+    o.worker = ev[i].worker;
+    o.lane = ev[i].lane;
+    o.stage = ev[i].stage;
+    o.n_deps = static_cast<std::int32_t>(ev[i].deps.size());
+    std::snprintf(o.kind, sizeof(o.kind), "%s", ev[i].kind.c_str());
+    std::snprintf(o.op, sizeof(o.op), "%s", ev[i].op.c_str());
+    o.t_start_us = ev[i].t_start_us;
+    o.t_end_us = ev[i].t_end_us;
+    o.task = ev[i].task;
+    o.deps = ev[i].deps.data();
+  }
+  return out;
+}
+}  // namespace detail
+
+// export_timeline / audit_timeline / audit_staged_run (inc/timeline.hpp:31-126), native.
+inline void export_timeline(const std::string& path, const std::vector<TimelineEvent>& ev) {
+  const auto c = detail::to_c(ev);
+  check(mg_timeline_export(path.c_str(), c.data(), static_cast<std::int64_t>(c.size())));
+}
+inline void audit_timeline(const std::vector<TimelineEvent>& ev) {
+  const auto c = detail::to_c(ev);
+  check(mg_timeline_audit(c.data(), static_cast<std::int64_t>(c.size())));
+}
+inline void audit_staged_run(const std::vector<TimelineEvent>& ev, int world, bool overlapped) {
+  const auto c = detail::to_c(ev);
+  check(mg_timeline_audit_staged(c.data(), static_cast<std::int64_t>(c.size()), world, overlapped ? 1 : 0));
+}
+
 template <class S>
 struct TrainArtifacts {
   std::vector<double> epoch_loss, epoch_acc, epoch_wall_us;
+  std::vector<TimelineEvent> timeline;  // every task of every epoch (CUDA events)
   std::vector<std::vector<std::uint64_t>> w_hashes;  // [epoch][rank]
   std::vector<DenseMatrix<S>> final_w;               // rank 0's replicas
   DenseMatrix<S> logits;                             // gathered post-training logits (permuted order)
@@ -399,6 +456,7 @@ inline TrainArtifacts<float> train_run(const Dataset<float>& ds, const GcnConfig
   check(mg_group_init_params(g.get()));
   TrainArtifacts<float> art;
   art.workers = opts.workers;
+  check(mg_group_set_timeline(g.get(), 1));
   for (int e = 1; e <= cfg.epochs; ++e) {
     double loss = 0, acc = 0, wall = 0;
     check(mg_group_train_step(g.get(), e, &loss, &acc, &wall));
@@ -410,6 +468,8 @@ inline TrainArtifacts<float> train_run(const Dataset<float>& ds, const GcnConfig
     art.w_hashes.push_back(std::move(hs));
     if (opts.on_epoch) opts.on_epoch(e, loss, acc, wall);
   }
+  art.timeline = detail::timeline(g.get());
+  check(mg_group_set_timeline(g.get(), 0));
   const int L = cfg.layers();
   if (opts.collect_logits) {
     double l = 0;

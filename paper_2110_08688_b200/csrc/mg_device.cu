@@ -832,7 +832,14 @@ class Step {
       const int th = tl_begin(k, 0, "other", "loss", -1, {w.last_task[0]});
       const int pi = prof_begin(w);
       if (w.rows > 0) {
-        k::softmax_xent<<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
+        const int C32 = static_cast<int>((C + 31) / 32);
+        if (C32 <= 2) k::softmax_xent<2><<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
+                                                         static_cast<int>(w.rows), static_cast<int>(C), w.labels,
+                                                         w.mask, inv_denom, w.partials);
+        else if (C32 <= 4) k::softmax_xent<4><<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
+                                                         static_cast<int>(w.rows), static_cast<int>(C), w.labels,
+                                                         w.mask, inv_denom, w.partials);
+        else k::softmax_xent<k::kLossCpl><<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
                                                          static_cast<int>(w.rows), static_cast<int>(C), w.labels,
                                                          w.mask, inv_denom, w.partials);
         MG_LAUNCHED();

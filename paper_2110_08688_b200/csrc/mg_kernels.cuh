@@ -569,6 +569,7 @@ __global__ void __launch_bounds__(256) gemm_exact(int M, int N, int K, const flo
 // fixed order so the reported loss is run-to-run deterministic.
 constexpr int kLossCpl = 8;
 
+template <int CPL>  // class chunks of 32 per lane row: C <= 32 * CPL
 __global__ void __launch_bounds__(256) softmax_xent(float* __restrict__ logits, int ld, int rows, int C,
                                                     const int* __restrict__ labels, const uint8_t* __restrict__ mask,
                                                     float inv_denom, double* __restrict__ partials) {
@@ -582,11 +583,11 @@ __global__ void __launch_bounds__(256) softmax_xent(float* __restrict__ logits, 
       continue;
     }
     const int label = labels[r];
-    float z[kLossCpl];
+    float z[CPL];
     float mx = -INFINITY;
     int arg = 0x7fffffff;
 #pragma unroll
-    for (int q = 0; q < kLossCpl; ++q) {
+    for (int q = 0; q < CPL; ++q) {
       const int j = lane + 32 * q;
       z[q] = j < C ? row[j] : -INFINITY;
       if (j < C && (arg == 0x7fffffff || z[q] > mx)) {
@@ -604,17 +605,18 @@ __global__ void __launch_bounds__(256) softmax_xent(float* __restrict__ logits, 
         arg = oa;
       }
     }
-    float se = 0.0f;
+    float se = 0.0f, ex[CPL];
 #pragma unroll
-    for (int q = 0; q < kLossCpl; ++q) {
+    for (int q = 0; q < CPL; ++q) {
       const int j = lane + 32 * q;
-      if (j < C) se += expf(z[q] - mx);
+      ex[q] = j < C ? expf(z[q] - mx) : 0.0f;
+      if (j < C) se += ex[q];
     }
 #pragma unroll
     for (int off = 16; off; off >>= 1) se += __shfl_xor_sync(0xffffffffu, se, off);
     float zlab = 0.0f;
 #pragma unroll
-    for (int q = 0; q < kLossCpl; ++q)
+    for (int q = 0; q < CPL; ++q)
       if (label == lane + 32 * q) zlab = z[q];
     zlab = __shfl_sync(0xffffffffu, zlab, label & 31);
     if (lane == 0) {
@@ -622,10 +624,10 @@ __global__ void __launch_bounds__(256) softmax_xent(float* __restrict__ logits, 
       my_corr += (arg == label) ? 1.0 : 0.0;
     }
 #pragma unroll
-    for (int q = 0; q < kLossCpl; ++q) {
+    for (int q = 0; q < CPL; ++q) {
       const int j = lane + 32 * q;
       if (j < C) {
-        float g = __fmul_rn(__fdiv_rn(expf(z[q] - mx), se), inv_denom);
+        float g = __fmul_rn(__fdiv_rn(ex[q], se), inv_denom);
         if (j == label) g = __fsub_rn(g, inv_denom);
         row[j] = g;
       }

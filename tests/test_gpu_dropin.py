@@ -30,6 +30,8 @@ def test_cpp_dropin_trains(tmp_path):
     ds = R.synth_graph(20000, 50.6, 0.7, 1, 100, 47)
     art = R.train_run(ds, R.GcnConfig([100, 256, 256, 47], epochs=3, permute=True), R.TrainOptions(devices=[0]))
     np.testing.assert_allclose(losses, art.epoch_loss, rtol=1e-6)
+    n_events = int(next(ln for ln in run.stdout.splitlines() if ln.startswith("timeline:")).split()[1])
+    assert n_events == len(art.timeline) > 0
 
 
 def test_on_epoch_and_logit_equivariance():
