@@ -208,6 +208,7 @@ struct FastLaunch {
   const int2* edges;
   float* scratch;  // n_segments x ld
   bool hubs_classed = false;  // edge records carry hub classes (upload_tile, FAST mode)
+  index_t src_rows = 0;       // rows of the gathered block (the tile's columns)
 };
 
 template <int G, int CPL>
@@ -221,6 +222,7 @@ static void launch_fast(const FastLaunch& t, const float* h, float* out, float* 
 }
 
 std::atomic<int> g_spmm_async{1};  // MG_SPMM_FAST gathers through the cp.async ring (spmm_fast_async)
+constexpr double kL2Bytes = 126.0 * (1 << 20);
 std::atomic<long long> g_hub_bytes{96ll << 20};  // L2 footprint of evict_last hub rows per gather (0 = no hints)
 
 // Largest hub class whose rows (10000 * 2^(k-1) of them, ld floats each) fit the hub footprint; -1 = no hints.
@@ -232,24 +234,35 @@ int hub_class_max(int ld) {
   return k;
 }
 
-template <int G, int CPL, int E, int D>
-static void launch_fast_async(const FastLaunch& t, const float* h, float* out, float* scratch, int ld, int nchunk,
-                              int acc, int relu, cudaStream_t s) {
+template <int G, int CPL, int E, int D, bool HINT>
+static void launch_fast_async_v(const FastLaunch& t, const float* h, float* out, float* scratch, int ld, int nchunk,
+                                int acc, int relu, int hub_max, cudaStream_t s) {
   constexpr int kThreads = 128;
   constexpr size_t smem = sizeof(float4) * kThreads * D * E * CPL;
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
-    MG_CUDA(cudaFuncSetAttribute(k::spmm_fast_async<G, CPL, E, D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    MG_CUDA(cudaFuncSetAttribute(k::spmm_fast_async<G, CPL, E, D, HINT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k::spmm_fast_async<G, CPL, E, D>, kThreads,
-                                                          smem));
+    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k::spmm_fast_async<G, CPL, E, D, HINT>,
+                                                          kThreads, smem));
     blocks_per_sm = std::max(1, blocks_per_sm);
   }
   const int gpb = kThreads / G;
   const int blocks = std::min(ceil_div(t.n_items, gpb), num_sms() * blocks_per_sm);
-  k::spmm_fast_async<G, CPL, E, D><<<blocks, kThreads, smem, s>>>(t.items, t.n_items, t.edges, h, out, scratch, ld,
-                                                                  nchunk, acc, relu, t.hubs_classed ? hub_class_max(ld) : -1);
+  k::spmm_fast_async<G, CPL, E, D, HINT><<<blocks, kThreads, smem, s>>>(t.items, t.n_items, t.edges, h, out, scratch,
+                                                                        ld, nchunk, acc, relu, hub_max);
   MG_LAUNCHED();
+}
+
+template <int G, int CPL, int E, int D>
+static void launch_fast_async(const FastLaunch& t, const float* h, float* out, float* scratch, int ld, int nchunk,
+                              int acc, int relu, cudaStream_t s) {
+  // hub hints only when the gathered block is well beyond the L2 (a block of a few L2 sizes is better
+  // served by plain LRU, which then keeps a large share of every row resident)
+  const bool big = static_cast<double>(t.src_rows) * ld * 4 > 4.0 * kL2Bytes;
+  const int hub_max = t.hubs_classed && big ? hub_class_max(ld) : -1;
+  if (hub_max >= 0) launch_fast_async_v<G, CPL, E, D, true>(t, h, out, scratch, ld, nchunk, acc, relu, hub_max, s);
+  else launch_fast_async_v<G, CPL, E, D, false>(t, h, out, scratch, ld, nchunk, acc, relu, -1, s);
 }
 
 // cp.async-pipelined variants for rows of >= 32 floats; false = use the register-gather kernel.
@@ -700,7 +713,7 @@ class Step {
         const int acc = j > 0, relu = relu_last && j == P_ - 1;
         const int pi = prof_begin(w);
         if (cfg_.spmm_mode == MG_SPMM_FAST) {
-          FastLaunch fl{t.items, t.n_items, t.hubs, t.n_hubs, t.edges, w.seg_scratch, t.hubs_classed};
+          FastLaunch fl{t.items, t.n_items, t.hubs, t.n_hubs, t.edges, w.seg_scratch, t.hubs_classed, t.cols};
           g_.kernels_last += spmm_fast(fl, recv[k], out[k], ld, acc, relu, w.s0);
           prof_end(w, pi, 0);
           mult_task[k][j] = tl_end(k, ts);

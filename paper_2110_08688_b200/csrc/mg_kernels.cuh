@@ -231,15 +231,17 @@ __device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, ui
 
 // hub_max >= 0: gathers of columns of class 1..hub_max are marked L2 evict_last (they stay resident:
 // the hub rows of the power-law graph are re-gathered by many rows), every other gather evict_first.
-template <int G, int CPL, int E, int D>
+template <int G, int CPL, int E, int D, bool HINT>
 __global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ items, int n_items,
                                                        const int2* __restrict__ edges, const float* __restrict__ h,
                                                        float* __restrict__ out, float* __restrict__ scratch, int ld,
                                                        int nchunk, int accumulate, int relu, int hub_max) {
   static_assert(G % E == 0 && (D - 1) * E <= G, "pipeline depth must stay within one record window");
-  uint64_t pol_last, pol_first;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_last));
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_first));
+  uint64_t pol_last = 0, pol_first = 0;
+  if (HINT) {
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_last));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_first));
+  }
   extern __shared__ float4 ring_all[];
   const int lane = threadIdx.x & (G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
@@ -273,14 +275,19 @@ __global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ 
         const int rec = __shfl_sync(gmask, src, i & (G - 1), G);
         if (i < n) {
           const float* hr = h + (size_t)(rec & kColMask) * ld;
-          const int cls = static_cast<int>(static_cast<unsigned>(rec) >> 28);
-          const uint64_t pol = (cls != 0 && cls <= hub_max) ? pol_last : pol_first;
+          if (HINT) {
+            const int cls = static_cast<int>(static_cast<unsigned>(rec) >> 28);
+            const uint64_t pol = (cls != 0 && cls <= hub_max) ? pol_last : pol_first;
 #pragma unroll
-          for (int k = 0; k < CPL; ++k) {
-            const int c = lane + k * G;
-            if (c < nchunk) {
-              if (hub_max >= 0) cp_async16_hint(slot + (e * CPL + k) * G + lane, hr + 4 * c, pol);
-              else cp_async16_cg(slot + (e * CPL + k) * G + lane, hr + 4 * c);
+            for (int k = 0; k < CPL; ++k) {
+              const int c = lane + k * G;
+              if (c < nchunk) cp_async16_hint(slot + (e * CPL + k) * G + lane, hr + 4 * c, pol);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              const int c = lane + k * G;
+              if (c < nchunk) cp_async16_cg(slot + (e * CPL + k) * G + lane, hr + 4 * c);
             }
           }
         }
