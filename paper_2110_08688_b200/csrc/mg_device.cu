@@ -506,27 +506,7 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
       for (index_t i = b; i < e; ++i) o[i] = static_cast<int>(t.row_ptr[r0 + i]);
     }, index_t(1) << 18);
   });
-  // FAST mode: rank the tile's columns by how often they are gathered and tag each record with the
-  // column's hub class (top 4 bits), so the gather can keep the hottest rows resident in L2.
-  std::vector<uint8_t> cls;
-  if (g.cfg.spmm_mode == MG_SPMM_FAST && g_hub_bytes.load() > 0 && d.nnz && t.cols < (index_t(1) << 28)) {
-    std::vector<index_t> cnt(static_cast<size_t>(t.cols), 0);
-    for (index_t i = 0; i < d.nnz; ++i) cnt[t.col[i]]++;
-    index_t maxc = 0;
-    for (index_t c : cnt) maxc = std::max(maxc, c);
-    std::vector<index_t> hist(static_cast<size_t>(maxc) + 2, 0);  // columns per count, most gathered first
-    for (index_t c : cnt) hist[maxc - c + 1]++;
-    for (size_t i = 1; i < hist.size(); ++i) hist[i] += hist[i - 1];
-    cls.assign(static_cast<size_t>(t.cols), 0);
-    for (index_t c = 0; c < t.cols; ++c) {
-      const index_t rank = hist[maxc - cnt[c]]++;
-      int k = 1;
-      while (k <= 7 && rank >= 10000 * (index_t(1) << (k - 1))) ++k;
-      cls[c] = static_cast<uint8_t>(k <= 7 ? k : 0);
-    }
-    d.hubs_classed = true;
-  }
-  if (d.nnz)  // {col (| hub class << 28), value bits} records
+  if (d.nnz)  // {col, value bits} records
     st.upload(d.edges, sizeof(int2) * d.nnz, [&](char* dst, size_t off, size_t len) {
       int2* o = reinterpret_cast<int2*>(dst);
       const index_t e0 = static_cast<index_t>(off / sizeof(int2));
@@ -534,11 +514,40 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
         for (index_t i = b; i < e; ++i) {
           int bits;
           std::memcpy(&bits, &t.val[e0 + i], 4);
-          const int c = t.col[e0 + i];
-          o[i] = make_int2(cls.empty() ? c : (c | (static_cast<int>(cls[c]) << 28)), bits);
+          o[i] = make_int2(t.col[e0 + i], bits);
         }
       }, index_t(1) << 18);
     });
+  // FAST mode: tag each record with its column's hub class (top 4 bits), computed on the device from the
+  // uploaded records: per-column gather counts, a histogram of the counts, and per-tier count thresholds
+  // (class k = gathered at least as often as the 10000 * 2^(k-1)-th most gathered column).
+  if (g.cfg.spmm_mode == MG_SPMM_FAST && g_hub_bytes.load() > 0 && d.nnz && t.cols < (index_t(1) << 28)) {
+    int* cnt = nullptr;
+    int* chist = nullptr;
+    MG_CUDA(cudaMalloc(&cnt, sizeof(int) * t.cols));
+    MG_CUDA(cudaMalloc(&chist, sizeof(int) * (k::kHubCountCap + 1)));
+    MG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * t.cols, cudaStreamLegacy));
+    MG_CUDA(cudaMemsetAsync(chist, 0, sizeof(int) * (k::kHubCountCap + 1), cudaStreamLegacy));
+    const int gb = num_sms() * 8;
+    k::hub_count<<<gb, 256, 0, cudaStreamLegacy>>>(d.edges, d.nnz, cnt);
+    k::hub_count_hist<<<gb, 256, 0, cudaStreamLegacy>>>(cnt, t.cols, chist);
+    std::vector<int> h(k::kHubCountCap + 1);
+    MG_CUDA(cudaMemcpy(h.data(), chist, sizeof(int) * h.size(), cudaMemcpyDeviceToHost));
+    k::HubTiers tiers{};
+    index_t seen = 0;
+    int tier = 0;
+    for (int c = k::kHubCountCap; c >= 1 && tier < 7; --c) {  // most gathered first
+      seen += h[c];
+      while (tier < 7 && seen >= 10000 * (index_t(1) << tier)) tiers.thr[tier++] = c;
+    }
+    for (; tier < 7; ++tier) tiers.thr[tier] = 1;  // fewer columns than the tier: everything gathered is in
+    k::hub_tag<<<gb, 256, 0, cudaStreamLegacy>>>(d.edges, d.nnz, cnt, tiers);
+    MG_LAUNCHED();
+    MG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+    cudaFree(cnt);
+    cudaFree(chist);
+    d.hubs_classed = true;
+  }
   if (g.cfg.spmm_mode == MG_SPMM_FAST) {
     std::vector<int4> items, hubs;
     build_fast_items(t.row_ptr, items, hubs, d.n_segments);

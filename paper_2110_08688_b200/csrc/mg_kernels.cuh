@@ -333,6 +333,32 @@ __global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ 
   }
 }
 
+// Hub classes of a FAST tile (upload time): gather counts per column, a histogram of the counts (capped),
+// and the tag pass: class k in 1..7 when count >= thr[k-1] (thr non-increasing), else 0.
+constexpr int kHubCountCap = 1 << 16;
+struct HubTiers {
+  int thr[7];
+};
+__global__ void hub_count(const int2* __restrict__ edges, long nnz, int* __restrict__ cnt) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < nnz; i += (long)gridDim.x * blockDim.x)
+    atomicAdd(cnt + (edges[i].x & kColMask), 1);
+}
+__global__ void hub_count_hist(const int* __restrict__ cnt, long cols, int* __restrict__ hist) {
+  for (long c = blockIdx.x * (long)blockDim.x + threadIdx.x; c < cols; c += (long)gridDim.x * blockDim.x)
+    atomicAdd(hist + min(cnt[c], kHubCountCap), 1);
+}
+__global__ void hub_tag(int2* __restrict__ edges, long nnz, const int* __restrict__ cnt, HubTiers t) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < nnz; i += (long)gridDim.x * blockDim.x) {
+    const int col = edges[i].x & kColMask;
+    const int c = cnt[col];
+    int k = 0;
+#pragma unroll
+    for (int q = 6; q >= 0; --q)
+      if (c >= t.thr[q]) k = q + 1;
+    edges[i].x = col | (k << 28);
+  }
+}
+
 // hubs[i] = {row, first segment, segment count}: out[row] = (acc ? out[row] : 0) + sum of its segments in
 // order, then relu. One CTA per hub row, threads over float4 chunks.
 __global__ void __launch_bounds__(256) spmm_fast_hubs(const int4* __restrict__ hubs, const float* __restrict__ scratch,
