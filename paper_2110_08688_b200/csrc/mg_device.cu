@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <future>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -449,20 +450,30 @@ T* dalloc_t(mg_group& g, Worker& w, size_t count) {
 // upload() returns only when they are complete.
 class Stager {
  public:
-  static constexpr size_t kChunk = size_t(64) << 20;
+  static constexpr size_t kChunk = size_t(128) << 20;
   // fill(dst, first_byte, bytes) writes bytes [first_byte, first_byte + bytes) of the payload into dst
   void upload(void* dev, size_t bytes, const std::function<void(char*, size_t, size_t)>& fill) {
     std::lock_guard<std::mutex> lk(mu_);
     const cudaStream_t s = cudaStreamLegacy;
     init();
+    using clk = std::chrono::steady_clock;
+    double t_wait = 0, t_fill = 0;
+    const auto t0 = clk::now();
     for (size_t off = 0, b = 0; off < bytes; off += kChunk, b ^= 1) {
       const size_t len = std::min(kChunk, bytes - off);
+      auto a = clk::now();
       MG_CUDA(cudaEventSynchronize(done_[b]));  // the previous DMA out of this buffer has finished
+      auto c = clk::now();
       fill(buf_[b], off, len);
+      t_wait += std::chrono::duration<double, std::milli>(c - a).count();
+      t_fill += std::chrono::duration<double, std::milli>(clk::now() - c).count();
       MG_CUDA(cudaMemcpyAsync(static_cast<char*>(dev) + off, buf_[b], len, cudaMemcpyHostToDevice, s));
       MG_CUDA(cudaEventRecord(done_[b], s));
     }
     MG_CUDA(cudaStreamSynchronize(s));
+    if (std::getenv("MGGCN_TIMING") && bytes > (size_t(16) << 20))
+      std::fprintf(stderr, "[mggcn] stage %7.1f MB: total %6.1f ms, fill %6.1f ms, wait %6.1f ms\n", bytes / 1e6,
+                   std::chrono::duration<double, std::milli>(clk::now() - t0).count(), t_fill, t_wait);
   }
   template <class T>
   void upload_array(T* dev, const T* src, size_t count) {
@@ -506,18 +517,24 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
       for (index_t i = b; i < e; ++i) o[i] = static_cast<int>(t.row_ptr[r0 + i]);
     }, index_t(1) << 18);
   });
-  if (d.nnz)  // {col, value bits} records
-    st.upload(d.edges, sizeof(int2) * d.nnz, [&](char* dst, size_t off, size_t len) {
-      int2* o = reinterpret_cast<int2*>(dst);
-      const index_t e0 = static_cast<index_t>(off / sizeof(int2));
-      parallel_for(static_cast<index_t>(len / sizeof(int2)), [&](index_t b, index_t e) {
-        for (index_t i = b; i < e; ++i) {
-          int bits;
-          std::memcpy(&bits, &t.val[e0 + i], 4);
-          o[i] = make_int2(t.col[e0 + i], bits);
-        }
-      }, index_t(1) << 18);
-    });
+  // FAST work lists are built on a host thread while the arrays upload
+  std::vector<int4> items, hubs;
+  std::future<void> lists;
+  if (g.cfg.spmm_mode == MG_SPMM_FAST)
+    lists = std::async(std::launch::async, [&] { build_fast_items(t.row_ptr, items, hubs, d.n_segments); });
+  if (d.nnz) {  // {col, value bits} records: both arrays go up as they are, the device interleaves them
+    int* tcol = nullptr;
+    float* tval = nullptr;
+    MG_CUDA(cudaMalloc(&tcol, sizeof(int) * d.nnz));
+    MG_CUDA(cudaMalloc(&tval, sizeof(float) * d.nnz));
+    st.upload_array(tcol, t.col.data(), static_cast<size_t>(d.nnz));
+    st.upload_array(tval, t.val.data(), static_cast<size_t>(d.nnz));
+    k::pack_edges<<<num_sms() * 8, 256, 0, cudaStreamLegacy>>>(tcol, tval, d.nnz, d.edges);
+    MG_LAUNCHED();
+    MG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+    cudaFree(tcol);
+    cudaFree(tval);
+  }
   // FAST mode: tag each record with its column's hub class (top 4 bits), computed on the device from the
   // uploaded records: per-column gather counts, a histogram of the counts, and per-tier count thresholds
   // (class k = gathered at least as often as the 10000 * 2^(k-1)-th most gathered column).
@@ -549,8 +566,7 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
     d.hubs_classed = true;
   }
   if (g.cfg.spmm_mode == MG_SPMM_FAST) {
-    std::vector<int4> items, hubs;
-    build_fast_items(t.row_ptr, items, hubs, d.n_segments);
+    lists.get();
     d.items = dalloc_t<int4>(g, w, std::max<size_t>(1, items.size()));
     d.hubs = dalloc_t<int4>(g, w, std::max<size_t>(1, hubs.size()));
     d.n_items = static_cast<int>(items.size());

@@ -333,6 +333,13 @@ __global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ 
   }
 }
 
+// Upload time: interleave the tile's column and value arrays into {col, value bits} records.
+__global__ void pack_edges(const int* __restrict__ col, const float* __restrict__ val, long nnz,
+                           int2* __restrict__ edges) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < nnz; i += (long)gridDim.x * blockDim.x)
+    edges[i] = make_int2(col[i], __float_as_int(val[i]));
+}
+
 // Hub classes of a FAST tile (upload time): gather counts per column, a histogram of the counts (capped),
 // and the tag pass: class k in 1..7 when count >= thr[k-1] (thr non-increasing), else 0.
 constexpr int kHubCountCap = 1 << 16;
