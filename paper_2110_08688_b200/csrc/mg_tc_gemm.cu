@@ -48,6 +48,7 @@ namespace tc {
 constexpr int BM = 128;            // tile rows = TMEM lanes
 constexpr int BK = 16;             // K per pipeline stage
 constexpr int kMaxStages = 8;
+constexpr int kTraceStages = 256, kTraceItems = 16;  // MGGCN_TC_TRACE clock trace sizes
 constexpr int kThreads = 320;      // 10 warps: 0 TMA, 1 MMA, 2-5 split, 6-9 epilogue
 constexpr int kPromoteKb = 16;     // TN: drain TMEM every 16 K blocks (256 rows)
 constexpr int kSmemBudget = 200 * 1024;  // smem stage ring
@@ -75,9 +76,11 @@ struct Params {
   int blk_first[9];      // first work item of each block (prefix over blocks)
   float* partial;        // [n_items][BM][npb]
   float* dbg;            // debugging aid (MGGCN_TC_DEBUG): first stage tiles + first TMEM rows, else null
+  long long* trace;      // MGGCN_TC_TRACE: CTA 0 clock64 per stage [kTraceStages][4] + per item [..][2]
   // v2
   int n_tiles;           // output column tiles of <= 128
   int bnr;               // B rows (tile columns) loaded per stage: min(np, 128) (TN: rounded to 32)
+  int nwst;              // v3: W ring stages (nst = A ring stages)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -92,6 +95,19 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 }
 __device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {  // non-blocking phase check
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
@@ -416,6 +432,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(const __grid_constant__ C
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && ac < kTraceItems)
+          p.trace[kTraceStages * 4 + ac * 2 + 1] = clock64();
       }
     }
   }
@@ -550,12 +568,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t sc = 0;
-      const uint32_t tx = static_cast<uint32_t>(MODE == TN ? a_bytes + b_bytes : stage);
+      // single-term TF32 never reads B lo: do not load it
+      const uint32_t tx = static_cast<uint32_t>(MODE == TN || p.terms != 3 ? a_bytes + b_bytes : stage);
       for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
         const Item2 I = item2_of(p, MODE, it);
         for (int kb = 0; kb < I.k.nkb; ++kb, ++sc) {
           const int s = sc % p.nst;
           if (sc >= static_cast<uint32_t>(p.nst)) mbar_wait(&empty[s], ((sc / p.nst) - 1) & 1);
+          if (p.trace && blockIdx.x == 0 && sc < kTraceStages) p.trace[sc * 4 + 0] = clock64();
           uint8_t* a = smem + s * stage;
           uint8_t* b = a + a_bytes;
           mbar_arrive_tx(&full[s], tx);
@@ -567,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
             const int k0 = kb * BK;
             tma_load_2d(a, &map_a, k0, static_cast<int>(I.k.row0), &full[s]);
             tma_load_2d(b, &map_bh, k0, I.n0, &full[s]);
-            tma_load_2d(b + b_bytes, &map_bl, k0, I.n0, &full[s]);
+            if (p.terms == 3) tma_load_2d(b + b_bytes, &map_bl, k0, I.n0, &full[s]);
           }
         }
       }
@@ -590,6 +610,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
           const int s = sc % p.nst;
           mbar_wait(&conv[s], (sc / p.nst) & 1);
           tc_fence_after();
+          if (p.trace && blockIdx.x == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 3] = clock64();
           if (lane == 0) {
             const uint32_t bh = smem_u32(smem + s * stage + a_bytes), bl = bh + b_bytes;
             const uint32_t ah = tmem + static_cast<uint32_t>(kAcol + s * 32), al = ah + 16;
@@ -617,6 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
     }
   } else if (warp < 6) {
     // ------------------------------------------------------------ split A into TMEM (+ split B for TN)
+    // Explicit shared-space loads of the raw tile (the aligned dynamic-smem pointer is generic to the compiler).
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int t = threadIdx.x - 64;
@@ -626,21 +648,23 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
       for (int kb = 0; kb < I.k.nkb; ++kb, ++sc) {
         const int s = sc % p.nst;
         mbar_wait(&full[s], (sc / p.nst) & 1);  // also implies the MMAs of this stage's last use are done
-        const float* araw = reinterpret_cast<const float*>(smem + s * stage);
+        if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 1] = clock64();
+        const uint32_t araw = smem_u32(smem + s * stage);
         float x[BK];
         if (MODE == TN) {
           const int valid = static_cast<int>(min(static_cast<long>(BK), I.k.k_end - (I.k.row0 + kb * BK)));
 #pragma unroll
-          for (int k = 0; k < BK; ++k) x[k] = k < valid ? araw[k * BM + row] : 0.0f;
+          for (int k = 0; k < BK; ++k) {
+            float v;
+            asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(araw + 4u * (k * BM + row)));
+            x[k] = k < valid ? v : 0.0f;
+          }
         } else {
 #pragma unroll
-          for (int k4 = 0; k4 < BK / 4; ++k4) {
-            const float4 v = reinterpret_cast<const float4*>(araw + row * BK)[k4];
-            x[4 * k4] = v.x;
-            x[4 * k4 + 1] = v.y;
-            x[4 * k4 + 2] = v.z;
-            x[4 * k4 + 3] = v.w;
-          }
+          for (int k4 = 0; k4 < BK / 4; ++k4)
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                         : "=f"(x[4 * k4]), "=f"(x[4 * k4 + 1]), "=f"(x[4 * k4 + 2]), "=f"(x[4 * k4 + 3])
+                         : "r"(araw + 4u * (row * BK + 4 * k4)));
         }
         uint32_t hi[BK], lo[BK];
 #pragma unroll
@@ -649,24 +673,32 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
           hi[k] = __float_as_uint(h);
           lo[k] = __float_as_uint(__fsub_rn(x[k], h));
         }
-        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(kAcol + s * 32);
-        tmem_st16(ta, hi);
-        if (p.terms == 3) tmem_st16(ta + 16, lo);
         if (MODE == TN && p.terms == 3) {  // B = G rows: split in place in smem (hi) + lo copy
-          uint8_t* bh = smem + s * stage + a_bytes;
-          uint8_t* bl = bh + b_bytes;
+          const uint32_t bh = smem_u32(smem + s * stage + a_bytes);
+          const uint32_t bl = bh + static_cast<uint32_t>(b_bytes);
           for (int q4 = t; q4 < b_bytes / 16; q4 += 128) {
-            float4 l;
-            const float4 h = split4(reinterpret_cast<float4*>(bh)[q4], l);
-            reinterpret_cast<float4*>(bh)[q4] = h;
-            reinterpret_cast<float4*>(bl)[q4] = l;
+            float4 v, l;
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                         : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                         : "r"(bh + 16u * q4));
+            const float4 h = split4(v, l);
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(bh + 16u * q4), "f"(h.x), "f"(h.y),
+                         "f"(h.z), "f"(h.w)
+                         : "memory");
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(bl + 16u * q4), "f"(l.x), "f"(l.y),
+                         "f"(l.z), "f"(l.w)
+                         : "memory");
           }
           fence_async_smem();
         }
+        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(kAcol + s * 32);
+        tmem_st16(ta, hi);
+        if (p.terms == 3) tmem_st16(ta + 16, lo);
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[s]);
+        if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 2] = clock64();
       }
     }
   } else {
@@ -691,6 +723,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
         const int buf = static_cast<int>(ac & 1);
         mbar_wait(&tfull[buf], (ac >> 1) & 1);
         tc_fence_after();
+        if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && ac < kTraceItems)
+          p.trace[kTraceStages * 4 + ac * 2 + 0] = clock64();
         if (MODE != TN && p.epi == 1) mbar_wait(&oldbar[q], tiles & 1);
         const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf * kTileN);
         for (int c = 0; c < nch; ++c) {
@@ -719,8 +753,257 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tempty[buf]);
+        if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && ac < kTraceItems)
+          p.trace[kTraceStages * 4 + ac * 2 + 1] = clock64();
       }
       // the finished 32-row slab leaves with bulk tensor stores (rows / columns past the end are clipped)
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        for (int c = 0; c < nch; ++c) tma_store_2d(&map_c, I.n0 + c * 32, static_cast<int>(grow0), bufs + c * 1024);
+        bulk_commit();
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+// ================================================================ v3 (NN / NT): wide stages, decoupled rings
+// The MGGCN_TC_TRACE clock trace of v2 showed the K-block pipeline stepping at ~900 cycles against 384
+// MMA cycles: the TMA engine was bounded by the number of 64-byte row segments per stage (A, W hi and W lo
+// boxes of 16 fp32 per row), not by bytes. v3 moves 32 K per stage with 128-byte rows (SWIZZLE_128B boxes,
+// half the segments per byte), and decouples the rings: the streamed operand A (HBM) has its own ring of
+// raw 16 KB tiles, released as soon as the split warps hold them in registers; W hi / lo (L2-resident)
+// have a shallow ring with their own producer warp; the 4 TMEM A slots (64 columns: hi | lo of 32 K) are
+// released by the MMA's own commit. Warps: 0 A producer, 1 MMA, 2-5 split, 6-9 epilogue, 10 W producer.
+constexpr int kThreads3 = 352;
+constexpr int BK3 = 32;
+constexpr int kMaxA3 = 12, kMaxW3 = 4, kTSlots3 = 4;
+
+// K-major SWIZZLE_128B: 8-row x 128-byte atoms, SBO = 1024 B between 8-row groups, LBO unused (16 B).
+__device__ __forceinline__ uint64_t desc_k128(uint32_t saddr) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(1) << 16) |
+         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__ CUtensorMap map_a,
+                                                         const __grid_constant__ CUtensorMap map_bh,
+                                                         const __grid_constant__ CUtensorMap map_bl,
+                                                         const __grid_constant__ CUtensorMap map_c, Params p) {
+  static_assert(MODE != TN, "v3 covers NN / NT");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t fullA[kMaxA3], emptyA[kMaxA3], fullW[kMaxW3], emptyW[kMaxW3], conv[kTSlots3], tslot[kTSlots3];
+  __shared__ uint64_t tfull[2], tempty[2], oldbar[4];
+  __shared__ uint32_t tmem_base_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nA = p.nst, nW = p.nwst;
+  constexpr int a_bytes = BM * BK3 * 4;  // raw A tile [128 rows][32 k], SWIZZLE_128B
+  const int b_bytes = p.bnr * BK3 * 4;   // one W tile (hi or lo), K-major [bnr][32 k], SWIZZLE_128B
+  uint8_t* aring = smem;                 // nA x a_bytes
+  uint8_t* wring = smem + nA * a_bytes;  // nW x (hi | lo)
+  float* epib = reinterpret_cast<float*>(wring + nW * 2 * b_bytes);
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < nA; ++s) {
+      mbar_init(&fullA[s], 1);
+      mbar_init(&emptyA[s], 4);
+    }
+    for (int s = 0; s < nW; ++s) {
+      mbar_init(&fullW[s], 1);
+      mbar_init(&emptyW[s], 1);
+    }
+    for (int s = 0; s < kTSlots3; ++s) {
+      mbar_init(&conv[s], 4);
+      mbar_init(&tslot[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 4);
+    }
+    for (int q = 0; q < 4; ++q) mbar_init(&oldbar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_bh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&map_bl)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base_s;
+  const int nkb = static_cast<int>((p.K + BK3 - 1) / BK3);
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ A producer (HBM stream, deep ring)
+    if (lane == 0) {
+      uint32_t sc = 0;
+      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+        const Item2 I = item2_of(p, MODE, it);
+        for (int kb = 0; kb < nkb; ++kb, ++sc) {
+          const int s = sc % nA;
+          if (sc >= static_cast<uint32_t>(nA)) mbar_wait(&emptyA[s], ((sc / nA) - 1) & 1);
+          if (p.trace && blockIdx.x == 0 && sc < kTraceStages) p.trace[sc * 4 + 0] = clock64();
+          mbar_arrive_tx(&fullA[s], static_cast<uint32_t>(a_bytes));
+          tma_load_2d(aring + s * a_bytes, &map_a, kb * BK3, static_cast<int>(I.k.row0), &fullA[s]);
+        }
+      }
+    }
+  } else if (warp == 10) {
+    // ------------------------------------------------------------ W producer (L2-resident, shallow ring)
+    if (lane == 0) {
+      uint32_t sc = 0;
+      const uint32_t tx = static_cast<uint32_t>(p.terms == 3 ? 2 * b_bytes : b_bytes);
+      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+        const Item2 I = item2_of(p, MODE, it);
+        for (int kb = 0; kb < nkb; ++kb, ++sc) {
+          const int s = sc % nW;
+          if (sc >= static_cast<uint32_t>(nW)) mbar_wait(&emptyW[s], ((sc / nW) - 1) & 1);
+          uint8_t* b = wring + s * 2 * b_bytes;
+          mbar_arrive_tx(&fullW[s], tx);
+          tma_load_2d(b, &map_bh, kb * BK3, I.n0, &fullW[s]);
+          if (p.terms == 3) tma_load_2d(b + b_bytes, &map_bl, kb * BK3, I.n0, &fullW[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (A from TMEM slots)
+    uint32_t sc = 0, ac = 0;
+    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++ac) {
+      const Item2 I = item2_of(p, MODE, it);
+      const uint32_t idesc = idesc_tf32(BM, I.nw, 0, 0);
+      const int buf = static_cast<int>(ac & 1);
+      if (ac >= 2u) mbar_wait(&tempty[buf], ((ac >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t d = tmem + static_cast<uint32_t>(buf * kTileN);
+      for (int kb = 0; kb < nkb; ++kb, ++sc) {
+        const int j = sc % kTSlots3, w = sc % nW;
+        mbar_wait(&conv[j], (sc / kTSlots3) & 1);
+        mbar_wait(&fullW[w], (sc / nW) & 1);
+        tc_fence_after();
+        if (p.trace && blockIdx.x == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 3] = clock64();
+        if (lane == 0) {
+          const uint32_t bh = smem_u32(wring + w * 2 * b_bytes), bl = bh + b_bytes;
+          const uint32_t ah = tmem + static_cast<uint32_t>(kAcol + j * 64), al = ah + 32;
+#pragma unroll
+          for (int kk = 0; kk < BK3 / 8; ++kk) {
+            const uint64_t dbh = desc_k128(bh + kk * 32);
+            const uint32_t first = (kb == 0 && kk == 0) ? 0u : 1u;
+            if (p.terms == 3) {
+              const uint64_t dbl = desc_k128(bl + kk * 32);
+              mma_tf32_ts(d, al + kk * 8, dbh, idesc, first);
+              mma_tf32_ts(d, ah + kk * 8, dbl, idesc, 1u);
+              mma_tf32_ts(d, ah + kk * 8, dbh, idesc, 1u);
+            } else {
+              mma_tf32_ts(d, ah + kk * 8, dbh, idesc, first);
+            }
+          }
+          mma_commit(&tslot[j]);   // TMEM A slot j reusable
+          mma_commit(&emptyW[w]);  // W slot w reusable
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mma_commit(&tfull[buf]);
+      __syncwarp();
+    }
+  } else if (warp < 6) {
+    // ------------------------------------------------------------ split: raw A (smem) -> hi / lo (TMEM slot)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    uint32_t sc = 0;
+    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+      for (int kb = 0; kb < nkb; ++kb, ++sc) {
+        const int s = sc % nA, j = sc % kTSlots3;
+        mbar_wait(&fullA[s], (sc / nA) & 1);
+        if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 1] = clock64();
+        // row r's 16-byte chunk c sits at r * 128 + ((c ^ (r & 7)) * 16) (SWIZZLE_128B)
+        const uint32_t rbase = smem_u32(aring + s * a_bytes) + static_cast<uint32_t>(row * 128);
+        float x[BK3];
+#pragma unroll
+        for (int c = 0; c < BK3 / 4; ++c)
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                       : "=f"(x[4 * c]), "=f"(x[4 * c + 1]), "=f"(x[4 * c + 2]), "=f"(x[4 * c + 3])
+                       : "r"(rbase + static_cast<uint32_t>(((c ^ (row & 7)) << 4))));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&emptyA[s]);  // the raw tile is in registers: the producer may refill
+        uint32_t hi[BK3], lo[BK3];
+#pragma unroll
+        for (int k = 0; k < BK3; ++k) {
+          const float h = p.terms == 3 ? __uint_as_float(__float_as_uint(x[k]) & 0xFFFFE000u) : x[k];
+          hi[k] = __float_as_uint(h);
+          lo[k] = __float_as_uint(__fsub_rn(x[k], h));
+        }
+        if (sc >= static_cast<uint32_t>(kTSlots3)) mbar_wait(&tslot[j], ((sc / kTSlots3) - 1) & 1);
+        tc_fence_after();
+        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(kAcol + j * 64);
+        tmem_st16(ta, hi);
+        tmem_st16(ta + 16, hi + 16);
+        if (p.terms == 3) {
+          tmem_st16(ta + 32, lo);
+          tmem_st16(ta + 48, lo + 16);
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[j]);
+        if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 2] = clock64();
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ epilogue (as v2, NN / NT)
+    const int q = warp & 3;
+    uint32_t ac = 0;
+    float* bufs = epib + q * (4 * 1024);  // 4 chunks of 32 x 32
+    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++ac) {
+      const Item2 I = item2_of(p, MODE, it);
+      const int nch = (I.nw + 31) / 32;
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+      const long grow0 = I.k.row0 + q * 32;
+      if (p.epi == 1 && lane == 0) {  // prefetch the relu_backward mask source
+        mbar_arrive_tx(&oldbar[q], static_cast<uint32_t>(nch * 4096));
+        for (int c = 0; c < nch; ++c)
+          tma_load_2d(bufs + c * 1024, &map_c, I.n0 + c * 32, static_cast<int>(grow0), &oldbar[q]);
+      }
+      const int buf = static_cast<int>(ac & 1);
+      mbar_wait(&tfull[buf], (ac >> 1) & 1);
+      tc_fence_after();
+      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && ac < kTraceItems)
+        p.trace[kTraceStages * 4 + ac * 2 + 0] = clock64();
+      if (p.epi == 1) mbar_wait(&oldbar[q], ac & 1);
+      const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf * kTileN);
+      for (int c = 0; c < nch; ++c) {
+        float v[32];
+        tmem_ld32(tbase + c * 32, v);
+        float* b = bufs + c * 1024;
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          float4 o = make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
+          float4* dst = sw128(b, lane, jj);
+          if (p.epi == 1) {
+            const float4 old = *dst;
+            o = make_float4(old.x > 0.0f ? o.x : 0.0f, old.y > 0.0f ? o.y : 0.0f, old.z > 0.0f ? o.z : 0.0f,
+                            old.w > 0.0f ? o.w : 0.0f);
+          } else if (p.epi == 2) {
+            o = make_float4(fmaxf(o.x, 0.0f), fmaxf(o.y, 0.0f), fmaxf(o.z, 0.0f), fmaxf(o.w, 0.0f));
+          }
+          *dst = o;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[buf]);
+      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && ac < kTraceItems)
+        p.trace[kTraceStages * 4 + ac * 2 + 1] = clock64();
       fence_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -822,7 +1105,7 @@ void check_ptr(const void* p, long ld, const char* what) {
 }
 
 // ---- v2 (A in TMEM) host side
-int g_gemm_version = 2;
+int g_gemm_version = 3;
 
 constexpr int kSmemBudget2 = 160 * 1024;  // v2 stage ring (+ kEpiBuf epilogue buffers)
 
@@ -839,6 +1122,29 @@ void finish_params2(Params& p, long N, bool tn, int terms) {
 }
 
 inline int smem_bytes2(const Params& p) { return p.nst * (BM * BK * 4 + 2 * p.bnr * BK * 4) + kEpiBuf + 1024; }
+
+// v3 (NN / NT): A ring as deep as the shared memory left after the W ring and the epilogue buffers.
+constexpr int kSmemMax3 = 232448 - 2048;  // sm_100 per-block maximum, minus static barriers and alignment
+void finish_params3(Params& p) {
+  const int wst = 2 * p.bnr * BK3 * 4, ast = BM * BK3 * 4;
+  p.nwst = std::max(2, std::min(kMaxW3, 64 * 1024 / wst));
+  p.nst = std::max(2, std::min(kMaxA3, (kSmemMax3 - 1024 - kEpiBuf - p.nwst * wst) / ast));
+}
+inline int smem_bytes3(const Params& p) {
+  return p.nst * BM * BK3 * 4 + p.nwst * 2 * p.bnr * BK3 * 4 + kEpiBuf + 1024;
+}
+template <int MODE>
+void launch3(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
+             cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    TC_CUDA(cudaFuncSetAttribute(gemm_tc3<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax3));
+    attr = true;
+  }
+  const int grid = std::max(1, std::min(p.n_items, num_sms()));
+  gemm_tc3<MODE><<<grid, kThreads3, smem_bytes3(p), s>>>(a, bh, bl, c, p);
+  TC_CUDA(cudaGetLastError());
+}
 
 template <int MODE>
 void launch2(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
@@ -861,7 +1167,7 @@ size_t nn_workspace_bytes(int64_t N, int64_t K) {
 }
 
 void set_gemm_version(int v) {
-  if (v != 1 && v != 2) throw ValueError("tuning: gemm_kernel must be 1 (SS) or 2 (A in TMEM)");
+  if (v < 1 || v > 3) throw ValueError("tuning: gemm_kernel must be 1 (SS), 2 (A in TMEM) or 3 (v2 + decoupled rings)");
   g_gemm_version = v;
 }
 
@@ -899,7 +1205,7 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
   p.C = C;
   p.ldc = ldc;
   p.epi = epi;
-  if (g_gemm_version == 2) {
+  if (g_gemm_version >= 2) {
     finish_params2(p, N, false, mode == MG_GEMM_TF32X3 ? 3 : 1);
     check_ptr(C, ldc, "C");
     p.m_tiles = static_cast<int>((M + BM - 1) / BM);
@@ -916,10 +1222,37 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
     const CUtensorMap mbh = make_map(bh, kp, p.np, kp, BK, p.bnr, CU_TENSOR_MAP_SWIZZLE_64B);
     const CUtensorMap mbl = make_map(bl, kp, p.np, kp, BK, p.bnr, CU_TENSOR_MAP_SWIZZLE_64B);
     const CUtensorMap mc = make_map(C, N, M, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-    if (!tb)
+    static long long* trace = [] {
+      long long* d = nullptr;
+      if (std::getenv("MGGCN_TC_TRACE")) TC_CUDA(cudaMallocManaged(&d, sizeof(long long) * (kTraceStages * 4 + kTraceItems * 2)));
+      return d;
+    }();
+    p.trace = trace;
+    if (trace) std::fill(trace, trace + kTraceStages * 4 + kTraceItems * 2, 0LL);
+    if (g_gemm_version == 3) {  // 32-K stages, SWIZZLE_128B boxes
+      finish_params3(p);
+      const CUtensorMap ma3 = make_map(A, K, M, lda, BK3, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+      const CUtensorMap mbh3 = make_map(bh, kp, p.np, kp, BK3, p.bnr, CU_TENSOR_MAP_SWIZZLE_128B);
+      const CUtensorMap mbl3 = make_map(bl, kp, p.np, kp, BK3, p.bnr, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (!tb) launch3<NN>(ma3, mbh3, mbl3, mc, p, s);
+      else launch3<NT>(ma3, mbh3, mbl3, mc, p, s);
+    } else if (!tb) {
       launch2<NN>(ma, mbh, mbl, mc, p, s);
-    else
+    } else {
       launch2<NT>(ma, mbh, mbl, mc, p, s);
+    }
+    if (trace) {
+      TC_CUDA(cudaDeviceSynchronize());
+      const long long t0 = trace[0];
+      std::fprintf(stderr, "[tc trace] %s M=%ld N=%ld K=%ld nst=%d items=%d (per stage: issue, full, conv, mma; cycles from first issue)\n",
+                   tb ? "NT" : "NN", static_cast<long>(M), static_cast<long>(N), static_cast<long>(K), p.nst, p.n_items);
+      for (int i = 0; i < 48; ++i)
+        std::fprintf(stderr, "  s%-3d %8lld %8lld %8lld %8lld\n", i, trace[i * 4] - t0, trace[i * 4 + 1] - t0,
+                     trace[i * 4 + 2] - t0, trace[i * 4 + 3] - t0);
+      for (int i = 0; i < 6; ++i)
+        std::fprintf(stderr, "  acc%-2d tfull %8lld done %8lld\n", i, trace[kTraceStages * 4 + 2 * i] - t0,
+                     trace[kTraceStages * 4 + 2 * i + 1] - t0);
+    }
     return 2;
   }
   finish_params(p, N, !tb, mode == MG_GEMM_TF32X3 ? 3 : 1);
@@ -970,7 +1303,7 @@ int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* l
   p.N = N;
   p.C = stage;
   p.ldc = ldc;
-  if (g_gemm_version == 2)
+  if (g_gemm_version >= 2)
     finish_params2(p, N, true, mode == MG_GEMM_TF32X3 ? 3 : 1);
   else
     finish_params(p, N, true, mode == MG_GEMM_TF32X3 ? 3 : 1);
@@ -986,14 +1319,14 @@ int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* l
     p.blk_first[g + 1] = p.blk_first[g] + static_cast<int>(chunks) * p.m_tiles;
     rows_hi = std::max<int64_t>(rows_hi, begin[g] + len[g]);
   }
-  p.n_items = p.blk_first[nblocks] * (g_gemm_version == 2 ? p.n_tiles : 1);
+  p.n_items = p.blk_first[nblocks] * (g_gemm_version >= 2 ? p.n_tiles : 1);
   const size_t need = sizeof(float) * static_cast<size_t>(p.blk_first[nblocks]) * BM * p.npb;
   if (p.n_items > 0 && (!ws || ws_bytes < need)) throw ValueError("tc gemm: TN split-K workspace too small");
   p.partial = ws;
   int kernels = 0;
   if (p.n_items > 0) {
     const CUtensorMap mb = make_map(G, N, rows_hi, ldg, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
-    if (g_gemm_version == 2) {  // A = H rows land raw ([16 k][128 m]) and go to TMEM transposed per lane
+    if (g_gemm_version >= 2) {  // A = H rows land raw ([16 k][128 m]) and go to TMEM transposed per lane
       const CUtensorMap ma = make_map(H, M, rows_hi, ldh, BM, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
       const CUtensorMap mc = make_map(ws, p.npb, static_cast<long>(p.blk_first[nblocks]) * BM, p.npb, 32, 32,
                                       CU_TENSOR_MAP_SWIZZLE_128B);

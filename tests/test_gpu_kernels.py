@@ -134,7 +134,9 @@ TC_SHAPES = [(1000, 256, 100), (777, 256, 256), (130, 48, 256), (300, 256, 47), 
 @pytest.mark.parametrize("mode,tol", [(R.GEMM_TF32X3, 1e-5), (R.GEMM_TF32, 5e-3)])
 @pytest.mark.parametrize("shape", TC_SHAPES)
 @pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False)])
-@pytest.mark.parametrize("kernel", [1, 2])  # 1: both operands split in smem (SS); 2: A split into TMEM (TS)
+# 1: both operands split in smem (SS); 2: A split into TMEM (TS); 3 (default): 2 with 32-K SWIZZLE_128B stages
+# and decoupled A / W rings for NN / NT (TN runs the v2 kernel under 3)
+@pytest.mark.parametrize("kernel", [1, 2, 3])
 def test_gemm_tcgen05(gemm_kernel, shape, ta, tb, mode, tol):
     from gpu_util import normwise
     m, n, k = shape
@@ -159,10 +161,10 @@ def test_gemm_tcgen05(gemm_kernel, shape, ta, tb, mode, tol):
 def gemm_kernel(kernel):
     R.set_tuning("gemm_kernel", kernel)
     yield kernel
-    R.set_tuning("gemm_kernel", 2)
+    R.set_tuning("gemm_kernel", 3)
 
 
-@pytest.mark.parametrize("kernel", [1, 2])
+@pytest.mark.parametrize("kernel", [1, 2, 3])
 def test_gemm_tcgen05_deterministic(gemm_kernel):
     rng = np.random.default_rng(5)
     a = rng.normal(size=(20000, 256)).astype(np.float32)
