@@ -1125,9 +1125,10 @@ inline int smem_bytes2(const Params& p) { return p.nst * (BM * BK * 4 + 2 * p.bn
 
 // v3 (NN / NT): A ring as deep as the shared memory left after the W ring and the epilogue buffers.
 constexpr int kSmemMax3 = 232448 - 2048;  // sm_100 per-block maximum, minus static barriers and alignment
+int g_w3_bytes = 64 * 1024;  // v3 W ring budget ("gemm3_wring", bytes)
 void finish_params3(Params& p) {
   const int wst = 2 * p.bnr * BK3 * 4, ast = BM * BK3 * 4;
-  p.nwst = std::max(2, std::min(kMaxW3, 64 * 1024 / wst));
+  p.nwst = std::max(2, std::min(kMaxW3, g_w3_bytes / wst));
   p.nst = std::max(2, std::min(kMaxA3, (kSmemMax3 - 1024 - kEpiBuf - p.nwst * wst) / ast));
 }
 inline int smem_bytes3(const Params& p) {
@@ -1166,6 +1167,11 @@ size_t nn_workspace_bytes(int64_t N, int64_t K) {
   return 2 * sizeof(float) * static_cast<size_t>((N + 15) / 16 * 16) * static_cast<size_t>((K + 3) / 4 * 4);
 }
 
+void set_w3_bytes(int bytes) {
+  if (bytes < 16 * 1024 || bytes > 160 * 1024) throw ValueError("tuning: gemm3_wring must be 16..160 KiB");
+  g_w3_bytes = bytes;
+}
+
 void set_gemm_version(int v) {
   if (v < 1 || v > 3) throw ValueError("tuning: gemm_kernel must be 1 (SS), 2 (A in TMEM) or 3 (v2 + decoupled rings)");
   g_gemm_version = v;
@@ -1184,6 +1190,33 @@ size_t tn_workspace_bytes(int64_t M, int64_t N, int64_t K) {
   const long m_tiles = (M + BM - 1) / BM;
   const long chunks = (K + g_split_rows - 1) / g_split_rows + 8;  // + one partial chunk per block boundary
   return sizeof(float) * static_cast<size_t>(chunks * m_tiles * BM * npb);
+}
+
+// MGGCN_TC_TRACE: CTA 0's clock64 per pipeline stage (issue, data in smem, A in TMEM, MMA issue) and per
+// accumulator (ready, drained), printed after the launch. Debug aid; it synchronises the device.
+long long* trace_buffer() {
+  static long long* t = [] {
+    long long* d = nullptr;
+    if (std::getenv("MGGCN_TC_TRACE"))
+      TC_CUDA(cudaMallocManaged(&d, sizeof(long long) * (kTraceStages * 4 + kTraceItems * 2)));
+    return d;
+  }();
+  if (t) std::fill(t, t + kTraceStages * 4 + kTraceItems * 2, 0LL);
+  return t;
+}
+void print_trace(const Params& p, const char* what) {
+  if (!p.trace) return;
+  TC_CUDA(cudaDeviceSynchronize());
+  const long long* t = p.trace;
+  const long long t0 = t[0];
+  std::fprintf(stderr, "[tc trace] %s M=%ld N=%ld K=%ld nst=%d items=%d (per stage: issue, full, conv, mma)\n", what,
+               p.M, p.N, p.K, p.nst, p.n_items);
+  for (int i = 0; i < 48; ++i)
+    std::fprintf(stderr, "  s%-3d %8lld %8lld %8lld %8lld\n", i, t[i * 4] - t0, t[i * 4 + 1] - t0, t[i * 4 + 2] - t0,
+                 t[i * 4 + 3] - t0);
+  for (int i = 0; i < kTraceItems; ++i)
+    std::fprintf(stderr, "  acc%-2d ready %8lld drained %8lld\n", i, t[kTraceStages * 4 + 2 * i] - t0,
+                 t[kTraceStages * 4 + 2 * i + 1] - t0);
 }
 
 int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
@@ -1222,13 +1255,7 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
     const CUtensorMap mbh = make_map(bh, kp, p.np, kp, BK, p.bnr, CU_TENSOR_MAP_SWIZZLE_64B);
     const CUtensorMap mbl = make_map(bl, kp, p.np, kp, BK, p.bnr, CU_TENSOR_MAP_SWIZZLE_64B);
     const CUtensorMap mc = make_map(C, N, M, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
-    static long long* trace = [] {
-      long long* d = nullptr;
-      if (std::getenv("MGGCN_TC_TRACE")) TC_CUDA(cudaMallocManaged(&d, sizeof(long long) * (kTraceStages * 4 + kTraceItems * 2)));
-      return d;
-    }();
-    p.trace = trace;
-    if (trace) std::fill(trace, trace + kTraceStages * 4 + kTraceItems * 2, 0LL);
+    p.trace = trace_buffer();
     if (g_gemm_version == 3) {  // 32-K stages, SWIZZLE_128B boxes
       finish_params3(p);
       const CUtensorMap ma3 = make_map(A, K, M, lda, BK3, BM, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -1241,18 +1268,7 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
     } else {
       launch2<NT>(ma, mbh, mbl, mc, p, s);
     }
-    if (trace) {
-      TC_CUDA(cudaDeviceSynchronize());
-      const long long t0 = trace[0];
-      std::fprintf(stderr, "[tc trace] %s M=%ld N=%ld K=%ld nst=%d items=%d (per stage: issue, full, conv, mma; cycles from first issue)\n",
-                   tb ? "NT" : "NN", static_cast<long>(M), static_cast<long>(N), static_cast<long>(K), p.nst, p.n_items);
-      for (int i = 0; i < 48; ++i)
-        std::fprintf(stderr, "  s%-3d %8lld %8lld %8lld %8lld\n", i, trace[i * 4] - t0, trace[i * 4 + 1] - t0,
-                     trace[i * 4 + 2] - t0, trace[i * 4 + 3] - t0);
-      for (int i = 0; i < 6; ++i)
-        std::fprintf(stderr, "  acc%-2d tfull %8lld done %8lld\n", i, trace[kTraceStages * 4 + 2 * i] - t0,
-                     trace[kTraceStages * 4 + 2 * i + 1] - t0);
-    }
+    print_trace(p, tb ? "NT" : "NN");
     return 2;
   }
   finish_params(p, N, !tb, mode == MG_GEMM_TF32X3 ? 3 : 1);
@@ -1330,7 +1346,9 @@ int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* l
       const CUtensorMap ma = make_map(H, M, rows_hi, ldh, BM, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
       const CUtensorMap mc = make_map(ws, p.npb, static_cast<long>(p.blk_first[nblocks]) * BM, p.npb, 32, 32,
                                       CU_TENSOR_MAP_SWIZZLE_128B);
+      p.trace = trace_buffer();
       launch2<TN>(ma, mb, mb, mc, p, s);
+      print_trace(p, "TN");
     } else {
       const CUtensorMap ma = make_map(H, M, rows_hi, ldh, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
       launch<TN>(ma, mb, p, s);

@@ -17,3 +17,13 @@ for _ in range(2):
 torch.cuda.synchronize()
 ref = (a[:4096].double() @ w.double()).float()
 print("max rel err (first 4096 rows):", float((c[:4096] - ref).abs().max() / ref.abs().max()))
+
+# TN (W-grad) at the C4 layer-1 shape: H^T G over 8 canonical blocks of the rows
+h = torch.randn(M, 256, device="cuda")
+g = torch.randn(M, 256, device="cuda")
+stage = torch.empty(8 * 256 * 256, device="cuda")
+import ctypes as C  # noqa: E402
+for _ in range(2):
+    R.dev_gemm(True, False, 256, 256, M, h.data_ptr(), 256, g.data_ptr(), 256, stage.data_ptr(), 256, 0,
+               R.GEMM_TF32X3)
+torch.cuda.synchronize()
