@@ -156,6 +156,11 @@ typedef struct mg_partition mg_partition;
 
 mg_status mg_prepare(const mg_dataset* ds, const mg_config* cfg, int32_t workers, int32_t only_rank,
                      mg_partition** out);
+/* The same partition (bit-identical tiles), with permute_graph / transpose / normalize_in_degree /
+ * tile_rows run on CUDA device `device` as radix sorts of (row, column) keys — the papers-scale path
+ * (SURVEY §8f row 1): no host COO, ~28 bytes of device memory per nonzero at the peak. */
+mg_status mg_prepare_device(const mg_dataset* ds, const mg_config* cfg, int32_t workers, int32_t only_rank,
+                            int32_t device, mg_partition** out);
 /* n, global mask count and the P+1 part bounds (PartitionVector::bounds). */
 mg_status mg_partition_info(const mg_partition* p, int64_t* n, int64_t* mask_count, int64_t* bounds);
 /* dir 0 = forward tiles of A_hat^T, dir 1 = backward tiles of A_hat (PreparedData::fwd/bwd_tiles). */

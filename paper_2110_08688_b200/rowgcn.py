@@ -414,9 +414,16 @@ class PreparedData:
         return x, lab, m, pf
 
 
-def prepare_data(ds: Dataset, cfg: GcnConfig, workers: int, only_rank: int = -1) -> PreparedData:
+def prepare_data(ds: Dataset, cfg: GcnConfig, workers: int, only_rank: int = -1,
+                 device: Optional[int] = None) -> PreparedData:
+    """inc/driver.hpp:87-117. device=None: host partitioner; device=k: the graph work on CUDA device k
+    (mg_prepare_device: radix sorts of (row, column) keys), bit-identical tiles."""
     out = C.c_void_p()
-    _check(lib().mg_prepare(ds._h, C.byref(cfg._c()), int(workers), int(only_rank), C.byref(out)))
+    if device is None:
+        _check(lib().mg_prepare(ds._h, C.byref(cfg._c()), int(workers), int(only_rank), C.byref(out)))
+    else:
+        _check(lib().mg_prepare_device(ds._h, C.byref(cfg._c()), int(workers), int(only_rank), int(device),
+                                       C.byref(out)))
     return PreparedData(out.value, workers)
 
 
