@@ -527,8 +527,13 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
     float* tval = nullptr;
     MG_CUDA(cudaMalloc(&tcol, sizeof(int) * d.nnz));
     MG_CUDA(cudaMalloc(&tval, sizeof(float) * d.nnz));
-    st.upload_array(tcol, t.col.data(), static_cast<size_t>(d.nnz));
-    st.upload_array(tval, t.val.data(), static_cast<size_t>(d.nnz));
+    if (is_pinned_host(t.col.data()) && is_pinned_host(t.val.data())) {  // one DMA each, no staging copy
+      MG_CUDA(cudaMemcpyAsync(tcol, t.col.data(), sizeof(int) * d.nnz, cudaMemcpyHostToDevice, cudaStreamLegacy));
+      MG_CUDA(cudaMemcpyAsync(tval, t.val.data(), sizeof(float) * d.nnz, cudaMemcpyHostToDevice, cudaStreamLegacy));
+    } else {
+      st.upload_array(tcol, t.col.data(), static_cast<size_t>(d.nnz));
+      st.upload_array(tval, t.val.data(), static_cast<size_t>(d.nnz));
+    }
     k::pack_edges<<<num_sms() * 8, 256, 0, cudaStreamLegacy>>>(tcol, tval, d.nnz, d.edges);
     MG_LAUNCHED();
     MG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
@@ -587,6 +592,11 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
 
 // Copies rows x cols (host, dense) into a device buffer with leading dimension ld (padding = 0).
 void upload_padded(float* dst, const float* src, index_t rows, index_t cols, index_t ld) {
+  if (cols == ld && rows * cols > 0 && is_pinned_host(src)) {
+    MG_CUDA(cudaMemcpyAsync(dst, src, sizeof(float) * rows * cols, cudaMemcpyHostToDevice, cudaStreamLegacy));
+    MG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+    return;
+  }
   if (cols == ld && rows * cols > 0) {
     stager().upload_array(dst, src, static_cast<size_t>(rows * cols));
     return;

@@ -12,6 +12,8 @@
 #include <mutex>
 #include <numeric>
 
+#include <cuda_runtime.h>
+
 #include "mg_internal.hpp"
 
 namespace mg {
@@ -21,6 +23,45 @@ thread_local std::string g_last_error;
 }
 
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+bool pinned_host_available() {
+  static const bool ok = [] {
+    int n = 0;
+    if (std::getenv("MGGCN_NO_PINNED") || cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+      cudaGetLastError();
+      return false;
+    }
+    return true;
+  }();
+  return ok;
+}
+void* pinned_host_alloc(size_t bytes, bool* pinned) {
+  *pinned = false;
+  void* p = nullptr;
+  if (bytes >= (size_t(1) << 20) && pinned_host_available() &&
+      cudaHostAlloc(&p, bytes, cudaHostAllocPortable) == cudaSuccess) {
+    *pinned = true;
+    return p;
+  }
+  cudaGetLastError();
+  p = std::malloc(bytes ? bytes : 1);
+  if (!p) throw std::bad_alloc();
+  return p;
+}
+bool is_pinned_host(const void* p) {  // also true for interior pointers of a pinned block
+  if (!p || !pinned_host_available()) return false;
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+void pinned_host_free(void* p, bool pinned) {
+  if (!p) return;
+  if (pinned) cudaFreeHost(p);
+  else std::free(p);
+}
 
 int host_threads() {
   static const int t = [] {

@@ -117,13 +117,40 @@ namespace mg {
 
 void validate_dataset_named(const mg_dataset& ds);  // Dataset::validate (inc/dataset.hpp:30-44)
 
+// Host storage for what group creation uploads (tile arrays, permuted features): page-locked when a CUDA
+// device is present, so the upload is one DMA at full link speed with no staging copy (pinning happens at
+// prepare time); plain heap memory otherwise (CPU-only hosts). Zero-initialised like std::vector.
+bool pinned_host_available();
+void* pinned_host_alloc(size_t bytes, bool* pinned);
+void pinned_host_free(void* p, bool pinned);
+bool is_pinned_host(const void* p);
+
+template <class T>
+struct UploadAlloc {
+  using value_type = T;
+  UploadAlloc() = default;
+  template <class U>
+  UploadAlloc(const UploadAlloc<U>&) {}
+  T* allocate(size_t n) {
+    bool pinned = false;
+    return static_cast<T*>(pinned_host_alloc(n * sizeof(T), &pinned));
+  }
+  void deallocate(T* p, size_t) { pinned_host_free(p, is_pinned_host(p)); }
+  template <class U>
+  bool operator==(const UploadAlloc<U>&) const { return true; }
+  template <class U>
+  bool operator!=(const UploadAlloc<U>&) const { return false; }
+};
+template <class T>
+using UploadVec = std::vector<T, UploadAlloc<T>>;
+
 // One tile of the symmetric row tiling (rowgcn::TilePlan, inc/partition.hpp:158-171) in the device
 // staging format: int64 row_ptr (host), int32 local column, fp32 value.
 struct Tile {
   index_t rows = 0, cols = 0;
   std::vector<index_t> row_ptr;
-  std::vector<std::int32_t> col;
-  std::vector<float> val;
+  UploadVec<std::int32_t> col;
+  UploadVec<float> val;
   index_t nnz() const { return static_cast<index_t>(col.size()); }
 };
 
@@ -135,7 +162,7 @@ struct mg_partition {
   int only_rank = -1;
   std::vector<mg::index_t> bounds;
   std::vector<mg::index_t> perm_forward;
-  std::vector<float> features;  // permuted, n x d0
+  mg::UploadVec<float> features;  // permuted, n x d0
   std::vector<std::int32_t> labels;
   std::vector<std::uint8_t> mask;
   // tiles[dir][i][j]; rows i != only_rank are left empty when only_rank >= 0
