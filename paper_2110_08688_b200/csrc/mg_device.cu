@@ -1101,6 +1101,8 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
       g_fast_segment = static_cast<int>(std::min<int64_t>(value, 1 << 24));
     } else if (k == "tn_chunk") {
       tc::set_tn_chunk(static_cast<int>(value));
+    } else if (k == "gemm3_cluster") {
+      tc::set_gemm3_cluster(static_cast<int>(value));
     } else if (k == "gemm3_wring") {
       tc::set_w3_bytes(static_cast<int>(value));
     } else if (k == "gemm_kernel") {

@@ -789,12 +789,32 @@ __device__ __forceinline__ uint64_t desc_k128(uint32_t saddr) {
          (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(2) << 61);
 }
 
-template <int MODE>
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar,
+                                               uint32_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3}], [%4], %5;\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar)), "h"(static_cast<uint16_t>(mask))
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint32_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(mask))
+      : "memory");
+}
+
+template <int MODE, int CL>
 __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__ CUtensorMap map_a,
                                                          const __grid_constant__ CUtensorMap map_bh,
                                                          const __grid_constant__ CUtensorMap map_bl,
                                                          const __grid_constant__ CUtensorMap map_c, Params p) {
   static_assert(MODE != TN, "v3 covers NN / NT");
+  static_assert(CL == 1 || CL == 2, "cluster of 1 or 2");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t fullA[kMaxA3], emptyA[kMaxA3], fullW[kMaxW3], emptyW[kMaxW3], conv[kTSlots3], tslot[kTSlots3];
@@ -815,7 +835,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
     }
     for (int s = 0; s < nW; ++s) {
       mbar_init(&fullW[s], 1);
-      mbar_init(&emptyW[s], 1);
+      mbar_init(&emptyW[s], CL);  // every CTA of the cluster reads the slot (W is multicast)
     }
     for (int s = 0; s < kTSlots3; ++s) {
       mbar_init(&conv[s], 4);
@@ -839,16 +859,32 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync();  // peers' barriers are initialised before any multicast reaches them
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
   const int nkb = static_cast<int>((p.K + BK3 - 1) / BK3);
+  // cluster-synchronous work list: the CL CTAs of a cluster take CL adjacent row tiles of the same
+  // output-column tile, so they consume the same W tiles in the same order (multicast once per cluster)
+  const int rank = static_cast<int>(blockIdx.x % CL), pair0 = static_cast<int>(blockIdx.x / CL);
+  const int npairs = static_cast<int>(gridDim.x / CL);
+  const int npi = ((p.m_tiles + CL - 1) / CL) * p.n_tiles;
+  auto item_of3 = [&](int pi) {
+    Item2 r;
+    const int nt = pi % p.n_tiles;
+    r.mi = (pi / p.n_tiles) * CL + rank;
+    r.n0 = nt * kTileN;
+    r.nw = min(kTileN, p.np - r.n0);
+    r.k.row0 = static_cast<long>(r.mi) * BM;
+    r.k.nkb = nkb;
+    return r;
+  };
 
   if (warp == 0) {
     // ------------------------------------------------------------ A producer (HBM stream, deep ring)
     if (lane == 0) {
       uint32_t sc = 0;
-      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
-        const Item2 I = item2_of(p, MODE, it);
+      for (int pi = pair0; pi < npi; pi += npairs) {
+        const Item2 I = item_of3(pi);
         for (int kb = 0; kb < nkb; ++kb, ++sc) {
           const int s = sc % nA;
           if (sc >= static_cast<uint32_t>(nA)) mbar_wait(&emptyA[s], ((sc / nA) - 1) & 1);
@@ -863,23 +899,31 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
     if (lane == 0) {
       uint32_t sc = 0;
       const uint32_t tx = static_cast<uint32_t>(p.terms == 3 ? 2 * b_bytes : b_bytes);
-      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
-        const Item2 I = item2_of(p, MODE, it);
+      const int half = p.bnr / CL;  // rows of the W tile this CTA loads (and multicasts to its peers)
+      for (int pi = pair0; pi < npi; pi += npairs) {
+        const Item2 I = item_of3(pi);
         for (int kb = 0; kb < nkb; ++kb, ++sc) {
           const int s = sc % nW;
           if (sc >= static_cast<uint32_t>(nW)) mbar_wait(&emptyW[s], ((sc / nW) - 1) & 1);
           uint8_t* b = wring + s * 2 * b_bytes;
           mbar_arrive_tx(&fullW[s], tx);
-          tma_load_2d(b, &map_bh, kb * BK3, I.n0, &fullW[s]);
-          if (p.terms == 3) tma_load_2d(b + b_bytes, &map_bl, kb * BK3, I.n0, &fullW[s]);
+          if (CL == 1) {
+            tma_load_2d(b, &map_bh, kb * BK3, I.n0, &fullW[s]);
+            if (p.terms == 3) tma_load_2d(b + b_bytes, &map_bl, kb * BK3, I.n0, &fullW[s]);
+          } else {
+            const uint32_t off = static_cast<uint32_t>(rank * half * BK3 * 4);
+            tma_load_2d_mc(b + off, &map_bh, kb * BK3, I.n0 + rank * half, &fullW[s], (1u << CL) - 1u);
+            if (p.terms == 3)
+              tma_load_2d_mc(b + b_bytes + off, &map_bl, kb * BK3, I.n0 + rank * half, &fullW[s], (1u << CL) - 1u);
+          }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (A from TMEM slots)
     uint32_t sc = 0, ac = 0;
-    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++ac) {
-      const Item2 I = item2_of(p, MODE, it);
+    for (int pi = pair0; pi < npi; pi += npairs, ++ac) {
+      const Item2 I = item_of3(pi);
       const uint32_t idesc = idesc_tf32(BM, I.nw, 0, 0);
       const int buf = static_cast<int>(ac & 1);
       if (ac >= 2u) mbar_wait(&tempty[buf], ((ac >> 1) - 1) & 1);
@@ -907,8 +951,9 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
               mma_tf32_ts(d, ah + kk * 8, dbh, idesc, first);
             }
           }
-          mma_commit(&tslot[j]);   // TMEM A slot j reusable
-          mma_commit(&emptyW[w]);  // W slot w reusable
+          mma_commit(&tslot[j]);  // TMEM A slot j reusable
+          if (CL == 1) mma_commit(&emptyW[w]);  // W slot w reusable
+          else mma_commit_mc(&emptyW[w], (1u << CL) - 1u);  // ... in every CTA of the cluster
         }
         __syncwarp();
       }
@@ -920,7 +965,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
     const int q = warp & 3;
     const int row = q * 32 + lane;
     uint32_t sc = 0;
-    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+    for (int pi = pair0; pi < npi; pi += npairs) {
       for (int kb = 0; kb < nkb; ++kb, ++sc) {
         const int s = sc % nA, j = sc % kTSlots3;
         mbar_wait(&fullA[s], (sc / nA) & 1);
@@ -963,8 +1008,8 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
     const int q = warp & 3;
     uint32_t ac = 0;
     float* bufs = epib + q * (4 * 1024);  // 4 chunks of 32 x 32
-    for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++ac) {
-      const Item2 I = item2_of(p, MODE, it);
+    for (int pi = pair0; pi < npi; pi += npairs, ++ac) {
+      const Item2 I = item_of3(pi);
       const int nch = (I.nw + 31) / 32;
       if (lane == 0) bulk_wait_read0();
       __syncwarp();
@@ -1015,6 +1060,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync();  // no CTA leaves while a peer may still multicast into it or arrive on it
   if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
@@ -1134,17 +1180,30 @@ void finish_params3(Params& p) {
 inline int smem_bytes3(const Params& p) {
   return p.nst * BM * BK3 * 4 + p.nwst * 2 * p.bnr * BK3 * 4 + kEpiBuf + 1024;
 }
-template <int MODE>
+int g_gemm3_cluster = 1;  // v3 cluster size for the W multicast ("gemm3_cluster": 1 or 2)
+template <int MODE, int CL>
 void launch3(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
              cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    TC_CUDA(cudaFuncSetAttribute(gemm_tc3<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax3));
+    TC_CUDA(cudaFuncSetAttribute(gemm_tc3<MODE, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax3));
     attr = true;
   }
-  const int grid = std::max(1, std::min(p.n_items, num_sms()));
-  gemm_tc3<MODE><<<grid, kThreads3, smem_bytes3(p), s>>>(a, bh, bl, c, p);
-  TC_CUDA(cudaGetLastError());
+  const int npi = ((p.m_tiles + CL - 1) / CL) * p.n_tiles;
+  const int grid = CL * std::max(1, std::min(npi, num_sms() / CL));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads3);
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem_bytes3(p));
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  TC_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc3<MODE, CL>, a, bh, bl, c, p));
 }
 
 template <int MODE>
@@ -1165,6 +1224,11 @@ void launch2(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl,
 
 size_t nn_workspace_bytes(int64_t N, int64_t K) {
   return 2 * sizeof(float) * static_cast<size_t>((N + 15) / 16 * 16) * static_cast<size_t>((K + 3) / 4 * 4);
+}
+
+void set_gemm3_cluster(int c) {
+  if (c != 1 && c != 2) throw ValueError("tuning: gemm3_cluster must be 1 or 2");
+  g_gemm3_cluster = c;
 }
 
 void set_w3_bytes(int bytes) {
@@ -1259,10 +1323,16 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
     if (g_gemm_version == 3) {  // 32-K stages, SWIZZLE_128B boxes
       finish_params3(p);
       const CUtensorMap ma3 = make_map(A, K, M, lda, BK3, BM, CU_TENSOR_MAP_SWIZZLE_128B);
-      const CUtensorMap mbh3 = make_map(bh, kp, p.np, kp, BK3, p.bnr, CU_TENSOR_MAP_SWIZZLE_128B);
-      const CUtensorMap mbl3 = make_map(bl, kp, p.np, kp, BK3, p.bnr, CU_TENSOR_MAP_SWIZZLE_128B);
-      if (!tb) launch3<NN>(ma3, mbh3, mbl3, mc, p, s);
-      else launch3<NT>(ma3, mbh3, mbl3, mc, p, s);
+      const int CL = g_gemm3_cluster;
+      const CUtensorMap mbh3 = make_map(bh, kp, p.np, kp, BK3, p.bnr / CL, CU_TENSOR_MAP_SWIZZLE_128B);
+      const CUtensorMap mbl3 = make_map(bl, kp, p.np, kp, BK3, p.bnr / CL, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (CL == 2) {
+        if (!tb) launch3<NN, 2>(ma3, mbh3, mbl3, mc, p, s);
+        else launch3<NT, 2>(ma3, mbh3, mbl3, mc, p, s);
+      } else {
+        if (!tb) launch3<NN, 1>(ma3, mbh3, mbl3, mc, p, s);
+        else launch3<NT, 1>(ma3, mbh3, mbl3, mc, p, s);
+      }
     } else if (!tb) {
       launch2<NN>(ma, mbh, mbl, mc, p, s);
     } else {

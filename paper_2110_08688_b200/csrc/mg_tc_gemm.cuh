@@ -23,6 +23,7 @@ int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* l
 size_t nn_workspace_bytes(int64_t N, int64_t K);
 void set_tn_chunk(int rows);
 void set_gemm_version(int v);
-void set_w3_bytes(int bytes);  // v3 W ring budget  // 1 = both operands in smem (SS), 2 = A split into TMEM (TS, default)  // TN split-K chunk length (rows, multiple of 32); set before creating groups
+void set_w3_bytes(int bytes);  // v3 W ring budget
+void set_gemm3_cluster(int c);  // v3 W multicast cluster (1 or 2)  // 1 = both operands in smem (SS), 2 = A split into TMEM (TS, default)  // TN split-K chunk length (rows, multiple of 32); set before creating groups
 }  // namespace tc
 }  // namespace mg

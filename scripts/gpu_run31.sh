@@ -1,0 +1,22 @@
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 180 python -c "
+import sys; sys.path.insert(0, '.')
+import torch, pytest
+from paper_2110_08688_b200 import rowgcn as R
+R.set_tuning('gemm3_cluster', 2)
+sys.exit(pytest.main(['tests/test_gpu_kernels.py', '-q', '-x', '-p', 'no:cacheprovider', '-k', 'tcgen05']))
+" 2>&1 | tail -3
+echo "rc=$?"
+for c in 1 2; do timeout 300 python - <<EOF2 2>&1 | tail -1
+import sys, json, io, contextlib, runpy
+sys.argv = ["bench.py", "--steps", "5", "--warmup", "3", "--no-cpu-baseline", "--no-e2e"]
+import torch
+from paper_2110_08688_b200 import rowgcn as R
+R.set_tuning("gemm3_cluster", $c)
+buf = io.StringIO()
+with contextlib.redirect_stdout(buf):
+    runpy.run_path("bench.py", run_name="__main__")
+d = json.loads(buf.getvalue().strip().splitlines()[-1])
+print("cluster $c", round(d["ms_per_step"], 2), d["breakdown_ms_per_step"])
+EOF2
+done
