@@ -4,6 +4,7 @@
 // communicator (NCCL, or the in-process rank-order transport when several workers share a device),
 // the staged 1D row-broadcast SpMM schedule on two streams with CUDA events, and the training step.
 // Reference: rowgcn inc/gcn.hpp (GcnWorker), inc/dist_spmm.hpp (staged SpMM), inc/collectives.hpp.
+#include <cub/device/device_radix_sort.cuh>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -135,6 +136,56 @@ void build_fast_items(const std::vector<index_t>& rp, std::vector<int4>& items, 
   for (int r : light)
     items[base + static_cast<size_t>(cnt[maxlen - (rp[r + 1] - rp[r])]++)] =
         make_int4(static_cast<int>(rp[r]), static_cast<int>(rp[r + 1]), r, 0);
+}
+
+// Hub-row half of build_fast_items: segment items + hub descriptors; *n_light = rows below the threshold.
+void build_hub_segments(const std::vector<index_t>& rp, std::vector<int4>& items, std::vector<int4>& hubs, int& nseg,
+                        index_t& n_light) {
+  const index_t rows = static_cast<index_t>(rp.size()) - 1;
+  const int ht = heavy_threshold(), seg = g_fast_segment.load();
+  items.clear();
+  hubs.clear();
+  nseg = 0;
+  n_light = 0;
+  for (index_t r = 0; r < rows; ++r) {
+    const index_t len = rp[r + 1] - rp[r];
+    if (len < ht) {
+      ++n_light;
+      continue;
+    }
+    const int first = nseg;
+    for (index_t e = rp[r]; e < rp[r + 1]; e += seg, ++nseg)
+      items.push_back(make_int4(static_cast<int>(e), static_cast<int>(std::min<index_t>(e + seg, rp[r + 1])),
+                                -(nseg + 1), 0));
+    hubs.push_back(make_int4(static_cast<int>(r), first, nseg - first, 0));
+  }
+}
+
+// Light-row half on the device: key = ht - length for rows below the threshold (2 ht for the others, which
+// sort last), a stable radix sort of (key, row), then {e0, e1, row, 0} items for the first n_light rows.
+void light_items_device(const int* rp, index_t rows, int ht, index_t n_light, int4* out) {
+  int *keys = nullptr, *keys2 = nullptr, *ids = nullptr, *ids2 = nullptr;
+  MG_CUDA(cudaMalloc(&keys, sizeof(int) * rows));
+  MG_CUDA(cudaMalloc(&keys2, sizeof(int) * rows));
+  MG_CUDA(cudaMalloc(&ids, sizeof(int) * rows));
+  MG_CUDA(cudaMalloc(&ids2, sizeof(int) * rows));
+  const int blocks = static_cast<int>(std::min<index_t>((rows + 255) / 256, 148 * 16));
+  k::light_keys<<<blocks, 256, 0, cudaStreamLegacy>>>(rp, static_cast<int>(rows), ht, keys, ids);
+  MG_LAUNCHED();
+  cub::DoubleBuffer<int> kb(keys, keys2), vb(ids, ids2);
+  int bits = 1;
+  while ((1 << bits) <= 2 * ht) ++bits;
+  size_t tmp = 0;
+  MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, static_cast<int>(rows), 0, bits, cudaStreamLegacy));
+  void* t = nullptr;
+  MG_CUDA(cudaMalloc(&t, std::max<size_t>(tmp, 16)));
+  MG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kb, vb, static_cast<int>(rows), 0, bits, cudaStreamLegacy));
+  k::light_fill<<<blocks, 256, 0, cudaStreamLegacy>>>(rp, vb.Current(), static_cast<int>(n_light), out);
+  MG_LAUNCHED();
+  MG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
+  for (void* q : {static_cast<void*>(keys), static_cast<void*>(keys2), static_cast<void*>(ids),
+                  static_cast<void*>(ids2), t})
+    cudaFree(q);
 }
 
 // Host-side construction of the launch lists for a tile (row order by decreasing length).
@@ -517,11 +568,7 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
       for (index_t i = b; i < e; ++i) o[i] = static_cast<int>(t.row_ptr[r0 + i]);
     }, index_t(1) << 18);
   });
-  // FAST work lists are built on a host thread while the arrays upload
-  std::vector<int4> items, hubs;
-  std::future<void> lists;
-  if (g.cfg.spmm_mode == MG_SPMM_FAST)
-    lists = std::async(std::launch::async, [&] { build_fast_items(t.row_ptr, items, hubs, d.n_segments); });
+  Stopwatch sw;
   if (d.nnz) {  // {col, value bits} records: both arrays go up as they are, the device interleaves them
     int* tcol = nullptr;
     float* tval = nullptr;
@@ -540,6 +587,7 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
     cudaFree(tcol);
     cudaFree(tval);
   }
+  sw.lap("  arrays");
   // FAST mode: tag each record with its column's hub class (top 4 bits), computed on the device from the
   // uploaded records: per-column gather counts, a histogram of the counts, and per-tier count thresholds
   // (class k = gathered at least as often as the 10000 * 2^(k-1)-th most gathered column).
@@ -570,14 +618,24 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
     cudaFree(chist);
     d.hubs_classed = true;
   }
+  sw.lap("  hub class");
   if (g.cfg.spmm_mode == MG_SPMM_FAST) {
-    lists.get();
-    d.items = dalloc_t<int4>(g, w, std::max<size_t>(1, items.size()));
+    // FAST work lists: hub-row segments on the host (few rows), then the light rows by decreasing length
+    // (ties in row order) as a stable device radix sort of (ht - length, row) — the same list
+    // build_fast_items makes on the host.
+    std::vector<int4> seg_items, hubs;
+    index_t n_light = 0;
+    build_hub_segments(t.row_ptr, seg_items, hubs, d.n_segments, n_light);
+    const size_t n_items = seg_items.size() + static_cast<size_t>(n_light);
+    d.items = dalloc_t<int4>(g, w, std::max<size_t>(1, n_items));
     d.hubs = dalloc_t<int4>(g, w, std::max<size_t>(1, hubs.size()));
-    d.n_items = static_cast<int>(items.size());
+    d.n_items = static_cast<int>(n_items);
     d.n_hubs = static_cast<int>(hubs.size());
-    if (!items.empty()) st.upload_array(d.items, items.data(), items.size());
+    if (!seg_items.empty())
+      MG_CUDA(cudaMemcpy(d.items, seg_items.data(), sizeof(int4) * seg_items.size(), cudaMemcpyHostToDevice));
     if (!hubs.empty()) MG_CUDA(cudaMemcpy(d.hubs, hubs.data(), sizeof(int4) * hubs.size(), cudaMemcpyHostToDevice));
+    if (n_light > 0) light_items_device(d.row_ptr, t.rows, heavy_threshold(), n_light, d.items + seg_items.size());
+    sw.lap("  lists");
     return;
   }
   std::vector<int> light, heavy;

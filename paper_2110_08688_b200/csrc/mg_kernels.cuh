@@ -333,6 +333,21 @@ __global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ 
   }
 }
 
+// Upload time, FAST work lists: sort keys for the light rows (ht - length; hub rows 2 ht) and the items.
+__global__ void light_keys(const int* __restrict__ rp, int rows, int ht, int* __restrict__ keys, int* __restrict__ ids) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
+    const int len = rp[r + 1] - rp[r];
+    keys[r] = len < ht ? ht - len : 2 * ht;
+    ids[r] = r;
+  }
+}
+__global__ void light_fill(const int* __restrict__ rp, const int* __restrict__ ids, int n_light, int4* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_light; i += gridDim.x * blockDim.x) {
+    const int r = ids[i];
+    out[i] = make_int4(rp[r], rp[r + 1], r, 0);
+  }
+}
+
 // Upload time: interleave the tile's column and value arrays into {col, value bits} records.
 __global__ void pack_edges(const int* __restrict__ col, const float* __restrict__ val, long nnz,
                            int2* __restrict__ edges) {
