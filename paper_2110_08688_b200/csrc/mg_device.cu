@@ -945,6 +945,9 @@ class Step {
         else if (C32 <= 4) k::softmax_xent<4><<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
                                                          static_cast<int>(w.rows), static_cast<int>(C), w.labels,
                                                          w.mask, inv_denom, w.partials);
+        else if (C32 <= 6) k::softmax_xent<6><<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
+                                                         static_cast<int>(w.rows), static_cast<int>(C), w.labels,
+                                                         w.mask, inv_denom, w.partials);
         else k::softmax_xent<k::kLossCpl><<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
                                                          static_cast<int>(w.rows), static_cast<int>(C), w.labels,
                                                          w.mask, inv_denom, w.partials);

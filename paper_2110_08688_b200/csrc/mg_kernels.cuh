@@ -631,20 +631,40 @@ __global__ void __launch_bounds__(256) softmax_xent(float* __restrict__ logits, 
   __shared__ double s_loss[8], s_corr[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double my_loss = 0.0, my_corr = 0.0;
-  for (int r = blockIdx.x * 8 + warp; r < rows; r += gridDim.x * 8) {
+  const int stride = gridDim.x * 8;
+  // the next row's logits, label and mask are loaded while the current row is reduced (one row per warp
+  // in flight was latency-bound)
+  auto load = [&](int r, float* z, int& label, int& m) {
+    m = 0;
+    if (r >= rows) return;
+    m = mask[r];
+    label = labels[r];
+    const float* row = logits + (size_t)r * ld;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) {
+      const int j = lane + 32 * q;
+      z[q] = j < C ? row[j] : -INFINITY;
+    }
+  };
+  float zn[CPL];
+  int label_n = 0, m_n = 0;
+  load(blockIdx.x * 8 + warp, zn, label_n, m_n);
+  for (int r = blockIdx.x * 8 + warp; r < rows; r += stride) {
+    float z[CPL];
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) z[q] = zn[q];
+    const int label = label_n, m = m_n;
+    load(r + stride, zn, label_n, m_n);
     float* row = logits + (size_t)r * ld;
-    if (!mask[r]) {
+    if (!m) {
       for (int j = lane; j < ld; j += 32) row[j] = 0.0f;
       continue;
     }
-    const int label = labels[r];
-    float z[CPL];
     float mx = -INFINITY;
     int arg = 0x7fffffff;
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
       const int j = lane + 32 * q;
-      z[q] = j < C ? row[j] : -INFINITY;
       if (j < C && (arg == 0x7fffffff || z[q] > mx)) {
         mx = z[q];
         arg = j;

@@ -522,8 +522,13 @@ __device__ __forceinline__ Item2 item2_of(const Params& p, int MODE_, int it) {
   return r;
 }
 
+// TN: 4 extra warps (10-13) split the B tile in smem while warps 2-5 split A into TMEM.
+constexpr int kThreadsTN = 448;
 template <int MODE>
-__global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ CUtensorMap map_a,
+constexpr int threads2() { return MODE == TN ? kThreadsTN : kThreads; }
+
+template <int MODE>
+__global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_constant__ CUtensorMap map_a,
                                                         const __grid_constant__ CUtensorMap map_bh,
                                                         const __grid_constant__ CUtensorMap map_bl,
                                                         const __grid_constant__ CUtensorMap map_c, Params p) {
@@ -540,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nst; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&conv[s], 4);
+      mbar_init(&conv[s], MODE == TN && p.terms == 3 ? 8 : 4);
       mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -673,7 +678,26 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
           hi[k] = __float_as_uint(h);
           lo[k] = __float_as_uint(__fsub_rn(x[k], h));
         }
-        if (MODE == TN && p.terms == 3) {  // B = G rows: split in place in smem (hi) + lo copy
+        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(kAcol + s * 32);
+        tmem_st16(ta, hi);
+        if (p.terms == 3) tmem_st16(ta + 16, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s]);
+        if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 2] = clock64();
+      }
+    }
+  } else if (warp >= 10) {
+    // ------------------------------------------------------------ TN: split B (G rows) in place (hi) + lo copy
+    if (MODE == TN && p.terms == 3) {
+      const int t = threadIdx.x - 320;
+      uint32_t sc = 0;
+      for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
+        const Item2 I = item2_of(p, MODE, it);
+        for (int kb = 0; kb < I.k.nkb; ++kb, ++sc) {
+          const int s = sc % p.nst;
+          mbar_wait(&full[s], (sc / p.nst) & 1);
           const uint32_t bh = smem_u32(smem + s * stage + a_bytes);
           const uint32_t bl = bh + static_cast<uint32_t>(b_bytes);
           for (int q4 = t; q4 < b_bytes / 16; q4 += 128) {
@@ -690,15 +714,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc2(const __grid_constant__ 
                          : "memory");
           }
           fence_async_smem();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&conv[s]);
         }
-        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(kAcol + s * 32);
-        tmem_st16(ta, hi);
-        if (p.terms == 3) tmem_st16(ta + 16, lo);
-        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[s]);
-        if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 2] = clock64();
       }
     }
   } else {
@@ -1216,7 +1234,7 @@ void launch2(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl,
     attr = true;
   }
   const int grid = std::max(1, std::min(p.n_items, num_sms()));
-  gemm_tc2<MODE><<<grid, kThreads, smem_bytes2(p), s>>>(a, bh, bl, c, p);
+  gemm_tc2<MODE><<<grid, threads2<MODE>(), smem_bytes2(p), s>>>(a, bh, bl, c, p);
   TC_CUDA(cudaGetLastError());
 }
 
