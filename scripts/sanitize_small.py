@@ -1,0 +1,20 @@
+"""Small end-to-end runs for compute-sanitizer: exact and FAST/TF32X3 training at P = 1 and 2 (in-process),
+the device partitioner, bench-spmm and a kernel-level SpMM with hub segments."""
+import os
+import sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402,F401
+from paper_2110_08688_b200 import rowgcn as R  # noqa: E402
+
+R.set_tuning("heavy_row", 64)  # hub segments + hub-row kernels on a small graph
+ds = R.synth_graph(3000, 12.0, 0.7, 2, 40, 5)
+for gm, sm in [(R.GEMM_EXACT, R.SPMM_EXACT), (R.GEMM_TF32X3, R.SPMM_FAST)]:
+    for P in (1, 2):
+        cfg = R.GcnConfig([40, 64, 5], epochs=2, seed=1, permute=True, overlap=P > 1, gemm_mode=gm, spmm_mode=sm)
+        art = R.train_run(ds, cfg, R.TrainOptions(workers=P, devices=[0] * P,
+                                                  transport=R.TRANSPORT_NCCL if P == 1 else R.TRANSPORT_LOCAL))
+        print("train", gm, sm, P, art.epoch_loss, flush=True)
+cfg = R.GcnConfig([40, 64, 5], epochs=1, seed=1, permute=True)
+R.prepare_data(ds, cfg, 2, device=0)
+print("bench_spmm", R.bench_spmm(ds, workers=2, devices=[0, 0], transport=R.TRANSPORT_LOCAL)["wall_us"] > 0)
