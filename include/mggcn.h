@@ -298,6 +298,19 @@ mg_status mg_dev_gemm(int32_t ta, int32_t tb, int64_t M, int64_t N, int64_t K, c
                       const float* B, int64_t ldb, float* Cm, int64_t ldc, int32_t epilogue, int32_t mode,
                       void* stream);
 
+/* rowgcn::softmax_xent_sum (inc/dense.hpp:241-277) plus the argmax correct count (inc/gcn.hpp:279-282) on
+ * device rows: logits[rows, classes] with leading dimension ld is replaced by the gradient
+ * (softmax - onehot) / denom on masked rows and 0 elsewhere (columns classes..ld zeroed). stats (HOST,
+ * 2 doubles) = {loss sum over masked rows, correct count}. Errors as the reference: ValueError for
+ * denom <= 0 ("empty mask") and for a masked label outside [0, classes); classes <= 256. Synchronous. */
+mg_status mg_dev_softmax_xent(float* logits, int64_t rows, int64_t classes, int64_t ld, const int32_t* labels,
+                              const uint8_t* mask, int64_t denom, double* stats, void* stream);
+/* rowgcn::adam_step (inc/gcn.hpp:61-85) on one device parameter array of `size` floats: m, v, w updated
+ * with the reference's float constants and operation order, grad zeroed. t >= 1 (ValueError otherwise).
+ * Synchronous. */
+mg_status mg_dev_adam(float* w, float* grad, float* m, float* v, int64_t size, double lr, double beta1, double beta2,
+                      double epsilon, int32_t t, void* stream);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -94,6 +94,10 @@ SIGNATURES = [
                               C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
     ("mg_dev_gemm", C.c_int, [C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int64,
                               C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p]),
+    ("mg_dev_softmax_xent", C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
+                                      C.c_void_p, C.c_void_p]),
+    ("mg_dev_adam", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_double, C.c_double,
+                              C.c_double, C.c_double, C.c_int32, C.c_void_p]),
 ]
 
 _lib = None

@@ -286,6 +286,21 @@ int hub_class_max(int ld) {
   return k;
 }
 
+// adam_step's constants (gcn.hpp:61-70): cast to float, bias corrections via std::pow in double.
+static k::AdamConsts adam_consts(double lr, double beta1, double beta2, double eps, int t) {
+  if (t < 1) throw ValueError("adam_step: step index must be >= 1, got " + std::to_string(t));
+  k::AdamConsts c{};
+  c.b1 = static_cast<float>(beta1);
+  c.b2 = static_cast<float>(beta2);
+  c.one_m_b1 = 1.0f - c.b1;
+  c.one_m_b2 = 1.0f - c.b2;
+  c.lr = static_cast<float>(lr);
+  c.eps = static_cast<float>(eps);
+  c.corr1 = 1.0f - static_cast<float>(std::pow(beta1, t));
+  c.corr2 = 1.0f - static_cast<float>(std::pow(beta2, t));
+  return c;
+}
+
 template <int G, int CPL, int E, int D, bool HINT>
 static void launch_fast_async_v(const FastLaunch& t, const float* h, float* out, float* scratch, int ld, int nchunk,
                                 int acc, int relu, int hub_max, cudaStream_t s) {
@@ -1053,18 +1068,7 @@ class Step {
 
   // -------------------------------------------------------------- finalize (gcn.hpp:354-377 + adam :61-85)
   void finalize(bool adam, int t) {
-    k::AdamConsts c{};
-    if (adam) {
-      if (t < 1) throw ValueError("adam_step: step index must be >= 1, got " + std::to_string(t));
-      c.b1 = static_cast<float>(cfg_.beta1);
-      c.b2 = static_cast<float>(cfg_.beta2);
-      c.one_m_b1 = 1.0f - c.b1;
-      c.one_m_b2 = 1.0f - c.b2;
-      c.lr = static_cast<float>(cfg_.lr);
-      c.eps = static_cast<float>(cfg_.epsilon);
-      c.corr1 = 1.0f - static_cast<float>(std::pow(cfg_.beta1, t));
-      c.corr2 = 1.0f - static_cast<float>(std::pow(cfg_.beta2, t));
-    }
+    const k::AdamConsts c = adam ? adam_consts(cfg_.lr, cfg_.beta1, cfg_.beta2, cfg_.epsilon, t) : k::AdamConsts{};
     for (size_t k = 0; k < nloc(); ++k) {
       Worker& w = W(k);
       dev(w);
@@ -1773,6 +1777,65 @@ mg_status mg_dev_gemm(int32_t ta, int32_t tb, int64_t M, int64_t N, int64_t K, c
       MG_CUDA(cudaStreamSynchronize(st));
       MG_CUDA(cudaFree(ws));
     }
+  });
+}
+
+mg_status mg_dev_softmax_xent(float* logits, int64_t rows, int64_t classes, int64_t ld, const int32_t* labels,
+                              const uint8_t* mask, int64_t denom, double* stats, void* stream) {
+  return guarded([&] {
+    if (rows < 0 || classes < 1 || ld < classes) throw ShapeError("softmax_xent: bad shape");
+    if (classes > 32 * k::kLossCpl)
+      throw ValueError("softmax_xent: at most " + std::to_string(32 * k::kLossCpl) + " classes per row");
+    if (denom <= 0) throw ValueError("softmax_xent: empty mask");
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    // the reference's label contract (dense.hpp:261-264), checked on the masked rows like the group's upload
+    std::vector<int32_t> hl(rows);
+    std::vector<uint8_t> hm(rows);
+    if (rows > 0) {
+      MG_CUDA(cudaMemcpyAsync(hl.data(), labels, sizeof(int32_t) * rows, cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaMemcpyAsync(hm.data(), mask, rows, cudaMemcpyDeviceToHost, s));
+      MG_CUDA(cudaStreamSynchronize(s));
+    }
+    for (int64_t v = 0; v < rows; ++v)
+      if (hm[v] && (hl[v] < 0 || hl[v] >= classes))
+        throw ValueError("softmax_xent: label " + std::to_string(hl[v]) + " out of range [0, " +
+                         std::to_string(classes) + ") at row " + std::to_string(v));
+    const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(rows, 8), num_sms() * 8)));
+    double* part = nullptr;
+    MG_CUDA(cudaMalloc(&part, sizeof(double) * (2 * blocks + 2)));
+    const float inv = 1.0f / static_cast<float>(denom);
+    const int R = static_cast<int>(rows), Cc = static_cast<int>(classes), L = static_cast<int>(ld);
+    const int C32 = (Cc + 31) / 32;
+    if (rows > 0) {
+      if (C32 <= 2) k::softmax_xent<2><<<blocks, 256, 0, s>>>(logits, L, R, Cc, labels, mask, inv, part);
+      else if (C32 <= 4) k::softmax_xent<4><<<blocks, 256, 0, s>>>(logits, L, R, Cc, labels, mask, inv, part);
+      else if (C32 <= 6) k::softmax_xent<6><<<blocks, 256, 0, s>>>(logits, L, R, Cc, labels, mask, inv, part);
+      else k::softmax_xent<k::kLossCpl><<<blocks, 256, 0, s>>>(logits, L, R, Cc, labels, mask, inv, part);
+      MG_LAUNCHED();
+    }
+    k::finalize_stats<<<1, 32, 0, s>>>(part, rows > 0 ? blocks : 0, part + 2 * blocks);
+    MG_LAUNCHED();
+    MG_CUDA(cudaMemcpyAsync(stats, part + 2 * blocks, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    MG_CUDA(cudaStreamSynchronize(s));
+    cudaFree(part);
+  });
+}
+
+mg_status mg_dev_adam(float* w, float* grad, float* m, float* v, int64_t size, double lr, double beta1, double beta2,
+                      double epsilon, int32_t t, void* stream) {
+  return guarded([&] {
+    const k::AdamConsts c = adam_consts(lr, beta1, beta2, epsilon, t);
+    if (size < 0 || size > INT32_MAX) throw ShapeError("adam_step: bad parameter count");
+    if (size == 0) return;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    float* stage = nullptr;  // finalize_adam reads the gradient as a one-block stage and zeroes `grad`
+    MG_CUDA(cudaMalloc(&stage, sizeof(float) * size));
+    MG_CUDA(cudaMemcpyAsync(stage, grad, sizeof(float) * size, cudaMemcpyDeviceToDevice, s));
+    const int n = static_cast<int>(size);
+    k::finalize_adam<<<std::min(1024, (n + 255) / 256), 256, 0, s>>>(n, 1, stage, w, grad, m, v, 1, c);
+    MG_LAUNCHED();
+    MG_CUDA(cudaStreamSynchronize(s));
+    cudaFree(stage);
   });
 }
 

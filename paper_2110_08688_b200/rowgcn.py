@@ -853,3 +853,17 @@ def dev_spmm(rows, row_ptr_ptr, edges_ptr, h_ptr, out_ptr, w, ld, accumulate=Fal
 def dev_gemm(ta, tb, M, N, K, a_ptr, lda, b_ptr, ldb, c_ptr, ldc, epilogue=0, mode=GEMM_EXACT, stream=0):
     _check(lib().mg_dev_gemm(int(ta), int(tb), M, N, K, C.c_void_p(a_ptr), lda, C.c_void_p(b_ptr), ldb,
                              C.c_void_p(c_ptr), ldc, epilogue, mode, C.c_void_p(stream)))
+
+
+def dev_softmax_xent(logits_ptr, rows, classes, ld, labels_ptr, mask_ptr, denom, stream=0):
+    """rowgcn::softmax_xent_sum on device rows, gradient in place; returns (loss_sum, correct)."""
+    st = (C.c_double * 2)()
+    _check(lib().mg_dev_softmax_xent(C.c_void_p(logits_ptr), rows, classes, ld, C.c_void_p(labels_ptr),
+                                     C.c_void_p(mask_ptr), denom, st, C.c_void_p(stream)))
+    return st[0], st[1]
+
+
+def dev_adam(w_ptr, grad_ptr, m_ptr, v_ptr, size, t, lr=0.01, beta1=0.9, beta2=0.999, epsilon=1e-8, stream=0):
+    """rowgcn::adam_step on one device parameter array (grad zeroed)."""
+    _check(lib().mg_dev_adam(C.c_void_p(w_ptr), C.c_void_p(grad_ptr), C.c_void_p(m_ptr), C.c_void_p(v_ptr), size,
+                             lr, beta1, beta2, epsilon, t, C.c_void_p(stream)))
