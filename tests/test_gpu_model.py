@@ -109,6 +109,20 @@ def test_p_invariance_bitwise():
             assert bits_equal(a, b)
 
 
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_empty_parts_more_workers_than_vertices(mode):
+    """tests/test_dist_spmm.cpp:123-131: P > n leaves some workers with no rows (empty tiles, empty
+    broadcasts); the trajectory equals P = 1 (bitwise in the exact modes, P-invariant in the fast ones)."""
+    ds = R.synth_graph(6, 2.0, 0.5, 3, 4, 2)
+    kw = {} if mode == "exact" else dict(gemm_mode=R.GEMM_TF32X3, spmm_mode=R.SPMM_FAST)
+    cfg = cfgx([4, 5, 2], epochs=3, seed=2, permute=True, overlap=True, **kw)
+    base = R.train_run(ds, cfg, R.TrainOptions(workers=1, devices=[0]))
+    dist = R.train_run(ds, cfg, R.TrainOptions(workers=8, devices=[0] * 8, transport=R.TRANSPORT_LOCAL))
+    assert dist.epoch_loss == base.epoch_loss
+    for a, b in zip(dist.final_w, base.final_w):
+        assert bits_equal(a, b)
+
+
 def test_overlap_on_equals_off():
     ds = R.synth_graph(600, 6.0, 0.6, 27, 4, 2)
     cfg = cfgx([4, 6, 2], epochs=3, seed=15)
