@@ -207,6 +207,10 @@ mg_status mg_group_compute_gradients(mg_group* g, double* loss, double* acc);
 mg_status mg_group_loss_only(mg_group* g, double* loss);
 /* GcnWorker::submit_forward (inc/gcn.hpp:238-267), synchronous. */
 mg_status mg_group_forward(mg_group* g);
+/* GcnWorker::submit_backward + submit_finalize(false) (gcn.hpp:292-377): the backward pass from the
+ * gradient currently in the logits buffer (MG_T_AHW of layer L-1), then W_G (MG_T_WGRAD) finalized without
+ * Adam. H_G lands in MG_T_AHW of layer 0 (masked by relu_backward), as in the reference. */
+mg_status mg_group_backward(mg_group* g);
 /* Asynchronous train step: enqueue only (no host sync). Results via mg_group_sync + mg_group_last_stats. */
 mg_status mg_group_train_step_async(mg_group* g, int32_t t);
 mg_status mg_group_sync(mg_group* g);

@@ -1453,6 +1453,19 @@ mg_status mg_group_forward(mg_group* g) {
   });
 }
 
+// GcnWorker::submit_backward + submit_finalize(false) (gcn.hpp:292-377): backward from whatever gradient
+// the logits buffer ahw[L-1] holds (e.g. written with mg_group_write), W_G finalized, no Adam.
+mg_status mg_group_backward(mg_group* g) {
+  return guarded([&] {
+    Step st(*g);
+    st.begin();
+    st.backward();
+    st.finalize(false, 0);
+    st.end();
+    sync_all(*g);
+  });
+}
+
 // GcnWorker::loss_only (gcn.hpp:189-205): forward, then the masked loss without touching the logits.
 // The loss kernel writes gradients in place, so the logits are preserved through hw (never larger).
 mg_status mg_group_loss_only(mg_group* g, double* loss) {

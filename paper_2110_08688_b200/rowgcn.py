@@ -516,6 +516,10 @@ class Group:
     def forward(self):
         _check(lib().mg_group_forward(self._h))
 
+    def backward(self):
+        """submit_backward + submit_finalize(false): backward from the gradient in the logits buffer."""
+        _check(lib().mg_group_backward(self._h))
+
     def set_timeline(self, on: bool):
         """Start (clearing) / stop recording TimelineEvents from CUDA events (mg_group_set_timeline)."""
         _check(lib().mg_group_set_timeline(self._h, int(bool(on))))

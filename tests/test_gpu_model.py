@@ -123,6 +123,37 @@ def test_empty_parts_more_workers_than_vertices(mode):
         assert bits_equal(a, b)
 
 
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_zero_upstream_and_backward_linearity(mode):
+    """tests/test_gcn.cpp:227-241: a zero logits gradient gives zero W_G and zero H_G (ahw[0]); and the
+    backward pass is linear in its upstream gradient — 2G gives exactly 2 W_G (power-of-two scaling)."""
+    kw = {} if mode == "exact" else dict(gemm_mode=R.GEMM_TF32X3, spmm_mode=R.SPMM_FAST)
+    dims = [4, 3, 2]
+    ds = R.synth_graph(300, 5.0, 0.6, 47, dims[0], dims[-1])
+    cfg = cfgx(dims, seed=3, permute=True, aggregate_input=False, **kw)
+    P = 2
+    with group(ds, cfg, P) as g:
+        g.forward()
+        for r in range(P):
+            g.write(R.T_AHW, len(dims) - 2, np.zeros((g.rows(r)[1], dims[-1]), np.float32), r)
+        g.backward()
+        for l in range(len(dims) - 1):
+            assert not g.read(R.T_WGRAD, l).any()
+        for r in range(P):
+            assert not g.read(R.T_AHW, 0, r).any()
+        rng = np.random.default_rng(1)
+        ups = [rng.normal(0, 1e-3, (g.rows(r)[1], dims[-1])).astype(np.float32) for r in range(P)]
+        wg = []
+        for scale in (1, 2):
+            g.forward()
+            for r in range(P):
+                g.write(R.T_AHW, len(dims) - 2, scale * ups[r], r)
+            g.backward()
+            wg.append([g.read(R.T_WGRAD, l) for l in range(len(dims) - 1)])
+        for a, b in zip(*wg):
+            assert a.any() and bits_equal(b, 2 * a)
+
+
 def test_overlap_on_equals_off():
     ds = R.synth_graph(600, 6.0, 0.6, 27, 4, 2)
     cfg = cfgx([4, 6, 2], epochs=3, seed=15)
