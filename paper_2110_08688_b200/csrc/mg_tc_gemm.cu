@@ -163,6 +163,29 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
                : "memory");
 }
+// Warp-wide issue: every lane of the MMA warp executes these with warp-uniform operands and elect.sync
+// picks the issuing lane inside the asm. Issuing from a lane-0 branch instead makes ptxas wrap every
+// tcgen05.mma in an ELECT / R2UR.BROADCAST loop over the active lanes, which measured ~56 cycles per MMA
+// (scripts/mma_probe.cu) against the 24 (N = 48) / 64 (N = 128) cycles the tensor core needs.
+__device__ __forceinline__ void mma_tf32_e(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_commit_e(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+      "}\n" ::"r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
   asm volatile(
@@ -305,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(const __grid_constant__ C
           const int s = sc % p.nst;
           mbar_wait(&conv[s], (sc / p.nst) & 1);
           tc_fence_after();
-          if (lane == 0) {
+          {  // whole warp, elected issue (see mma_tf32_e)
             const uint32_t ah = smem_u32(smem + s * stage), bh = ah + a_bytes;
             const uint32_t al = ah + half, bl = bh + half;
 #pragma unroll
@@ -317,18 +340,18 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(const __grid_constant__ C
               if (p.terms == 3) {
                 const uint64_t dal = A_MN ? desc_mn128(al + ao) : desc_k64(al + ao);
                 const uint64_t dbl = B_MN ? desc_mn128(bl + bo) : desc_k64(bl + bo);
-                mma_tf32(d, dal, dbh, idesc, first);
-                mma_tf32(d, dah, dbl, idesc, 1u);
-                mma_tf32(d, dah, dbh, idesc, 1u);
+                mma_tf32_e(d, dal, dbh, idesc, first);
+                mma_tf32_e(d, dah, dbl, idesc, 1u);
+                mma_tf32_e(d, dah, dbh, idesc, 1u);
               } else {
-                mma_tf32(d, dah, dbh, idesc, first);
+                mma_tf32_e(d, dah, dbh, idesc, first);
               }
             }
-            mma_commit(&empty[s]);
+            mma_commit_e(&empty[s]);
           }
           __syncwarp();
         }
-        if (lane == 0) mma_commit(&tfull[buf]);
+        mma_commit_e(&tfull[buf]);
         __syncwarp();
       }
     }
@@ -477,6 +500,32 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       "}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
 }
+// The three 3xTF32 terms of one K = 8 step, lo*hi + hi*lo + hi*hi, behind one elect (the operand
+// conversions to uniform registers are shared by the three instructions).
+__device__ __forceinline__ void mma3_tf32_ts_e(uint32_t tmem_d, uint32_t a_hi, uint32_t a_lo, uint64_t b_hi,
+                                               uint64_t b_lo, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, 1;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(a_hi), "r"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void mma_tf32_ts_e(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -616,7 +665,7 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
           mbar_wait(&conv[s], (sc / p.nst) & 1);
           tc_fence_after();
           if (p.trace && blockIdx.x == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 3] = clock64();
-          if (lane == 0) {
+          {  // whole warp, elected issue (see mma_tf32_e)
             const uint32_t bh = smem_u32(smem + s * stage + a_bytes), bl = bh + b_bytes;
             const uint32_t ah = tmem + static_cast<uint32_t>(kAcol + s * 32), al = ah + 16;
 #pragma unroll
@@ -626,18 +675,16 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
               const uint32_t first = (kb == kb0 && kk == 0) ? 0u : 1u;
               if (p.terms == 3) {
                 const uint64_t dbl = B_MN ? desc_mn128(bl + bo) : desc_k64(bl + bo);
-                mma_tf32_ts(d, al + kk * 8, dbh, idesc, first);
-                mma_tf32_ts(d, ah + kk * 8, dbl, idesc, 1u);
-                mma_tf32_ts(d, ah + kk * 8, dbh, idesc, 1u);
+                mma3_tf32_ts_e(d, ah + kk * 8, al + kk * 8, dbh, dbl, idesc, first);
               } else {
-                mma_tf32_ts(d, ah + kk * 8, dbh, idesc, first);
+                mma_tf32_ts_e(d, ah + kk * 8, dbh, idesc, first);
               }
             }
-            mma_commit(&empty[s]);
+            mma_commit_e(&empty[s]);
           }
           __syncwarp();
         }
-        if (lane == 0) mma_commit(&tfull[buf]);
+        mma_commit_e(&tfull[buf]);
         __syncwarp();
       }
     }
@@ -825,6 +872,16 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint32_t mask) {
       "h"(static_cast<uint16_t>(mask))
       : "memory");
 }
+__device__ __forceinline__ void mma_commit_mc_e(uint64_t* bar, uint32_t mask) {
+  asm volatile(
+      "{\n"
+      ".reg .pred e;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "h"(static_cast<uint16_t>(mask))
+      : "memory");
+}
 
 template <int MODE, int CL>
 __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__ CUtensorMap map_a,
@@ -953,7 +1010,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
         mbar_wait(&fullW[w], (sc / nW) & 1);
         tc_fence_after();
         if (p.trace && blockIdx.x == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 3] = clock64();
-        if (lane == 0) {
+        {  // whole warp, elected issue (see mma_tf32_e)
           const uint32_t bh = smem_u32(wring + w * 2 * b_bytes), bl = bh + b_bytes;
           const uint32_t ah = tmem + static_cast<uint32_t>(kAcol + j * 64), al = ah + 32;
 #pragma unroll
@@ -961,21 +1018,18 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
             const uint64_t dbh = desc_k128(bh + kk * 32);
             const uint32_t first = (kb == 0 && kk == 0) ? 0u : 1u;
             if (p.terms == 3) {
-              const uint64_t dbl = desc_k128(bl + kk * 32);
-              mma_tf32_ts(d, al + kk * 8, dbh, idesc, first);
-              mma_tf32_ts(d, ah + kk * 8, dbl, idesc, 1u);
-              mma_tf32_ts(d, ah + kk * 8, dbh, idesc, 1u);
+              mma3_tf32_ts_e(d, ah + kk * 8, al + kk * 8, dbh, desc_k128(bl + kk * 32), idesc, first);
             } else {
-              mma_tf32_ts(d, ah + kk * 8, dbh, idesc, first);
+              mma_tf32_ts_e(d, ah + kk * 8, dbh, idesc, first);
             }
           }
-          mma_commit(&tslot[j]);  // TMEM A slot j reusable
-          if (CL == 1) mma_commit(&emptyW[w]);  // W slot w reusable
-          else mma_commit_mc(&emptyW[w], (1u << CL) - 1u);  // ... in every CTA of the cluster
+          mma_commit_e(&tslot[j]);  // TMEM A slot j reusable
+          if (CL == 1) mma_commit_e(&emptyW[w]);  // W slot w reusable
+          else mma_commit_mc_e(&emptyW[w], (1u << CL) - 1u);  // ... in every CTA of the cluster
         }
         __syncwarp();
       }
-      if (lane == 0) mma_commit(&tfull[buf]);
+      mma_commit_e(&tfull[buf]);
       __syncwarp();
     }
   } else if (warp < 6) {
