@@ -500,6 +500,36 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       "}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
 }
+// One 32-K stage of 3xTF32 (4 K steps x 3 terms) behind one elect, the K-step operand offsets computed
+// inside the asm (+8 TMEM columns, +32 bytes = +2 in a K-major SWIZZLE_128B descriptor's address field).
+__device__ __forceinline__ void mma12_tf32_ts_e(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
+                                                uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      ".reg .b32 ah1, ah2, ah3, al1, al2, al3;\n"
+      ".reg .b64 bh1, bh2, bh3, bl1, bl2, bl3;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "add.u32 ah1, %1, 8;\nadd.u32 ah2, %1, 16;\nadd.u32 ah3, %1, 24;\n"
+      "add.u32 al1, %2, 8;\nadd.u32 al2, %2, 16;\nadd.u32 al3, %2, 24;\n"
+      "add.u64 bh1, %3, 2;\nadd.u64 bh2, %3, 4;\nadd.u64 bh3, %3, 6;\n"
+      "add.u64 bl1, %4, 2;\nadd.u64 bl2, %4, 4;\nadd.u64 bl3, %4, 6;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al1], bh1, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah1], bl1, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah1], bh1, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al2], bh2, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah2], bl2, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah2], bh2, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al3], bh3, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah3], bl3, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah3], bh3, %5, 1;\n"
+      "}\n" ::"r"(d),
+      "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc));
+}
 // The three 3xTF32 terms of one K = 8 step, lo*hi + hi*lo + hi*hi, behind one elect (the operand
 // conversions to uniform registers are shared by the three instructions).
 __device__ __forceinline__ void mma3_tf32_ts_e(uint32_t tmem_d, uint32_t a_hi, uint32_t a_lo, uint64_t b_hi,
@@ -1013,15 +1043,13 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
         {  // whole warp, elected issue (see mma_tf32_e)
           const uint32_t bh = smem_u32(wring + w * 2 * b_bytes), bl = bh + b_bytes;
           const uint32_t ah = tmem + static_cast<uint32_t>(kAcol + j * 64), al = ah + 32;
+          static_assert(BK3 == 32, "mma12_tf32_ts_e issues one 32-K stage");
+          if (p.terms == 3) {
+            mma12_tf32_ts_e(d, ah, al, desc_k128(bh), desc_k128(bl), idesc, kb == 0 ? 0u : 1u);
+          } else {
 #pragma unroll
-          for (int kk = 0; kk < BK3 / 8; ++kk) {
-            const uint64_t dbh = desc_k128(bh + kk * 32);
-            const uint32_t first = (kb == 0 && kk == 0) ? 0u : 1u;
-            if (p.terms == 3) {
-              mma3_tf32_ts_e(d, ah + kk * 8, al + kk * 8, dbh, desc_k128(bl + kk * 32), idesc, first);
-            } else {
-              mma_tf32_ts_e(d, ah + kk * 8, dbh, idesc, first);
-            }
+            for (int kk = 0; kk < BK3 / 8; ++kk)
+              mma_tf32_ts_e(d, ah + kk * 8, desc_k128(bh + kk * 32), idesc, (kb == 0 && kk == 0) ? 0u : 1u);
           }
           mma_commit_e(&tslot[j]);  // TMEM A slot j reusable
           if (CL == 1) mma_commit_e(&emptyW[w]);  // W slot w reusable
