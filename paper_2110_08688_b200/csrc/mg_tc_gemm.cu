@@ -874,6 +874,21 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
 // raw 16 KB tiles, released as soon as the split warps hold them in registers; W hi / lo (L2-resident)
 // have a shallow ring with their own producer warp; the 4 TMEM A slots (64 columns: hi | lo of 32 K) are
 // released by the MMA's own commit. Warps: 0 A producer, 1 MMA, 2-5 split, 6-9 epilogue, 10 W producer.
+// Ring cursor (slot, phase parity, wrapped) for rings whose depth is a runtime value: replaces sc % n and
+// sc / n (an integer division per stage in every role's loop).
+struct RingPos {
+  int n, idx = 0;
+  uint32_t phase = 0;
+  bool wrapped = false;
+  __device__ explicit RingPos(int n_) : n(n_) {}
+  __device__ void next() {
+    if (++idx == n) {
+      idx = 0;
+      phase ^= 1u;
+      wrapped = true;
+    }
+  }
+};
 constexpr int kThreads3 = 352;
 constexpr int BK3 = 32;
 constexpr int kMaxA3 = 12, kMaxW3 = 4, kTSlots3 = 4;
@@ -988,11 +1003,12 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
     // ------------------------------------------------------------ A producer (HBM stream, deep ring)
     if (lane == 0) {
       uint32_t sc = 0;
+      RingPos r(nA);
       for (int pi = pair0; pi < npi; pi += npairs) {
         const Item2 I = item_of3(pi);
-        for (int kb = 0; kb < nkb; ++kb, ++sc) {
-          const int s = sc % nA;
-          if (sc >= static_cast<uint32_t>(nA)) mbar_wait(&emptyA[s], ((sc / nA) - 1) & 1);
+        for (int kb = 0; kb < nkb; ++kb, ++sc, r.next()) {
+          const int s = r.idx;
+          if (r.wrapped) mbar_wait(&emptyA[s], r.phase ^ 1u);
           if (p.trace && blockIdx.x == 0 && sc < kTraceStages) p.trace[sc * 4 + 0] = clock64();
           mbar_arrive_tx(&fullA[s], static_cast<uint32_t>(a_bytes));
           tma_load_2d(aring + s * a_bytes, &map_a, kb * BK3, static_cast<int>(I.k.row0), &fullA[s]);
@@ -1002,14 +1018,14 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
   } else if (warp == 10) {
     // ------------------------------------------------------------ W producer (L2-resident, shallow ring)
     if (lane == 0) {
-      uint32_t sc = 0;
+      RingPos r(nW);
       const uint32_t tx = static_cast<uint32_t>(p.terms == 3 ? 2 * b_bytes : b_bytes);
       const int half = p.bnr / CL;  // rows of the W tile this CTA loads (and multicasts to its peers)
       for (int pi = pair0; pi < npi; pi += npairs) {
         const Item2 I = item_of3(pi);
-        for (int kb = 0; kb < nkb; ++kb, ++sc) {
-          const int s = sc % nW;
-          if (sc >= static_cast<uint32_t>(nW)) mbar_wait(&emptyW[s], ((sc / nW) - 1) & 1);
+        for (int kb = 0; kb < nkb; ++kb, r.next()) {
+          const int s = r.idx;
+          if (r.wrapped) mbar_wait(&emptyW[s], r.phase ^ 1u);
           uint8_t* b = wring + s * 2 * b_bytes;
           mbar_arrive_tx(&fullW[s], tx);
           if (CL == 1) {
@@ -1027,6 +1043,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (A from TMEM slots)
     uint32_t sc = 0, ac = 0;
+    RingPos rw(nW);
     for (int pi = pair0; pi < npi; pi += npairs, ++ac) {
       const Item2 I = item_of3(pi);
       const uint32_t idesc = idesc_tf32(BM, I.nw, 0, 0);
@@ -1034,10 +1051,10 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
       if (ac >= 2u) mbar_wait(&tempty[buf], ((ac >> 1) - 1) & 1);
       tc_fence_after();
       const uint32_t d = tmem + static_cast<uint32_t>(buf * kTileN);
-      for (int kb = 0; kb < nkb; ++kb, ++sc) {
-        const int j = sc % kTSlots3, w = sc % nW;
+      for (int kb = 0; kb < nkb; ++kb, ++sc, rw.next()) {
+        const int j = sc % kTSlots3, w = rw.idx;
         mbar_wait(&conv[j], (sc / kTSlots3) & 1);
-        mbar_wait(&fullW[w], (sc / nW) & 1);
+        mbar_wait(&fullW[w], rw.phase);
         tc_fence_after();
         if (p.trace && blockIdx.x == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 3] = clock64();
         {  // whole warp, elected issue (see mma_tf32_e)
@@ -1065,10 +1082,11 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
     const int q = warp & 3;
     const int row = q * 32 + lane;
     uint32_t sc = 0;
+    RingPos ra(nA);
     for (int pi = pair0; pi < npi; pi += npairs) {
-      for (int kb = 0; kb < nkb; ++kb, ++sc) {
-        const int s = sc % nA, j = sc % kTSlots3;
-        mbar_wait(&fullA[s], (sc / nA) & 1);
+      for (int kb = 0; kb < nkb; ++kb, ++sc, ra.next()) {
+        const int s = ra.idx, j = sc % kTSlots3;
+        mbar_wait(&fullA[s], ra.phase);
         if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 1] = clock64();
         // row r's 16-byte chunk c sits at r * 128 + ((c ^ (r & 7)) * 16) (SWIZZLE_128B)
         const uint32_t rbase = smem_u32(aring + s * a_bytes) + static_cast<uint32_t>(row * 128);
