@@ -210,6 +210,21 @@ __device__ __forceinline__ float4 split4(float4 x, float4& lo) {
   return h;
 }
 
+// Ring cursor (slot, phase parity, wrapped) for rings whose depth is a runtime value: replaces sc % n and
+// sc / n (an integer division per stage in every role's loop).
+struct RingPos {
+  int n, idx = 0;
+  uint32_t phase = 0;
+  bool wrapped = false;
+  __device__ explicit RingPos(int n_) : n(n_) {}
+  __device__ void next() {
+    if (++idx == n) {
+      idx = 0;
+      phase ^= 1u;
+      wrapped = true;
+    }
+  }
+};
 // ---------------------------------------------------------------- work decomposition
 struct Item {
   long row0;    // NN/NT: first output row. TN: first K row (local)
@@ -652,13 +667,14 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       uint32_t sc = 0;
+      RingPos rp(p.nst);
       // single-term TF32 never reads B lo: do not load it
       const uint32_t tx = static_cast<uint32_t>(MODE == TN || p.terms != 3 ? a_bytes + b_bytes : stage);
       for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
         const Item2 I = item2_of(p, MODE, it);
-        for (int kb = 0; kb < I.k.nkb; ++kb, ++sc) {
-          const int s = sc % p.nst;
-          if (sc >= static_cast<uint32_t>(p.nst)) mbar_wait(&empty[s], ((sc / p.nst) - 1) & 1);
+        for (int kb = 0; kb < I.k.nkb; ++kb, ++sc, rp.next()) {
+          const int s = rp.idx;
+          if (rp.wrapped) mbar_wait(&empty[s], rp.phase ^ 1u);
           if (p.trace && blockIdx.x == 0 && sc < kTraceStages) p.trace[sc * 4 + 0] = clock64();
           uint8_t* a = smem + s * stage;
           uint8_t* b = a + a_bytes;
@@ -679,6 +695,7 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (A from TMEM)
     uint32_t sc = 0, ac = 0;
+    RingPos rp(p.nst);
     for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
       const Item2 I = item2_of(p, MODE, it);
       const uint32_t idesc = idesc_tf32(BM, I.nw, 0, B_MN ? 1 : 0);
@@ -690,9 +707,9 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
         if (ac >= 2u) mbar_wait(&tempty[buf], ((ac >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem + static_cast<uint32_t>(buf * kTileN);
-        for (int kb = kb0; kb < kb1; ++kb, ++sc) {
-          const int s = sc % p.nst;
-          mbar_wait(&conv[s], (sc / p.nst) & 1);
+        for (int kb = kb0; kb < kb1; ++kb, ++sc, rp.next()) {
+          const int s = rp.idx;
+          mbar_wait(&conv[s], rp.phase);
           tc_fence_after();
           if (p.trace && blockIdx.x == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 3] = clock64();
           {  // whole warp, elected issue (see mma_tf32_e)
@@ -725,11 +742,12 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
     const int row = q * 32 + lane;
     const int t = threadIdx.x - 64;
     uint32_t sc = 0;
+    RingPos rp(p.nst);
     for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
       const Item2 I = item2_of(p, MODE, it);
-      for (int kb = 0; kb < I.k.nkb; ++kb, ++sc) {
-        const int s = sc % p.nst;
-        mbar_wait(&full[s], (sc / p.nst) & 1);  // also implies the MMAs of this stage's last use are done
+      for (int kb = 0; kb < I.k.nkb; ++kb, ++sc, rp.next()) {
+        const int s = rp.idx;
+        mbar_wait(&full[s], rp.phase);  // also implies the MMAs of this stage's last use are done
         if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 1] = clock64();
         const uint32_t araw = smem_u32(smem + s * stage);
         float x[BK];
@@ -769,12 +787,12 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
     // ------------------------------------------------------------ TN: split B (G rows) in place (hi) + lo copy
     if (MODE == TN && p.terms == 3) {
       const int t = threadIdx.x - 320;
-      uint32_t sc = 0;
+      RingPos rp(p.nst);
       for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
         const Item2 I = item2_of(p, MODE, it);
-        for (int kb = 0; kb < I.k.nkb; ++kb, ++sc) {
-          const int s = sc % p.nst;
-          mbar_wait(&full[s], (sc / p.nst) & 1);
+        for (int kb = 0; kb < I.k.nkb; ++kb, rp.next()) {
+          const int s = rp.idx;
+          mbar_wait(&full[s], rp.phase);
           const uint32_t bh = smem_u32(smem + s * stage + a_bytes);
           const uint32_t bl = bh + static_cast<uint32_t>(b_bytes);
           for (int q4 = t; q4 < b_bytes / 16; q4 += 128) {
@@ -874,21 +892,6 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
 // raw 16 KB tiles, released as soon as the split warps hold them in registers; W hi / lo (L2-resident)
 // have a shallow ring with their own producer warp; the 4 TMEM A slots (64 columns: hi | lo of 32 K) are
 // released by the MMA's own commit. Warps: 0 A producer, 1 MMA, 2-5 split, 6-9 epilogue, 10 W producer.
-// Ring cursor (slot, phase parity, wrapped) for rings whose depth is a runtime value: replaces sc % n and
-// sc / n (an integer division per stage in every role's loop).
-struct RingPos {
-  int n, idx = 0;
-  uint32_t phase = 0;
-  bool wrapped = false;
-  __device__ explicit RingPos(int n_) : n(n_) {}
-  __device__ void next() {
-    if (++idx == n) {
-      idx = 0;
-      phase ^= 1u;
-      wrapped = true;
-    }
-  }
-};
 constexpr int kThreads3 = 352;
 constexpr int BK3 = 32;
 constexpr int kMaxA3 = 12, kMaxW3 = 4, kTSlots3 = 4;
