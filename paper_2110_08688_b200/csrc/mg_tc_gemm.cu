@@ -515,6 +515,29 @@ __device__ __forceinline__ void mma_tf32_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       "}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
 }
+// One 16-K stage of 3xTF32 (2 K steps x 3 terms) behind one elect; BOFF = the descriptor increment of one
+// K step (+1024 B = 64 for the MN-major SWIZZLE_128B_BASE32B B tiles, +32 B = 2 for K-major SWIZZLE_64B).
+template <int BOFF>
+__device__ __forceinline__ void mma6_tf32_ts_e(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
+                                               uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      ".reg .b32 ah1, al1;\n"
+      ".reg .b64 bh1, bl1;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "add.u32 ah1, %1, 8;\nadd.u32 al1, %2, 8;\n"
+      "add.u64 bh1, %3, %7;\nadd.u64 bl1, %4, %7;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al1], bh1, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah1], bl1, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah1], bh1, %5, 1;\n"
+      "}\n" ::"r"(d),
+      "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc), "n"(BOFF));
+}
 // One 32-K stage of 3xTF32 (4 K steps x 3 terms) behind one elect, the K-step operand offsets computed
 // inside the asm (+8 TMEM columns, +32 bytes = +2 in a K-major SWIZZLE_128B descriptor's address field).
 __device__ __forceinline__ void mma12_tf32_ts_e(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
@@ -715,16 +738,16 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
           {  // whole warp, elected issue (see mma_tf32_e)
             const uint32_t bh = smem_u32(smem + s * stage + a_bytes), bl = bh + b_bytes;
             const uint32_t ah = tmem + static_cast<uint32_t>(kAcol + s * 32), al = ah + 16;
+            static_assert(BK == 16, "mma6_tf32_ts_e issues one 16-K stage");
+            if (p.terms == 3) {
+              const uint64_t dbh = B_MN ? desc_mn128(bh) : desc_k64(bh), dbl = B_MN ? desc_mn128(bl) : desc_k64(bl);
+              mma6_tf32_ts_e<B_MN ? 64 : 2>(d, ah, al, dbh, dbl, idesc, kb == kb0 ? 0u : 1u);
+            } else {
 #pragma unroll
-            for (int kk = 0; kk < BK / 8; ++kk) {
-              const uint32_t bo = B_MN ? kk * 1024 : kk * 32;
-              const uint64_t dbh = B_MN ? desc_mn128(bh + bo) : desc_k64(bh + bo);
-              const uint32_t first = (kb == kb0 && kk == 0) ? 0u : 1u;
-              if (p.terms == 3) {
-                const uint64_t dbl = B_MN ? desc_mn128(bl + bo) : desc_k64(bl + bo);
-                mma3_tf32_ts_e(d, ah + kk * 8, al + kk * 8, dbh, dbl, idesc, first);
-              } else {
-                mma_tf32_ts_e(d, ah + kk * 8, dbh, idesc, first);
+              for (int kk = 0; kk < BK / 8; ++kk) {
+                const uint32_t bo = B_MN ? kk * 1024 : kk * 32;
+                mma_tf32_ts_e(d, ah + kk * 8, B_MN ? desc_mn128(bh + bo) : desc_k64(bh + bo), idesc,
+                              (kb == kb0 && kk == 0) ? 0u : 1u);
               }
             }
             mma_commit_e(&empty[s]);
