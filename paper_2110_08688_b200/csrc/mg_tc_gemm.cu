@@ -140,8 +140,8 @@ __device__ __forceinline__ uint64_t desc_k64(uint32_t saddr) {
 // CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): 4 k-rows x 128-byte (32 fp32 along M/N) atoms, 32-byte chunks
 // XOR-swizzled by the row. LBO = 2048 B between atoms along M/N (one {32, 16} TMA box each),
 // SBO = 512 B between consecutive 4-row atoms along K; one K = 8 MMA spans two of them.
-__device__ __forceinline__ uint64_t desc_mn128(uint32_t saddr) {
-  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(2048 >> 4) << 16) |
+__device__ __forceinline__ uint64_t desc_mn128(uint32_t saddr, uint32_t lbo = 2048) {
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFF) | (static_cast<uint64_t>(lbo >> 4) << 16) |
          (static_cast<uint64_t>(512 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) | (static_cast<uint64_t>(1) << 61);
 }
 // kind::tf32 instruction descriptor: D f32 (bit 4), A/B tf32 (2 at bits 7, 10), majors (bits 15, 16),
@@ -233,11 +233,11 @@ struct Item {
   int nkb;      // K blocks of the item
 };
 
-__device__ __forceinline__ Item item_of(const Params& p, int MODE_, int it) {
+__device__ __forceinline__ Item item_of(const Params& p, int MODE_, int it, int bk = BK) {
   Item r{};
   if (MODE_ != TN) {
     r.row0 = static_cast<long>(it) * BM;
-    r.nkb = static_cast<int>((p.K + BK - 1) / BK);
+    r.nkb = static_cast<int>((p.K + bk - 1) / bk);
     return r;
   }
   int g = 0;
@@ -248,7 +248,7 @@ __device__ __forceinline__ Item item_of(const Params& p, int MODE_, int it) {
   r.row0 = p.blk_begin[g] + static_cast<long>(c) * p.chunk_rows;
   const long end = p.blk_begin[g] + p.blk_len[g];
   r.k_end = (r.row0 + p.chunk_rows < end) ? r.row0 + p.chunk_rows : end;
-  r.nkb = static_cast<int>((r.k_end - r.row0 + BK - 1) / BK);
+  r.nkb = static_cast<int>((r.k_end - r.row0 + bk - 1) / bk);
   return r;
 }
 
@@ -540,6 +540,7 @@ __device__ __forceinline__ void mma6_tf32_ts_e(uint32_t d, uint32_t ah, uint32_t
 }
 // One 32-K stage of 3xTF32 (4 K steps x 3 terms) behind one elect, the K-step operand offsets computed
 // inside the asm (+8 TMEM columns, +32 bytes = +2 in a K-major SWIZZLE_128B descriptor's address field).
+template <int BOFF = 2>
 __device__ __forceinline__ void mma12_tf32_ts_e(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
                                                 uint32_t idesc, uint32_t acc) {
   asm volatile(
@@ -551,8 +552,8 @@ __device__ __forceinline__ void mma12_tf32_ts_e(uint32_t d, uint32_t ah, uint32_
       "setp.ne.b32 p, %6, 0;\n"
       "add.u32 ah1, %1, 8;\nadd.u32 ah2, %1, 16;\nadd.u32 ah3, %1, 24;\n"
       "add.u32 al1, %2, 8;\nadd.u32 al2, %2, 16;\nadd.u32 al3, %2, 24;\n"
-      "add.u64 bh1, %3, 2;\nadd.u64 bh2, %3, 4;\nadd.u64 bh3, %3, 6;\n"
-      "add.u64 bl1, %4, 2;\nadd.u64 bl2, %4, 4;\nadd.u64 bl3, %4, 6;\n"
+      "add.u64 bh1, %3, %7;\nadd.u64 bh2, %3, %8;\nadd.u64 bh3, %3, %9;\n"
+      "add.u64 bl1, %4, %7;\nadd.u64 bl2, %4, %8;\nadd.u64 bl3, %4, %9;\n"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%2], %3, %5, p;\n"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %4, %5, 1;\n"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %3, %5, 1;\n"
@@ -566,7 +567,7 @@ __device__ __forceinline__ void mma12_tf32_ts_e(uint32_t d, uint32_t ah, uint32_
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah3], bl3, %5, 1;\n"
       "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah3], bh3, %5, 1;\n"
       "}\n" ::"r"(d),
-      "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc));
+      "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc), "n"(BOFF), "n"(2 * BOFF), "n"(3 * BOFF));
 }
 // The three 3xTF32 terms of one K = 8 step, lo*hi + hi*lo + hi*hi, behind one elect (the operand
 // conversions to uniform registers are shared by the three instructions).
@@ -629,13 +630,13 @@ struct Item2 {
   int n0;   // first output column of the tile
   int nw;   // tile columns (multiple of 16, <= 128)
 };
-__device__ __forceinline__ Item2 item2_of(const Params& p, int MODE_, int it) {
+__device__ __forceinline__ Item2 item2_of(const Params& p, int MODE_, int it, int bk = BK) {
   Item2 r;
   r.mi = it / p.n_tiles;
   const int nt = it - r.mi * p.n_tiles;
   r.n0 = nt * kTileN;
   r.nw = min(kTileN, p.np - r.n0);
-  r.k = item_of(p, MODE_, r.mi);
+  r.k = item_of(p, MODE_, r.mi, bk);
   return r;
 }
 
@@ -643,6 +644,11 @@ __device__ __forceinline__ Item2 item2_of(const Params& p, int MODE_, int it) {
 constexpr int kThreadsTN = 448;
 template <int MODE>
 constexpr int threads2() { return MODE == TN ? kThreadsTN : kThreads; }
+// v2 K rows per stage: TN streams 32 (one 12-MMA issue block per stage, half the per-stage barrier and
+// commit overhead of 16), NN / NT keep 16 (their K-major SWIZZLE_64B B tiles).
+template <int MODE>
+__host__ __device__ constexpr int bk2() { return MODE == TN ? 32 : BK; }
+constexpr int kPromoteRows = 256;  // TN: drain TMEM every 256 K rows
 
 template <int MODE>
 __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_constant__ CUtensorMap map_a,
@@ -655,8 +661,11 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
   __shared__ uint32_t tmem_base_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr bool B_MN = MODE == TN;  // NN/NT read the pre-split K-major B
-  const int a_bytes = BM * BK * 4;    // raw A tile (no swizzle): NN/NT [128 rows][16 k], TN [16 k][128 m]
-  const int b_bytes = p.bnr * BK * 4;  // one B tile (bnr = tile columns held per stage)
+  constexpr int BKV = bk2<MODE>();
+  constexpr int kPromote = kPromoteRows / BKV;  // TN: K blocks per TMEM drain
+  constexpr uint32_t kBox = 32 * BKV * 4;      // TN: bytes of one {32 n, BKV k} B box (LBO along N)
+  const int a_bytes = BM * BKV * 4;    // raw A tile (no swizzle): NN/NT [128 rows][16 k], TN [32 k][128 m]
+  const int b_bytes = p.bnr * BKV * 4;  // one B tile (bnr = tile columns held per stage)
   const int stage = a_bytes + 2 * b_bytes;  // A raw | B hi | B lo
 
   if (threadIdx.x == 0) {
@@ -694,7 +703,7 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
       // single-term TF32 never reads B lo: do not load it
       const uint32_t tx = static_cast<uint32_t>(MODE == TN || p.terms != 3 ? a_bytes + b_bytes : stage);
       for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
-        const Item2 I = item2_of(p, MODE, it);
+        const Item2 I = item2_of(p, MODE, it, BKV);
         for (int kb = 0; kb < I.k.nkb; ++kb, ++sc, rp.next()) {
           const int s = rp.idx;
           if (rp.wrapped) mbar_wait(&empty[s], rp.phase ^ 1u);
@@ -703,11 +712,11 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
           uint8_t* b = a + a_bytes;
           mbar_arrive_tx(&full[s], tx);
           if (MODE == TN) {
-            const int k0 = static_cast<int>(I.k.row0) + kb * BK;
+            const int k0 = static_cast<int>(I.k.row0) + kb * BKV;
             tma_load_2d(a, &map_a, I.k.mt * BM, k0, &full[s]);
-            for (int j = 0; j < p.bnr / 32; ++j) tma_load_2d(b + j * 2048, &map_bh, I.n0 + j * 32, k0, &full[s]);
+            for (int j = 0; j < p.bnr / 32; ++j) tma_load_2d(b + j * kBox, &map_bh, I.n0 + j * 32, k0, &full[s]);
           } else {
-            const int k0 = kb * BK;
+            const int k0 = kb * BKV;
             tma_load_2d(a, &map_a, k0, static_cast<int>(I.k.row0), &full[s]);
             tma_load_2d(b, &map_bh, k0, I.n0, &full[s]);
             if (p.terms == 3) tma_load_2d(b + b_bytes, &map_bl, k0, I.n0, &full[s]);
@@ -720,12 +729,12 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
     uint32_t sc = 0, ac = 0;
     RingPos rp(p.nst);
     for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
-      const Item2 I = item2_of(p, MODE, it);
+      const Item2 I = item2_of(p, MODE, it, BKV);
       const uint32_t idesc = idesc_tf32(BM, I.nw, 0, B_MN ? 1 : 0);
-      const int groups = MODE == TN ? (I.k.nkb + kPromoteKb - 1) / kPromoteKb : 1;
+      const int groups = MODE == TN ? (I.k.nkb + kPromote - 1) / kPromote : 1;
       for (int gi = 0; gi < groups; ++gi, ++ac) {
-        const int kb0 = MODE == TN ? gi * kPromoteKb : 0;
-        const int kb1 = MODE == TN ? min(I.k.nkb, kb0 + kPromoteKb) : I.k.nkb;
+        const int kb0 = MODE == TN ? gi * kPromote : 0;
+        const int kb1 = MODE == TN ? min(I.k.nkb, kb0 + kPromote) : I.k.nkb;
         const int buf = static_cast<int>(ac & 1);
         if (ac >= 2u) mbar_wait(&tempty[buf], ((ac >> 1) - 1) & 1);
         tc_fence_after();
@@ -737,16 +746,17 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
           if (p.trace && blockIdx.x == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 3] = clock64();
           {  // whole warp, elected issue (see mma_tf32_e)
             const uint32_t bh = smem_u32(smem + s * stage + a_bytes), bl = bh + b_bytes;
-            const uint32_t ah = tmem + static_cast<uint32_t>(kAcol + s * 32), al = ah + 16;
-            static_assert(BK == 16, "mma6_tf32_ts_e issues one 16-K stage");
+            const uint32_t ah = tmem + static_cast<uint32_t>(kAcol + s * 2 * BKV), al = ah + BKV;
             if (p.terms == 3) {
-              const uint64_t dbh = B_MN ? desc_mn128(bh) : desc_k64(bh), dbl = B_MN ? desc_mn128(bl) : desc_k64(bl);
-              mma6_tf32_ts_e<B_MN ? 64 : 2>(d, ah, al, dbh, dbl, idesc, kb == kb0 ? 0u : 1u);
+              const uint64_t dbh = B_MN ? desc_mn128(bh, kBox) : desc_k64(bh);
+              const uint64_t dbl = B_MN ? desc_mn128(bl, kBox) : desc_k64(bl);
+              if (BKV == 32) mma12_tf32_ts_e<B_MN ? 64 : 2>(d, ah, al, dbh, dbl, idesc, kb == kb0 ? 0u : 1u);
+              else mma6_tf32_ts_e<B_MN ? 64 : 2>(d, ah, al, dbh, dbl, idesc, kb == kb0 ? 0u : 1u);
             } else {
 #pragma unroll
-              for (int kk = 0; kk < BK / 8; ++kk) {
+              for (int kk = 0; kk < BKV / 8; ++kk) {
                 const uint32_t bo = B_MN ? kk * 1024 : kk * 32;
-                mma_tf32_ts_e(d, ah + kk * 8, B_MN ? desc_mn128(bh + bo) : desc_k64(bh + bo), idesc,
+                mma_tf32_ts_e(d, ah + kk * 8, B_MN ? desc_mn128(bh + bo, kBox) : desc_k64(bh + bo), idesc,
                               (kb == kb0 && kk == 0) ? 0u : 1u);
               }
             }
@@ -767,38 +777,41 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
     uint32_t sc = 0;
     RingPos rp(p.nst);
     for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
-      const Item2 I = item2_of(p, MODE, it);
+      const Item2 I = item2_of(p, MODE, it, BKV);
       for (int kb = 0; kb < I.k.nkb; ++kb, ++sc, rp.next()) {
         const int s = rp.idx;
         mbar_wait(&full[s], rp.phase);  // also implies the MMAs of this stage's last use are done
         if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 1] = clock64();
         const uint32_t araw = smem_u32(smem + s * stage);
-        float x[BK];
+        float x[BKV];
         if (MODE == TN) {
-          const int valid = static_cast<int>(min(static_cast<long>(BK), I.k.k_end - (I.k.row0 + kb * BK)));
+          const int valid = static_cast<int>(min(static_cast<long>(BKV), I.k.k_end - (I.k.row0 + kb * BKV)));
 #pragma unroll
-          for (int k = 0; k < BK; ++k) {
+          for (int k = 0; k < BKV; ++k) {
             float v;
             asm volatile("ld.shared.f32 %0, [%1];\n" : "=f"(v) : "r"(araw + 4u * (k * BM + row)));
             x[k] = k < valid ? v : 0.0f;
           }
         } else {
 #pragma unroll
-          for (int k4 = 0; k4 < BK / 4; ++k4)
+          for (int k4 = 0; k4 < BKV / 4; ++k4)
             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
                          : "=f"(x[4 * k4]), "=f"(x[4 * k4 + 1]), "=f"(x[4 * k4 + 2]), "=f"(x[4 * k4 + 3])
-                         : "r"(araw + 4u * (row * BK + 4 * k4)));
+                         : "r"(araw + 4u * (row * BKV + 4 * k4)));
         }
-        uint32_t hi[BK], lo[BK];
+        uint32_t hi[BKV], lo[BKV];
 #pragma unroll
-        for (int k = 0; k < BK; ++k) {
+        for (int k = 0; k < BKV; ++k) {
           const float h = p.terms == 3 ? __uint_as_float(__float_as_uint(x[k]) & 0xFFFFE000u) : x[k];
           hi[k] = __float_as_uint(h);
           lo[k] = __float_as_uint(__fsub_rn(x[k], h));
         }
-        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(kAcol + s * 32);
-        tmem_st16(ta, hi);
-        if (p.terms == 3) tmem_st16(ta + 16, lo);
+        const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(kAcol + s * 2 * BKV);
+#pragma unroll
+        for (int c = 0; c < BKV / 16; ++c) {
+          tmem_st16(ta + 16 * c, hi + 16 * c);
+          if (p.terms == 3) tmem_st16(ta + BKV + 16 * c, lo + 16 * c);
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         tc_fence_before();
         __syncwarp();
@@ -812,7 +825,7 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
       const int t = threadIdx.x - 320;
       RingPos rp(p.nst);
       for (int it = blockIdx.x; it < p.n_items; it += gridDim.x) {
-        const Item2 I = item2_of(p, MODE, it);
+        const Item2 I = item2_of(p, MODE, it, BKV);
         for (int kb = 0; kb < I.k.nkb; ++kb, rp.next()) {
           const int s = rp.idx;
           mbar_wait(&full[s], rp.phase);
@@ -843,7 +856,7 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
     uint32_t ac = 0, tiles = 0;
     float* bufs = reinterpret_cast<float*>(smem + p.nst * stage) + q * (4 * 1024);  // 4 chunks of 32 x 32
     for (int it = blockIdx.x; it < p.n_items; it += gridDim.x, ++tiles) {
-      const Item2 I = item2_of(p, MODE, it);
+      const Item2 I = item2_of(p, MODE, it, BKV);
       const int nch = (I.nw + 31) / 32;
       // buffers are free once the previous tile's bulk stores have read them
       if (lane == 0) bulk_wait_read0();
@@ -854,7 +867,7 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
         for (int c = 0; c < nch; ++c)
           tma_load_2d(bufs + c * 1024, &map_c, I.n0 + c * 32, static_cast<int>(grow0), &oldbar[q]);
       }
-      const int groups = MODE == TN ? (I.k.nkb + kPromoteKb - 1) / kPromoteKb : 1;
+      const int groups = MODE == TN ? (I.k.nkb + kPromote - 1) / kPromote : 1;
       for (int gi = 0; gi < groups; ++gi, ++ac) {
         const int buf = static_cast<int>(ac & 1);
         mbar_wait(&tfull[buf], (ac >> 1) & 1);
@@ -1307,11 +1320,14 @@ void finish_params2(Params& p, long N, bool tn, int terms) {
   p.n_tiles = (p.np + kTileN - 1) / kTileN;
   p.bnr = std::min(p.np, kTileN);
   if (tn) p.bnr = (p.bnr + 31) / 32 * 32;
-  const int stage = BM * BK * 4 + 2 * p.bnr * BK * 4;
-  p.nst = std::max(2, std::min(kMaxStages, kSmemBudget2 / stage));
+  const int bk = tn ? bk2<TN>() : bk2<NN>();
+  const int stage = BM * bk * 4 + 2 * p.bnr * bk * 4;
+  // TMEM: the A slots (2 * bk columns each, hi | lo) live above the two 128-column accumulators
+  const int tmem_slots = (512 - kAcol) / (2 * bk);
+  p.nst = std::max(2, std::min({kMaxStages, tmem_slots, kSmemBudget2 / stage}));
 }
 
-inline int smem_bytes2(const Params& p) { return p.nst * (BM * BK * 4 + 2 * p.bnr * BK * 4) + kEpiBuf + 1024; }
+inline int smem_bytes2(const Params& p, int bk) { return p.nst * (BM * bk * 4 + 2 * p.bnr * bk * 4) + kEpiBuf + 1024; }
 
 // v3 (NN / NT): A ring as deep as the shared memory left after the W ring and the epilogue buffers.
 constexpr int kSmemMax3 = 232448 - 2048;  // sm_100 per-block maximum, minus static barriers and alignment
@@ -1360,7 +1376,7 @@ void launch2(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl,
     attr = true;
   }
   const int grid = std::max(1, std::min(p.n_items, num_sms()));
-  gemm_tc2<MODE><<<grid, threads2<MODE>(), smem_bytes2(p), s>>>(a, bh, bl, c, p);
+  gemm_tc2<MODE><<<grid, threads2<MODE>(), smem_bytes2(p, bk2<MODE>()), s>>>(a, bh, bl, c, p);
   TC_CUDA(cudaGetLastError());
 }
 
@@ -1555,9 +1571,10 @@ int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* l
   p.partial = ws;
   int kernels = 0;
   if (p.n_items > 0) {
-    const CUtensorMap mb = make_map(G, N, rows_hi, ldg, 32, BK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+    const int bk = g_gemm_version >= 2 ? bk2<TN>() : BK;  // K rows per stage of the kernel that runs
+    const CUtensorMap mb = make_map(G, N, rows_hi, ldg, 32, bk, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
     if (g_gemm_version >= 2) {  // A = H rows land raw ([16 k][128 m]) and go to TMEM transposed per lane
-      const CUtensorMap ma = make_map(H, M, rows_hi, ldh, BM, BK, CU_TENSOR_MAP_SWIZZLE_NONE);
+      const CUtensorMap ma = make_map(H, M, rows_hi, ldh, BM, bk, CU_TENSOR_MAP_SWIZZLE_NONE);
       const CUtensorMap mc = make_map(ws, p.npb, static_cast<long>(p.blk_first[nblocks]) * BM, p.npb, 32, 32,
                                       CU_TENSOR_MAP_SWIZZLE_128B);
       p.trace = trace_buffer();
