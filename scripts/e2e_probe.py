@@ -7,10 +7,13 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ.setdefault("MGGCN_TIMING", "1")
 from paper_2110_08688_b200 import rowgcn as R  # noqa: E402
 
+SHAPES = {"c4": (2449029, 50.6, [100, 256, 256, 47]), "c2": (169343, 13.6, [128, 256, 256, 40]),
+          "c1": (2708, 3.9, [1433, 16, 7])}
+n, deg, dims = SHAPES[sys.argv[1] if len(sys.argv) > 1 else "c4"]
 t0 = time.time()
-ds = R.synth_graph(2449029, 50.6, 0.7, 1, 100, 47)
+ds = R.synth_graph(n, deg, 0.7, 1, dims[0], dims[-1])
 t1 = time.time()
-cfg = R.GcnConfig([100, 256, 256, 47], epochs=10, seed=1, permute=True)
+cfg = R.GcnConfig(dims, epochs=10, seed=1, permute=True)
 prep = R.prepare_data(ds, cfg, 1)
 t2 = time.time()
 print(f"synth {t1 - t0:.2f} s, prepare {t2 - t1:.2f} s", flush=True)
@@ -20,12 +23,16 @@ for rep in range(2):
     b = time.time()
     g.init_params()
     c = time.time()
+    st = []
     for t in range(1, 11):
+        s0 = time.time()
         g.train_step(t)
+        st.append(1e3 * (time.time() - s0))
     d = time.time()
     ws = g.params(0)
     e = time.time()
     g.close()
     f = time.time()
     print(f"create {1e3 * (b - a):.1f} ms, init {1e3 * (c - b):.1f} ms, 10 steps {1e3 * (d - c):.1f} ms, "
-          f"params {1e3 * (e - d):.1f} ms, close {1e3 * (f - e):.1f} ms", flush=True)
+          f"params {1e3 * (e - d):.1f} ms, close {1e3 * (f - e):.1f} ms; steps " + " ".join(f"{x:.1f}" for x in st),
+          flush=True)

@@ -58,6 +58,8 @@ def run(name, reps=5):
 if __name__ == "__main__":
     if "--trace" in sys.argv:
         run(sys.argv[sys.argv.index("--trace") + 1])
+    elif "--only" in sys.argv:
+        run(sys.argv[sys.argv.index("--only") + 1], reps=1)
     else:
         for nm in SHAPES:
             run(nm)

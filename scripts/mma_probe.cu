@@ -37,12 +37,16 @@ __device__ __forceinline__ void mma_ts_elect(uint32_t d, uint32_t a_tmem, uint64
 
 // the GeMM's issue loop: descriptors from a rotating W slot, lane 0 only (WARP = 0) or warp-wide with
 // elect.sync inside the asm (WARP = 1)
-template <int N, int WARP>
+template <int N, int WARP, int FENCE = 0>
 __global__ void __launch_bounds__(128, 1) probe_loop(long long* out, int groups) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bar2;
+  __shared__ uint64_t bar2, done_bar;
   __shared__ uint32_t tbase;
   uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&done_bar)));
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&done_bar)) : "memory");
+  }
   for (int i = threadIdx.x; i < (4 * 2 * N * 128) / 16; i += blockDim.x) reinterpret_cast<int4*>(s)[i] = make_int4(0, 0, 0, 0);
   if (threadIdx.x == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar2)));
@@ -66,6 +70,16 @@ __global__ void __launch_bounds__(128, 1) probe_loop(long long* out, int groups)
       const uint32_t d = tmem + static_cast<uint32_t>((g / 8) & 1) * 128u;
       const uint32_t bh = smem_u32(s + w * 2 * b_bytes), bl = bh + b_bytes;
       const uint32_t ah = tmem + 256u + static_cast<uint32_t>(j * 64), al = ah + 32;
+      if (FENCE >= 2)
+        asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W_%=;\n}\n"
+                     ::"r"(smem_u32(&done_bar)) : "memory");
+      if (FENCE >= 1) asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      if (FENCE >= 3) {
+        if ((threadIdx.x & 31) == 0)
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&bar2))
+                       : "memory");
+        __syncwarp();
+      }
       if (WARP == 0) {
         if ((threadIdx.x & 31) == 0) {
 #pragma unroll
@@ -112,14 +126,14 @@ __global__ void __launch_bounds__(128, 1) probe_loop(long long* out, int groups)
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
-template <int N, int WARP>
+template <int N, int WARP, int FENCE = 0>
 void run_loop(const char* name, long long* d_out, int nsm) {
   const int groups = 2000;
   const size_t smem = 4 * 2 * N * 128 + 1024;
-  cudaFuncSetAttribute(probe_loop<N, WARP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  probe_loop<N, WARP><<<nsm, 128, smem>>>(d_out, 10);
+  cudaFuncSetAttribute(probe_loop<N, WARP, FENCE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  probe_loop<N, WARP, FENCE><<<nsm, 128, smem>>>(d_out, 10);
   cudaDeviceSynchronize();
-  probe_loop<N, WARP><<<nsm, 128, smem>>>(d_out, groups);
+  probe_loop<N, WARP, FENCE><<<nsm, 128, smem>>>(d_out, groups);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); return; }
   long long h[2];
@@ -292,9 +306,10 @@ int main() {
   cudaMalloc(&src, 4096ull * 4096 * 4);  // 64 MB: an L2-sized stream
   cudaMemset(src, 0, 4096ull * 4096 * 4);
   g_src = src;
-  run_loop<48, 0>("loop N=48 lane0", d, nsm);
-  run_loop<48, 1>("loop N=48 warp+elect", d, nsm);
-  run_loop<128, 0>("loop N=128 lane0", d, nsm);
-  run_loop<128, 1>("loop N=128 warp+elect", d, nsm);
+  run_loop<128, 1, 0>("loop N=128 elect", d, nsm);
+  run_loop<128, 1, 1>("loop N=128 +fence", d, nsm);
+  run_loop<128, 1, 2>("loop N=128 +wait+fence", d, nsm);
+  run_loop<48, 1, 0>("loop N=48 elect", d, nsm);
+  run_loop<48, 1, 2>("loop N=48 +wait+fence", d, nsm);
   return 0;
 }
