@@ -929,6 +929,8 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
 // have a shallow ring with their own producer warp; the 4 TMEM A slots (64 columns: hi | lo of 32 K) are
 // released by the MMA's own commit. Warps: 0 A producer, 1 MMA, 2-5 split, 6-9 epilogue, 10 W producer.
 constexpr int kThreads3 = 352;
+constexpr int kEpiChunks3 = 2;                      // epilogue 32 x 32 buffers per warp
+constexpr int kEpiBuf3 = 4 * kEpiChunks3 * 4096;   // 4 epilogue warps
 constexpr int BK3 = 32;
 constexpr int kMaxA3 = 12, kMaxW3 = 4, kTSlots3 = 4;
 
@@ -1161,56 +1163,66 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
       }
     }
   } else {
-    // ------------------------------------------------------------ epilogue (as v2, NN / NT)
+    // ------------------------------------------------------------ epilogue (NN / NT)
+    // kEpiChunks3 (2) 32 x 32 buffers per warp: a 128-column tile leaves in two halves, each with its own
+    // bulk stores (and relu_backward mask prefetch); the shared memory saved goes to a deeper W ring.
     const int q = warp & 3;
-    uint32_t ac = 0;
-    float* bufs = epib + q * (4 * 1024);  // 4 chunks of 32 x 32
+    uint32_t ac = 0, mph = 0;
+    float* bufs = epib + q * (kEpiChunks3 * 1024);
     for (int pi = pair0; pi < npi; pi += npairs, ++ac) {
       const Item2 I = item_of3(pi);
       const int nch = (I.nw + 31) / 32;
-      if (lane == 0) bulk_wait_read0();
-      __syncwarp();
       const long grow0 = I.k.row0 + q * 32;
-      if (p.epi == 1 && lane == 0) {  // prefetch the relu_backward mask source
-        mbar_arrive_tx(&oldbar[q], static_cast<uint32_t>(nch * 4096));
-        for (int c = 0; c < nch; ++c)
-          tma_load_2d(bufs + c * 1024, &map_c, I.n0 + c * 32, static_cast<int>(grow0), &oldbar[q]);
-      }
       const int buf = static_cast<int>(ac & 1);
-      mbar_wait(&tfull[buf], (ac >> 1) & 1);
-      tc_fence_after();
-      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && ac < kTraceItems)
-        p.trace[kTraceStages * 4 + ac * 2 + 0] = clock64();
-      if (p.epi == 1) mbar_wait(&oldbar[q], ac & 1);
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf * kTileN);
-      for (int c = 0; c < nch; ++c) {
-        float v[32];
-        tmem_ld32(tbase + c * 32, v);
-        float* b = bufs + c * 1024;
-#pragma unroll
-        for (int jj = 0; jj < 8; ++jj) {
-          float4 o = make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
-          float4* dst = sw128(b, lane, jj);
-          if (p.epi == 1) {
-            const float4 old = *dst;
-            o = make_float4(old.x > 0.0f ? o.x : 0.0f, old.y > 0.0f ? o.y : 0.0f, old.z > 0.0f ? o.z : 0.0f,
-                            old.w > 0.0f ? o.w : 0.0f);
-          } else if (p.epi == 2) {
-            o = make_float4(fmaxf(o.x, 0.0f), fmaxf(o.y, 0.0f), fmaxf(o.z, 0.0f), fmaxf(o.w, 0.0f));
-          }
-          *dst = o;
+      for (int c0 = 0; c0 < nch; c0 += kEpiChunks3) {
+        const int cn = min(kEpiChunks3, nch - c0);
+        if (lane == 0) bulk_wait_read0();  // the buffers' previous bulk stores have read them
+        __syncwarp();
+        if (p.epi == 1 && lane == 0) {  // prefetch the relu_backward mask source
+          mbar_arrive_tx(&oldbar[q], static_cast<uint32_t>(cn * 4096));
+          for (int c = 0; c < cn; ++c)
+            tma_load_2d(bufs + c * 1024, &map_c, I.n0 + (c0 + c) * 32, static_cast<int>(grow0), &oldbar[q]);
         }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[buf]);
-      if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && ac < kTraceItems)
-        p.trace[kTraceStages * 4 + ac * 2 + 1] = clock64();
-      fence_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        for (int c = 0; c < nch; ++c) tma_store_2d(&map_c, I.n0 + c * 32, static_cast<int>(grow0), bufs + c * 1024);
-        bulk_commit();
+        if (c0 == 0) {
+          mbar_wait(&tfull[buf], (ac >> 1) & 1);
+          tc_fence_after();
+          if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && ac < kTraceItems)
+            p.trace[kTraceStages * 4 + ac * 2 + 0] = clock64();
+        }
+        if (p.epi == 1) mbar_wait(&oldbar[q], (mph++) & 1);
+        for (int c = 0; c < cn; ++c) {
+          float v[32];
+          tmem_ld32(tbase + (c0 + c) * 32, v);
+          float* b = bufs + c * 1024;
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            float4 o = make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
+            float4* dst = sw128(b, lane, jj);
+            if (p.epi == 1) {
+              const float4 old = *dst;
+              o = make_float4(old.x > 0.0f ? o.x : 0.0f, old.y > 0.0f ? o.y : 0.0f, old.z > 0.0f ? o.z : 0.0f,
+                              old.w > 0.0f ? o.w : 0.0f);
+            } else if (p.epi == 2) {
+              o = make_float4(fmaxf(o.x, 0.0f), fmaxf(o.y, 0.0f), fmaxf(o.z, 0.0f), fmaxf(o.w, 0.0f));
+            }
+            *dst = o;
+          }
+        }
+        if (c0 + kEpiChunks3 >= nch) {  // the whole accumulator has been read: the MMA may reuse it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[buf]);
+          if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && ac < kTraceItems)
+            p.trace[kTraceStages * 4 + ac * 2 + 1] = clock64();
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          for (int c = 0; c < cn; ++c)
+            tma_store_2d(&map_c, I.n0 + (c0 + c) * 32, static_cast<int>(grow0), bufs + c * 1024);
+          bulk_commit();
+        }
       }
     }
     if (lane == 0) bulk_wait0();
@@ -1331,14 +1343,14 @@ inline int smem_bytes2(const Params& p, int bk) { return p.nst * (BM * bk * 4 + 
 
 // v3 (NN / NT): A ring as deep as the shared memory left after the W ring and the epilogue buffers.
 constexpr int kSmemMax3 = 232448 - 2048;  // sm_100 per-block maximum, minus static barriers and alignment
-int g_w3_bytes = 64 * 1024;  // v3 W ring budget ("gemm3_wring", bytes)
+int g_w3_bytes = 96 * 1024;  // v3 W ring budget ("gemm3_wring", bytes): 3 stages of a 128-column tile
 void finish_params3(Params& p) {
   const int wst = 2 * p.bnr * BK3 * 4, ast = BM * BK3 * 4;
   p.nwst = std::max(2, std::min(kMaxW3, g_w3_bytes / wst));
-  p.nst = std::max(2, std::min(kMaxA3, (kSmemMax3 - 1024 - kEpiBuf - p.nwst * wst) / ast));
+  p.nst = std::max(2, std::min(kMaxA3, (kSmemMax3 - 1024 - kEpiBuf3 - p.nwst * wst) / ast));
 }
 inline int smem_bytes3(const Params& p) {
-  return p.nst * BM * BK3 * 4 + p.nwst * 2 * p.bnr * BK3 * 4 + kEpiBuf + 1024;
+  return p.nst * BM * BK3 * 4 + p.nwst * 2 * p.bnr * BK3 * 4 + kEpiBuf3 + 1024;
 }
 int g_gemm3_cluster = 1;  // v3 cluster size for the W multicast ("gemm3_cluster": 1 or 2)
 template <int MODE, int CL>
