@@ -81,6 +81,7 @@ struct Params {
   int n_tiles;           // output column tiles of <= 128
   int bnr;               // B rows (tile columns) loaded per stage: min(np, 128) (TN: rounded to 32)
   int nwst;              // v3: W ring stages (nst = A ring stages)
+  int epi_chunks;        // v3: 32 x 32 epilogue buffers per epilogue warp (2, or 4 with the relu_backward mask)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -929,8 +930,6 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
 // have a shallow ring with their own producer warp; the 4 TMEM A slots (64 columns: hi | lo of 32 K) are
 // released by the MMA's own commit. Warps: 0 A producer, 1 MMA, 2-5 split, 6-9 epilogue, 10 W producer.
 constexpr int kThreads3 = 352;
-constexpr int kEpiChunks3 = 2;                      // epilogue 32 x 32 buffers per warp
-constexpr int kEpiBuf3 = 4 * kEpiChunks3 * 4096;   // 4 epilogue warps
 constexpr int BK3 = 32;
 constexpr int kMaxA3 = 12, kMaxW3 = 4, kTSlots3 = 4;
 
@@ -1164,19 +1163,21 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
     }
   } else {
     // ------------------------------------------------------------ epilogue (NN / NT)
-    // kEpiChunks3 (2) 32 x 32 buffers per warp: a 128-column tile leaves in two halves, each with its own
-    // bulk stores (and relu_backward mask prefetch); the shared memory saved goes to a deeper W ring.
+    // p.epi_chunks 32 x 32 buffers per warp. NN: 2, a 128-column tile leaves in two halves, each with its
+    // own bulk stores, and the shared memory saved goes to a deeper W ring. NT with the relu_backward mask:
+    // 4, the whole tile's mask prefetched at once (a second HBM round trip per tile measured slower).
     const int q = warp & 3;
+    const int ech = p.epi_chunks;
     uint32_t ac = 0, mph = 0;
-    float* bufs = epib + q * (kEpiChunks3 * 1024);
+    float* bufs = epib + q * (ech * 1024);
     for (int pi = pair0; pi < npi; pi += npairs, ++ac) {
       const Item2 I = item_of3(pi);
       const int nch = (I.nw + 31) / 32;
       const long grow0 = I.k.row0 + q * 32;
       const int buf = static_cast<int>(ac & 1);
       const uint32_t tbase = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(buf * kTileN);
-      for (int c0 = 0; c0 < nch; c0 += kEpiChunks3) {
-        const int cn = min(kEpiChunks3, nch - c0);
+      for (int c0 = 0; c0 < nch; c0 += ech) {
+        const int cn = min(ech, nch - c0);
         if (lane == 0) bulk_wait_read0();  // the buffers' previous bulk stores have read them
         __syncwarp();
         if (p.epi == 1 && lane == 0) {  // prefetch the relu_backward mask source
@@ -1209,7 +1210,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
             *dst = o;
           }
         }
-        if (c0 + kEpiChunks3 >= nch) {  // the whole accumulator has been read: the MMA may reuse it
+        if (c0 + ech >= nch) {  // the whole accumulator has been read: the MMA may reuse it
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[buf]);
@@ -1346,11 +1347,13 @@ constexpr int kSmemMax3 = 232448 - 2048;  // sm_100 per-block maximum, minus sta
 int g_w3_bytes = 96 * 1024;  // v3 W ring budget ("gemm3_wring", bytes): 3 stages of a 128-column tile
 void finish_params3(Params& p) {
   const int wst = 2 * p.bnr * BK3 * 4, ast = BM * BK3 * 4;
-  p.nwst = std::max(2, std::min(kMaxW3, g_w3_bytes / wst));
-  p.nst = std::max(2, std::min(kMaxA3, (kSmemMax3 - 1024 - kEpiBuf3 - p.nwst * wst) / ast));
+  p.epi_chunks = p.epi == 1 ? 4 : 2;
+  const int wbytes = p.epi == 1 ? std::min(g_w3_bytes, 64 * 1024) : g_w3_bytes;
+  p.nwst = std::max(2, std::min(kMaxW3, wbytes / wst));
+  p.nst = std::max(2, std::min(kMaxA3, (kSmemMax3 - 1024 - 4 * p.epi_chunks * 4096 - p.nwst * wst) / ast));
 }
 inline int smem_bytes3(const Params& p) {
-  return p.nst * BM * BK3 * 4 + p.nwst * 2 * p.bnr * BK3 * 4 + kEpiBuf3 + 1024;
+  return p.nst * BM * BK3 * 4 + p.nwst * 2 * p.bnr * BK3 * 4 + 4 * p.epi_chunks * 4096 + 1024;
 }
 int g_gemm3_cluster = 1;  // v3 cluster size for the W multicast ("gemm3_cluster": 1 or 2)
 template <int MODE, int CL>
