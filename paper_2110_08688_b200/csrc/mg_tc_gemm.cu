@@ -821,7 +821,10 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
       }
     }
   } else if (warp >= 10) {
-    // ------------------------------------------------------------ TN: split B (G rows) in place (hi) + lo copy
+    // ------------------------------------------------------------ TN: B (G rows) lo copy
+    // kind::tf32 reads the raw fp32 tile as its hi part: the tensor core drops the low 13 mantissa bits,
+    // exactly the x & 0xFFFFE000 of split4, so only lo = x - hi is written (half the shared-memory
+    // stores of rewriting hi in place; the kernel is shared-memory-bandwidth bound at this stage).
     if (MODE == TN && p.terms == 3) {
       const int t = threadIdx.x - 320;
       RingPos rp(p.nst);
@@ -837,10 +840,7 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
                          : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                          : "r"(bh + 16u * q4));
-            const float4 h = split4(v, l);
-            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(bh + 16u * q4), "f"(h.x), "f"(h.y),
-                         "f"(h.z), "f"(h.w)
-                         : "memory");
+            (void)split4(v, l);
             asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(bl + 16u * q4), "f"(l.x), "f"(l.y),
                          "f"(l.z), "f"(l.w)
                          : "memory");
