@@ -286,6 +286,20 @@ int hub_class_max(int ld) {
   return k;
 }
 
+// Masked softmax-CE over `rows` logits rows of C classes: up to 48 classes a row takes half a warp (two
+// rows per warp, half the shuffle rounds per row), wider rows a whole warp.
+static void launch_softmax_xent(int C, int blocks, cudaStream_t s, float* logits, int ld, int rows, const int* labels,
+                                const uint8_t* mask, float inv_denom, double* partials) {
+  if (C <= 16) k::softmax_xent<1, 16><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
+  else if (C <= 32) k::softmax_xent<2, 16><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
+  else if (C <= 48) k::softmax_xent<3, 16><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
+  else if (C <= 64) k::softmax_xent<2><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
+  else if (C <= 128) k::softmax_xent<4><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
+  else if (C <= 192) k::softmax_xent<6><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
+  else k::softmax_xent<k::kLossCpl><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
+  MG_LAUNCHED();
+}
+
 // adam_step's constants (gcn.hpp:61-70): cast to float, bias corrections via std::pow in double.
 static k::AdamConsts adam_consts(double lr, double beta1, double beta2, double eps, int t) {
   if (t < 1) throw ValueError("adam_step: step index must be >= 1, got " + std::to_string(t));
@@ -953,20 +967,8 @@ class Step {
       const int th = tl_begin(k, 0, "other", "loss", -1, {w.last_task[0]});
       const int pi = prof_begin(w);
       if (w.rows > 0) {
-        const int C32 = static_cast<int>((C + 31) / 32);
-        if (C32 <= 2) k::softmax_xent<2><<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
-                                                         static_cast<int>(w.rows), static_cast<int>(C), w.labels,
-                                                         w.mask, inv_denom, w.partials);
-        else if (C32 <= 4) k::softmax_xent<4><<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
-                                                         static_cast<int>(w.rows), static_cast<int>(C), w.labels,
-                                                         w.mask, inv_denom, w.partials);
-        else if (C32 <= 6) k::softmax_xent<6><<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
-                                                         static_cast<int>(w.rows), static_cast<int>(C), w.labels,
-                                                         w.mask, inv_denom, w.partials);
-        else k::softmax_xent<k::kLossCpl><<<w.loss_blocks, 256, 0, w.s0>>>(w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
-                                                         static_cast<int>(w.rows), static_cast<int>(C), w.labels,
-                                                         w.mask, inv_denom, w.partials);
-        MG_LAUNCHED();
+        launch_softmax_xent(static_cast<int>(C), w.loss_blocks, w.s0, w.ahw[L_ - 1], static_cast<int>(g_.ld[L_]),
+                            static_cast<int>(w.rows), w.labels, w.mask, inv_denom, w.partials);
         ++g_.kernels_last;
       }
       k::finalize_stats<<<1, 32, 0, w.s0>>>(w.partials, w.rows > 0 ? w.loss_blocks : 0, w.stats);
@@ -1818,14 +1820,7 @@ mg_status mg_dev_softmax_xent(float* logits, int64_t rows, int64_t classes, int6
     MG_CUDA(cudaMalloc(&part, sizeof(double) * (2 * blocks + 2)));
     const float inv = 1.0f / static_cast<float>(denom);
     const int R = static_cast<int>(rows), Cc = static_cast<int>(classes), L = static_cast<int>(ld);
-    const int C32 = (Cc + 31) / 32;
-    if (rows > 0) {
-      if (C32 <= 2) k::softmax_xent<2><<<blocks, 256, 0, s>>>(logits, L, R, Cc, labels, mask, inv, part);
-      else if (C32 <= 4) k::softmax_xent<4><<<blocks, 256, 0, s>>>(logits, L, R, Cc, labels, mask, inv, part);
-      else if (C32 <= 6) k::softmax_xent<6><<<blocks, 256, 0, s>>>(logits, L, R, Cc, labels, mask, inv, part);
-      else k::softmax_xent<k::kLossCpl><<<blocks, 256, 0, s>>>(logits, L, R, Cc, labels, mask, inv, part);
-      MG_LAUNCHED();
-    }
+    if (rows > 0) launch_softmax_xent(Cc, blocks, s, logits, L, R, labels, mask, inv, part);
     k::finalize_stats<<<1, 32, 0, s>>>(part, rows > 0 ? blocks : 0, part + 2 * blocks);
     MG_LAUNCHED();
     MG_CUDA(cudaMemcpyAsync(stats, part + 2 * blocks, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));

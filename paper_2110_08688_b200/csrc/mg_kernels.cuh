@@ -624,55 +624,58 @@ __global__ void __launch_bounds__(256) gemm_exact(int M, int N, int K, const flo
 // fixed order so the reported loss is run-to-run deterministic.
 constexpr int kLossCpl = 8;
 
-template <int CPL>  // class chunks of 32 per lane row: C <= 32 * CPL
+template <int CPL, int LPR = 32>  // LPR lanes per row (32 or 16: two rows per warp), C <= LPR * CPL
 __global__ void __launch_bounds__(256) softmax_xent(float* __restrict__ logits, int ld, int rows, int C,
                                                     const int* __restrict__ labels, const uint8_t* __restrict__ mask,
                                                     float inv_denom, double* __restrict__ partials) {
+  static_assert(LPR == 32 || LPR == 16, "a row spans a warp or a half warp");
+  constexpr int RPW = 32 / LPR;  // rows per warp
   __shared__ double s_loss[8], s_corr[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lr = lane & (LPR - 1), slot = lane / LPR;
   double my_loss = 0.0, my_corr = 0.0;
-  const int stride = gridDim.x * 8;
+  const int stride = gridDim.x * 8 * RPW;
   // the next row's logits, label and mask are loaded while the current row is reduced (one row per warp
-  // in flight was latency-bound)
+  // in flight was latency-bound); rows past the end read as masked
   auto load = [&](int r, float* z, int& label, int& m) {
     m = 0;
+    label = 0;
+#pragma unroll
+    for (int q = 0; q < CPL; ++q) z[q] = -INFINITY;
     if (r >= rows) return;
     m = mask[r];
     label = labels[r];
     const float* row = logits + (size_t)r * ld;
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
-      const int j = lane + 32 * q;
-      z[q] = j < C ? row[j] : -INFINITY;
+      const int j = lr + LPR * q;
+      if (j < C) z[q] = row[j];
     }
   };
   float zn[CPL];
   int label_n = 0, m_n = 0;
-  load(blockIdx.x * 8 + warp, zn, label_n, m_n);
-  for (int r = blockIdx.x * 8 + warp; r < rows; r += stride) {
+  load((blockIdx.x * 8 + warp) * RPW + slot, zn, label_n, m_n);
+  // warp-uniform loop over groups of RPW rows: every lane takes part in every shuffle
+  for (int base = (blockIdx.x * 8 + warp) * RPW; base < rows; base += stride) {
+    const int r = base + slot;
     float z[CPL];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) z[q] = zn[q];
     const int label = label_n, m = m_n;
     load(r + stride, zn, label_n, m_n);
-    float* row = logits + (size_t)r * ld;
-    if (!m) {
-      for (int j = lane; j < ld; j += 32) row[j] = 0.0f;
-      continue;
-    }
     float mx = -INFINITY;
     int arg = 0x7fffffff;
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
-      const int j = lane + 32 * q;
+      const int j = lr + LPR * q;
       if (j < C && (arg == 0x7fffffff || z[q] > mx)) {
         mx = z[q];
         arg = j;
       }
     }
-    // (max, first index) warp reduction: strictly greater wins, ties keep the smaller index
+    // (max, first index) reduction over the row's lanes: strictly greater wins, ties keep the smaller index
 #pragma unroll
-    for (int off = 16; off; off >>= 1) {
+    for (int off = LPR / 2; off; off >>= 1) {
       const float om = __shfl_xor_sync(0xffffffffu, mx, off);
       const int oa = __shfl_xor_sync(0xffffffffu, arg, off);
       if (oa != 0x7fffffff && (arg == 0x7fffffff || om > mx || (om == mx && oa < arg))) {
@@ -683,31 +686,42 @@ __global__ void __launch_bounds__(256) softmax_xent(float* __restrict__ logits, 
     float se = 0.0f, ex[CPL];
 #pragma unroll
     for (int q = 0; q < CPL; ++q) {
-      const int j = lane + 32 * q;
+      const int j = lr + LPR * q;
       ex[q] = j < C ? expf(z[q] - mx) : 0.0f;
       if (j < C) se += ex[q];
     }
 #pragma unroll
-    for (int off = 16; off; off >>= 1) se += __shfl_xor_sync(0xffffffffu, se, off);
+    for (int off = LPR / 2; off; off >>= 1) se += __shfl_xor_sync(0xffffffffu, se, off);
     float zlab = 0.0f;
 #pragma unroll
     for (int q = 0; q < CPL; ++q)
-      if (label == lane + 32 * q) zlab = z[q];
-    zlab = __shfl_sync(0xffffffffu, zlab, label & 31);
-    if (lane == 0) {
-      my_loss += (double)(logf(se) - (zlab - mx));
-      my_corr += (arg == label) ? 1.0 : 0.0;
-    }
+      if (label == lr + LPR * q) zlab = z[q];
+    zlab = __shfl_sync(0xffffffffu, zlab, label & (LPR - 1), LPR);
+    if (r < rows) {
+      float* row = logits + (size_t)r * ld;
+      if (!m) {
+        for (int j = lr; j < ld; j += LPR) row[j] = 0.0f;
+      } else {
+        if (lr == 0) {
+          my_loss += (double)(logf(se) - (zlab - mx));
+          my_corr += (arg == label) ? 1.0 : 0.0;
+        }
 #pragma unroll
-    for (int q = 0; q < CPL; ++q) {
-      const int j = lane + 32 * q;
-      if (j < C) {
-        float g = __fmul_rn(__fdiv_rn(ex[q], se), inv_denom);
-        if (j == label) g = __fsub_rn(g, inv_denom);
-        row[j] = g;
+        for (int q = 0; q < CPL; ++q) {
+          const int j = lr + LPR * q;
+          if (j < C) {
+            float g = __fmul_rn(__fdiv_rn(ex[q], se), inv_denom);
+            if (j == label) g = __fsub_rn(g, inv_denom);
+            row[j] = g;
+          }
+        }
+        for (int j = C + lr; j < ld; j += LPR) row[j] = 0.0f;
       }
     }
-    for (int j = C + lane; j < ld; j += 32) row[j] = 0.0f;
+  }
+  if (RPW == 2) {  // the second row slot's leader (lane 16) hands its sums to lane 0
+    my_loss += __shfl_down_sync(0xffffffffu, my_loss, 16);
+    my_corr += __shfl_down_sync(0xffffffffu, my_corr, 16);
   }
   if (lane == 0) {
     s_loss[warp] = my_loss;
