@@ -18,6 +18,7 @@
 #include <functional>
 #include <future>
 #include <memory>
+#include <map>
 #include <mutex>
 #include <numeric>
 #include <string>
@@ -161,14 +162,89 @@ void build_hub_segments(const std::vector<index_t>& rp, std::vector<int4>& items
   }
 }
 
+// Device blocks released by destroyed groups and by group-creation temporaries stay cached for later
+// allocations of the same (rounded) size on the same device: cudaMalloc / cudaFree of GB-sized blocks
+// (page mapping; cudaFree synchronises the device) made group creation take 5-70 ms or 0.1-0.7 s from
+// run to run. A failed cudaMalloc releases the device's cached blocks and retries.
+class BlockCache {
+ public:
+  static constexpr size_t kCap = size_t(32) << 30;  // cached bytes per device
+  static size_t round(size_t bytes) {
+    const size_t q = bytes >= (size_t(1) << 20) ? (size_t(1) << 20) : 4096;
+    return (std::max<size_t>(bytes, 16) + q - 1) / q * q;
+  }
+  void* get(int dev, size_t bytes) {  // bytes already rounded; the caller has set the device
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      auto it = free_.find({dev, bytes});
+      if (it != free_.end()) {
+        void* p = it->second;
+        free_.erase(it);
+        cached_[dev] -= bytes;
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) {
+      (void)cudaGetLastError();
+      release(dev);
+      MG_CUDA(cudaMalloc(&p, bytes));
+    }
+    return p;
+  }
+  void put(int dev, void* p, size_t bytes) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu_);
+    if (cached_[dev] + bytes > kCap) {  // bounded: the rest of the process (torch, NCCL) needs memory too
+      cudaFree(p);
+      return;
+    }
+    free_.insert({{dev, bytes}, p});
+    cached_[dev] += bytes;
+  }
+  void release(int dev) {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (auto it = free_.begin(); it != free_.end();) {
+      if (it->first.first == dev) {
+        cudaFree(it->second);
+        it = free_.erase(it);
+      } else {
+        ++it;
+      }
+    }
+    cached_[dev] = 0;
+  }
+
+ private:
+  std::mutex mu_;
+  std::multimap<std::pair<int, size_t>, void*> free_;
+  std::map<int, size_t> cached_;
+};
+BlockCache& block_cache() {
+  static BlockCache* c = new BlockCache();  // process lifetime
+  return *c;
+}
+int cur_device() {
+  int d = 0;
+  MG_CUDA(cudaGetDevice(&d));
+  return d;
+}
+// A create-time temporary from the cache (released with tmp_free once its users have completed).
+template <class T>
+T* tmp_alloc(size_t count, size_t& bytes) {
+  bytes = BlockCache::round(sizeof(T) * count);
+  return static_cast<T*>(block_cache().get(cur_device(), bytes));
+}
+inline void tmp_free(void* p, size_t bytes) { block_cache().put(cur_device(), p, bytes); }
+
 // Light-row half on the device: key = ht - length for rows below the threshold (2 ht for the others, which
 // sort last), a stable radix sort of (key, row), then {e0, e1, row, 0} items for the first n_light rows.
 void light_items_device(const int* rp, index_t rows, int ht, index_t n_light, int4* out) {
-  int *keys = nullptr, *keys2 = nullptr, *ids = nullptr, *ids2 = nullptr;
-  MG_CUDA(cudaMalloc(&keys, sizeof(int) * rows));
-  MG_CUDA(cudaMalloc(&keys2, sizeof(int) * rows));
-  MG_CUDA(cudaMalloc(&ids, sizeof(int) * rows));
-  MG_CUDA(cudaMalloc(&ids2, sizeof(int) * rows));
+  size_t bk = 0, bt = 0;
+  int* keys = tmp_alloc<int>(rows, bk);
+  int* keys2 = tmp_alloc<int>(rows, bk);
+  int* ids = tmp_alloc<int>(rows, bk);
+  int* ids2 = tmp_alloc<int>(rows, bk);
   const int blocks = static_cast<int>(std::min<index_t>((rows + 255) / 256, 148 * 16));
   k::light_keys<<<blocks, 256, 0, cudaStreamLegacy>>>(rp, static_cast<int>(rows), ht, keys, ids);
   MG_LAUNCHED();
@@ -177,15 +253,15 @@ void light_items_device(const int* rp, index_t rows, int ht, index_t n_light, in
   while ((1 << bits) <= 2 * ht) ++bits;
   size_t tmp = 0;
   MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, static_cast<int>(rows), 0, bits, cudaStreamLegacy));
-  void* t = nullptr;
-  MG_CUDA(cudaMalloc(&t, std::max<size_t>(tmp, 16)));
+  void* t = tmp_alloc<char>(tmp, bt);
   MG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kb, vb, static_cast<int>(rows), 0, bits, cudaStreamLegacy));
   k::light_fill<<<blocks, 256, 0, cudaStreamLegacy>>>(rp, vb.Current(), static_cast<int>(n_light), out);
   MG_LAUNCHED();
   MG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
   for (void* q : {static_cast<void*>(keys), static_cast<void*>(keys2), static_cast<void*>(ids),
-                  static_cast<void*>(ids2), t})
-    cudaFree(q);
+                  static_cast<void*>(ids2)})
+    tmp_free(q, bk);
+  tmp_free(t, bt);
 }
 
 // Host-side construction of the launch lists for a tile (row order by decreasing length).
@@ -462,7 +538,7 @@ struct Worker {
   size_t tl_used = 0;
   cudaEvent_t tl_base = nullptr;
   uint64_t last_task[2] = {0, 0};  // last recorded task per lane (WorkerCtx::last, collectives.hpp)
-  std::vector<void*> allocs;
+  std::vector<std::pair<void*, size_t>> allocs;  // block cache entries (pointer, rounded bytes)
   index_t bytes = 0;
 };
 
@@ -509,11 +585,11 @@ namespace {
 
 void* dalloc(mg_group& g, Worker& w, size_t bytes) {
   if (g.sealed) g.step_allocs++;
-  void* p = nullptr;
   MG_CUDA(cudaSetDevice(w.device));
-  MG_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16)));
+  const size_t rb = BlockCache::round(bytes);
+  void* p = block_cache().get(w.device, rb);
   MG_CUDA(cudaMemset(p, 0, std::max<size_t>(bytes, 16)));
-  w.allocs.push_back(p);
+  w.allocs.push_back({p, rb});
   w.bytes += static_cast<index_t>(bytes);
   return p;
 }
@@ -599,10 +675,9 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
   });
   Stopwatch sw;
   if (d.nnz) {  // {col, value bits} records: both arrays go up as they are, the device interleaves them
-    int* tcol = nullptr;
-    float* tval = nullptr;
-    MG_CUDA(cudaMalloc(&tcol, sizeof(int) * d.nnz));
-    MG_CUDA(cudaMalloc(&tval, sizeof(float) * d.nnz));
+    size_t bc = 0, bv = 0;
+    int* tcol = tmp_alloc<int>(static_cast<size_t>(d.nnz), bc);
+    float* tval = tmp_alloc<float>(static_cast<size_t>(d.nnz), bv);
     if (is_pinned_host(t.col.data()) && is_pinned_host(t.val.data())) {  // one DMA each, no staging copy
       MG_CUDA(cudaMemcpyAsync(tcol, t.col.data(), sizeof(int) * d.nnz, cudaMemcpyHostToDevice, cudaStreamLegacy));
       MG_CUDA(cudaMemcpyAsync(tval, t.val.data(), sizeof(float) * d.nnz, cudaMemcpyHostToDevice, cudaStreamLegacy));
@@ -613,18 +688,17 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
     k::pack_edges<<<num_sms() * 8, 256, 0, cudaStreamLegacy>>>(tcol, tval, d.nnz, d.edges);
     MG_LAUNCHED();
     MG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
-    cudaFree(tcol);
-    cudaFree(tval);
+    tmp_free(tcol, bc);
+    tmp_free(tval, bv);
   }
   sw.lap("  arrays");
   // FAST mode: tag each record with its column's hub class (top 4 bits), computed on the device from the
   // uploaded records: per-column gather counts, a histogram of the counts, and per-tier count thresholds
   // (class k = gathered at least as often as the 10000 * 2^(k-1)-th most gathered column).
   if (g.cfg.spmm_mode == MG_SPMM_FAST && g_hub_bytes.load() > 0 && d.nnz && t.cols < (index_t(1) << 28)) {
-    int* cnt = nullptr;
-    int* chist = nullptr;
-    MG_CUDA(cudaMalloc(&cnt, sizeof(int) * t.cols));
-    MG_CUDA(cudaMalloc(&chist, sizeof(int) * (k::kHubCountCap + 1)));
+    size_t bc = 0, bh = 0;
+    int* cnt = tmp_alloc<int>(static_cast<size_t>(t.cols), bc);
+    int* chist = tmp_alloc<int>(static_cast<size_t>(k::kHubCountCap + 1), bh);
     MG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * t.cols, cudaStreamLegacy));
     MG_CUDA(cudaMemsetAsync(chist, 0, sizeof(int) * (k::kHubCountCap + 1), cudaStreamLegacy));
     const int gb = num_sms() * 8;
@@ -643,8 +717,8 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
     k::hub_tag<<<gb, 256, 0, cudaStreamLegacy>>>(d.edges, d.nnz, cnt, tiers);
     MG_LAUNCHED();
     MG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));
-    cudaFree(cnt);
-    cudaFree(chist);
+    tmp_free(cnt, bc);
+    tmp_free(chist, bh);
     d.hubs_classed = true;
   }
   sw.lap("  hub class");
@@ -1627,7 +1701,7 @@ void mg_group_destroy(mg_group* g) {
     cudaSetDevice(w.device);
     cudaDeviceSynchronize();
     if (w.comm) ncclCommDestroy(w.comm);
-    for (void* p : w.allocs) cudaFree(p);
+    for (auto& a : w.allocs) block_cache().put(w.device, a.first, a.second);
     if (w.h_stats) cudaFreeHost(w.h_stats);
     for (cudaEvent_t e : {w.prior, w.heavy_fork, w.heavy_join, w.loss_done, w.stats_done, w.src_ready, w.copy_done,
                           w.ar_ready, w.ar_done, w.t_start, w.t_end})
