@@ -17,7 +17,7 @@ cfg = R.GcnConfig(dims, epochs=10, seed=1, permute=True)
 prep = R.prepare_data(ds, cfg, 1)
 t2 = time.time()
 print(f"synth {t1 - t0:.2f} s, prepare {t2 - t1:.2f} s", flush=True)
-for rep in range(2):
+for rep in range(int(os.environ.get("REPS", "2"))):
     a = time.time()
     g = R.Group(cfg, prep, 1, devices=[0])
     b = time.time()
