@@ -174,6 +174,32 @@ def test_gemm_tcgen05_deterministic(gemm_kernel):
     assert bits_equal(r1, r2)
 
 
+@pytest.mark.parametrize("knob,value", [("gemm3_cluster", 2), ("gemm3_wring", 64 << 10), ("gemm3_wring", 128 << 10)])
+def test_gemm_v3_variants_bitwise(knob, value):
+    """The v3 NN / NT pipeline variants (2-CTA W multicast, W-ring depth) reorder no arithmetic: every
+    epilogue gives the default kernel's bits."""
+    rng = np.random.default_rng(17)
+    cases = [((777, 256), (256, 256), False), ((1000, 100), (100, 256), False), ((513, 47), (256, 47), True),
+             ((300, 256), (48, 256), True)]
+    base = []
+    for (am, ak), bs, tb in cases:
+        a = rng.uniform(-1, 1, (am, ak)).astype(np.float32)
+        b = rng.uniform(-1, 1, bs).astype(np.float32)
+        n = bs[0] if tb else bs[1]
+        c0 = rng.normal(size=(am, n)).astype(np.float32)
+        base.append((a, b, tb, c0, [run_gemm(a, b, False, tb, epi=e, c0=c0 if e == 1 else None, mode=R.GEMM_TF32X3)
+                                    for e in (0, 1, 2)]))
+    default = 96 << 10 if knob == "gemm3_wring" else 1
+    R.set_tuning(knob, value)
+    try:
+        for a, b, tb, c0, outs in base:
+            for e, ref in zip((0, 1, 2), outs):
+                got = run_gemm(a, b, False, tb, epi=e, c0=c0 if e == 1 else None, mode=R.GEMM_TF32X3)
+                assert bits_equal(got, ref), (knob, value, a.shape, tb, e)
+    finally:
+        R.set_tuning(knob, default)
+
+
 # ---------------------------------------------------------------------------- MG_SPMM_FAST
 # FMA and hub rows cut into fixed segments summed in order: deterministic, and as close to the exact
 # (fp64) product as the reference's own serial fp32 sum is (normwise <= 1e-5 here, the model-level
