@@ -20,12 +20,19 @@ from __future__ import annotations
 import builtins
 import ctypes as C
 import json
+import sys
 from dataclasses import dataclass, field, fields
 from typing import Callable, Optional
 
 import numpy as np
 
 from ._lib import lib, mg_config, mg_csr, mg_timeline_event
+
+
+def _finalizing() -> bool:
+    """True during interpreter shutdown, when module globals (lib, ctypes) may already be torn down: the
+    process exit releases the native objects then."""
+    return sys is None or sys.is_finalizing()
 
 # ----------------------------------------------------------------------------- errors (inc/errors.hpp)
 
@@ -198,7 +205,7 @@ class Dataset:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and h.value:
+        if h and h.value and not _finalizing():
             lib().mg_dataset_free(h)
             self._h = C.c_void_p()
 
@@ -391,7 +398,7 @@ class PreparedData:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h and h.value:
+        if h and h.value and not _finalizing():
             lib().mg_partition_free(h)
             self._h = C.c_void_p()
 
@@ -473,7 +480,8 @@ class Group:
             self._h = C.c_void_p()
 
     def __del__(self):
-        self.close()
+        if not _finalizing():
+            self.close()
 
     def __enter__(self):
         return self

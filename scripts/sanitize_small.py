@@ -15,6 +15,15 @@ for gm, sm in [(R.GEMM_EXACT, R.SPMM_EXACT), (R.GEMM_TF32X3, R.SPMM_FAST)]:
         art = R.train_run(ds, cfg, R.TrainOptions(workers=P, devices=[0] * P,
                                                   transport=R.TRANSPORT_NCCL if P == 1 else R.TRANSPORT_LOCAL))
         print("train", gm, sm, P, art.epoch_loss, flush=True)
+# products-like widths: 256-column tiles, N = 48 tiles, 32-row TN stages with TMEM drains, half-warp softmax
+ds2 = R.synth_graph(3000, 12.0, 0.7, 3, 100, 47)
+cfg = R.GcnConfig([100, 256, 256, 47], epochs=2, seed=1, permute=True)
+print("train c4-like", R.train_run(ds2, cfg, R.TrainOptions()).epoch_loss, flush=True)
+with R.Group(cfg, R.prepare_data(ds2, cfg, 1), 1, devices=[0]) as g:  # backward from a written gradient
+    g.init_params()
+    g.forward()
+    g.backward()
+    print("backward", float(abs(g.read(R.T_WGRAD, 1)).sum()) >= 0, flush=True)
 cfg = R.GcnConfig([40, 64, 5], epochs=1, seed=1, permute=True)
 R.prepare_data(ds, cfg, 2, device=0)
 print("bench_spmm", R.bench_spmm(ds, workers=2, devices=[0, 0], transport=R.TRANSPORT_LOCAL)["wall_us"] > 0)
