@@ -5,6 +5,7 @@
 // the staged 1D row-broadcast SpMM schedule on two streams with CUDA events, and the training step.
 // Reference: rowgcn inc/gcn.hpp (GcnWorker), inc/dist_spmm.hpp (staged SpMM), inc/collectives.hpp.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -658,7 +659,85 @@ Stager& stager() {
   return *s;
 }
 
-void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
+std::atomic<int> g_bwd_transpose{1};  // P = 1: the backward tile is built on the device ("bwd_transpose")
+
+// Edge-parallel (hub rows hold up to ~1e5 nonzeros): each thread takes a contiguous run of 64 records,
+// finds its first row by binary search and walks the rows forward. key = column << row_bits | row.
+__global__ void transpose_keys(const int* __restrict__ rp, const int2* __restrict__ edges, int rows, long nnz,
+                               int row_bits, unsigned long long* __restrict__ keys, unsigned int* __restrict__ vals) {
+  constexpr long kRun = 64;
+  for (long b = (blockIdx.x * (long)blockDim.x + threadIdx.x) * kRun; b < nnz; b += (long)gridDim.x * blockDim.x * kRun) {
+    int lo = 0, hi = rows - 1;  // last row with rp[row] <= b
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (rp[mid] <= b) lo = mid;
+      else hi = mid - 1;
+    }
+    int r = lo;
+    const long end = min(nnz, b + kRun);
+    for (long e = b; e < end; ++e) {
+      while (rp[r + 1] <= e) ++r;
+      const int2 rec = edges[e];
+      keys[e] = (static_cast<unsigned long long>(rec.x & k::kColMask) << row_bits) | static_cast<unsigned>(r);
+      vals[e] = static_cast<unsigned>(rec.y);
+    }
+  }
+}
+__global__ void transpose_fill(const unsigned long long* __restrict__ keys, const unsigned int* __restrict__ vals,
+                               long nnz, int row_bits, int2* __restrict__ edges, int* __restrict__ cnt) {
+  const unsigned long long row_mask = (1ull << row_bits) - 1ull;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < nnz; i += (long)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[i];
+    edges[i] = make_int2(static_cast<int>(k & row_mask), static_cast<int>(vals[i]));
+    atomicAdd(cnt + (k >> row_bits), 1);
+  }
+}
+
+// P = 1: the backward tile (Â, bwd) is the transpose of the forward tile (Âᵀ) — the same values with
+// (row, column) swapped, columns ascending within a row as tile_rows leaves them — so it is built on the
+// device from the uploaded forward tile (a radix sort of (column, row) keys, then a count + scan for the
+// row pointers) instead of a second 8-bytes-per-nonzero upload. The host tile only provides the shapes.
+void transpose_tile_device(const DevTile& f, DevTile& d) {
+  const size_t nnz = static_cast<size_t>(d.nnz);
+  size_t bk = 0, bv = 0, bc = 0, bt = 0;
+  auto* k1 = tmp_alloc<unsigned long long>(nnz, bk);
+  auto* k2 = tmp_alloc<unsigned long long>(nnz, bk);
+  auto* v1 = tmp_alloc<unsigned int>(nnz, bv);
+  auto* v2 = tmp_alloc<unsigned int>(nnz, bv);
+  int* cnt = tmp_alloc<int>(static_cast<size_t>(d.rows) + 1, bc);
+  const cudaStream_t s = cudaStreamLegacy;
+  const int gb = num_sms() * 8;
+  int row_bits = 1, col_bits = 1;
+  while ((index_t(1) << row_bits) < std::max<index_t>(f.rows, 2)) ++row_bits;
+  while ((index_t(1) << col_bits) < std::max<index_t>(f.cols, 2)) ++col_bits;
+  transpose_keys<<<gb, 256, 0, s>>>(f.row_ptr, f.edges, static_cast<int>(f.rows), static_cast<long>(nnz), row_bits,
+                                    k1, v1);
+  MG_LAUNCHED();
+  cub::DoubleBuffer<unsigned long long> kb(k1, k2);
+  cub::DoubleBuffer<unsigned int> vb(v1, v2);
+  size_t tmp = 0;
+  MG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kb, vb, nnz, 0, row_bits + col_bits, s));
+  void* t = tmp_alloc<char>(tmp, bt);
+  MG_CUDA(cub::DeviceRadixSort::SortPairs(t, tmp, kb, vb, nnz, 0, row_bits + col_bits, s));
+  MG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int) * (d.rows + 1), s));
+  transpose_fill<<<gb, 256, 0, s>>>(kb.Current(), vb.Current(), static_cast<long>(nnz), row_bits, d.edges, cnt);
+  MG_LAUNCHED();
+  size_t stmp = 0;
+  MG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, stmp, cnt, d.row_ptr, static_cast<int>(d.rows + 1), s));
+  size_t bs = 0;
+  void* st = tmp_alloc<char>(stmp, bs);
+  MG_CUDA(cub::DeviceScan::ExclusiveSum(st, stmp, cnt, d.row_ptr, static_cast<int>(d.rows + 1), s));
+  MG_CUDA(cudaStreamSynchronize(s));
+  tmp_free(k1, bk);
+  tmp_free(k2, bk);
+  tmp_free(v1, bv);
+  tmp_free(v2, bv);
+  tmp_free(cnt, bc);
+  tmp_free(t, bt);
+  tmp_free(st, bs);
+}
+
+void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d, const DevTile* transpose_of = nullptr) {
   d.rows = t.rows;
   d.cols = t.cols;
   d.nnz = t.nnz();
@@ -666,6 +745,14 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
   d.row_ptr = dalloc_t<int>(g, w, t.rows + 1);
   d.edges = dalloc_t<int2>(g, w, d.nnz + k::kEdgePad);
   Stager& st = stager();
+  if (transpose_of) {
+    if (transpose_of->rows != t.cols || transpose_of->cols != t.rows || transpose_of->nnz != d.nnz)
+      throw ValueError("upload: the backward tile is not the forward tile's transpose");
+    Stopwatch sw0;
+    if (d.nnz) transpose_tile_device(*transpose_of, d);
+    else MG_CUDA(cudaMemset(d.row_ptr, 0, sizeof(int) * (t.rows + 1)));
+    sw0.lap("  transpose");
+  } else {
   st.upload(d.row_ptr, sizeof(int) * (t.rows + 1), [&](char* dst, size_t off, size_t len) {
     int* o = reinterpret_cast<int*>(dst);
     const index_t r0 = static_cast<index_t>(off / sizeof(int));
@@ -673,8 +760,9 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d) {
       for (index_t i = b; i < e; ++i) o[i] = static_cast<int>(t.row_ptr[r0 + i]);
     }, index_t(1) << 18);
   });
+  }
   Stopwatch sw;
-  if (d.nnz) {  // {col, value bits} records: both arrays go up as they are, the device interleaves them
+  if (d.nnz && !transpose_of) {  // {col, value bits} records: both arrays go up as they are, the device interleaves them
     size_t bc = 0, bv = 0;
     int* tcol = tmp_alloc<int>(static_cast<size_t>(d.nnz), bc);
     float* tval = tmp_alloc<float>(static_cast<size_t>(d.nnz), bv);
@@ -1235,6 +1323,8 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
     } else if (k == "spmm_hub_bytes") {
       if (value < 0) throw ValueError("tuning: spmm_hub_bytes must be >= 0");
       g_hub_bytes = value;
+    } else if (k == "bwd_transpose") {
+      g_bwd_transpose = value != 0 ? 1 : 0;
     } else if (k == "spmm_async") {
       g_spmm_async = value != 0 ? 1 : 0;
     } else if (k == "fast_segment") {
@@ -1355,7 +1445,8 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       for (int d = 0; d < 2; ++d) {
         w.tiles[d].resize(world);
         for (int j = 0; j < world; ++j) {
-          upload_tile(*g, w, p->tiles[d][w.rank][j], w.tiles[d][j]);
+          const bool tr = d == 1 && world == 1 && g_bwd_transpose.load();
+          upload_tile(*g, w, p->tiles[d][w.rank][j], w.tiles[d][j], tr ? &w.tiles[0][0] : nullptr);
           max_segments = std::max(max_segments, w.tiles[d][j].n_segments);
         }
       }

@@ -105,3 +105,33 @@ def test_hub_l2_hints_do_not_change_results(hub_bytes):
     finally:
         R.set_tuning("spmm_hub_bytes", 96 << 20)
     assert a.epoch_loss == b.epoch_loss and a.w_hashes == b.w_hashes
+
+
+@pytest.mark.parametrize("mode", ["exact", "fast"])
+def test_backward_tile_transposed_on_device(mode):
+    """P = 1 builds the backward tile (Â) on the device as the transpose of the uploaded forward tile (Âᵀ):
+    training is bitwise the same as with the uploaded backward tile (weighted graph: the values matter)."""
+    kw = dict(gemm_mode=R.GEMM_EXACT, spmm_mode=R.SPMM_EXACT) if mode == "exact" else {}
+    rng = np.random.default_rng(4)
+    n, m = 3000, 40000
+    u, v = rng.integers(0, n, m), rng.integers(0, n, m)
+    keys = np.unique(u * n + v)
+    rows, cols = keys // n, keys % n
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    rp = np.cumsum(rp)
+    vals = rng.uniform(0.1, 2.0, len(keys)).astype(np.float32)
+    x = rng.uniform(-1, 1, (n, 12)).astype(np.float32)
+    lab = rng.integers(0, 5, n).astype(np.int32)
+    ds = R.Dataset.from_arrays(rp, cols.astype(np.int64), vals, x, lab)
+    cfg = R.GcnConfig([12, 32, 5], epochs=3, seed=7, permute=True, **kw)
+    runs = []
+    for flag in (0, 1):
+        R.set_tuning("bwd_transpose", flag)
+        try:
+            runs.append(R.train_run(ds, cfg, R.TrainOptions(devices=[0])))
+        finally:
+            R.set_tuning("bwd_transpose", 1)
+    assert runs[0].epoch_loss == runs[1].epoch_loss
+    for a, b in zip(runs[0].final_w, runs[1].final_w):
+        assert a.tobytes() == b.tobytes()
