@@ -1440,10 +1440,22 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       }
       w.t_start = mk_event(true);
       w.t_end = mk_event(true);
+      // rows: x_local (gcn.hpp:127-132). Page-locked features of the padded width go up on a copy stream
+      // while the backward tiles are processed (after the forward tiles' DMAs, so the two do not share
+      // the link); otherwise synchronously after the tiles.
+      w.x = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));
+      const float* xsrc = p->features.data() + w.r0 * p->d0;
+      const bool x_async = p->d0 == g->ld[0] && w.rows > 0 && is_pinned_host(xsrc);
+      cudaStream_t xs = nullptr;
       // tiles
       int max_segments = 0;
       for (int d = 0; d < 2; ++d) {
         w.tiles[d].resize(world);
+        if (d == 1 && x_async) {
+          MG_CUDA(cudaStreamCreateWithFlags(&xs, cudaStreamNonBlocking));
+          MG_CUDA(cudaStreamSynchronize(cudaStreamLegacy));  // w.x's zero-fill precedes the copy stream's DMA
+          MG_CUDA(cudaMemcpyAsync(w.x, xsrc, sizeof(float) * w.rows * p->d0, cudaMemcpyHostToDevice, xs));
+        }
         for (int j = 0; j < world; ++j) {
           const bool tr = d == 1 && world == 1 && g_bwd_transpose.load();
           upload_tile(*g, w, p->tiles[d][w.rank][j], w.tiles[d][j], tr ? &w.tiles[0][0] : nullptr);
@@ -1452,9 +1464,12 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       }
       if (max_segments > 0) w.seg_scratch = dalloc_t<float>(*g, w, static_cast<size_t>(max_segments) * g->ld_max);
       sw.lap("tiles");
-      // rows: x_local, labels, mask (gcn.hpp:127-132)
-      w.x = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));
-      upload_padded(w.x, p->features.data() + w.r0 * p->d0, w.rows, p->d0, g->ld[0]);
+      if (xs) {
+        MG_CUDA(cudaStreamSynchronize(xs));
+        MG_CUDA(cudaStreamDestroy(xs));
+      } else {
+        upload_padded(w.x, xsrc, w.rows, p->d0, g->ld[0]);
+      }
       w.labels = dalloc_t<int>(*g, w, std::max<index_t>(1, w.rows));
       w.mask = dalloc_t<uint8_t>(*g, w, std::max<index_t>(1, w.rows));
       if (w.rows) {
