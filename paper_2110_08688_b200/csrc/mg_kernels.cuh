@@ -740,12 +740,19 @@ __global__ void __launch_bounds__(256) softmax_xent(float* __restrict__ logits, 
 }
 
 __global__ void finalize_stats(const double* __restrict__ partials, int nblocks, double* __restrict__ stats) {
+  // one warp: lane l sums blocks l, l + 32, ... in order, then a fixed xor tree — the same order every
+  // run (a serial sum over ~1200 partial pairs took ~80 us)
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < nblocks; i += 32) {
+    a += partials[2 * i];
+    b += partials[2 * i + 1];
+  }
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, off);
+    b += __shfl_xor_sync(0xffffffffu, b, off);
+  }
   if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double a = 0.0, b = 0.0;
-    for (int i = 0; i < nblocks; ++i) {
-      a += partials[2 * i];
-      b += partials[2 * i + 1];
-    }
     stats[0] = a;
     stats[1] = b;
   }
