@@ -363,13 +363,13 @@ int hub_class_max(int ld) {
   return k;
 }
 
-// Masked softmax-CE over `rows` logits rows of C classes: up to 48 classes a row takes half a warp (two
-// rows per warp, half the shuffle rounds per row), wider rows a whole warp.
+// Masked softmax-CE over `rows` logits rows of C classes: up to 48 classes a row takes a quarter warp (four
+// rows per warp, 3 shuffle rounds per reduction), wider rows a whole warp.
 static void launch_softmax_xent(int C, int blocks, cudaStream_t s, float* logits, int ld, int rows, const int* labels,
                                 const uint8_t* mask, float inv_denom, double* partials) {
-  if (C <= 16) k::softmax_xent<1, 16><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
-  else if (C <= 32) k::softmax_xent<2, 16><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
-  else if (C <= 48) k::softmax_xent<3, 16><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
+  if (C <= 16) k::softmax_xent<2, 8><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
+  else if (C <= 32) k::softmax_xent<4, 8><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
+  else if (C <= 48) k::softmax_xent<6, 8><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
   else if (C <= 64) k::softmax_xent<2><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
   else if (C <= 128) k::softmax_xent<4><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
   else if (C <= 192) k::softmax_xent<6><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);

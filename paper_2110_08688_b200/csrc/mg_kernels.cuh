@@ -628,7 +628,7 @@ template <int CPL, int LPR = 32>  // LPR lanes per row (32 or 16: two rows per w
 __global__ void __launch_bounds__(256) softmax_xent(float* __restrict__ logits, int ld, int rows, int C,
                                                     const int* __restrict__ labels, const uint8_t* __restrict__ mask,
                                                     float inv_denom, double* __restrict__ partials) {
-  static_assert(LPR == 32 || LPR == 16, "a row spans a warp or a half warp");
+  static_assert(LPR == 32 || LPR == 16 || LPR == 8, "a row spans a warp, a half or a quarter warp");
   constexpr int RPW = 32 / LPR;  // rows per warp
   __shared__ double s_loss[8], s_corr[8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -719,9 +719,11 @@ __global__ void __launch_bounds__(256) softmax_xent(float* __restrict__ logits, 
       }
     }
   }
-  if (RPW == 2) {  // the second row slot's leader (lane 16) hands its sums to lane 0
-    my_loss += __shfl_down_sync(0xffffffffu, my_loss, 16);
-    my_corr += __shfl_down_sync(0xffffffffu, my_corr, 16);
+  // the other row slots' leaders (lanes LPR, 2 LPR, ...) hand their sums to lane 0
+#pragma unroll
+  for (int off = LPR; off < 32; off <<= 1) {
+    my_loss += __shfl_down_sync(0xffffffffu, my_loss, off);
+    my_corr += __shfl_down_sync(0xffffffffu, my_corr, off);
   }
   if (lane == 0) {
     s_loss[warp] = my_loss;
