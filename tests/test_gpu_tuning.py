@@ -135,3 +135,18 @@ def test_backward_tile_transposed_on_device(mode):
     assert runs[0].epoch_loss == runs[1].epoch_loss
     for a, b in zip(runs[0].final_w, runs[1].final_w):
         assert a.tobytes() == b.tobytes()
+
+
+def test_block_cache_reuses_memory_across_groups():
+    """Destroyed groups' device blocks are cached and reused: creating and destroying groups of the same
+    shape repeatedly does not grow the device's used memory, and results do not change."""
+    ds = R.synth_graph(20000, 10.0, 0.7, 5, 32, 6)
+    cfg = R.GcnConfig([32, 64, 6], epochs=2, seed=3, permute=True)
+    first = R.train_run(ds, cfg, R.TrainOptions(devices=[0]))
+    torch.cuda.synchronize()
+    free0, total = torch.cuda.mem_get_info()
+    for _ in range(4):
+        again = R.train_run(ds, cfg, R.TrainOptions(devices=[0]))
+        assert again.epoch_loss == first.epoch_loss
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 64 << 20  # the repeats ran out of the cache
