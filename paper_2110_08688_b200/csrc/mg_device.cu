@@ -661,22 +661,16 @@ Stager& stager() {
 
 std::atomic<int> g_bwd_transpose{1};  // P = 1: the backward tile is built on the device ("bwd_transpose")
 
-// Edge-parallel (hub rows hold up to ~1e5 nonzeros): each thread takes a contiguous run of 64 records,
-// finds its first row by binary search and walks the rows forward. key = column << row_bits | row.
+// A warp per row (hub rows hold up to ~1e5 nonzeros; the lanes stride through the row, coalesced).
+// key = column << row_bits | row.
 __global__ void transpose_keys(const int* __restrict__ rp, const int2* __restrict__ edges, int rows, long nnz,
                                int row_bits, unsigned long long* __restrict__ keys, unsigned int* __restrict__ vals) {
-  constexpr long kRun = 64;
-  for (long b = (blockIdx.x * (long)blockDim.x + threadIdx.x) * kRun; b < nnz; b += (long)gridDim.x * blockDim.x * kRun) {
-    int lo = 0, hi = rows - 1;  // last row with rp[row] <= b
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (rp[mid] <= b) lo = mid;
-      else hi = mid - 1;
-    }
-    int r = lo;
-    const long end = min(nnz, b + kRun);
-    for (long e = b; e < end; ++e) {
-      while (rp[r + 1] <= e) ++r;
+  (void)nnz;
+  const int lane = threadIdx.x & 31;
+  const int warps = gridDim.x * (blockDim.x >> 5);
+  for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < rows; r += warps) {
+    const int e1 = rp[r + 1];
+    for (int e = rp[r] + lane; e < e1; e += 32) {
       const int2 rec = edges[e];
       keys[e] = (static_cast<unsigned long long>(rec.x & k::kColMask) << row_bits) | static_cast<unsigned>(r);
       vals[e] = static_cast<unsigned>(rec.y);
