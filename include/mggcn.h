@@ -91,7 +91,12 @@ int32_t mg_abi_version(void);
  *   "tn_chunk"   W-grad split-K chunk in rows (multiple of 256, default 4096)
  *   "fast_segment"  hub-row segment length of MG_SPMM_FAST (default 2048)
  *   "spmm_slab" / "spmm_narrow_group"  SpMM launch-geometry experiments (default 0 = off)
- *   "gemm_kernel"  tcgen05 GeMM variant: 1 = both split operands in smem, 2 = A split into TMEM (default). */
+ *   "spmm_async"   MG_SPMM_FAST gathers through the cp.async shared-memory ring (default 1)
+ *   "spmm_hub_bytes"  L2 footprint of the rows given evict_last priority (default 96 MiB; 0 = no hints)
+ *   "gemm_kernel"  tcgen05 GeMM variant: 1 = both split operands in smem, 2 = A split into TMEM,
+ *                  3 = 2 with 32-K stages and decoupled A / W rings for NN / NT (default)
+ *   "gemm3_wring"  v3 W-ring budget in bytes (default 96 KiB), "gemm3_cluster" 1 or 2 (W multicast)
+ *   "bwd_transpose"  one worker: build the backward tile on the device from the forward one (default 1) */
 mg_status mg_set_tuning(const char* key, int64_t value);
 
 /* ---------------------------------------------------------------- host datasets
