@@ -141,6 +141,94 @@ void run_loop(const char* name, long long* d_out, int nsm) {
   printf("%-26s issue %6.1f cyc/mma  complete %6.1f cyc/mma\n", name, h[0] / (groups * 12.0), h[1] / (groups * 12.0));
 }
 
+// kind::f16 (fp16 inputs, fp32 accumulate): D f32 (bit 4), A/B f16 (format 0 at bits 7, 10), K = 16.
+__host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
+  return (1u << 4) | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
+template <int N, bool TS>
+__global__ void __launch_bounds__(128, 1) probe_f16(long long* out, int groups) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar2;
+  __shared__ uint32_t tbase;
+  uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem) + 1023) & ~uintptr_t(1023));
+  for (int i = threadIdx.x; i < (2 * 256 * 128 + 128 * 128) / 16; i += blockDim.x) reinterpret_cast<int4*>(s)[i] = make_int4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar2)));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tmem = tbase;
+  if (threadIdx.x < 32) {
+    const uint32_t idesc = idesc_f16(128, N);
+    const uint32_t bs = smem_u32(s), as = bs + 2 * 256 * 128;
+    long long t0 = clock64();
+    for (int g = 0; g < groups; ++g) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {  // 4 K steps of 16 = one 64-K stage
+        const uint64_t b = desc_k128(bs + kk * 32), a = desc_k128(as + kk * 32);
+        const uint32_t at = tmem + 256 + kk * 8;
+#pragma unroll
+        for (int t = 0; t < 3; ++t) {
+          if (TS)
+            asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, 1, 0;\n"
+                         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n"
+                         ::"r"(tmem), "r"(at), "l"(b), "r"(idesc));
+          else
+            asm volatile("{\n.reg .pred p, e;\nelect.sync _|e, 0xffffffff;\nsetp.ne.b32 p, 1, 0;\n"
+                         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
+                         ::"r"(tmem), "l"(a), "l"(b), "r"(idesc));
+        }
+      }
+      __syncwarp();
+    }
+    long long t1 = clock64();
+    if ((threadIdx.x & 31) == 0) {
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&bar2)) : "memory");
+      asm volatile("{\n.reg .pred p;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n@!p bra W_%=;\n}\n"
+                   ::"r"(smem_u32(&bar2)) : "memory");
+    }
+    __syncwarp();
+    long long t2 = clock64();
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      out[0] = t1 - t0;
+      out[1] = t2 - t0;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+template <int N, bool TS>
+void run_f16(const char* name, long long* d_out, int nsm) {
+  const int groups = 2000;
+  const size_t smem = 2 * 256 * 128 + 128 * 128 + 1024;
+  cudaFuncSetAttribute(probe_f16<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  probe_f16<N, TS><<<nsm, 128, smem>>>(d_out, 10);
+  cudaDeviceSynchronize();
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  probe_f16<N, TS><<<nsm, 128, smem>>>(d_out, groups);
+  cudaEventRecord(b);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(e)); return; }
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  long long h[2];
+  cudaMemcpy(h, d_out, sizeof(h), cudaMemcpyDeviceToHost);
+  const double mmas = groups * 12.0;
+  printf("%-26s issue %6.1f cyc/mma  complete %6.1f cyc/mma  %.0f f16 TFLOP/s (K = 16 per MMA)\n", name, h[0] / mmas,
+         h[1] / mmas, 2.0 * 128 * N * 16 * mmas * nsm / (ms * 1e-3) / 1e12);
+}
+
 template <int N, bool TS, int NACC, int CONT, int ORD>
 __global__ void __launch_bounds__(384, 1) probe(long long* out, int groups, const float* gsrc) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -306,10 +394,10 @@ int main() {
   cudaMalloc(&src, 4096ull * 4096 * 4);  // 64 MB: an L2-sized stream
   cudaMemset(src, 0, 4096ull * 4096 * 4);
   g_src = src;
-  run_loop<128, 1, 0>("loop N=128 elect", d, nsm);
-  run_loop<128, 1, 1>("loop N=128 +fence", d, nsm);
-  run_loop<128, 1, 2>("loop N=128 +wait+fence", d, nsm);
-  run_loop<48, 1, 0>("loop N=48 elect", d, nsm);
-  run_loop<48, 1, 2>("loop N=48 +wait+fence", d, nsm);
+  run_loop<128, 1, 0>("tf32 loop N=128 elect", d, nsm);
+  run_f16<128, false>("f16 ss N=128", d, nsm);
+  run_f16<128, true>("f16 ts N=128", d, nsm);
+  run_f16<256, true>("f16 ts N=256", d, nsm);
+  run_f16<48, true>("f16 ts N=48", d, nsm);
   return 0;
 }
