@@ -364,14 +364,14 @@ int hub_class_max(int ld) {
 }
 
 // Masked softmax-CE over `rows` logits rows of C classes: up to 48 classes a row takes a quarter warp (four
-// rows per warp, 3 shuffle rounds per reduction), wider rows a whole warp.
+// rows per warp, 3 shuffle rounds per reduction), up to 176 (papers: 172) half a warp, wider rows a warp.
 static void launch_softmax_xent(int C, int blocks, cudaStream_t s, float* logits, int ld, int rows, const int* labels,
                                 const uint8_t* mask, float inv_denom, double* partials) {
   if (C <= 16) k::softmax_xent<2, 8><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
   else if (C <= 32) k::softmax_xent<4, 8><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
   else if (C <= 48) k::softmax_xent<6, 8><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
-  else if (C <= 64) k::softmax_xent<2><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
-  else if (C <= 128) k::softmax_xent<4><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
+  else if (C <= 96) k::softmax_xent<6, 16><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
+  else if (C <= 176) k::softmax_xent<11, 16><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
   else if (C <= 192) k::softmax_xent<6><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
   else k::softmax_xent<k::kLossCpl><<<blocks, 256, 0, s>>>(logits, ld, rows, C, labels, mask, inv_denom, partials);
   MG_LAUNCHED();
