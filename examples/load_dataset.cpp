@@ -13,7 +13,7 @@ int main(int argc, char** argv) {
     return 2;
   }
   try {
-    const R::Dataset<float> ds = R::load_dataset(argv[1], argv[2], argv[3], argc > 4 ? argv[4] : "");
+    const R::Dataset<float> ds = R::load_dataset<float>(argv[1], argv[2], argv[3], argc > 4 ? argv[4] : "");
     long train = 0;
     for (auto m : ds.train_mask) train += m;
     double fsum = 0;

@@ -15,7 +15,7 @@ int main(int argc, char** argv) {
   const int epochs = argc > 2 ? std::atoi(argv[2]) : 5;
   const int workers = argc > 3 ? std::atoi(argv[3]) : 1;
   try {
-    const R::Dataset<float> ds = R::synth_graph(n, 50.6, 0.7, 1, 100, 47);
+    const R::Dataset<float> ds = R::synth_graph<float>(n, 50.6, 0.7, 1, 100, 47);
     R::GcnConfig cfg;
     cfg.layer_dims = {100, 256, 256, 47};
     cfg.epochs = epochs;
@@ -32,8 +32,8 @@ int main(int argc, char** argv) {
     R::audit_timeline(art.timeline);  // the CUDA-event timeline obeys the reference's audit rules
     R::export_timeline("/tmp/mggcn_products.timeline.json", art.timeline);
     std::printf("timeline: %zu events\n", art.timeline.size());
-    R::write_checkpoint("/tmp/mggcn_products.ckpt", art.final_w);
-    const auto back = R::read_checkpoint("/tmp/mggcn_products.ckpt");
+    R::write_checkpoint("/tmp/mggcn_products.ckpt", art.final_w, cfg);
+    const auto back = R::read_checkpoint<float>("/tmp/mggcn_products.ckpt");
     return back.size() == art.final_w.size() ? 0 : 1;
   } catch (const std::exception& e) {
     std::fprintf(stderr, "error: %s\n", e.what());

@@ -145,12 +145,41 @@ mg_status mg_dense_view(const mg_dense* d, int64_t* rows, int64_t* cols, const f
 void mg_dense_free(mg_dense* d);
 /* write_dense<float> (dense.hpp:293-307): "MGDM", u64 rows, u64 cols, u8 4, payload. */
 mg_status mg_dense_write(const char* path, int64_t rows, int64_t cols, const float* data);
+/* from_coo<float> (sparse.hpp:59-90): n x n CSR from `count` edges (src[e] -> dst[e], weight[e]); rows
+ * sorted, duplicate (src, dst) weights summed (in edge order). ValueError on an out-of-range endpoint. */
+mg_status mg_graph_from_coo(int64_t n, int64_t count, const int64_t* src, const int64_t* dst, const float* weight,
+                            mg_graph** out);
+/* add_self_loops<float> (dataset.hpp:60-73): a unit (u, u) entry in every row that lacks one, rebuilt like
+ * from_coo (sparse.hpp:59-90). The result is an owned graph (mg_graph_view / mg_graph_free). */
+mg_status mg_graph_add_self_loops(const mg_csr* a, mg_graph** out);
 /* load_labels (dataset.hpp:218-234). *count = number of labels; dst (capacity entries) may be NULL to
  * query the count first. */
 mg_status mg_labels_load(const char* path, int32_t* dst, int64_t capacity, int64_t* count);
 /* load_masks (dataset.hpp:237-262) for n vertices; each non-NULL output gets n bytes when its key is
  * present. *present: bit 0 train, bit 1 val, bit 2 test. */
 mg_status mg_masks_load(const char* path, int64_t n, uint8_t* train, uint8_t* val, uint8_t* test, int32_t* present);
+
+/* ---------------------------------------------------------------- checkpoints and JSON documents
+ * write_checkpoint / read_checkpoint<float> (inc/driver.hpp:255-299): every W as an MGDM block ("MGDM",
+ * u64 rows, u64 cols, u8 width 4, payload) back to back, plus the sidecar <path>.json holding
+ * config_to_json(cfg) (driver.hpp:59-71) as nlohmann::json::dump(1) writes it (byte-identical).
+ * Errors: MG_IO_ERROR "cannot open <path> ..." / "short write to <path>"; MG_PARSE_ERROR on a bad magic,
+ * a dtype width other than 4 or a truncated block. */
+typedef struct mg_checkpoint mg_checkpoint;
+mg_status mg_checkpoint_write(const char* path, int32_t count, const int64_t* rows, const int64_t* cols,
+                              const float* const* data, const mg_config* cfg);
+mg_status mg_checkpoint_read(const char* path, mg_checkpoint** out);
+int32_t mg_checkpoint_count(const mg_checkpoint* ck);
+mg_status mg_checkpoint_view(const mg_checkpoint* ck, int32_t i, int64_t* rows, int64_t* cols, const float** data);
+void mg_checkpoint_free(mg_checkpoint* ck);
+/* config_to_json(cfg).dump(indent) (driver.hpp:59-71; indent < 0 = compact) and BreakdownReport::to_json()
+ * .dump(indent) / text_table() (inc/breakdown.hpp:27-58) over runtime_breakdown totals
+ * {spmm, gemm, activation, loss, adam, comm}. *length = text length; buf (capacity bytes, may be NULL)
+ * receives the NUL-terminated text, truncated to capacity - 1. */
+mg_status mg_config_to_json(const mg_config* cfg, int32_t indent, char* buf, int64_t capacity, int64_t* length);
+mg_status mg_breakdown_to_json(const double totals_us[6], int32_t indent, char* buf, int64_t capacity,
+                               int64_t* length);
+mg_status mg_breakdown_text(const double totals_us[6], char* buf, int64_t capacity, int64_t* length);
 
 /* ---------------------------------------------------------------- partitioner
  * rowgcn::prepare_data (inc/driver.hpp:87-117): random_permutation (partition.hpp:69-79), permute

@@ -10,17 +10,21 @@
 //   GcnConfig                 inc/gcn.hpp:14-36           + gemm_mode / spmm_mode
 //   parse_config / materialize_config  driver.hpp:24-57   same (generic over the JSON type)
 //   CsrMatrix / DenseMatrix / Dataset   sparse.hpp / dense.hpp / dataset.hpp
-//   synth_graph<float>        inc/dataset.hpp:287-334     bit-identical output
-//   load_dataset / load_graph / load_features / load_labels / load_masks / read_dense / write_dense
-//                             inc/dataset.hpp:84-280, dense.hpp:290-335
+//   synth_graph<S>            inc/dataset.hpp:287-334     bit-identical output
+//   add_self_loops<S>         inc/dataset.hpp:60-73
+//   load_dataset<S> / load_graph<S> / load_features<S> / load_labels / load_masks / read_dense<S> /
+//   write_dense<S>            inc/dataset.hpp:84-280, dense.hpp:290-335
 //   prepare_data / PreparedData  driver.hpp:75-117        bit-identical tiles
-//   TrainOptions / TrainArtifacts / train_run  driver.hpp:119-206
-//   GradArtifacts / grad_run  driver.hpp:209-251
-//   write_checkpoint / read_checkpoint  driver.hpp:255-299  (MGDM blocks + JSON sidecar)
+//   GroupOptions / TrainOptions / TrainArtifacts / train_run<S>  driver.hpp:119-206, collectives.hpp:41-44
+//   GradArtifacts / grad_run<S>  driver.hpp:209-251
+//   config_to_json            driver.hpp:59-71            byte-identical dump()
+//   write_checkpoint / read_checkpoint<S>  driver.hpp:255-299  (MGDM blocks + <path>.json sidecar)
+//   runtime_breakdown / BreakdownReport / export_timeline / audits  breakdown.hpp, timeline.hpp
 //
 // The device work runs on the GPUs of this process (one GcnWorker per rank, two CUDA streams each,
-// NCCL or the in-process transport between them). Only float is provided: train_run<double> stays
-// with the CPU reference.
+// NCCL or the in-process transport between them). The templates are instantiable for S = float only:
+// S = double is rejected at compile time (the B200 step trains in fp32; train_run<double> stays with the
+// CPU reference), so a reference caller compiles unchanged for float.
 #pragma once
 
 #include <cstdint>
@@ -29,8 +33,10 @@
 #include <fstream>
 #include <functional>
 #include <memory>
+#include <random>
 #include <stdexcept>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "mggcn.h"
@@ -51,6 +57,14 @@ struct IoError : std::runtime_error { using std::runtime_error::runtime_error; }
 struct CudaError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct NcclError : std::runtime_error { using std::runtime_error::runtime_error; };
 
+// The device path computes in fp32: every rowgcn template here is instantiable for S = float only.
+template <class S>
+constexpr void require_float() {
+  static_assert(std::is_same<S, float>::value,
+                "mggcn::rowgcn: the B200 training step runs in float (fp32 with 3xTF32 GeMMs); "
+                "instantiate with S = float (rowgcn<double> stays with the CPU reference)");
+}
+
 inline void check(mg_status s) {
   if (s == MG_OK) return;
   const std::string m = mg_last_error();
@@ -68,7 +82,29 @@ inline void check(mg_status s) {
   }
 }
 
+// ---------------------------------------------------------------- Rng (inc/rng.hpp)
+// std::mt19937_64 (standard-mandated stream) with modulo bounded draws and 53-bit uniforms: the same
+// numbers as the reference's Rng and as the library's generator / Glorot init.
+class Rng {
+ public:
+  explicit Rng(std::uint64_t seed) : gen_(seed) {}
+  std::uint64_t next() { return gen_(); }
+  std::uint64_t below(std::uint64_t n) { return gen_() % n; }
+  double uniform() { return static_cast<double>(gen_() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+
+ private:
+  std::mt19937_64 gen_;
+};
+
 // ---------------------------------------------------------------- containers
+template <class S>
+struct CooEdge {  // inc/sparse.hpp:16-21
+  index_t src = 0;
+  index_t dst = 0;
+  S weight = S(1);
+};
+
 template <class S>
 struct CsrMatrix {  // inc/sparse.hpp:25-55
   index_t rows = 0, cols = 0;
@@ -105,6 +141,11 @@ struct Dataset {  // inc/dataset.hpp:19-56
   std::vector<std::uint8_t> train_mask, val_mask, test_mask;
   std::string name;
   index_t n() const { return graph.rows; }
+  void validate() const;  // Dataset::validate (inc/dataset.hpp:30-44), defined below
+  std::vector<std::uint8_t> effective_mask() const {  // inc/dataset.hpp:46-49
+    if (!train_mask.empty()) return train_mask;
+    return std::vector<std::uint8_t>(static_cast<size_t>(n()), 1);
+  }
   int num_classes() const {
     std::int32_t c = 0;
     for (auto l : labels) c = l > c ? l : c;
@@ -239,10 +280,7 @@ inline Dataset<float> from_handle(mg_dataset* p, const std::string& name) {
   if (te) ds.test_mask.assign(te, te + n);
   return ds;
 }
-inline CsrMatrix<float> graph_from(int32_t format, const std::string& path) {
-  mg_graph* h = nullptr;
-  check(mg_graph_load(path.c_str(), format, &h));
-  std::unique_ptr<mg_graph, void (*)(mg_graph*)> guard(h, mg_graph_free);
+inline CsrMatrix<float> graph_view(const mg_graph* h) {
   mg_csr g;
   check(mg_graph_view(h, &g));
   CsrMatrix<float> m;
@@ -252,6 +290,12 @@ inline CsrMatrix<float> graph_from(int32_t format, const std::string& path) {
   m.col_idx.assign(g.col_idx, g.col_idx + g.row_ptr[g.rows]);
   m.values.assign(g.values, g.values + g.row_ptr[g.rows]);
   return m;
+}
+inline CsrMatrix<float> graph_from(int32_t format, const std::string& path) {
+  mg_graph* h = nullptr;
+  check(mg_graph_load(path.c_str(), format, &h));
+  std::unique_ptr<mg_graph, void (*)(mg_graph*)> guard(h, mg_graph_free);
+  return graph_view(h);
 }
 inline DenseMatrix<float> dense_from(mg_status (*fn)(const char*, mg_dense**), const std::string& path) {
   mg_dense* h = nullptr;
@@ -266,22 +310,81 @@ inline DenseMatrix<float> dense_from(mg_status (*fn)(const char*, mg_dense**), c
 }
 }  // namespace detail
 
-// rowgcn::synth_graph<float> (inc/dataset.hpp:287-334), bit-identical.
-inline Dataset<float> synth_graph(index_t n, double avg_degree, double exponent, std::uint64_t seed,
-                                  index_t feature_dim = 16, int classes = 4) {
+// rowgcn::synth_graph<S> (inc/dataset.hpp:287-334), bit-identical.
+template <class S>
+Dataset<S> synth_graph(index_t n, double avg_degree, double exponent, std::uint64_t seed, index_t feature_dim = 16,
+                       int classes = 4) {
+  require_float<S>();
   detail::DatasetHandle h;
   check(mg_dataset_synth(n, avg_degree, exponent, seed, feature_dim, classes, &h.p));
   return detail::from_handle(h.p, "synth-n" + std::to_string(n) + "-d" + std::to_string(avg_degree));
 }
 
+template <class S>
+inline void Dataset<S>::validate() const {
+  require_float<S>();
+  auto h = detail::to_handle(*this);
+  check(mg_dataset_validate(h.p));
+}
+
+// from_coo (inc/sparse.hpp:59-90).
+template <class S>
+CsrMatrix<S> from_coo(std::vector<CooEdge<S>> edges, index_t n) {
+  require_float<S>();
+  std::vector<std::int64_t> src(edges.size()), dst(edges.size());
+  std::vector<float> w(edges.size());
+  for (size_t e = 0; e < edges.size(); ++e) {
+    src[e] = edges[e].src;
+    dst[e] = edges[e].dst;
+    w[e] = edges[e].weight;
+  }
+  mg_graph* g = nullptr;
+  check(mg_graph_from_coo(n, static_cast<std::int64_t>(edges.size()), src.data(), dst.data(), w.data(), &g));
+  std::unique_ptr<mg_graph, void (*)(mg_graph*)> guard(g, mg_graph_free);
+  return detail::graph_view(g);
+}
+
+// add_self_loops (inc/dataset.hpp:60-73).
+template <class S>
+CsrMatrix<S> add_self_loops(const CsrMatrix<S>& a) {
+  require_float<S>();
+  const mg_csr c{a.rows, a.cols, a.row_ptr.data(), a.col_idx.data(), a.values.data()};
+  mg_graph* g = nullptr;
+  check(mg_graph_add_self_loops(&c, &g));
+  std::unique_ptr<mg_graph, void (*)(mg_graph*)> guard(g, mg_graph_free);
+  return detail::graph_view(g);
+}
+
 // On-disk formats (inc/dataset.hpp:84-280, inc/dense.hpp:290-335): native multi-threaded loaders,
 // same syntax, messages and exception types as the reference.
-inline CsrMatrix<float> load_matrix_market(const std::string& path) { return detail::graph_from(1, path); }
-inline CsrMatrix<float> load_edge_list(const std::string& path) { return detail::graph_from(2, path); }
-inline CsrMatrix<float> load_graph(const std::string& path) { return detail::graph_from(0, path); }
-inline DenseMatrix<float> load_features(const std::string& path) { return detail::dense_from(mg_dense_load, path); }
-inline DenseMatrix<float> read_dense(const std::string& path) { return detail::dense_from(mg_dense_read, path); }
-inline void write_dense(const std::string& path, const DenseMatrix<float>& m) {
+template <class S>
+CsrMatrix<S> load_matrix_market(const std::string& path) {
+  require_float<S>();
+  return detail::graph_from(1, path);
+}
+template <class S>
+CsrMatrix<S> load_edge_list(const std::string& path) {
+  require_float<S>();
+  return detail::graph_from(2, path);
+}
+template <class S>
+CsrMatrix<S> load_graph(const std::string& path) {
+  require_float<S>();
+  return detail::graph_from(0, path);
+}
+template <class S>
+DenseMatrix<S> load_features(const std::string& path) {
+  require_float<S>();
+  return detail::dense_from(mg_dense_load, path);
+}
+template <class S>
+DenseMatrix<S> read_dense(const std::string& path) {
+  require_float<S>();
+  return detail::dense_from(mg_dense_read, path);
+}
+template <class S>
+void write_dense(const std::string& path, const DenseMatrix<S>& m) {
+  require_float<S>();
   check(mg_dense_write(path.c_str(), m.rows(), m.cols(), m.data()));
 }
 inline std::vector<std::int32_t> load_labels(const std::string& path) {
@@ -300,8 +403,10 @@ inline void load_masks(const std::string& path, index_t n, std::vector<std::uint
   if (present & 2) val = std::move(b);
   if (present & 4) test = std::move(c);
 }
-inline Dataset<float> load_dataset(const std::string& graph_path, const std::string& features_path,
-                                   const std::string& labels_path, const std::string& masks_path = "") {
+template <class S>
+Dataset<S> load_dataset(const std::string& graph_path, const std::string& features_path,
+                        const std::string& labels_path, const std::string& masks_path = "") {
+  require_float<S>();
   detail::DatasetHandle h;
   check(mg_dataset_load(graph_path.c_str(), features_path.c_str(), labels_path.c_str(),
                         masks_path.empty() ? nullptr : masks_path.c_str(), &h.p));
@@ -341,8 +446,15 @@ inline PreparedData prepare_data(const Dataset<float>& ds, const GcnConfig& cfg,
 }
 
 // ---------------------------------------------------------------- driver (inc/driver.hpp:119-251)
+// rowgcn::GroupOptions (inc/collectives.hpp:41-44). Accepted for source compatibility and ignored: the
+// link delay is an injected cost of the reference's simulated links; here the links are NVLink / NCCL.
+struct GroupOptions {
+  double link_delay_ns_per_byte = 0.0;
+};
+
 struct TrainOptions {
   int workers = 1;
+  GroupOptions group;  // ignored (see GroupOptions)
   bool collect_logits = false;
   std::function<void(int, double, double, double)> on_epoch;  // (epoch, loss, acc, wall_us) on rank 0
   std::vector<int> devices;  // CUDA device per rank; default rank % #devices
@@ -404,6 +516,71 @@ inline void audit_staged_run(const std::vector<TimelineEvent>& ev, int world, bo
   check(mg_timeline_audit_staged(c.data(), static_cast<std::int64_t>(c.size()), world, overlapped ? 1 : 0));
 }
 
+// A JSON document the reference returns as nlohmann::json (config_to_json, BreakdownReport::to_json):
+// dump(indent) gives the same text nlohmann::json::dump(indent) does (mggcn.h).
+class JsonText {
+ public:
+  explicit JsonText(std::function<mg_status(int, char*, std::int64_t, std::int64_t*)> f) : f_(std::move(f)) {}
+  std::string dump(int indent = -1) const {
+    std::int64_t n = 0;
+    check(f_(indent, nullptr, 0, &n));
+    std::string s(static_cast<size_t>(n) + 1, '\0');
+    check(f_(indent, &s[0], n + 1, &n));
+    s.resize(static_cast<size_t>(n));
+    return s;
+  }
+
+ private:
+  std::function<mg_status(int, char*, std::int64_t, std::int64_t*)> f_;
+};
+
+// config_to_json (inc/driver.hpp:59-71).
+inline JsonText config_to_json(const GcnConfig& cfg) {
+  return JsonText([cfg](int indent, char* b, std::int64_t cap, std::int64_t* n) {
+    const mg_config c = cfg.c();
+    return mg_config_to_json(&c, indent, b, cap, n);
+  });
+}
+
+// BreakdownReport / runtime_breakdown (inc/breakdown.hpp:17-82) over the CUDA-event timeline.
+struct BreakdownReport {
+  double spmm_us = 0, gemm_us = 0, activation_us = 0, loss_us = 0, adam_us = 0, comm_us = 0;
+  double total_us() const { return spmm_us + gemm_us + activation_us + loss_us + adam_us + comm_us; }
+  double frac(double v) const {
+    const double t = total_us();
+    return t > 0 ? v / t : 0.0;
+  }
+  JsonText to_json() const {
+    const std::vector<double> t{spmm_us, gemm_us, activation_us, loss_us, adam_us, comm_us};
+    return JsonText([t](int indent, char* b, std::int64_t cap, std::int64_t* n) {
+      return mg_breakdown_to_json(t.data(), indent, b, cap, n);
+    });
+  }
+  std::string text_table() const {
+    const double t[6] = {spmm_us, gemm_us, activation_us, loss_us, adam_us, comm_us};
+    std::int64_t n = 0;
+    check(mg_breakdown_text(t, nullptr, 0, &n));
+    std::string s(static_cast<size_t>(n) + 1, '\0');
+    check(mg_breakdown_text(t, &s[0], n + 1, &n));
+    s.resize(static_cast<size_t>(n));
+    return s;
+  }
+};
+
+inline BreakdownReport runtime_breakdown(const std::vector<TimelineEvent>& ev) {
+  const auto c = detail::to_c(ev);
+  double t[6] = {0, 0, 0, 0, 0, 0};
+  check(mg_timeline_breakdown(c.data(), static_cast<std::int64_t>(c.size()), t));
+  BreakdownReport r;
+  r.spmm_us = t[0];
+  r.gemm_us = t[1];
+  r.activation_us = t[2];
+  r.loss_us = t[3];
+  r.adam_us = t[4];
+  r.comm_us = t[5];
+  return r;
+}
+
 template <class S>
 struct TrainArtifacts {
   std::vector<double> epoch_loss, epoch_acc, epoch_wall_us;
@@ -446,7 +623,9 @@ inline DenseMatrix<float> read(mg_group* g, int rank, int which, int layer, inde
 }
 }  // namespace detail
 
-inline TrainArtifacts<float> train_run(const Dataset<float>& ds, const GcnConfig& cfg, const TrainOptions& opts) {
+template <class S>
+TrainArtifacts<S> train_run(const Dataset<S>& ds, const GcnConfig& cfg, const TrainOptions& opts) {
+  require_float<S>();
   cfg.validate();
   if (cfg.layer_dims.front() != ds.features.cols())
     throw ConfigError("config: layer_dims[0]=" + std::to_string(cfg.layer_dims.front()) +
@@ -488,7 +667,9 @@ inline TrainArtifacts<float> train_run(const Dataset<float>& ds, const GcnConfig
   return art;
 }
 
-inline GradArtifacts<float> grad_run(const Dataset<float>& ds, const GcnConfig& cfg, int workers) {
+template <class S>
+GradArtifacts<S> grad_run(const Dataset<S>& ds, const GcnConfig& cfg, int workers) {
+  require_float<S>();
   cfg.validate();
   const PreparedData prep = prepare_data(ds, cfg, workers);
   auto g = detail::make_group(cfg, prep, workers, {}, MG_TRANSPORT_AUTO);
@@ -514,41 +695,37 @@ inline GradArtifacts<float> grad_run(const Dataset<float>& ds, const GcnConfig& 
   return art;
 }
 
-// inc/driver.hpp:255-299: every W as an MGDM block ("MGDM", u64 rows, u64 cols, u8 4, payload).
-inline void write_checkpoint(const std::string& path, const std::vector<DenseMatrix<float>>& ws) {
-  std::ofstream f(path, std::ios::binary);
-  if (!f) throw IoError("cannot open " + path + " for writing");
+// write_checkpoint (inc/driver.hpp:255-274): every W as an MGDM block back to back, plus <path>.json with
+// config_to_json(cfg); byte-identical files (mggcn.h).
+template <class S>
+void write_checkpoint(const std::string& path, const std::vector<DenseMatrix<S>>& ws, const GcnConfig& cfg) {
+  require_float<S>();
+  std::vector<std::int64_t> rows, cols;
+  std::vector<const float*> data;
   for (const auto& w : ws) {
-    f.write("MGDM", 4);
-    const std::uint64_t r = static_cast<std::uint64_t>(w.rows()), c = static_cast<std::uint64_t>(w.cols());
-    const std::uint8_t width = 4;
-    f.write(reinterpret_cast<const char*>(&r), 8);
-    f.write(reinterpret_cast<const char*>(&c), 8);
-    f.write(reinterpret_cast<const char*>(&width), 1);
-    f.write(reinterpret_cast<const char*>(w.data()), static_cast<std::streamsize>(4 * w.size()));
+    rows.push_back(w.rows());
+    cols.push_back(w.cols());
+    data.push_back(w.data());
   }
-  if (!f) throw IoError("short write to " + path);
+  const mg_config c = cfg.c();
+  check(mg_checkpoint_write(path.c_str(), static_cast<std::int32_t>(ws.size()), rows.data(), cols.data(), data.data(),
+                            &c));
 }
 
-inline std::vector<DenseMatrix<float>> read_checkpoint(const std::string& path) {
-  std::ifstream f(path, std::ios::binary);
-  if (!f) throw IoError("cannot open " + path);
-  std::vector<DenseMatrix<float>> ws;
-  while (true) {
-    char magic[4];
-    f.read(magic, 4);
-    if (!f) break;
-    if (std::memcmp(magic, "MGDM", 4) != 0) throw ParseError(path + ": bad checkpoint block magic");
-    std::uint64_t r = 0, c = 0;
-    std::uint8_t width = 0;
-    f.read(reinterpret_cast<char*>(&r), 8);
-    f.read(reinterpret_cast<char*>(&c), 8);
-    f.read(reinterpret_cast<char*>(&width), 1);
-    if (!f || width != 4)
-      throw ParseError(path + ": checkpoint dtype width " + std::to_string(width) + " does not match run dtype 4");
-    DenseMatrix<float> w(static_cast<index_t>(r), static_cast<index_t>(c));
-    f.read(reinterpret_cast<char*>(w.data()), static_cast<std::streamsize>(4 * w.size()));
-    if (!f) throw ParseError(path + ": truncated checkpoint block");
+// read_checkpoint<S> (inc/driver.hpp:276-299).
+template <class S>
+std::vector<DenseMatrix<S>> read_checkpoint(const std::string& path) {
+  require_float<S>();
+  mg_checkpoint* ck = nullptr;
+  check(mg_checkpoint_read(path.c_str(), &ck));
+  std::unique_ptr<mg_checkpoint, void (*)(mg_checkpoint*)> guard(ck, mg_checkpoint_free);
+  std::vector<DenseMatrix<S>> ws;
+  for (std::int32_t i = 0; i < mg_checkpoint_count(ck); ++i) {
+    std::int64_t r = 0, c = 0;
+    const float* d = nullptr;
+    check(mg_checkpoint_view(ck, i, &r, &c, &d));
+    DenseMatrix<S> w(r, c);
+    if (r * c > 0) std::memcpy(w.data(), d, sizeof(float) * static_cast<size_t>(r * c));
     ws.push_back(std::move(w));
   }
   return ws;

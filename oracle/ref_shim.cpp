@@ -406,6 +406,49 @@ MODEL_FUNCS(double, f64)
 
 uint64_t ref_fnv1a(const void* data, uint64_t len, uint64_t h) { return fnv1a(data, len, h); }
 
+// write_checkpoint<float> (driver.hpp:255-274) and config_to_json(cfg).dump(indent) (driver.hpp:59-71).
+int ref_write_checkpoint_f32(const char* path, int32_t count, const int64_t* rows, const int64_t* cols,
+                             const float* const* data, const RefCfg* c) {
+  return guarded([&] {
+    std::vector<DenseMatrix<float>> ws;
+    for (int32_t i = 0; i < count; ++i) {
+      DenseMatrix<float> w(rows[i], cols[i]);
+      std::memcpy(w.data(), data[i], sizeof(float) * static_cast<size_t>(rows[i] * cols[i]));
+      ws.push_back(std::move(w));
+    }
+    write_checkpoint(path, ws, to_cfg(c));
+  });
+}
+int ref_config_json(const RefCfg* c, int32_t indent, char* buf, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    const std::string s = config_to_json(to_cfg(c)).dump(indent);
+    *len = static_cast<int64_t>(s.size());
+    if (buf && cap > 0) {
+      const size_t n = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+int ref_breakdown_json(const double* t, int32_t indent, char* buf, int64_t cap, int64_t* len) {
+  return guarded([&] {
+    BreakdownReport r;
+    r.spmm_us = t[0];
+    r.gemm_us = t[1];
+    r.activation_us = t[2];
+    r.loss_us = t[3];
+    r.adam_us = t[4];
+    r.comm_us = t[5];
+    const std::string s = r.to_json().dump(indent) + "\n" + r.text_table();
+    *len = static_cast<int64_t>(s.size());
+    if (buf && cap > 0) {
+      const size_t n = std::min<size_t>(s.size(), static_cast<size_t>(cap - 1));
+      std::memcpy(buf, s.data(), n);
+      buf[n] = 0;
+    }
+  });
+}
+
 // ---------------------------------------------------------------- on-disk formats (dataset.hpp:84-280)
 // Datasets returned here may be partial (graph only / features only); ref_ds_info / ref_ds_export and
 // ref_ds_feat_shape read them.

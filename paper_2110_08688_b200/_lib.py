@@ -53,6 +53,16 @@ SIGNATURES = [
     ("mg_dense_view", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("mg_dense_free", None, [C.c_void_p]),
     ("mg_dense_write", C.c_int, [C.c_char_p, C.c_int64, C.c_int64, C.c_void_p]),
+    ("mg_graph_from_coo", C.c_int, [C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("mg_graph_add_self_loops", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("mg_checkpoint_write", C.c_int, [C.c_char_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("mg_checkpoint_read", C.c_int, [C.c_char_p, C.c_void_p]),
+    ("mg_checkpoint_count", C.c_int32, [C.c_void_p]),
+    ("mg_checkpoint_view", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("mg_checkpoint_free", None, [C.c_void_p]),
+    ("mg_config_to_json", C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_int64, C.c_void_p]),
+    ("mg_breakdown_to_json", C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_int64, C.c_void_p]),
+    ("mg_breakdown_text", C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, C.c_void_p]),
     ("mg_labels_load", C.c_int, [C.c_char_p, C.c_void_p, C.c_int64, C.c_void_p]),
     ("mg_masks_load", C.c_int, [C.c_char_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("mg_prepare", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),

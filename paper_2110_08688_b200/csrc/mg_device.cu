@@ -397,13 +397,14 @@ static void launch_fast_async_v(const FastLaunch& t, const float* h, float* out,
                                 int acc, int relu, int hub_max, cudaStream_t s) {
   constexpr int kThreads = 128;
   constexpr size_t smem = sizeof(float4) * kThreads * D * E * CPL;
-  static int blocks_per_sm = 0;
-  if (!blocks_per_sm) {
+  static std::atomic<unsigned long long> attr{0};
+  static std::atomic<int> blocks_per_sm{1};
+  if (first_on_device(attr, cur_device())) {
     MG_CUDA(cudaFuncSetAttribute(k::spmm_fast_async<G, CPL, E, D, HINT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k::spmm_fast_async<G, CPL, E, D, HINT>,
-                                                          kThreads, smem));
-    blocks_per_sm = std::max(1, blocks_per_sm);
+    int b = 0;
+    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k::spmm_fast_async<G, CPL, E, D, HINT>, kThreads, smem));
+    blocks_per_sm = std::max(1, b);
   }
   const int gpb = kThreads / G;
   const int blocks = std::min(ceil_div(t.n_items, gpb), num_sms() * blocks_per_sm);
@@ -474,12 +475,10 @@ static int spmm_fast(const FastLaunch& t, const float* h, float* out, index_t ld
 
 static int spmm_heavy(const SpmmLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, cudaStream_t s) {
   if (t.n_heavy <= 0) return 0;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr, cur_device()))
     MG_CUDA(cudaFuncSetAttribute(k::spmm_exact_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(k::kHeavySmem)));
-    attr = true;
-  }
   const int nslab = ceil_div(ld, k::kHeavySlab);
   k::spmm_exact_heavy<<<t.n_heavy * nslab, k::kHeavyThreads, k::kHeavySmem, s>>>(t.row_ptr, t.edges, t.heavy, nslab, h, out,
                                                                    static_cast<int>(ld), acc, relu);

@@ -29,6 +29,8 @@ struct ProtocolError : Error { explicit ProtocolError(const std::string& m) : Er
 struct ConfigError : Error { explicit ConfigError(const std::string& m) : Error(MG_CONFIG_ERROR, m) {} };
 struct CudaError : Error { explicit CudaError(const std::string& m) : Error(MG_CUDA_ERROR, m) {} };
 struct NcclError : Error { explicit NcclError(const std::string& m) : Error(MG_NCCL_ERROR, m) {} };
+struct ParseError : Error { explicit ParseError(const std::string& m) : Error(MG_PARSE_ERROR, m) {} };
+struct IoError : Error { explicit IoError(const std::string& m) : Error(MG_IO_ERROR, m) {} };
 
 void set_last_error(const std::string& msg);
 
@@ -50,6 +52,13 @@ mg_status guarded(F&& f) {
 }
 
 inline std::string shape_str(index_t r, index_t c) { return std::to_string(r) + "x" + std::to_string(c); }
+
+// Per-device one-time setup (kernel attributes such as the dynamic shared-memory limit live in each
+// device's context): true the first time it is called with `dev` for this `seen` mask (devices < 64).
+inline bool first_on_device(std::atomic<unsigned long long>& seen, int dev) {
+  const unsigned long long bit = 1ull << (static_cast<unsigned>(dev) & 63u);
+  return (seen.fetch_or(bit) & bit) == 0;
+}
 
 // ---------------------------------------------------------------- host parallel_for
 int host_threads();

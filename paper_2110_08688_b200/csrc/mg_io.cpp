@@ -31,9 +31,6 @@
 
 namespace mg {
 
-struct ParseError : Error { explicit ParseError(const std::string& m) : Error(MG_PARSE_ERROR, m) {} };
-struct IoError : Error { explicit IoError(const std::string& m) : Error(MG_IO_ERROR, m) {} };
-
 namespace io {
 
 std::string read_file(const std::string& path) {
@@ -871,6 +868,83 @@ mg_status mg_graph_view(const mg_graph* g, mg_csr* out) {
 }
 
 void mg_graph_free(mg_graph* g) { delete g; }
+
+// from_coo (inc/sparse.hpp:59-90): edges range-checked against n, rows sorted by (src, dst), duplicate
+// (src, dst) weights summed (in edge order: a stable sort, where the reference's std::sort leaves the order
+// of equal keys unspecified).
+mg_status mg_graph_from_coo(int64_t n, int64_t count, const int64_t* src, const int64_t* dst, const float* weight,
+                            mg_graph** out) {
+  return guarded([&] {
+    if (!out || n < 0 || count < 0 || (count > 0 && (!src || !dst || !weight)))
+      throw ValueError("from_coo: bad argument");
+    for (int64_t e = 0; e < count; ++e)
+      if (src[e] < 0 || src[e] >= n || dst[e] < 0 || dst[e] >= n)
+        throw ValueError("from_coo: edge (" + std::to_string(src[e]) + ", " + std::to_string(dst[e]) +
+                         ") out of range for n=" + std::to_string(n));
+    // counting sort by source row (stable), then a stable sort of each row by destination
+    std::vector<index_t> start(static_cast<size_t>(n) + 1, 0);
+    for (int64_t e = 0; e < count; ++e) ++start[static_cast<size_t>(src[e]) + 1];
+    for (index_t u = 0; u < n; ++u) start[static_cast<size_t>(u) + 1] += start[static_cast<size_t>(u)];
+    std::vector<std::pair<index_t, float>> byrow(static_cast<size_t>(count));
+    std::vector<index_t> fill(start.begin(), start.end() - 1);
+    for (int64_t e = 0; e < count; ++e) byrow[static_cast<size_t>(fill[static_cast<size_t>(src[e])]++)] = {dst[e], weight[e]};
+    auto g = std::make_unique<mg_graph>();
+    Csr& m = g->csr;
+    m.rows = m.cols = n;
+    m.row_ptr.assign(static_cast<size_t>(n) + 1, 0);
+    for (index_t u = 0; u < n; ++u) {
+      auto b = byrow.begin() + start[static_cast<size_t>(u)], e = byrow.begin() + start[static_cast<size_t>(u) + 1];
+      std::stable_sort(b, e, [](const auto& x, const auto& y) { return x.first < y.first; });
+      for (auto it = b; it != e;) {
+        const index_t v = it->first;
+        float w = it->second;
+        for (++it; it != e && it->first == v; ++it) w += it->second;
+        m.col_idx.push_back(v);
+        m.values.push_back(w);
+      }
+      m.row_ptr[static_cast<size_t>(u) + 1] = static_cast<index_t>(m.col_idx.size());
+    }
+    *out = g.release();
+  });
+}
+
+// add_self_loops (inc/dataset.hpp:60-73): a unit (u, u) entry wherever row u lacks one, rebuilt as
+// from_coo does (inc/sparse.hpp:59-90): rows sorted by column, duplicate entries summed, range-checked
+// against n = rows.
+mg_status mg_graph_add_self_loops(const mg_csr* a, mg_graph** out) {
+  return guarded([&] {
+    if (!a || !out || a->rows < 0 || (a->rows > 0 && !a->row_ptr)) throw ValueError("add_self_loops: bad argument");
+    const index_t n = a->rows;
+    auto g = std::make_unique<mg_graph>();
+    Csr& m = g->csr;
+    m.rows = m.cols = n;
+    m.row_ptr.assign(static_cast<size_t>(n) + 1, 0);
+    std::vector<std::pair<index_t, float>> row;
+    for (index_t u = 0; u < n; ++u) {
+      row.clear();
+      bool diag = false;
+      for (index_t e = a->row_ptr[u]; e < a->row_ptr[u + 1]; ++e) {
+        const index_t v = a->col_idx[e];
+        if (v < 0 || v >= n)
+          throw ValueError("from_coo: edge (" + std::to_string(u) + ", " + std::to_string(v) +
+                           ") out of range for n=" + std::to_string(n));
+        diag = diag || v == u;
+        row.push_back({v, a->values[e]});
+      }
+      if (!diag) row.push_back({u, 1.0f});
+      std::stable_sort(row.begin(), row.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+      for (size_t i = 0; i < row.size();) {
+        const index_t v = row[i].first;
+        float w = row[i].second;
+        for (++i; i < row.size() && row[i].first == v; ++i) w += row[i].second;
+        m.col_idx.push_back(v);
+        m.values.push_back(w);
+      }
+      m.row_ptr[static_cast<size_t>(u) + 1] = static_cast<index_t>(m.col_idx.size());
+    }
+    *out = g.release();
+  });
+}
 
 mg_status mg_dense_load(const char* path, mg_dense** out) {
   return guarded([&] {

@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -1280,6 +1281,12 @@ CUtensorMap make_map(const float* base, long inner, long outer, long ld, int box
   return m;
 }
 
+int cur_dev() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+
 int num_sms() {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -1304,12 +1311,10 @@ inline int smem_bytes(const Params& p) {
 
 template <int MODE>
 void launch(const CUtensorMap& a, const CUtensorMap& b, const Params& p, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr, cur_dev()))
     TC_CUDA(cudaFuncSetAttribute(gemm_tc<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemBudget + kEpiSmem + 1024));
-    attr = true;
-  }
   const int grid = std::max(1, std::min(p.n_items, num_sms()));
   gemm_tc<MODE><<<grid, kThreads, smem_bytes(p), s>>>(a, b, p);
   TC_CUDA(cudaGetLastError());
@@ -1359,11 +1364,9 @@ int g_gemm3_cluster = 1;  // v3 cluster size for the W multicast ("gemm3_cluster
 template <int MODE, int CL>
 void launch3(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
              cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr, cur_dev()))
     TC_CUDA(cudaFuncSetAttribute(gemm_tc3<MODE, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax3));
-    attr = true;
-  }
   const int npi = ((p.m_tiles + CL - 1) / CL) * p.n_tiles;
   const int grid = CL * std::max(1, std::min(npi, num_sms() / CL));
   cudaLaunchConfig_t cfg{};
@@ -1384,12 +1387,10 @@ void launch3(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl,
 template <int MODE>
 void launch2(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
              cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr, cur_dev()))
     TC_CUDA(cudaFuncSetAttribute(gemm_tc2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemBudget2 + kEpiBuf + 1024));
-    attr = true;
-  }
   const int grid = std::max(1, std::min(p.n_items, num_sms()));
   gemm_tc2<MODE><<<grid, threads2<MODE>(), smem_bytes2(p, bk2<MODE>()), s>>>(a, bh, bl, c, p);
   TC_CUDA(cudaGetLastError());

@@ -5,6 +5,8 @@ reference's own tests:
   errors      inc/errors.hpp:10-39          ShapeError, ValueError, ... (+ CudaError, NcclError)
   GcnConfig   inc/gcn.hpp:14-36             + gemm_mode / spmm_mode (device arithmetic)
   parse_config / materialize_config / config_to_json   inc/driver.hpp:19-71
+  write_checkpoint / read_checkpoint        inc/driver.hpp:255-299
+  from_coo / add_self_loops                 inc/sparse.hpp:59-90, inc/dataset.hpp:60-73
   Dataset, synth_graph                      inc/dataset.hpp:19-56, :287-334
   load_dataset / load_graph / load_matrix_market / load_edge_list / load_features / load_labels /
   load_masks, read_dense / write_dense      inc/dataset.hpp:84-280, inc/dense.hpp:290-335
@@ -178,6 +180,48 @@ def config_to_json(cfg: GcnConfig) -> dict:
             "order_swap": cfg.order_swap}
 
 
+def _text(fn, *args) -> str:
+    n = C.c_int64()
+    _check(fn(*args, None, 0, C.byref(n)))
+    buf = C.create_string_buffer(n.value + 1)
+    _check(fn(*args, buf, n.value + 1, C.byref(n)))
+    return buf.raw[:n.value].decode()
+
+
+def config_to_json_text(cfg: GcnConfig, indent: int = -1) -> str:
+    """config_to_json(cfg).dump(indent) as the reference's nlohmann::json writes it (byte-identical)."""
+    return _text(lib().mg_config_to_json, C.byref(cfg._c()), int(indent))
+
+
+def write_checkpoint(path, ws, cfg: GcnConfig):
+    """write_checkpoint<float> (driver.hpp:255-274): MGDM blocks back to back + <path>.json sidecar."""
+    arrs = [np.ascontiguousarray(w, np.float32) for w in ws]
+    for a in arrs:
+        if a.ndim != 2:
+            raise ShapeError(f"write_checkpoint: expected matrices, got shape {a.shape}")
+    rows = np.array([a.shape[0] for a in arrs], np.int64)
+    cols = np.array([a.shape[1] for a in arrs], np.int64)
+    ptrs = (C.c_void_p * max(1, len(arrs)))(*[a.ctypes.data for a in arrs])
+    _check(lib().mg_checkpoint_write(_enc(path), len(arrs), _p(rows), _p(cols), ptrs, C.byref(cfg._c())))
+
+
+def read_checkpoint(path) -> list:
+    """read_checkpoint<float> (driver.hpp:276-299)."""
+    h = C.c_void_p()
+    _check(lib().mg_checkpoint_read(_enc(path), C.byref(h)))
+    try:
+        out = []
+        for i in range(lib().mg_checkpoint_count(h)):
+            r, c, d = C.c_int64(), C.c_int64(), C.c_void_p()
+            _check(lib().mg_checkpoint_view(h, i, C.byref(r), C.byref(c), C.byref(d)))
+            n = r.value * c.value
+            out.append(np.zeros((r.value, c.value), np.float32) if n == 0 else
+                       np.ctypeslib.as_array(C.cast(d, C.POINTER(C.c_float)), (n,)).reshape(r.value, c.value).copy())
+        return out
+    finally:
+        lib().mg_checkpoint_free(h)
+
+
 # ----------------------------------------------------------------------------- dataset (inc/dataset.hpp)
 
 
@@ -299,6 +343,46 @@ def _graph(fmt: int, path) -> tuple:
         return rp, ci, v
     finally:
         lib().mg_graph_free(h)
+
+
+def _graph_out(h) -> tuple:
+    try:
+        g = mg_csr()
+        _check(lib().mg_graph_view(h, C.byref(g)))
+        n = g.rows
+        rp = np.ctypeslib.as_array(C.cast(g.row_ptr, C.POINTER(C.c_int64)), (n + 1,)).copy()
+        nnz = int(rp[-1])
+        if nnz == 0:
+            return rp, np.zeros(0, np.int64), np.zeros(0, np.float32)
+        ci = np.ctypeslib.as_array(C.cast(g.col_idx, C.POINTER(C.c_int64)), (nnz,)).copy()
+        v = np.ctypeslib.as_array(C.cast(g.values, C.POINTER(C.c_float)), (nnz,)).copy()
+        return rp, ci, v
+    finally:
+        lib().mg_graph_free(h)
+
+
+def from_coo(src, dst, weight, n: int) -> tuple:
+    """from_coo<float> (sparse.hpp:59-90): (row_ptr, col_idx, values), rows sorted, duplicates summed."""
+    s = np.ascontiguousarray(src, np.int64)
+    d = np.ascontiguousarray(dst, np.int64)
+    w = np.ascontiguousarray(weight, np.float32)
+    if not (len(s) == len(d) == len(w)):
+        raise ShapeError("from_coo: src / dst / weight lengths differ")
+    h = C.c_void_p()
+    _check(lib().mg_graph_from_coo(int(n), len(s), _p(s), _p(d), _p(w), C.byref(h)))
+    return _graph_out(h)
+
+
+def add_self_loops(row_ptr, col_idx, values, cols=None) -> tuple:
+    """add_self_loops<float> (dataset.hpp:60-73)."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx, np.int64)
+    v = np.ascontiguousarray(values, np.float32)
+    n = len(rp) - 1
+    g = mg_csr(n, n if cols is None else int(cols), rp.ctypes.data, ci.ctypes.data, v.ctypes.data)
+    h = C.c_void_p()
+    _check(lib().mg_graph_add_self_loops(C.byref(g), C.byref(h)))
+    return _graph_out(h)
 
 
 def load_graph(path):

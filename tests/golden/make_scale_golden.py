@@ -1,0 +1,138 @@
+"""Full-size parity fixtures from the UNMODIFIED reference (oracle/_ref, compiled by oracle/build_ref.sh).
+
+Run in the build container (8+ cores, ~25 GB RAM for C4; /root/reference is not on the GPU box):
+
+    python tests/golden/make_scale_golden.py [partition] [traj] [c4step]
+
+Writes, next to this script:
+  scale_partition.json  sha256 of the reference's synth_graph output and of every prepare_data array
+                        (permutation, permuted features / labels / mask, bounds, every forward and backward
+                        tile) for the (config, P) pairs of tests/scale_common.PARTITION_CASES
+                        (inc/dataset.hpp:287-334, inc/driver.hpp:87-117)
+  scale_traj.npz        3-epoch train_run of C2 (full 169K-vertex arxiv shape) and of the products 1/16
+                        sample: f64 and f32 losses, f32 final W, and the sha256 of the f32 forward
+                        activations (step_dump, EXACT parity) (inc/driver.hpp:140-206)
+  scale_c4step.npz      teacher-forced train_step(1) at full C4 (workers = 8): loss, W_G and W after Adam in
+                        full; forward activations, loss gradient and H-grads on a row sample plus hub rows;
+                        per-tensor max |x| and per-column sums (inc/gcn.hpp:175-184)
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(HERE))
+from oracle.pyoracle import Ref, make_cfg  # noqa: E402
+from scale_common import (PARTITION_CASES, SCALE, c4_sample_rows, colsums, dataset_digest, sha,  # noqa: E402
+                          tile_digest)
+
+EPOCHS = 3
+
+
+def log(*a):
+    print(f"[{time.strftime('%H:%M:%S')}]", *a, flush=True)
+
+
+def synth(ref, name, dtype=np.float32):
+    c = SCALE[name]
+    return ref.synth(c["n"], c["deg"], 0.7, 1, c["dims"][0], c["dims"][-1], dtype=dtype)
+
+
+def partition(ref):
+    out = {}
+    by_cfg = {}
+    for name, P in PARTITION_CASES:
+        by_cfg.setdefault(name, []).append(P)
+    for name, parts in by_cfg.items():
+        ds = synth(ref, name)
+        out[name] = {"dataset": dataset_digest(ds.row_ptr, ds.col_idx, ds.values, ds.features, ds.labels),
+                     "n": ds.n, "nnz": ds.nnz, "parts": {}}
+        log(name, "synth", ds.n, ds.nnz)
+        for P in parts:
+            cfg = make_cfg(SCALE[name]["dims"], seed=1, permute=True, overlap=P > 1)
+            p = ref.prepare(ds, cfg, P)
+            out[name]["parts"][str(P)] = {
+                "bounds": [int(b) for b in p.bounds], "mask_count": int(p.mask_count),
+                "perm_forward": sha(p.perm_forward), "features": sha(p.features), "labels": sha(p.labels),
+                "mask": sha(p.mask),
+                "tiles": {f"{d},{i},{j}": tile_digest(*p.tiles[d][i][j])
+                          for d in (0, 1) for i in range(P) for j in range(P)},
+                "nnz": {f"{d},{i},{j}": int(p.tiles[d][i][j][0][-1])
+                        for d in (0, 1) for i in range(P) for j in range(P)}}
+            log(name, "P", P, "done")
+            del p
+        del ds
+    with open(os.path.join(HERE, "scale_partition.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
+def traj(ref):
+    g = {}
+    for name in ("c2", "c4s16"):
+        dims = SCALE[name]["dims"]
+        cfg = make_cfg(dims, epochs=EPOCHS, seed=1, permute=True)
+        d32 = synth(ref, name)
+        r32 = ref.train_run(d32, cfg, 1)
+        g[f"{name}_f32_loss"] = r32["loss"]
+        g[f"{name}_f32_acc"] = r32["acc"]
+        for l, w in enumerate(r32["final_w"]):
+            g[f"{name}_f32_w{l}"] = w
+        log(name, "f32", r32["loss"])
+        dump = ref.step_dump(d32, make_cfg(dims, seed=1, permute=True), 1)
+        for l, a in enumerate(dump["ahw_fwd"]):
+            g[f"{name}_fwd_sha{l}"] = np.frombuffer(sha(np.asarray(a, np.float32)).encode(), np.uint8)
+        del d32, dump
+        d64 = synth(ref, name, np.float64)
+        r64 = ref.train_run(d64, cfg, 1, np.float64)
+        g[f"{name}_f64_loss"] = r64["loss"]
+        log(name, "f64", r64["loss"])
+        del d64
+    np.savez_compressed(os.path.join(HERE, "scale_traj.npz"), **g)
+
+
+def c4step(ref):
+    name = "c4"
+    dims = SCALE[name]["dims"]
+    L = len(dims) - 1
+    ds = synth(ref, name)
+    fwd, _ = ref.random_permutation(ds.n, 1)
+    deg_new = np.empty(ds.n, np.int64)
+    deg_new[fwd] = np.diff(ds.row_ptr)
+    rows = c4_sample_rows(ds.n, deg_new)
+    log("c4 synth; sample rows", len(rows))
+    d = ref.step_dump(ds, make_cfg(dims, seed=1, permute=True, overlap=True), 8)
+    log("c4 step_dump loss", d["loss"])
+    g = {"rows": rows, "loss": np.array([d["loss"]])}
+    for l in range(L):
+        g[f"wgrad{l}"] = d["w_grad"][l]
+        g[f"wafter{l}"] = d["w_after"][l]
+    tensors = {f"fwd{l}": d["ahw_fwd"][l] for l in range(L)}
+    tensors["loss_grad"] = d["loss_grad"]
+    tensors.update({f"bwd{l}": d["ahw_bwd"][l] for l in range(L - 1)})  # H-grads (relu-masked)
+    for k, a in tensors.items():
+        a = np.asarray(a).reshape(ds.n, -1)
+        g[f"{k}_rows"] = a[rows]
+        g[f"{k}_max"] = np.array([np.max(np.abs(a))], np.float64)
+        s, sa = colsums(a)
+        g[f"{k}_colsum"] = s
+        g[f"{k}_colabs"] = sa
+    np.savez_compressed(os.path.join(HERE, "scale_c4step.npz"), **g)
+
+
+def main():
+    which = sys.argv[1:] or ["partition", "traj", "c4step"]
+    ref = Ref()
+    ref.set_spmm_threads(max(1, (os.cpu_count() or 8)))
+    for w in which:
+        t = time.time()
+        {"partition": partition, "traj": traj, "c4step": c4step}[w](ref)
+        log(w, f"{time.time() - t:.0f} s")
+
+
+if __name__ == "__main__":
+    main()

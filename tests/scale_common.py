@@ -1,0 +1,55 @@
+"""Shared by tests/golden/make_scale_golden.py (fixture generator, build container) and the scale parity
+tests: the benchmarked configurations (BASELINE.json configs, bench.py CONFIGS) and the digests that pin
+the reference's own outputs at full size without committing gigabytes of arrays.
+
+Digests are sha256 over raw little-endian bytes in the reference's layouts (inc/sparse.hpp:25-55 int64
+row_ptr / col_idx, fp32 values; inc/dense.hpp:30-118 row-major fp32), so equal digests = bit-identical.
+"""
+import hashlib
+
+import numpy as np
+
+# synth_graph(n, avg_degree, 0.7, seed 1, d0, classes) + the 3-layer model of each config
+SCALE = {
+    "c2": dict(n=169343, deg=13.6, dims=[128, 256, 256, 40]),
+    "c3": dict(n=232965, deg=497.0, dims=[602, 256, 256, 41]),
+    "c4": dict(n=2449029, deg=50.6, dims=[100, 256, 256, 47]),
+    # the reference arm's bounded sample of C4 (bench.py reference_epoch_sample: 1/16 of the vertices)
+    "c4s16": dict(n=153064, deg=50.6, dims=[100, 256, 256, 47]),
+}
+# partition digests are pinned for these (config, P) pairs (VERDICT r1 "next round" item 1)
+PARTITION_CASES = [("c2", 1), ("c2", 2), ("c3", 1), ("c3", 8), ("c4", 1), ("c4", 8)]
+# rows of the C4 teacher-forced step dump kept in full: a seeded uniform sample plus the top hub rows
+C4_SAMPLE_ROWS = 512
+C4_HUB_ROWS = 32
+
+
+def sha(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def tile_digest(rp, ci, v) -> str:
+    return sha(np.asarray(rp, np.int64), np.asarray(ci, np.int64), np.asarray(v, np.float32))
+
+
+def dataset_digest(rp, ci, v, features, labels) -> dict:
+    return {"graph": tile_digest(rp, ci, v), "features": sha(np.asarray(features, np.float32)),
+            "labels": sha(np.asarray(labels, np.int32))}
+
+
+def c4_sample_rows(n: int, degree_new_ids: np.ndarray) -> np.ndarray:
+    """Row ids (permuted order) kept in full from the C4 step dump: C4_SAMPLE_ROWS uniform rows (seed 0) plus
+    the C4_HUB_ROWS highest-degree rows (the hub rows that the FAST SpMM cuts into segments)."""
+    rng = np.random.default_rng(0)
+    uni = rng.choice(n, C4_SAMPLE_ROWS, replace=False)
+    hubs = np.argsort(degree_new_ids, kind="stable")[-C4_HUB_ROWS:]
+    return np.unique(np.concatenate([uni, hubs])).astype(np.int64)
+
+
+def colsums(a: np.ndarray):
+    """Whole-tensor property: per-column sum and sum of |x| in fp64 (|ours - ref| <= tol * abs-sum)."""
+    a = np.asarray(a, np.float64)
+    return a.sum(0), np.abs(a).sum(0)

@@ -49,3 +49,47 @@ def test_on_epoch_and_logit_equivariance():
     np.testing.assert_allclose(plain.epoch_loss, perm.epoch_loss, rtol=1e-5)
     pf = R.prepare_data(ds, cfg, 2).rows_export(4)[3]
     np.testing.assert_allclose(plain.logits, perm.logits[pf], rtol=1e-4, atol=1e-5)
+
+
+DROPIN = os.path.join(ROOT, "tests", "dropin", "_build", "dropin_main")
+
+
+@pytest.mark.skipif(not os.path.exists(DROPIN), reason="tests/dropin/build_dropin.sh runs in the build container")
+def test_reference_test_cases_run_on_the_gpu():
+    """The train_run / grad_run cases of the reference's tests/test_gcn.cpp:213-348 (P-invariance of W_G and
+    of the W trajectory for P in {1,2,4,8}, overlap on == off, seeded determinism, loss decrease), compiled
+    unchanged against include/mggcn/rowgcn.hpp, pass on the device path (default modes)."""
+    r = subprocess.run([DROPIN, "cases"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.count("ok: ") == 5
+
+
+@pytest.mark.skipif(not os.path.exists(DROPIN), reason="tests/dropin/build_dropin.sh runs in the build container")
+def test_reference_run_train_on_the_gpu(tmp_path):
+    """The reference CLI's run_train<S> (tools/main.cpp:56-101) on files: epoch lines, summary, checkpoint +
+    sidecar; the trained W equals the Python mirror's train_run on the same files."""
+    import json
+    ds = R.synth_graph(3000, 10.0, 0.7, 7, 24, 5)
+    rp, ci, _ = ds.graph
+    with open(tmp_path / "g.edges", "w") as f:
+        for u in range(ds.n):
+            for e in range(rp[u], rp[u + 1]):
+                f.write(f"{u} {ci[e]}\n")
+    R.write_dense(tmp_path / "x.bin", ds.features)
+    (tmp_path / "y.txt").write_text("\n".join(str(int(x)) for x in ds.labels) + "\n")
+    (tmp_path / "cfg.json").write_text(json.dumps({"hidden_dims": [32, 16], "epochs": 4, "seed": 3}))
+    ck = tmp_path / "w.ckpt"
+    r = subprocess.run([DROPIN, "train", str(tmp_path / "g.edges"), str(tmp_path / "x.bin"), str(tmp_path / "y.txt"),
+                        str(tmp_path / "cfg.json"), str(ck), "2"], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert [x["epoch"] for x in lines[:-1]] == [1, 2, 3, 4] and lines[-1]["epochs"] == 4
+    side = json.loads((tmp_path / "w.ckpt.json").read_text())
+    assert side["layer_dims"] == [24, 32, 16, 5] and side["permute"] is True
+    ws = R.read_checkpoint(ck)
+    loaded = R.load_dataset(tmp_path / "g.edges", tmp_path / "x.bin", tmp_path / "y.txt")
+    cfg = R.GcnConfig([24, 32, 16, 5], epochs=4, seed=3, permute=True)
+    art = R.train_run(loaded, cfg, R.TrainOptions(workers=2, devices=[0, 0]))
+    np.testing.assert_allclose([x["loss"] for x in lines[:-1]], art.epoch_loss, rtol=1e-12)
+    for a, b in zip(ws, art.final_w):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
