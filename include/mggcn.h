@@ -23,7 +23,7 @@
 extern "C" {
 #endif
 
-#define MG_ABI_VERSION 2
+#define MG_ABI_VERSION 3
 
 typedef enum mg_status {
   MG_OK = 0,
@@ -74,6 +74,15 @@ typedef struct mg_config {
    * forward and backward d1-wide ones (the association inc/gcn.hpp:254-260 uses under order_swap, carried
    * into the backward). Mathematically the same gradient; float order differs, so EXACT ignores it. */
   int32_t aggregate_input;
+  /* Default-off extensions (no reference analogue: the reference has neither; no parity claim;
+   * not part of the config JSON schema). bias = 1: every layer adds a learned bias row b_l (zero-initialised,
+   * Adam-updated, its gradient reduced over the canonical W-grad blocks like W_G). dropout = p in [0, 1):
+   * during train_step / compute_gradients each hidden layer's output (after bias + ReLU) is kept with
+   * probability 1 - p and scaled by 1 / (1 - p); the mask is a counter hash of (seed, step, layer, global
+   * row, column), fused into the producing kernel's epilogue and recovered by relu_backward from the
+   * output itself. loss_only / forward (evaluation) apply no dropout. */
+  int32_t bias;
+  double dropout;
 } mg_config;
 
 /* Fills the reference defaults (inc/gcn.hpp:16-25): lr 0.01, betas 0.9/0.999, eps 1e-8, 100 epochs,
@@ -96,7 +105,11 @@ int32_t mg_abi_version(void);
  *   "gemm_kernel"  tcgen05 GeMM variant: 1 = both split operands in smem, 2 = A split into TMEM,
  *                  3 = 2 with 32-K stages and decoupled A / W rings for NN / NT (default)
  *   "gemm3_wring"  v3 W-ring budget in bytes (default 96 KiB), "gemm3_cluster" 1 or 2 (W multicast)
- *   "bwd_transpose"  one worker: build the backward tile on the device from the forward one (default 1) */
+ *   "bwd_transpose"  one worker: build the backward tile on the device from the forward one (default 1)
+ *   "block_cache"  1 (default): device blocks of destroyed groups are kept for reuse; 0: released (cold runs)
+ *   "watchdog_ms"  host-wait timeout after which a group is aborted with MG_SHUTDOWN_ERROR (default 0 = none)
+ *   "debug_stall_us" / "nccl_single"  test hooks: a spin kernel at every step start; an NCCL communicator
+ *                  (and NCCL collectives) for one-rank groups too */
 mg_status mg_set_tuning(const char* key, int64_t value);
 
 /* ---------------------------------------------------------------- host datasets
@@ -229,6 +242,12 @@ mg_status mg_nccl_unique_id(uint8_t id[128]);
 mg_status mg_group_create(const mg_config* cfg, const mg_partition* p, int32_t world, int32_t n_local,
                           const int32_t* local_ranks, const int32_t* devices, const uint8_t* nccl_id,
                           int32_t transport, mg_group** out);
+/* DeviceGroup::abort (collectives.cpp:42-52), callable from any thread: the current or next host wait on the
+ * group aborts its NCCL communicators (ncclCommAbort) and fails with MG_SHUTDOWN_ERROR "device group aborted:
+ * ..."; every later call on the group fails the same way (mg_group_destroy still releases it). Host waits
+ * also abort on an asynchronous NCCL error (a peer that died) and, with mg_set_tuning("watchdog_ms", T), when
+ * a step, a collective or communicator creation has not completed within T ms (a peer that never arrived). */
+mg_status mg_group_abort(mg_group* g);
 /* GcnWorker::init_params (inc/gcn.hpp:163-173): Glorot from Rng(seed) on the host, replicated. */
 mg_status mg_group_init_params(mg_group* g);
 /* GcnWorker::train_step(t) (inc/gcn.hpp:175-184). Synchronous; loss = global masked mean, acc =
@@ -258,7 +277,9 @@ typedef enum mg_tensor {
   MG_T_X = 4,      /* local_rows x d0     x_local */
   MG_T_ADAM_M = 5,
   MG_T_ADAM_V = 6,
-  MG_T_WSTAGE = 7  /* 8 d_l x d_{l+1}   the canonical-block W-grad staging buffer */
+  MG_T_WSTAGE = 7, /* 8 d_l x d_{l+1}   the canonical-block W-grad staging buffer */
+  MG_T_BIAS = 8,   /* 1 x d_{l+1}        bias row of layer l (cfg.bias) */
+  MG_T_BIAS_GRAD = 9 /* 1 x d_{l+1}      its gradient (like MG_T_WGRAD) */
 } mg_tensor;
 
 /* Copies a tensor of local worker `rank` to/from host memory in the reference's dense layout

@@ -163,6 +163,8 @@ struct GcnConfig {
   int gemm_mode = MG_GEMM_TF32X3;  // see DESIGN.md: EXACT is bitwise, TF32X3/FAST meet rel 1e-4
   int spmm_mode = MG_SPMM_FAST;
   bool aggregate_input = true;  // FAST only: layer 0 as (A X) W0 (mggcn.h)
+  bool bias = false;            // default-off extensions, no reference analogue (mggcn.h)
+  double dropout = 0.0;
   int layers() const { return static_cast<int>(layer_dims.size()) - 1; }
   mg_config c() const {
     mg_config m;
@@ -182,6 +184,8 @@ struct GcnConfig {
     m.gemm_mode = gemm_mode;
     m.spmm_mode = spmm_mode;
     m.aggregate_input = aggregate_input;
+    m.bias = bias;
+    m.dropout = dropout;
     return m;
   }
   void validate() const {

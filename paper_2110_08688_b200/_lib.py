@@ -21,7 +21,7 @@ class mg_config(C.Structure):
                 ("beta2", C.c_double), ("epsilon", C.c_double), ("epochs", C.c_int32), ("seed", C.c_uint64),
                 ("permute", C.c_uint8), ("overlap", C.c_uint8), ("skip_first_backward_spmm", C.c_uint8),
                 ("order_swap", C.c_uint8), ("gemm_mode", C.c_int32), ("spmm_mode", C.c_int32),
-                ("aggregate_input", C.c_int32)]
+                ("aggregate_input", C.c_int32), ("bias", C.c_int32), ("dropout", C.c_double)]
 
 
 class mg_timeline_event(C.Structure):
@@ -63,6 +63,7 @@ SIGNATURES = [
     ("mg_config_to_json", C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_int64, C.c_void_p]),
     ("mg_breakdown_to_json", C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_int64, C.c_void_p]),
     ("mg_breakdown_text", C.c_int, [C.c_void_p, C.c_char_p, C.c_int64, C.c_void_p]),
+    ("mg_group_abort", C.c_int, [C.c_void_p]),
     ("mg_labels_load", C.c_int, [C.c_char_p, C.c_void_p, C.c_int64, C.c_void_p]),
     ("mg_masks_load", C.c_int, [C.c_char_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("mg_prepare", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),

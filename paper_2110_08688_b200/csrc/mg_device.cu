@@ -40,10 +40,13 @@ namespace mg {
                       std::to_string(__LINE__) + ")");                                                 \
     }                                                                                                  \
   } while (0)
+// Communicators are non-blocking (ncclCommInitRankConfig, blocking = 0) so a lost peer can be detected and
+// the communicator aborted: calls may return ncclInProgress, and nccl_settle() completes them.
 #define MG_NCCL(x)                                                                                     \
   do {                                                                                                 \
     ncclResult_t _r = (x);                                                                             \
-    if (_r != ncclSuccess) throw NcclError(std::string(#x) + ": " + ncclGetErrorString(_r));          \
+    if (_r != ncclSuccess && _r != ncclInProgress)                                                     \
+      throw NcclError(std::string(#x) + ": " + ncclGetErrorString(_r));                                \
   } while (0)
 #define MG_LAUNCHED() MG_CUDA(cudaGetLastError())
 
@@ -53,6 +56,9 @@ inline index_t pad4(index_t d) { return (d + 3) / 4 * 4; }
 inline int ceil_div(index_t a, index_t b) { return static_cast<int>((a + b - 1) / b); }
 
 std::atomic<int> g_heavy_row{4096};
+std::atomic<long long> g_watchdog_ms{0};  // host-wait timeout before the group is aborted (0 = none)
+std::atomic<long long> g_debug_stall_us{0};  // test hook: a spin kernel of this length at every step start
+std::atomic<int> g_nccl_single{0};  // test hook: one-rank groups also get an NCCL communicator (exercised path)
 std::atomic<int> g_profile{0};
 std::atomic<int> g_spmm_slab{0};  // floats per column-slab pass of the SpMM (0 = the whole width, <= 1024)
 std::atomic<int> g_narrow_group{0};  // lanes per row for widths of 33..64 floats (0 = 16, or 4 / 8)
@@ -193,10 +199,11 @@ class BlockCache {
     }
     return p;
   }
+  std::atomic<bool> enabled{true};  // "block_cache" 0: every block goes back to the driver (cold-start runs)
   void put(int dev, void* p, size_t bytes) {
     if (!p) return;
     std::lock_guard<std::mutex> lk(mu_);
-    if (cached_[dev] + bytes > kCap) {  // bounded: the rest of the process (torch, NCCL) needs memory too
+    if (!enabled.load() || cached_[dev] + bytes > kCap) {  // bounded: torch / NCCL need memory too
       cudaFree(p);
       return;
     }
@@ -291,18 +298,19 @@ struct SpmmLaunch {
 
 template <int G, int CPL>
 static void launch_rows(const SpmmLaunch& t, const float* h, float* out, int ld, int nchunk, int acc, int relu,
-                        cudaStream_t s) {
+                        const k::Epi& ep, cudaStream_t s) {
   if (t.n_light <= 0) return;
   const int gpb = 256 / G;
   const int blocks = std::min(ceil_div(t.n_light, gpb), num_sms() * 16);
   k::spmm_exact_rows<G, CPL><<<blocks, 256, 0, s>>>(t.row_ptr, t.edges, t.light, t.n_light, h, out, ld, nchunk, acc,
-                                                    relu);
+                                                    relu, ep);
   MG_LAUNCHED();
 }
 
 // Light rows: pick the lane-group size G and chunks-per-lane CPL from the float4 width; widths above
 // 1024 floats are processed in column slabs (each slab re-walks the row's nonzeros).
-static int spmm_light(const SpmmLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, cudaStream_t s) {
+static int spmm_light(const SpmmLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, const k::Epi& ep0,
+                      cudaStream_t s) {
   const int nchunk_all = static_cast<int>(ld / 4);
   int launches = 0;
   const int step = slab_chunks();
@@ -311,19 +319,22 @@ static int spmm_light(const SpmmLaunch& t, const float* h, float* out, index_t l
     const float* hs = h + 4 * c0;
     float* os = out + 4 * c0;
     const int L = static_cast<int>(ld);
-    if (nchunk <= 1) launch_rows<1, 1>(t, hs, os, L, nchunk, acc, relu, s);
-    else if (nchunk <= 2) launch_rows<2, 1>(t, hs, os, L, nchunk, acc, relu, s);
-    else if (nchunk <= 4) launch_rows<4, 1>(t, hs, os, L, nchunk, acc, relu, s);
-    else if (nchunk <= 8) launch_rows<8, 1>(t, hs, os, L, nchunk, acc, relu, s);
-    else if (nchunk <= 16 && narrow_group() == 4 && nchunk <= 12) launch_rows<4, 3>(t, hs, os, L, nchunk, acc, relu, s);
-    else if (nchunk <= 16 && narrow_group() == 8) launch_rows<8, 2>(t, hs, os, L, nchunk, acc, relu, s);
-    else if (nchunk <= 16) launch_rows<16, 1>(t, hs, os, L, nchunk, acc, relu, s);
-    else if (nchunk <= 32) launch_rows<32, 1>(t, hs, os, L, nchunk, acc, relu, s);
-    else if (nchunk <= 64) launch_rows<32, 2>(t, hs, os, L, nchunk, acc, relu, s);
-    else if (nchunk <= 96) launch_rows<32, 3>(t, hs, os, L, nchunk, acc, relu, s);
-    else if (nchunk <= 128) launch_rows<32, 4>(t, hs, os, L, nchunk, acc, relu, s);
-    else if (nchunk <= 192) launch_rows<32, 6>(t, hs, os, L, nchunk, acc, relu, s);
-    else launch_rows<32, 8>(t, hs, os, L, nchunk, acc, relu, s);
+    k::Epi ep = ep0;
+    if (ep.bias) ep.bias += 4 * c0;
+    ep.key += static_cast<unsigned long long>(4 * c0) * 0x9E3779B97F4A7C15ull;  // column offset of the slab
+    if (nchunk <= 1) launch_rows<1, 1>(t, hs, os, L, nchunk, acc, relu, ep, s);
+    else if (nchunk <= 2) launch_rows<2, 1>(t, hs, os, L, nchunk, acc, relu, ep, s);
+    else if (nchunk <= 4) launch_rows<4, 1>(t, hs, os, L, nchunk, acc, relu, ep, s);
+    else if (nchunk <= 8) launch_rows<8, 1>(t, hs, os, L, nchunk, acc, relu, ep, s);
+    else if (nchunk <= 16 && narrow_group() == 4 && nchunk <= 12) launch_rows<4, 3>(t, hs, os, L, nchunk, acc, relu, ep, s);
+    else if (nchunk <= 16 && narrow_group() == 8) launch_rows<8, 2>(t, hs, os, L, nchunk, acc, relu, ep, s);
+    else if (nchunk <= 16) launch_rows<16, 1>(t, hs, os, L, nchunk, acc, relu, ep, s);
+    else if (nchunk <= 32) launch_rows<32, 1>(t, hs, os, L, nchunk, acc, relu, ep, s);
+    else if (nchunk <= 64) launch_rows<32, 2>(t, hs, os, L, nchunk, acc, relu, ep, s);
+    else if (nchunk <= 96) launch_rows<32, 3>(t, hs, os, L, nchunk, acc, relu, ep, s);
+    else if (nchunk <= 128) launch_rows<32, 4>(t, hs, os, L, nchunk, acc, relu, ep, s);
+    else if (nchunk <= 192) launch_rows<32, 6>(t, hs, os, L, nchunk, acc, relu, ep, s);
+    else launch_rows<32, 8>(t, hs, os, L, nchunk, acc, relu, ep, s);
     ++launches;
   }
   return launches;
@@ -342,11 +353,11 @@ struct FastLaunch {
 
 template <int G, int CPL>
 static void launch_fast(const FastLaunch& t, const float* h, float* out, float* scratch, int ld, int nchunk, int acc,
-                        int relu, cudaStream_t s) {
+                        int relu, const k::Epi& ep, cudaStream_t s) {
   const int gpb = 256 / G;
   const int blocks = std::min(ceil_div(t.n_items, gpb), num_sms() * 16);
   k::spmm_fast_items<G, CPL><<<blocks, 256, 0, s>>>(t.items, t.n_items, t.edges, h, out, scratch, ld, nchunk, acc,
-                                                    relu);
+                                                    relu, ep);
   MG_LAUNCHED();
 }
 
@@ -394,7 +405,7 @@ static k::AdamConsts adam_consts(double lr, double beta1, double beta2, double e
 
 template <int G, int CPL, int E, int D, bool HINT>
 static void launch_fast_async_v(const FastLaunch& t, const float* h, float* out, float* scratch, int ld, int nchunk,
-                                int acc, int relu, int hub_max, cudaStream_t s) {
+                                int acc, int relu, int hub_max, const k::Epi& ep, cudaStream_t s) {
   constexpr int kThreads = 128;
   constexpr size_t smem = sizeof(float4) * kThreads * D * E * CPL;
   static std::atomic<unsigned long long> attr{0};
@@ -409,35 +420,36 @@ static void launch_fast_async_v(const FastLaunch& t, const float* h, float* out,
   const int gpb = kThreads / G;
   const int blocks = std::min(ceil_div(t.n_items, gpb), num_sms() * blocks_per_sm);
   k::spmm_fast_async<G, CPL, E, D, HINT><<<blocks, kThreads, smem, s>>>(t.items, t.n_items, t.edges, h, out, scratch,
-                                                                        ld, nchunk, acc, relu, hub_max);
+                                                                        ld, nchunk, acc, relu, hub_max, ep);
   MG_LAUNCHED();
 }
 
 template <int G, int CPL, int E, int D>
 static void launch_fast_async(const FastLaunch& t, const float* h, float* out, float* scratch, int ld, int nchunk,
-                              int acc, int relu, cudaStream_t s) {
+                              int acc, int relu, const k::Epi& ep, cudaStream_t s) {
   // hub hints only when the gathered block is well beyond the L2 (a block of a few L2 sizes is better
   // served by plain LRU, which then keeps a large share of every row resident)
   const bool big = static_cast<double>(t.src_rows) * ld * 4 > 4.0 * kL2Bytes;
   const int hub_max = t.hubs_classed && big ? hub_class_max(ld) : -1;
-  if (hub_max >= 0) launch_fast_async_v<G, CPL, E, D, true>(t, h, out, scratch, ld, nchunk, acc, relu, hub_max, s);
-  else launch_fast_async_v<G, CPL, E, D, false>(t, h, out, scratch, ld, nchunk, acc, relu, -1, s);
+  if (hub_max >= 0) launch_fast_async_v<G, CPL, E, D, true>(t, h, out, scratch, ld, nchunk, acc, relu, hub_max, ep, s);
+  else launch_fast_async_v<G, CPL, E, D, false>(t, h, out, scratch, ld, nchunk, acc, relu, -1, ep, s);
 }
 
 // cp.async-pipelined variants for rows of >= 32 floats; false = use the register-gather kernel.
 static bool launch_fast_pipelined(const FastLaunch& t, const float* hs, float* os, float* ss, int L, int nchunk,
-                                  int acc, int relu, cudaStream_t s) {
+                                  int acc, int relu, const k::Epi& ep, cudaStream_t s) {
   if (!g_spmm_async.load() || nchunk < 8) return false;
-  if (nchunk <= 16) launch_fast_async<16, 1, 4, 4>(t, hs, os, ss, L, nchunk, acc, relu, s);
-  else if (nchunk <= 32) launch_fast_async<32, 1, 4, 4>(t, hs, os, ss, L, nchunk, acc, relu, s);
-  else if (nchunk <= 64) launch_fast_async<32, 2, 4, 4>(t, hs, os, ss, L, nchunk, acc, relu, s);
-  else if (nchunk <= 128) launch_fast_async<32, 4, 2, 4>(t, hs, os, ss, L, nchunk, acc, relu, s);
+  if (nchunk <= 16) launch_fast_async<16, 1, 4, 4>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+  else if (nchunk <= 32) launch_fast_async<32, 1, 4, 4>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+  else if (nchunk <= 64) launch_fast_async<32, 2, 4, 4>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+  else if (nchunk <= 128) launch_fast_async<32, 4, 2, 4>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
   else return false;
   return true;
 }
 
 // MG_SPMM_FAST: one gather pass over rows + hub segments, then the ordered hub-segment sum.
-static int spmm_fast(const FastLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, cudaStream_t s) {
+static int spmm_fast(const FastLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, const k::Epi& ep0,
+                     cudaStream_t s) {
   int launches = 0;
   const int nchunk_all = static_cast<int>(ld / 4);
   if (t.n_items > 0) {
@@ -448,32 +460,36 @@ static int spmm_fast(const FastLaunch& t, const float* h, float* out, index_t ld
       float* os = out + 4 * c0;
       float* ss = t.scratch ? t.scratch + 4 * c0 : nullptr;
       const int L = static_cast<int>(ld);
-      if (launch_fast_pipelined(t, hs, os, ss, L, nchunk, acc, relu, s)) {
-      } else if (nchunk <= 1) launch_fast<1, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
-      else if (nchunk <= 2) launch_fast<2, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
-      else if (nchunk <= 4) launch_fast<4, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
-      else if (nchunk <= 8) launch_fast<8, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
-      else if (nchunk <= 12 && narrow_group() == 4) launch_fast<4, 3>(t, hs, os, ss, L, nchunk, acc, relu, s);
-      else if (nchunk <= 16 && narrow_group() == 8) launch_fast<8, 2>(t, hs, os, ss, L, nchunk, acc, relu, s);
-      else if (nchunk <= 16) launch_fast<16, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
-      else if (nchunk <= 32) launch_fast<32, 1>(t, hs, os, ss, L, nchunk, acc, relu, s);
-      else if (nchunk <= 64) launch_fast<32, 2>(t, hs, os, ss, L, nchunk, acc, relu, s);
-      else if (nchunk <= 96) launch_fast<32, 3>(t, hs, os, ss, L, nchunk, acc, relu, s);
-      else if (nchunk <= 128) launch_fast<32, 4>(t, hs, os, ss, L, nchunk, acc, relu, s);
-      else if (nchunk <= 192) launch_fast<32, 6>(t, hs, os, ss, L, nchunk, acc, relu, s);
-      else launch_fast<32, 8>(t, hs, os, ss, L, nchunk, acc, relu, s);
+      k::Epi ep = ep0;
+      if (ep.bias) ep.bias += 4 * c0;
+      ep.key += static_cast<unsigned long long>(4 * c0) * 0x9E3779B97F4A7C15ull;  // column offset of the slab
+      if (launch_fast_pipelined(t, hs, os, ss, L, nchunk, acc, relu, ep, s)) {
+      } else if (nchunk <= 1) launch_fast<1, 1>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+      else if (nchunk <= 2) launch_fast<2, 1>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+      else if (nchunk <= 4) launch_fast<4, 1>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+      else if (nchunk <= 8) launch_fast<8, 1>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+      else if (nchunk <= 12 && narrow_group() == 4) launch_fast<4, 3>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+      else if (nchunk <= 16 && narrow_group() == 8) launch_fast<8, 2>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+      else if (nchunk <= 16) launch_fast<16, 1>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+      else if (nchunk <= 32) launch_fast<32, 1>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+      else if (nchunk <= 64) launch_fast<32, 2>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+      else if (nchunk <= 96) launch_fast<32, 3>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+      else if (nchunk <= 128) launch_fast<32, 4>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+      else if (nchunk <= 192) launch_fast<32, 6>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
+      else launch_fast<32, 8>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
       ++launches;
     }
   }
   if (t.n_hubs > 0) {
-    k::spmm_fast_hubs<<<t.n_hubs, 256, 0, s>>>(t.hubs, t.scratch, out, static_cast<int>(ld), acc, relu);
+    k::spmm_fast_hubs<<<t.n_hubs, 256, 0, s>>>(t.hubs, t.scratch, out, static_cast<int>(ld), acc, relu, ep0);
     MG_LAUNCHED();
     ++launches;
   }
   return launches;
 }
 
-static int spmm_heavy(const SpmmLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, cudaStream_t s) {
+static int spmm_heavy(const SpmmLaunch& t, const float* h, float* out, index_t ld, int acc, int relu, const k::Epi& ep,
+                      cudaStream_t s) {
   if (t.n_heavy <= 0) return 0;
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr, cur_device()))
@@ -481,7 +497,7 @@ static int spmm_heavy(const SpmmLaunch& t, const float* h, float* out, index_t l
                                  static_cast<int>(k::kHeavySmem)));
   const int nslab = ceil_div(ld, k::kHeavySlab);
   k::spmm_exact_heavy<<<t.n_heavy * nslab, k::kHeavyThreads, k::kHeavySmem, s>>>(t.row_ptr, t.edges, t.heavy, nslab, h, out,
-                                                                   static_cast<int>(ld), acc, relu);
+                                                                   static_cast<int>(ld), acc, relu, ep);
   MG_LAUNCHED();
   return 1;
 }
@@ -489,11 +505,11 @@ static int spmm_heavy(const SpmmLaunch& t, const float* h, float* out, index_t l
 // GeMM dispatch: exact SIMT or tcgen05 (mg_tc_gemm.cuh).
 static int gemm_launch(int mode, bool ta, bool tb, index_t M, index_t N, index_t K, const float* A, index_t lda,
                        const float* B, index_t ldb, float* Cm, index_t ldc, int epi, cudaStream_t s,
-                       float* ws = nullptr, size_t ws_bytes = 0) {
+                       float* ws = nullptr, size_t ws_bytes = 0, const k::Epi& ep = k::Epi{}) {
   if (M <= 0 || N <= 0) return 0;
-  if (mode != MG_GEMM_EXACT) return tc::gemm(mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, ws, ws_bytes, s);
+  if (mode != MG_GEMM_EXACT) return tc::gemm(mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, ws, ws_bytes, s, ep);
   dim3 grid(ceil_div(M, k::kGBM), ceil_div(N, k::kGBN));
-#define MG_G(TA, TB, E) k::gemm_exact<TA, TB, E><<<grid, 256, 0, s>>>((int)M, (int)N, (int)K, A, lda, B, ldb, Cm, ldc)
+#define MG_G(TA, TB, E) k::gemm_exact<TA, TB, E><<<grid, 256, 0, s>>>((int)M, (int)N, (int)K, A, lda, B, ldb, Cm, ldc, ep)
   if (!ta && !tb) {
     if (epi == 0) MG_G(false, false, 0); else if (epi == 1) MG_G(false, false, 1); else MG_G(false, false, 2);
   } else if (ta && !tb) {
@@ -525,6 +541,8 @@ struct Worker {
   float* seg_scratch = nullptr;  // MG_SPMM_FAST hub-row segment partials (max segments x ld_max)
   float* ws = nullptr;  // tcgen05 TN split-K partials (W-grad), private to this worker's stream
   size_t ws_bytes = 0;
+  float* bias_part = nullptr;  // cfg.bias: per-chunk column sums of the bias gradient
+  int bias_chunks = 0;
   double* stats = nullptr;
   double* h_stats = nullptr;  // pinned
   int loss_blocks = 0;
@@ -553,6 +571,10 @@ struct mg_group {
   mg::index_t wblocks[9] = {};  // canonical W-grad blocks uniform_partition(n, 8), driver.hpp:156
   std::vector<mg::index_t> ld;  // padded widths per dim
   mg::index_t ld_max = 4, max_part = 0;
+  // floats per layer parameter array: W (ld_l x ld_{l+1}) plus, with cfg.bias, the bias row after it; the
+  // same layout for W_G, Adam m / v and each canonical staging block, so the W-grad all-reduce, the block
+  // sum and Adam cover the bias with no extra launches
+  mg::index_t pstride(int l) const { return (ld[l] + (cfg.bias ? 1 : 0)) * ld[l + 1]; }
   std::vector<std::unique_ptr<mg::Worker>> workers;
   bool sealed = false;  // set after construction: allocations afterwards count as step allocations
   mg::index_t step_allocs = 0;
@@ -565,6 +587,10 @@ struct mg_group {
   std::vector<std::pair<int, int>> prof_pending;  // (kind, index of the start event)
   double last_loss = 0, last_acc = 0;
   bool stats_pending = false;
+  // DeviceGroup::abort (collectives.cpp:42-52): a request from any thread, served by the next host wait
+  std::atomic<bool> abort_requested{false};
+  bool aborted = false;
+  std::string abort_reason;
   // timeline (rowgcn::TimelineEvent, collectives.hpp:24-34): one record per task, times resolved on drain
   struct TlRec {
     int worker_k, lane, stage;
@@ -860,16 +886,69 @@ void download_padded(float* dst, const float* src, index_t rows, index_t cols, i
                        cudaMemcpyDeviceToHost));
 }
 
+// The bias rows of the 8 canonical staging blocks (stride block_stride from `out`) from the local rows of G.
+int bias_grad_blocks(Worker& w, const float* G, index_t ld, const int64_t* begin, const int64_t* len, float* out,
+                     index_t block_stride, cudaStream_t s) {
+  k::BlockRanges br{};
+  for (int b = 0; b < 8; ++b) {
+    br.begin[b] = begin[b];
+    br.len[b] = len[b];
+  }
+  if (w.bias_chunks > 0) {
+    k::bias_partials<<<dim3(w.bias_chunks, 8), 256, 0, s>>>(G, static_cast<int>(ld), br, w.bias_chunks, w.bias_part);
+    MG_LAUNCHED();
+  }
+  k::bias_reduce<<<std::max(1, static_cast<int>((8 * ld + 255) / 256)), 256, 0, s>>>(
+      w.bias_part, br, w.bias_chunks, static_cast<int>(ld), out, block_stride);
+  MG_LAUNCHED();
+  return w.bias_chunks > 0 ? 2 : 1;
+}
+
 cudaEvent_t mk_event(bool timing = false) {
   cudaEvent_t e;
   MG_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
   return e;
 }
 
+void nccl_settle(mg_group& g);
+void check_alive(mg_group& g);
+
+// Test hook ("debug_stall_us"): a kernel that spins for `us` microseconds (a stand-in for a peer that never
+// arrives, so the watchdog / abort path can be exercised on one device).
+__global__ void stall_kernel(long long ns) {
+  long long t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 >= ns) break;
+    __nanosleep(1000);
+  }
+}
+
 // ---------------------------------------------------------------- the step (one process, all local workers)
 class Step {
  public:
   explicit Step(mg_group& g) : g_(g), cfg_(g.cfg), L_(g.cfg.layers()), P_(g.world) {}
+  // training pass (dropout active) of step t, vs an evaluation forward (mg_group_forward / loss_only)
+  void set_training(int t) {
+    train_ = true;
+    t_ = t;
+  }
+
+  // The fused output epilogue of layer l on worker w (mg_epi.cuh): its bias row and, for a hidden layer in
+  // a training pass, the dropout stream of (seed, step, layer).
+  k::Epi out_epi(const Worker& w, int l, bool hidden) const {
+    k::Epi e;
+    if (cfg_.bias) e.bias = w.W[l] + g_.ld[l] * g_.ld[l + 1];
+    if (hidden && train_ && cfg_.dropout > 0.0) {
+      e.thr = static_cast<unsigned>(std::min(4294967295.0, std::floor(cfg_.dropout * 4294967296.0)));
+      e.scale = static_cast<float>(1.0 / (1.0 - cfg_.dropout));
+      e.key = k::mix64(cfg_.seed ^ k::mix64(static_cast<unsigned long long>(t_) * 1024ull + static_cast<unsigned>(l) + 1ull));
+    }
+    e.row0 = w.r0;
+    return e;
+  }
 
   Worker& W(size_t k) { return *g_.workers[k]; }
   size_t nloc() const { return g_.workers.size(); }
@@ -878,7 +957,7 @@ class Step {
   // -------------------------------------------------------------- collectives
   // DeviceGroup::broadcast_bytes (collectives.cpp:110-125) on the comm streams.
   void bcast(int root, size_t count, const std::vector<float*>& bufs) {
-    if (P_ == 1) return;
+    if (P_ == 1 && !W(0).comm) return;
     if (g_.transport == MG_TRANSPORT_NCCL) {
       MG_NCCL(ncclGroupStart());
       for (size_t k = 0; k < nloc(); ++k) {
@@ -887,6 +966,7 @@ class Step {
         MG_NCCL(ncclBroadcast(bufs[k], bufs[k], count, ncclFloat, root, w.comm, w.s1));
       }
       MG_NCCL(ncclGroupEnd());
+      nccl_settle(g_);
       return;
     }
     // in-process: receivers copy from the root's buffer once it is ready; the root's comm stream then
@@ -912,7 +992,7 @@ class Step {
   // DeviceGroup::all_reduce_sum (collectives.hpp:76-94), no-op at P == 1.
   template <class T>
   void allreduce(size_t count, const std::vector<T*>& bufs) {
-    if (P_ == 1 || count == 0) return;
+    if ((P_ == 1 && !W(0).comm) || count == 0) return;
     if (g_.transport == MG_TRANSPORT_NCCL) {
       MG_NCCL(ncclGroupStart());
       for (size_t k = 0; k < nloc(); ++k) {
@@ -921,6 +1001,7 @@ class Step {
         MG_NCCL(ncclAllReduce(bufs[k], bufs[k], count, sizeof(T) == 8 ? ncclDouble : ncclFloat, ncclSum, w.comm, w.s1));
       }
       MG_NCCL(ncclGroupEnd());
+      nccl_settle(g_);
       return;
     }
     Worker& R = W(0);
@@ -953,7 +1034,7 @@ class Step {
   //   spmm(j) <- broadcast(j);   broadcast(j) <- spmm(j-2) overlapped / spmm(j-1) otherwise / prior.
   // relu_last fuses the forward ReLU into the final stage's epilogue.
   void staged_spmm(int dir, index_t width, const std::vector<float*>& src, const std::vector<float*>& out,
-                   bool relu_last) {
+                   bool relu_last, int epi_layer = -1) {
     const index_t ld = pad4(width);
     const bool ov = cfg_.overlap;
     std::vector<uint64_t> prior_task(nloc());
@@ -988,10 +1069,12 @@ class Step {
         const DevTile& t = w.tiles[dir][j];
         SpmmLaunch sl{t.row_ptr, t.edges, t.light, t.n_light, t.heavy, t.n_heavy};
         const int acc = j > 0, relu = relu_last && j == P_ - 1;
+        // the layer's bias / dropout ride on the final stage's output write
+        const k::Epi ep = (epi_layer >= 0 && j == P_ - 1) ? out_epi(w, epi_layer, relu_last) : k::Epi{};
         const int pi = prof_begin(w);
         if (cfg_.spmm_mode == MG_SPMM_FAST) {
           FastLaunch fl{t.items, t.n_items, t.hubs, t.n_hubs, t.edges, w.seg_scratch, t.hubs_classed, t.cols};
-          g_.kernels_last += spmm_fast(fl, recv[k], out[k], ld, acc, relu, w.s0);
+          g_.kernels_last += spmm_fast(fl, recv[k], out[k], ld, acc, relu, ep, w.s0);
           prof_end(w, pi, 0);
           mult_task[k][j] = tl_end(k, ts);
           MG_CUDA(cudaEventRecord(w.mult[j], w.s0));
@@ -1000,10 +1083,10 @@ class Step {
         if (t.n_heavy > 0) {  // hub rows run beside the light rows on the side stream
           MG_CUDA(cudaEventRecord(w.heavy_fork, w.s0));
           MG_CUDA(cudaStreamWaitEvent(w.s2, w.heavy_fork, 0));
-          g_.kernels_last += spmm_heavy(sl, recv[k], out[k], ld, acc, relu, w.s2);
+          g_.kernels_last += spmm_heavy(sl, recv[k], out[k], ld, acc, relu, ep, w.s2);
           MG_CUDA(cudaEventRecord(w.heavy_join, w.s2));
         }
-        g_.kernels_last += spmm_light(sl, recv[k], out[k], ld, acc, relu, w.s0);
+        g_.kernels_last += spmm_light(sl, recv[k], out[k], ld, acc, relu, ep, w.s0);
         if (t.n_heavy > 0) MG_CUDA(cudaStreamWaitEvent(w.s0, w.heavy_join, 0));
         prof_end(w, pi, 0);
         mult_task[k][j] = tl_end(k, ts);
@@ -1014,11 +1097,12 @@ class Step {
 
   // one GeMM task ("gemm", op, layer) on the compute lane, depending on the lane's previous task
   void gemm(size_t k, const char* op, int layer, bool ta, bool tb, index_t M, index_t N, index_t K, const float* A,
-            index_t lda, const float* B, index_t ldb, float* Cm, index_t ldc, int epi) {
+            index_t lda, const float* B, index_t ldb, float* Cm, index_t ldc, int epi, const k::Epi& ep = k::Epi{}) {
     Worker& w = W(k);
     const int th = tl_begin(k, 0, "gemm", op, layer, {w.last_task[0]});
     const int pi = prof_begin(w);
-    g_.kernels_last += gemm_launch(cfg_.gemm_mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, w.s0, w.ws, w.ws_bytes);
+    g_.kernels_last += gemm_launch(cfg_.gemm_mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, w.s0, w.ws, w.ws_bytes,
+                                   ep);
     prof_end(w, pi, 1);
     tl_end(k, th);
   }
@@ -1083,7 +1167,8 @@ class Step {
         for (size_t k = 0; k < nloc(); ++k) {
           Worker& w = W(k);
           dev(w);
-          gemm(k, "hw", 0, false, false, w.rows, ldl1, dl, w.ax, ldl, w.W[0], ldl1, w.ahw[0], ldl1, L_ > 1 ? 2 : 0);
+          gemm(k, "hw", 0, false, false, w.rows, ldl1, dl, w.ax, ldl, w.W[0], ldl1, w.ahw[0], ldl1, L_ > 1 ? 2 : 0,
+               out_epi(w, 0, L_ > 1));
         }
         continue;
       }
@@ -1099,12 +1184,13 @@ class Step {
         }
         out[k] = swap ? w.hw : w.ahw[l];
       }
-      staged_spmm(0, swap ? dl : dl1, src, out, !swap && l < L_ - 1);
+      staged_spmm(0, swap ? dl : dl1, src, out, !swap && l < L_ - 1, swap ? -1 : l);
       if (swap) {
         for (size_t k = 0; k < nloc(); ++k) {
           Worker& w = W(k);
           dev(w);
-          gemm(k, "hw", l, false, false, w.rows, ldl1, dl, w.hw, ldl, w.W[l], ldl1, w.ahw[l], ldl1, l < L_ - 1 ? 2 : 0);
+          gemm(k, "hw", l, false, false, w.rows, ldl1, dl, w.hw, ldl, w.W[l], ldl1, w.ahw[l], ldl1, l < L_ - 1 ? 2 : 0,
+               out_epi(w, l, l < L_ - 1));
         }
       }
     }
@@ -1168,7 +1254,7 @@ class Step {
       // W_G staging over the 8 canonical row blocks (gcn.hpp:309-331), then one all-reduce.
       std::vector<float*> stg(nloc());
       std::vector<int> trd(nloc(), -1);
-      const index_t bs = ldl * ldl1;
+      const index_t bs = g_.pstride(l);
       for (size_t k = 0; k < nloc(); ++k) {
         Worker& w = W(k);
         dev(w);
@@ -1199,6 +1285,15 @@ class Step {
             prof_end(w, pi, 1);
           }
         }
+        if (cfg_.bias) {  // the bias row of every canonical block: column sums of dL/dz_l = ahw[l]
+          int64_t begin[8], len[8];
+          for (int b = 0; b < 8; ++b) {
+            const index_t a = std::max(g_.wblocks[b], w.r0), e = std::min(g_.wblocks[b + 1], w.r0 + w.rows);
+            begin[b] = std::max<index_t>(0, a - w.r0);
+            len[b] = std::max<index_t>(0, e - a);
+          }
+          g_.kernels_last += bias_grad_blocks(w, w.ahw[l], ldl1, begin, len, w.stage[l] + ldl * ldl1, bs, w.s0);
+        }
         const uint64_t wg_task = tl_end(k, tw);
         MG_CUDA(cudaEventRecord(w.wg_done[l], w.s0));
         MG_CUDA(cudaStreamWaitEvent(w.s1, w.wg_done[l], 0));
@@ -1216,7 +1311,8 @@ class Step {
         for (size_t k = 0; k < nloc(); ++k) {
           Worker& w = W(k);
           dev(w);
-          gemm(k, "hgrad", l, false, true, w.rows, ldl, dl1, grad_rows[k], ldl1, w.W[l], ldl1, w.ahw[l - 1], ldl, 1);
+          gemm(k, "hgrad", l, false, true, w.rows, ldl, dl1, grad_rows[k], ldl1, w.W[l], ldl1, w.ahw[l - 1], ldl, 1,
+               out_epi(w, l - 1, true));
         }
       }
       (void)dl;
@@ -1235,7 +1331,7 @@ class Step {
       const int th = tl_begin(k, 0, "other", adam ? "adam" : "wgrad_final", -1, std::move(deps));
       const int pi = prof_begin(w);
       for (int l = 0; l < L_; ++l) {
-        const int size = static_cast<int>(g_.ld[l] * g_.ld[l + 1]);
+        const int size = static_cast<int>(g_.pstride(l));
         k::finalize_adam<<<std::min(1024, (size + 255) / 256), 256, 0, w.s0>>>(size, 8, w.stage[l], w.W[l], w.WG[l],
                                                                               w.M[l], w.V[l], adam ? 1 : 0, c);
         MG_LAUNCHED();
@@ -1248,7 +1344,13 @@ class Step {
 
   void begin() {
     g_.kernels_last = 0;
+    check_alive(g_);
     if (!g_.labels_ok) throw ValueError(g_.label_error);
+    if (const long long us = g_debug_stall_us.load()) {
+      dev(W(0));
+      stall_kernel<<<1, 1, 0, W(0).s0>>>(us * 1000);
+      MG_LAUNCHED();
+    }
     for (size_t k = 0; k < nloc(); ++k) {
       Worker& w = W(k);
       dev(w);
@@ -1272,21 +1374,91 @@ class Step {
   const Config& cfg_;
   int L_, P_;
   std::vector<std::vector<uint64_t>> red_task_ = std::vector<std::vector<uint64_t>>(g_.workers.size());
+  bool train_ = false;
+  int t_ = 1;
 };
 
+// ---------------------------------------------------------------- failure handling
+// Every host wait polls instead of blocking: it serves mg_group_abort requests, surfaces asynchronous NCCL
+// errors (a peer that died or never arrived) and enforces the "watchdog_ms" timeout. Any of them aborts
+// the group — ncclCommAbort on its communicators, which releases the device from a collective waiting
+// for a lost peer — and raises ShutdownError, like DeviceGroup::abort (collectives.cpp:33-52) wakes every
+// waiter with ShutdownError. An aborted group refuses further work.
+[[noreturn]] void abort_group(mg_group& g, const std::string& why) {
+  if (!g.aborted) {
+    g.aborted = true;
+    g.abort_reason = why;
+    for (auto& wp : g.workers)
+      if (wp->comm) {
+        cudaSetDevice(wp->device);
+        ncclCommAbort(wp->comm);
+        wp->comm = nullptr;
+      }
+  }
+  throw ShutdownError("device group aborted: " + g.abort_reason);
+}
+
+void check_alive(mg_group& g) {
+  if (g.aborted) throw ShutdownError("device group aborted: " + g.abort_reason);
+  if (g.abort_requested.load()) abort_group(g, "abort requested");
+}
+
+// Polls done() until it returns cudaSuccess; cudaErrorNotReady keeps waiting, anything else throws.
+template <class Query>
+void wait_for(mg_group& g, Query done, const char* what) {
+  using clk = std::chrono::steady_clock;
+  const auto t0 = clk::now();
+  const long long limit = g_watchdog_ms.load();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t e = done();
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) {
+      (void)cudaGetLastError();
+      throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+    }
+    check_alive(g);
+    for (auto& wp : g.workers)
+      if (wp->comm) {
+        ncclResult_t st = ncclSuccess;
+        ncclCommGetAsyncError(wp->comm, &st);
+        if (st != ncclSuccess && st != ncclInProgress)
+          abort_group(g, std::string("NCCL error on rank ") + std::to_string(wp->rank) + ": " + ncclGetErrorString(st));
+      }
+    if (limit > 0 && std::chrono::duration<double, std::milli>(clk::now() - t0).count() > static_cast<double>(limit))
+      abort_group(g, std::string(what) + " did not complete within watchdog_ms=" + std::to_string(limit));
+    if (spin < 256) std::this_thread::yield();
+    else std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+// Completes non-blocking NCCL calls (init, grouped collectives) on every local communicator.
+void nccl_settle(mg_group& g) {
+  for (auto& wp : g.workers) {
+    if (!wp->comm) continue;
+    ncclComm_t c = wp->comm;
+    wait_for(g, [c] {
+      ncclResult_t st = ncclSuccess;
+      ncclCommGetAsyncError(c, &st);
+      if (st == ncclInProgress) return cudaErrorNotReady;
+      if (st != ncclSuccess) throw NcclError(std::string("NCCL: ") + ncclGetErrorString(st));
+      return cudaSuccess;
+    }, "NCCL call");
+  }
+}
+
 void sync_all(mg_group& g) {
+  check_alive(g);
   for (auto& wp : g.workers) {
     MG_CUDA(cudaSetDevice(wp->device));
-    MG_CUDA(cudaStreamSynchronize(wp->s0));
-    MG_CUDA(cudaStreamSynchronize(wp->s1));
-    MG_CUDA(cudaStreamSynchronize(wp->s2));
+    for (cudaStream_t s : {wp->s0, wp->s1, wp->s2}) wait_for(g, [s] { return cudaStreamQuery(s); }, "stream");
   }
 }
 
 void read_stats(mg_group& g) {
   Worker& w = *g.workers[0];
   MG_CUDA(cudaSetDevice(w.device));
-  MG_CUDA(cudaEventSynchronize(w.stats_done));
+  cudaEvent_t e = w.stats_done;
+  wait_for(g, [e] { return cudaEventQuery(e); }, "step statistics");
   g.last_loss = w.h_stats[0] / static_cast<double>(g.mask_count);
   g.last_acc = w.h_stats[1] / static_cast<double>(g.mask_count);
 }
@@ -1305,6 +1477,14 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
     if (k == "heavy_row") {
       if (value < 1) throw ValueError("tuning: heavy_row must be >= 1");
       g_heavy_row = static_cast<int>(std::min<int64_t>(value, 1 << 30));
+    } else if (k == "watchdog_ms") {
+      if (value < 0) throw ValueError("tuning: watchdog_ms must be >= 0 (0 = no timeout)");
+      g_watchdog_ms = value;
+    } else if (k == "debug_stall_us") {
+      if (value < 0) throw ValueError("tuning: debug_stall_us must be >= 0");
+      g_debug_stall_us = value;
+    } else if (k == "nccl_single") {
+      g_nccl_single = value != 0 ? 1 : 0;
     } else if (k == "profile") {
       g_profile = value != 0 ? 1 : 0;
     } else if (k == "spmm_narrow_group") {
@@ -1316,6 +1496,10 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
     } else if (k == "spmm_hub_bytes") {
       if (value < 0) throw ValueError("tuning: spmm_hub_bytes must be >= 0");
       g_hub_bytes = value;
+    } else if (k == "block_cache") {
+      block_cache().enabled = value != 0;
+      if (!value)
+        for (int d = 0; d < 64 && d < mg_device_count(); ++d) block_cache().release(d);
     } else if (k == "bwd_transpose") {
       g_bwd_transpose = value != 0 ? 1 : 0;
     } else if (k == "spmm_async") {
@@ -1360,7 +1544,8 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
                           int32_t transport, mg_group** out) {
   return guarded([&] {
     if (!p || !out || n_local < 1 || !local_ranks || !devices) throw ValueError("group: bad arguments");
-    auto g = std::make_unique<mg_group>();
+    // a failure part-way releases what was built (streams, events, device blocks, communicators)
+    std::unique_ptr<mg_group, void (*)(mg_group*)> g(new mg_group(), mg_group_destroy);
     g->cfg = to_config(cfgp);
     const Config& cfg = g->cfg;
     if (cfg.dims.front() != p->d0)
@@ -1478,7 +1663,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       if (cfg.aggregate_first()) w.ax = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));
       // parameters, Adam state, W-grad staging (gcn.hpp:150-158), padded ld_l x ld_{l+1}
       for (int l = 0; l < L; ++l) {
-        const index_t sz = g->ld[l] * g->ld[l + 1];
+        const index_t sz = g->pstride(l);
         w.W.push_back(dalloc_t<float>(*g, w, sz));
         w.WG.push_back(dalloc_t<float>(*g, w, sz));
         w.M.push_back(dalloc_t<float>(*g, w, sz));
@@ -1497,6 +1682,15 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
                                  tc::nn_workspace_bytes(g->ld[l], g->ld[l + 1])});
         w.ws = static_cast<float*>(dalloc(*g, w, w.ws_bytes));
       }
+      if (cfg.bias) {
+        index_t kmax = 0;
+        for (int b = 0; b < 8; ++b) {
+          const index_t a = std::max(g->wblocks[b], w.r0), e = std::min(g->wblocks[b + 1], w.r0 + w.rows);
+          kmax = std::max(kmax, e - a);
+        }
+        w.bias_chunks = static_cast<int>((kmax + k::kBiasChunk - 1) / k::kBiasChunk);
+        w.bias_part = dalloc_t<float>(*g, w, std::max<size_t>(1, static_cast<size_t>(8) * w.bias_chunks * g->ld_max));
+      }
       w.loss_blocks = std::max(1, std::min(ceil_div(w.rows, 8), num_sms() * 8));
       w.partials = dalloc_t<double>(*g, w, 2 * w.loss_blocks);
       w.stats = dalloc_t<double>(*g, w, 2);
@@ -1504,21 +1698,21 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       g->workers.push_back(std::move(wp));
       sw.lap("buffers");
     }
-    if (transport == MG_TRANSPORT_NCCL && world > 1) {
-      if (n_local == world && !nccl_id) {
-        std::vector<ncclComm_t> comms(n_local);
-        MG_NCCL(ncclCommInitAll(comms.data(), n_local, devs.data()));
-        for (int k = 0; k < n_local; ++k) g->workers[k]->comm = comms[k];
-      } else {
-        ncclUniqueId u;
-        std::memcpy(&u, nccl_id, 128);
-        MG_NCCL(ncclGroupStart());
-        for (int k = 0; k < n_local; ++k) {
-          MG_CUDA(cudaSetDevice(g->workers[k]->device));
-          MG_NCCL(ncclCommInitRank(&g->workers[k]->comm, world, u, g->workers[k]->rank));
-        }
-        MG_NCCL(ncclGroupEnd());
+    if (transport == MG_TRANSPORT_NCCL && (world > 1 || g_nccl_single.load())) {
+      // non-blocking communicators (see MG_NCCL): a peer that never arrives surfaces as a watchdog abort
+      // instead of a hang inside ncclCommInitRank
+      ncclUniqueId u;
+      if (nccl_id) std::memcpy(&u, nccl_id, 128);
+      else MG_NCCL(ncclGetUniqueId(&u));  // every rank is in this process
+      ncclConfig_t nc = NCCL_CONFIG_INITIALIZER;
+      nc.blocking = 0;
+      MG_NCCL(ncclGroupStart());
+      for (int k = 0; k < n_local; ++k) {
+        MG_CUDA(cudaSetDevice(g->workers[k]->device));
+        MG_NCCL(ncclCommInitRankConfig(&g->workers[k]->comm, world, u, g->workers[k]->rank, &nc));
       }
+      MG_NCCL(ncclGroupEnd());
+      nccl_settle(*g);
     }
     sw.lap("nccl");
     for (auto& wp : g->workers) {
@@ -1533,6 +1727,15 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
 
 // GcnWorker::init_params (gcn.hpp:163-173): one Rng(seed) across layers, Glorot-uniform in double,
 // cast to float; identical on every worker (the reference broadcasts rank 0's draw).
+// DeviceGroup::abort (collectives.cpp:42-52): callable from any thread; the next (or current) host wait on
+// the group aborts its communicators and raises ShutdownError, and the group refuses further work.
+mg_status mg_group_abort(mg_group* g) {
+  return guarded([&] {
+    if (!g) throw ValueError("group: null");
+    g->abort_requested = true;
+  });
+}
+
 mg_status mg_group_init_params(mg_group* g) {
   return guarded([&] {
     Rng rng(g->cfg.seed);
@@ -1545,7 +1748,8 @@ mg_status mg_group_init_params(mg_group* g) {
       for (auto& wp : g->workers) {
         MG_CUDA(cudaSetDevice(wp->device));
         upload_padded(wp->W[l], w.data(), dl, dl1, g->ld[l + 1]);
-        const size_t sz = sizeof(float) * g->ld[l] * g->ld[l + 1];
+        const size_t sz = sizeof(float) * g->pstride(l);
+        if (g->cfg.bias) MG_CUDA(cudaMemset(wp->W[l] + g->ld[l] * g->ld[l + 1], 0, sizeof(float) * g->ld[l + 1]));
         MG_CUDA(cudaMemset(wp->M[l], 0, sz));
         MG_CUDA(cudaMemset(wp->V[l], 0, sz));
         MG_CUDA(cudaMemset(wp->WG[l], 0, sz));
@@ -1556,6 +1760,7 @@ mg_status mg_group_init_params(mg_group* g) {
 
 static void enqueue_train(mg_group* g, int t, bool adam) {
   Step st(*g);
+  st.set_training(t);
   st.begin();
   st.forward();
   st.loss_grad();
@@ -1696,6 +1901,13 @@ static TensorView tensor_view(mg_group* g, Worker& w, int which, int layer) {
       // 8 blocks of (ld_l x ld_{l+1}); exposed as 8 d_l x d_{l+1} blocks stacked
       return {w.stage[layer], 8 * g->cfg.dims[layer], g->cfg.dims[layer + 1], g->ld[layer + 1]};
     }
+    case MG_T_BIAS:
+    case MG_T_BIAS_GRAD: {
+      need_layer();
+      if (!g->cfg.bias) throw ValueError("tensor: the group has no bias (config bias = 0)");
+      float* base = which == MG_T_BIAS ? w.W[layer] : w.WG[layer];
+      return {base + g->ld[layer] * g->ld[layer + 1], 1, g->cfg.dims[layer + 1], g->ld[layer + 1]};
+    }
     default: throw ValueError("tensor: unknown id " + std::to_string(which));
   }
 }
@@ -1709,7 +1921,7 @@ mg_status mg_group_read(mg_group* g, int32_t rank, int32_t which, int32_t layer,
     if (count != v.rows * v.cols)
       throw ShapeError("tensor: count " + std::to_string(count) + " != " + shape_str(v.rows, v.cols));
     if (which == MG_T_WSTAGE) {
-      const index_t dl = g->cfg.dims[layer], bs = g->ld[layer] * g->ld[layer + 1];
+      const index_t dl = g->cfg.dims[layer], bs = g->pstride(layer);
       for (int b = 0; b < 8; ++b) download_padded(dst + b * dl * v.cols, v.p + b * bs, dl, v.cols, v.ld);
       return;
     }
@@ -1799,18 +2011,19 @@ void mg_group_destroy(mg_group* g) {
     Worker& w = *wp;
     cudaSetDevice(w.device);
     cudaDeviceSynchronize();
-    if (w.comm) ncclCommDestroy(w.comm);
+    (void)cudaGetLastError();
+    // an aborted communicator is gone already; a drained one has nothing in flight, so abort = release
+    if (w.comm) ncclCommAbort(w.comm);
     for (auto& a : w.allocs) block_cache().put(w.device, a.first, a.second);
     if (w.h_stats) cudaFreeHost(w.h_stats);
     for (cudaEvent_t e : {w.prior, w.heavy_fork, w.heavy_join, w.loss_done, w.stats_done, w.src_ready, w.copy_done,
                           w.ar_ready, w.ar_done, w.t_start, w.t_end})
-      cudaEventDestroy(e);
+      if (e) cudaEventDestroy(e);
     for (auto* vec : {&w.bc_done, &w.mult, &w.wg_done, &w.red_done, &w.tl_pool})
       for (cudaEvent_t e : *vec) cudaEventDestroy(e);
     if (w.tl_base) cudaEventDestroy(w.tl_base);
-    cudaStreamDestroy(w.s0);
-    cudaStreamDestroy(w.s1);
-    cudaStreamDestroy(w.s2);
+    for (cudaStream_t st : {w.s0, w.s1, w.s2})
+      if (st) cudaStreamDestroy(st);
   }
   if (!g->workers.empty()) cudaSetDevice(g->workers[0]->device);
   for (cudaEvent_t e : g->prof_pool) cudaEventDestroy(e);
@@ -1915,7 +2128,7 @@ mg_status mg_dev_spmm(int64_t rows, const int32_t* row_ptr, const void* edges, c
       if (!hubs.empty()) MG_CUDA(cudaMemcpy(dh, hubs.data(), sizeof(int4) * hubs.size(), cudaMemcpyHostToDevice));
       FastLaunch fl{di, static_cast<int>(items.size()), dh, static_cast<int>(hubs.size()),
                     static_cast<const int2*>(edges), sc};
-      spmm_fast(fl, h, out, ld, accumulate, relu, s);
+      spmm_fast(fl, h, out, ld, accumulate, relu, k::Epi{}, s);
       MG_CUDA(cudaStreamSynchronize(s));
       cudaFree(di);
       cudaFree(dh);
@@ -1939,8 +2152,8 @@ mg_status mg_dev_spmm(int64_t rows, const int32_t* row_ptr, const void* edges, c
     }
     SpmmLaunch sl{row_ptr, ep ? ep : static_cast<const int2*>(edges), dl, static_cast<int>(light.size()), dh,
                   static_cast<int>(heavy.size())};
-    spmm_heavy(sl, h, out, ld, accumulate, relu, s);
-    spmm_light(sl, h, out, ld, accumulate, relu, s);
+    spmm_heavy(sl, h, out, ld, accumulate, relu, k::Epi{}, s);
+    spmm_light(sl, h, out, ld, accumulate, relu, k::Epi{}, s);
     MG_CUDA(cudaStreamSynchronize(s));
     cudaFree(dl);
     cudaFree(dh);

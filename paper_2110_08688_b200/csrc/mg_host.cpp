@@ -6,6 +6,7 @@
 // but restructured for a many-core host: counting sorts, per-row sorts and per-column sums run in
 // parallel where the reference's result does not depend on the order of independent work.
 #include <algorithm>
+#include <limits>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -145,6 +146,11 @@ Config to_config(const mg_config* c) {
   if (c->aggregate_input != 0 && c->aggregate_input != 1)
     throw ConfigError("config: aggregate_input must be 0 or 1, got " + std::to_string(c->aggregate_input));
   cfg.aggregate_input = c->aggregate_input != 0;
+  if (c->bias != 0 && c->bias != 1) throw ConfigError("config: bias must be 0 or 1, got " + std::to_string(c->bias));
+  cfg.bias = c->bias != 0;
+  if (!(c->dropout >= 0.0 && c->dropout < 1.0))
+    throw ConfigError("config: dropout must be in [0, 1), got " + std::to_string(c->dropout));
+  cfg.dropout = c->dropout;
   if (cfg.layers() < 1)
     throw ConfigError("config: need at least one layer (layer_dims has " + std::to_string(cfg.dims.size()) +
                       " entries)");
@@ -165,33 +171,44 @@ void Csr::validate() const {
   if (row_ptr[0] != 0) throw ValueError("csr: row_ptr[0] != 0");
   if (row_ptr[rows] != nnz()) throw ValueError("csr: row_ptr[rows] != nnz");
   if (values.size() != col_idx.size()) throw ValueError("csr: values/col_idx length mismatch");
-  std::atomic<index_t> bad_row{-1};
-  std::atomic<int> bad_kind{0};
+  // Rows are checked in parallel chunks; each chunk keeps its first violation in (row, entry) order and the
+  // lowest row wins, so the error is the one the reference's serial scan reports first, with its message.
+  struct Bad {
+    index_t row = -1, col = 0;
+    int kind = 0;
+  };
+  std::mutex mu;
+  Bad first;
+  std::atomic<index_t> first_row{std::numeric_limits<index_t>::max()};
   parallel_for(rows, [&](index_t b, index_t e) {
-    for (index_t u = b; u < e && bad_row.load() < 0; ++u) {
+    Bad mine;
+    for (index_t u = b; u < e && mine.row < 0 && u < first_row.load(); ++u) {
       if (row_ptr[u] > row_ptr[u + 1]) {
-        bad_kind = 1;
-        bad_row = u;
-        return;
+        mine = {u, 0, 1};
+        break;
       }
       for (index_t k = row_ptr[u]; k < row_ptr[u + 1]; ++k) {
         if (col_idx[k] < 0 || col_idx[k] >= cols) {
-          bad_kind = 2;
-          bad_row = u;
-          return;
+          mine = {u, col_idx[k], 2};
+          break;
         }
         if (k > row_ptr[u] && col_idx[k] <= col_idx[k - 1]) {
-          bad_kind = 3;
-          bad_row = u;
-          return;
+          mine = {u, 0, 3};
+          break;
         }
       }
     }
+    if (mine.row < 0) return;
+    std::lock_guard<std::mutex> lk(mu);
+    if (first.row < 0 || mine.row < first.row) {
+      first = mine;
+      first_row = mine.row;
+    }
   });
-  if (bad_row.load() >= 0) {
-    const std::string r = std::to_string(bad_row.load());
-    if (bad_kind == 1) throw ValueError("csr: row_ptr not nondecreasing");
-    if (bad_kind == 2) throw ValueError("csr: col out of range in row " + r);
+  if (first.row >= 0) {
+    const std::string r = std::to_string(first.row);
+    if (first.kind == 1) throw ValueError("csr: row_ptr not nondecreasing");
+    if (first.kind == 2) throw ValueError("csr: col " + std::to_string(first.col) + " out of range in row " + r);
     throw ValueError("csr: columns not strictly increasing in row " + r);
   }
 }

@@ -26,6 +26,7 @@ struct Error : std::runtime_error {
 struct ShapeError : Error { explicit ShapeError(const std::string& m) : Error(MG_SHAPE_ERROR, m) {} };
 struct ValueError : Error { explicit ValueError(const std::string& m) : Error(MG_VALUE_ERROR, m) {} };
 struct ProtocolError : Error { explicit ProtocolError(const std::string& m) : Error(MG_PROTOCOL_ERROR, m) {} };
+struct ShutdownError : Error { explicit ShutdownError(const std::string& m) : Error(MG_SHUTDOWN_ERROR, m) {} };
 struct ConfigError : Error { explicit ConfigError(const std::string& m) : Error(MG_CONFIG_ERROR, m) {} };
 struct CudaError : Error { explicit CudaError(const std::string& m) : Error(MG_CUDA_ERROR, m) {} };
 struct NcclError : Error { explicit NcclError(const std::string& m) : Error(MG_NCCL_ERROR, m) {} };
@@ -90,6 +91,8 @@ struct Config {
   int gemm_mode = MG_GEMM_TF32X3;
   int spmm_mode = MG_SPMM_EXACT;
   bool aggregate_input = false;
+  bool bias = false;     // default-off extension: learned bias per layer (mggcn.h)
+  double dropout = 0.0;  // default-off extension: dropout probability of hidden-layer outputs (mggcn.h)
   int layers() const { return static_cast<int>(dims.size()) - 1; }
   // Layer 0 as (Â·X)·W0 with Â·X kept for W0's gradient: one d0-wide SpMM replaces the d1-wide forward
   // and backward ones. Reassociation changes the float order, so only in MG_SPMM_FAST.

@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "mg_epi.cuh"
+
 namespace mg {
 namespace k {
 
@@ -28,6 +30,7 @@ __device__ __forceinline__ void axpy4(float4& acc, float v, const float4& x) {
   acc.w = fma_free(acc.w, v, x.w);
 }
 __device__ __forceinline__ float relu1(float x) { return x > 0.0f ? x : 0.0f; }  // dense.hpp:214
+
 
 // FAST-mode edge records carry a hub class in the top 4 bits of the column (mg_device.cu upload_tile):
 // class k in 1..7 = the column is among the 10000 * 2^(k-1) most gathered of its tile, 0 = no class.
@@ -61,7 +64,7 @@ template <int G, int CPL>
 __global__ void __launch_bounds__(256) spmm_exact_rows(const int* __restrict__ row_ptr, const int2* __restrict__ edges,
                                                        const int* __restrict__ order, int n_order,
                                                        const float* __restrict__ h, float* __restrict__ out, int ld,
-                                                       int nchunk, int accumulate, int relu) {
+                                                       int nchunk, int accumulate, int relu, Epi ep) {
   constexpr int U = (CPL <= 2) ? 4 : 2;
   const int lane = threadIdx.x & (G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
@@ -114,11 +117,7 @@ __global__ void __launch_bounds__(256) spmm_exact_rows(const int* __restrict__ r
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       const int c = lane + k * G;
-      if (c < nchunk) {
-        float4 a = acc[k];
-        if (relu) a = make_float4(relu1(a.x), relu1(a.y), relu1(a.z), relu1(a.w));
-        *reinterpret_cast<float4*>(orow + 4 * c) = a;
-      }
+      if (c < nchunk) *reinterpret_cast<float4*>(orow + 4 * c) = epi4(acc[k], relu, ep, r, 4 * c);
     }
   }
 }
@@ -143,7 +142,7 @@ template <int G, int CPL>
 __global__ void __launch_bounds__(256) spmm_fast_items(const int4* __restrict__ items, int n_items,
                                                        const int2* __restrict__ edges, const float* __restrict__ h,
                                                        float* __restrict__ out, float* __restrict__ scratch, int ld,
-                                                       int nchunk, int accumulate, int relu) {
+                                                       int nchunk, int accumulate, int relu, Epi ep) {
   constexpr int U = (CPL <= 2) ? 4 : 2;
   const int lane = threadIdx.x & (G - 1);
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
@@ -197,11 +196,7 @@ __global__ void __launch_bounds__(256) spmm_fast_items(const int4* __restrict__ 
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       const int c = lane + k * G;
-      if (c < nchunk) {
-        float4 a = acc[k];
-        if (relu && !seg) a = make_float4(relu1(a.x), relu1(a.y), relu1(a.z), relu1(a.w));
-        *reinterpret_cast<float4*>(orow + 4 * c) = a;
-      }
+      if (c < nchunk) *reinterpret_cast<float4*>(orow + 4 * c) = seg ? acc[k] : epi4(acc[k], relu, ep, it.z, 4 * c);
     }
   }
 }
@@ -235,7 +230,7 @@ template <int G, int CPL, int E, int D, bool HINT>
 __global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ items, int n_items,
                                                        const int2* __restrict__ edges, const float* __restrict__ h,
                                                        float* __restrict__ out, float* __restrict__ scratch, int ld,
-                                                       int nchunk, int accumulate, int relu, int hub_max) {
+                                                       int nchunk, int accumulate, int relu, int hub_max, Epi ep) {
   static_assert(G % E == 0 && (D - 1) * E <= G, "pipeline depth must stay within one record window");
   uint64_t pol_last = 0, pol_first = 0;
   if (HINT) {
@@ -324,11 +319,7 @@ __global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ 
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       const int c = lane + k * G;
-      if (c < nchunk) {
-        float4 a = acc[k];
-        if (relu && !seg) a = make_float4(relu1(a.x), relu1(a.y), relu1(a.z), relu1(a.w));
-        *reinterpret_cast<float4*>(orow + 4 * c) = a;
-      }
+      if (c < nchunk) *reinterpret_cast<float4*>(orow + 4 * c) = seg ? acc[k] : epi4(acc[k], relu, ep, it.z, 4 * c);
     }
   }
 }
@@ -384,7 +375,7 @@ __global__ void hub_tag(int2* __restrict__ edges, long nnz, const int* __restric
 // hubs[i] = {row, first segment, segment count}: out[row] = (acc ? out[row] : 0) + sum of its segments in
 // order, then relu. One CTA per hub row, threads over float4 chunks.
 __global__ void __launch_bounds__(256) spmm_fast_hubs(const int4* __restrict__ hubs, const float* __restrict__ scratch,
-                                                      float* __restrict__ out, int ld, int accumulate, int relu) {
+                                                      float* __restrict__ out, int ld, int accumulate, int relu, Epi ep) {
   const int4 hb = hubs[blockIdx.x];
   float* orow = out + (size_t)hb.x * ld;
   for (int c = threadIdx.x; c < ld / 4; c += blockDim.x) {
@@ -396,8 +387,7 @@ __global__ void __launch_bounds__(256) spmm_fast_hubs(const int4* __restrict__ h
       s.z += p.z;
       s.w += p.w;
     }
-    if (relu) s = make_float4(relu1(s.x), relu1(s.y), relu1(s.z), relu1(s.w));
-    *reinterpret_cast<float4*>(orow + 4 * c) = s;
+    *reinterpret_cast<float4*>(orow + 4 * c) = epi4(s, relu, ep, hb.x, 4 * c);
   }
 }
 
@@ -452,7 +442,7 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __r
                                                                   const int2* __restrict__ edges,
                                                                   const int* __restrict__ heavy, int nslab,
                                                                   const float* __restrict__ h, float* __restrict__ out,
-                                                                  int ld, int accumulate, int relu) {
+                                                                  int ld, int accumulate, int relu, Epi ep) {
   extern __shared__ __align__(128) float smem[];
   float* buf = smem;                                                            // [NST][B][SLAB] h slabs
   int2* ering = reinterpret_cast<int2*>(smem + kHeavyNst * kHeavyB * kHeavySlab);  // [ESLOTS][B + 2] edge records
@@ -536,7 +526,7 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __r
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (active) out[(size_t)r * ld + my_col] = relu ? relu1(acc) : acc;
+    if (active) out[(size_t)r * ld + my_col] = (ep.bias || ep.thr) ? epi1(acc, relu, ep, r, my_col) : (relu ? relu1(acc) : acc);
   }
 }
 
@@ -544,13 +534,14 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __r
 // C[M,N] = op(A) op(B) with the reference's per-element order: k ascending, separate multiply and
 // add; NN/TN skip zero A entries (dense.hpp:165, :177); NT forms the dot product then adds it to a
 // zeroed output (dense.hpp:189-191, i.e. 0 + acc). 64x64 tiles, 256 threads, 4x4 outputs each.
-// EPI 0: store; 1: relu_backward in place, C = C_old > 0 ? r : 0 (dense.hpp:221-231); 2: relu.
+// EPI 0: store; 1: relu_backward in place, C = C_old > 0 ? r : 0 (dense.hpp:221-231); 2: relu. EPI 0 / 2
+// add the optional bias and apply the optional dropout (Epi); EPI 1 scales the kept entries by 1 / (1 - p).
 constexpr int kGBM = 64, kGBN = 64, kGBK = 16;
 
 template <bool TA, bool TB, int EPI>
 __global__ void __launch_bounds__(256) gemm_exact(int M, int N, int K, const float* __restrict__ A, long lda,
                                                   const float* __restrict__ B, long ldb, float* __restrict__ C,
-                                                  long ldc) {
+                                                  long ldc, Epi ep) {
   __shared__ float As[kGBK][kGBM + 4];
   __shared__ float Bs[kGBK][kGBN + 4];
   const int tid = threadIdx.x;
@@ -610,8 +601,8 @@ __global__ void __launch_bounds__(256) gemm_exact(int M, int N, int K, const flo
       float r = acc[i][j];
       if (TB) r = __fadd_rn(0.0f, r);  // out(i,j) += acc on a zeroed out
       float* cp = C + m * ldc + n;
-      if (EPI == 1) r = (*cp > 0.0f) ? r : 0.0f;
-      if (EPI == 2) r = relu1(r);
+      if (EPI == 1) r = (*cp > 0.0f) ? (ep.thr ? __fmul_rn(r, ep.scale) : r) : 0.0f;  // dropout-kept: x 1/(1-p)
+      else r = epi1(r, EPI == 2, ep, m, n);
       *cp = r;
     }
   }
@@ -786,6 +777,37 @@ __global__ void finalize_adam(int size, int blocks, const float* __restrict__ st
     v[i] = vi;
     w[i] = __fsub_rn(w[i], __fdiv_rn(__fmul_rn(c.lr, mhat), __fadd_rn(__fsqrt_rn(vhat), c.eps)));
     g[i] = 0.0f;
+  }
+}
+
+// ============================================================================ bias gradient (extension)
+// dL/db_l = column sums of dL/dz_l over the rows of each canonical W-grad block (gcn.hpp:309-331 applied to
+// a bias row), deterministic: fixed 1024-row chunks from the block's first local row, each folded
+// sequentially per column, then the chunk partials summed in chunk order. For P | 8 no block spans two
+// workers (uniform_partition bounds coincide), so the result is bitwise P-invariant like W_G.
+constexpr int kBiasChunk = 1024;
+struct BlockRanges {
+  long long begin[8], len[8];
+};
+__global__ void bias_partials(const float* __restrict__ G, int ld, BlockRanges br, int max_chunks,
+                              float* __restrict__ partial) {
+  const int b = blockIdx.y, c = blockIdx.x;
+  const long long r0 = br.begin[b] + static_cast<long long>(c) * kBiasChunk;
+  const long long r1 = min(r0 + kBiasChunk, br.begin[b] + br.len[b]);
+  for (int col = threadIdx.x; col < ld; col += blockDim.x) {
+    float acc = 0.0f;
+    for (long long r = r0; r < r1; ++r) acc = __fadd_rn(acc, G[r * ld + col]);
+    partial[(static_cast<long long>(b) * max_chunks + c) * ld + col] = acc;
+  }
+}
+__global__ void bias_reduce(const float* __restrict__ partial, BlockRanges br, int max_chunks, int ld,
+                            float* __restrict__ out, long long block_stride) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 8 * ld; i += gridDim.x * blockDim.x) {
+    const int b = i / ld, col = i % ld;
+    const int nch = static_cast<int>((br.len[b] + kBiasChunk - 1) / kBiasChunk);
+    float s = 0.0f;
+    for (int c = 0; c < nch; ++c) s = __fadd_rn(s, partial[(static_cast<long long>(b) * max_chunks + c) * ld + col]);
+    out[b * block_stride + col] = s;
   }
 }
 

@@ -10,7 +10,7 @@
 // the UMMA canonical smem layouts: K-major operands (A of NN/NT, B of NT) as SWIZZLE_64B boxes
 // {16 k, rows}; MN-major operands (B = W of NN, both operands of TN, which are K x M row-major in HBM)
 // as SWIZZLE_128B boxes {32 mn, 16 k} — no transposition anywhere. Warps 2-5 split each element
-// in place, x = hi + lo with hi = x & 0xffffe000 (exact in TF32) and lo = x - hi (exact in fp32), and
+// in place, x = hi + lo with hi and lo both rounded to nearest TF32 (split_hi / split_lo below), and
 // mask TN rows past the chunk end. Warp 1 (one lane) issues tcgen05.mma.kind::tf32 (M = 128,
 // N <= 256, K = 8) into one of two TMEM accumulators:
 //   TF32X3: D += A_lo B_hi + A_hi B_lo + A_hi B_hi      TF32: D += A_hi B_hi
@@ -83,6 +83,7 @@ struct Params {
   int bnr;               // B rows (tile columns) loaded per stage: min(np, 128) (TN: rounded to 32)
   int nwst;              // v3: W ring stages (nst = A ring stages)
   int epi_chunks;        // v3: 32 x 32 epilogue buffers per epilogue warp (2, or 4 with the relu_backward mask)
+  k::Epi ep;             // fused bias / dropout (EPI 0, 2) and the dropout scale of the relu_backward mask (EPI 1)
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -202,14 +203,42 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+// 3xTF32 splits round to nearest: x = hi + lo with hi = rn_tf32(x) and lo = rn_tf32(x - hi), so every
+// dropped part (the rounding of lo, the omitted lo*lo product) has a data-independent sign. Truncated
+// splits (hi = x & 0xFFFFE000, lo left for the tensor core to truncate) leave errors with the sign of x,
+// which add up coherently over a long K: W-grads at C4 (K = 306K rows per canonical block) came out
+// ~1.6e-4 (normwise) off the fp32 reference; with round-to-nearest splits they are ~1e-6.
+__device__ __forceinline__ float tf32_rn(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ float split_hi(float x) { return tf32_rn(x); }
+__device__ __forceinline__ float split_lo(float x, float hi) { return tf32_rn(__fsub_rn(x, hi)); }
+// lo part for an operand whose hi part is the raw fp32 tile (kind::tf32 truncates it: hi = x & 0xFFFFE000)
+__device__ __forceinline__ float split_lo_trunc(float x) {
+  return tf32_rn(__fsub_rn(x, __uint_as_float(__float_as_uint(x) & 0xFFFFE000u)));
+}
 __device__ __forceinline__ float4 split4(float4 x, float4& lo) {
   float4 h;
-  h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-  h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-  h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-  h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-  lo = make_float4(__fsub_rn(x.x, h.x), __fsub_rn(x.y, h.y), __fsub_rn(x.z, h.z), __fsub_rn(x.w, h.w));
+  h.x = split_hi(x.x);
+  h.y = split_hi(x.y);
+  h.z = split_hi(x.z);
+  h.w = split_hi(x.w);
+  lo = make_float4(split_lo(x.x, h.x), split_lo(x.y, h.y), split_lo(x.z, h.z), split_lo(x.w, h.w));
   return h;
+}
+
+// The NN / NT epilogue on 4 consecutive outputs of row `row`, columns col..col+3: 1 = relu_backward mask
+// (kept entries x 1/(1-p) under dropout), 2 = relu, 0 = store; bias / dropout per mg_epi.cuh.
+__device__ __forceinline__ float4 gemm_epi(float4 o, float4 old, const Params& p, long row, int col) {
+  if (p.epi == 1) {
+    if (p.ep.thr) o = make_float4(__fmul_rn(o.x, p.ep.scale), __fmul_rn(o.y, p.ep.scale), __fmul_rn(o.z, p.ep.scale),
+                                  __fmul_rn(o.w, p.ep.scale));
+    return make_float4(old.x > 0.0f ? o.x : 0.0f, old.y > 0.0f ? o.y : 0.0f, old.z > 0.0f ? o.z : 0.0f,
+                       old.w > 0.0f ? o.w : 0.0f);
+  }
+  return k::epi4(o, p.epi == 2, p.ep, row, col);
 }
 
 // Ring cursor (slot, phase parity, wrapped) for rings whose depth is a runtime value: replaces sc % n and
@@ -462,8 +491,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_tc(const __grid_constant__ C
             for (int r = 0; r < 32; ++r) {
               if (r < nrows) {
                 float x = stg[r * 33 + lane];
-                if (p.epi == 1) x = old[r] > 0.0f ? x : 0.0f;
-                if (p.epi == 2) x = x > 0.0f ? x : 0.0f;
+                if (p.epi == 1) x = old[r] > 0.0f ? (p.ep.thr ? __fmul_rn(x, p.ep.scale) : x) : 0.0f;
+                else x = k::epi1(x, p.epi == 2, p.ep, g0 + r, static_cast<int>(c));
                 dst[static_cast<long>(r) * p.ldc] = x;
               }
             }
@@ -620,9 +649,9 @@ __global__ void split_b(const float* __restrict__ W, long ldw, int trans, int np
     const long n = i / kp, k = i % kp;
     float x = 0.0f;
     if (n < nvalid && k < kvalid) x = trans ? W[k * ldw + n] : W[n * ldw + k];
-    const float h = terms == 3 ? __uint_as_float(__float_as_uint(x) & 0xFFFFE000u) : x;
+    const float h = terms == 3 ? split_hi(x) : x;
     hi[i] = h;
-    lo[i] = terms == 3 ? __fsub_rn(x, h) : 0.0f;
+    lo[i] = terms == 3 ? split_lo(x, h) : 0.0f;
   }
 }
 
@@ -804,9 +833,9 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
         uint32_t hi[BKV], lo[BKV];
 #pragma unroll
         for (int k = 0; k < BKV; ++k) {
-          const float h = p.terms == 3 ? __uint_as_float(__float_as_uint(x[k]) & 0xFFFFE000u) : x[k];
+          const float h = p.terms == 3 ? split_hi(x[k]) : x[k];
           hi[k] = __float_as_uint(h);
-          lo[k] = __float_as_uint(__fsub_rn(x[k], h));
+          lo[k] = __float_as_uint(p.terms == 3 ? split_lo(x[k], h) : 0.0f);
         }
         const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(kAcol + s * 2 * BKV);
 #pragma unroll
@@ -823,9 +852,10 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
     }
   } else if (warp >= 10) {
     // ------------------------------------------------------------ TN: B (G rows) lo copy
-    // kind::tf32 reads the raw fp32 tile as its hi part: the tensor core drops the low 13 mantissa bits,
-    // exactly the x & 0xFFFFE000 of split4, so only lo = x - hi is written (half the shared-memory
-    // stores of rewriting hi in place; the kernel is shared-memory-bandwidth bound at this stage).
+    // kind::tf32 reads the raw fp32 tile as its hi part: the tensor core drops the low 13 mantissa bits
+    // (hi = x & 0xFFFFE000), so only lo = rn_tf32(x - hi) is written (half the shared-memory stores of
+    // rewriting hi in place; the kernel is shared-memory-bandwidth bound at this stage). lo rounds to
+    // nearest, and A's split does too, so the omitted A_lo * B_lo term has no systematic sign.
     if (MODE == TN && p.terms == 3) {
       const int t = threadIdx.x - 320;
       RingPos rp(p.nst);
@@ -841,7 +871,7 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
                          : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                          : "r"(bh + 16u * q4));
-            (void)split4(v, l);
+            l = make_float4(split_lo_trunc(v.x), split_lo_trunc(v.y), split_lo_trunc(v.z), split_lo_trunc(v.w));
             asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(bl + 16u * q4), "f"(l.x), "f"(l.y),
                          "f"(l.z), "f"(l.w)
                          : "memory");
@@ -891,12 +921,8 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
                 const float4 pv = *dst;
                 o = make_float4(__fadd_rn(pv.x, o.x), __fadd_rn(pv.y, o.y), __fadd_rn(pv.z, o.z), __fadd_rn(pv.w, o.w));
               }
-            } else if (p.epi == 1) {
-              const float4 old = *dst;
-              o = make_float4(old.x > 0.0f ? o.x : 0.0f, old.y > 0.0f ? o.y : 0.0f, old.z > 0.0f ? o.z : 0.0f,
-                              old.w > 0.0f ? o.w : 0.0f);
-            } else if (p.epi == 2) {
-              o = make_float4(fmaxf(o.x, 0.0f), fmaxf(o.y, 0.0f), fmaxf(o.z, 0.0f), fmaxf(o.w, 0.0f));
+            } else {
+              o = gemm_epi(o, p.epi == 1 ? *dst : o, p, grow0 + lane, I.n0 + c * 32 + 4 * j);
             }
             *dst = o;
           }
@@ -1142,9 +1168,9 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
         uint32_t hi[BK3], lo[BK3];
 #pragma unroll
         for (int k = 0; k < BK3; ++k) {
-          const float h = p.terms == 3 ? __uint_as_float(__float_as_uint(x[k]) & 0xFFFFE000u) : x[k];
+          const float h = p.terms == 3 ? split_hi(x[k]) : x[k];
           hi[k] = __float_as_uint(h);
-          lo[k] = __float_as_uint(__fsub_rn(x[k], h));
+          lo[k] = __float_as_uint(p.terms == 3 ? split_lo(x[k], h) : 0.0f);
         }
         if (sc >= static_cast<uint32_t>(kTSlots3)) mbar_wait(&tslot[j], ((sc / kTSlots3) - 1) & 1);
         tc_fence_after();
@@ -1201,13 +1227,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
           for (int jj = 0; jj < 8; ++jj) {
             float4 o = make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
             float4* dst = sw128(b, lane, jj);
-            if (p.epi == 1) {
-              const float4 old = *dst;
-              o = make_float4(old.x > 0.0f ? o.x : 0.0f, old.y > 0.0f ? o.y : 0.0f, old.z > 0.0f ? o.z : 0.0f,
-                              old.w > 0.0f ? o.w : 0.0f);
-            } else if (p.epi == 2) {
-              o = make_float4(fmaxf(o.x, 0.0f), fmaxf(o.y, 0.0f), fmaxf(o.z, 0.0f), fmaxf(o.w, 0.0f));
-            }
+            o = gemm_epi(o, p.epi == 1 ? *dst : o, p, grow0 + lane, I.n0 + (c0 + c) * 32 + 4 * jj);
             *dst = o;
           }
         }
@@ -1460,7 +1480,7 @@ void print_trace(const Params& p, const char* what) {
 }
 
 int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
-         int64_t ldb, float* C, int64_t ldc, int epi, float* ws, size_t ws_bytes, cudaStream_t s) {
+         int64_t ldb, float* C, int64_t ldc, int epi, float* ws, size_t ws_bytes, cudaStream_t s, const k::Epi& ep) {
   if (ta) {
     const int64_t begin[1] = {0}, len[1] = {K};
     return gemm_tn_blocks(mode, 1, begin, len, M, N, A, lda, B, ldb, C, ldc, 0, ws, ws_bytes, s);
@@ -1478,6 +1498,7 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
   p.C = C;
   p.ldc = ldc;
   p.epi = epi;
+  p.ep = ep;
   if (g_gemm_version >= 2) {
     finish_params2(p, N, false, mode == MG_GEMM_TF32X3 ? 3 : 1);
     check_ptr(C, ldc, "C");

@@ -5,13 +5,16 @@
 #include <cstddef>
 #include <cstdint>
 
+#include "mg_epi.cuh"
+
 namespace mg {
 namespace tc {
 bool available();
 // C = op(A) op(B) (+ epilogue), row-major with leading dimensions; returns kernels launched.
 // TN (ta) needs a split-K workspace of tn_workspace_bytes(M, N, K) (one per concurrent stream).
 int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
-         int64_t ldb, float* C, int64_t ldc, int epi, float* ws, size_t ws_bytes, cudaStream_t s);
+         int64_t ldb, float* C, int64_t ldc, int epi, float* ws, size_t ws_bytes, cudaStream_t s,
+         const k::Epi& ep = k::Epi{});
 size_t tn_workspace_bytes(int64_t M, int64_t N, int64_t K);
 // W-grad over up to 8 canonical row blocks in one launch: stage + g*block_stride (M x N, ld ldc) =
 // H[begin_g : begin_g + len_g]^T G[same rows]; empty blocks are written as zeros. Deterministic and

@@ -85,7 +85,7 @@ _STATUS = {1: ShapeError, 2: ValueError, 3: ProtocolError, 4: ShutdownError, 5: 
 GEMM_EXACT, GEMM_TF32X3, GEMM_TF32 = 0, 1, 2
 SPMM_EXACT, SPMM_FAST = 0, 1
 TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1, 2
-T_W, T_WGRAD, T_AHW, T_HW, T_X, T_ADAM_M, T_ADAM_V, T_WSTAGE = range(8)
+T_W, T_WGRAD, T_AHW, T_HW, T_X, T_ADAM_M, T_ADAM_V, T_WSTAGE, T_BIAS, T_BIAS_GRAD = range(10)
 
 
 def _check(rc: int):
@@ -117,6 +117,8 @@ class GcnConfig:
     gemm_mode: int = GEMM_TF32X3  # production default; GEMM_EXACT/SPMM_EXACT give bitwise parity
     spmm_mode: int = SPMM_FAST
     aggregate_input: bool = True  # FAST only: layer 0 as (A X) W0, A X reused for W0's gradient (mggcn.h)
+    bias: bool = False     # default-off extension (no reference analogue): learned bias per layer
+    dropout: float = 0.0   # default-off extension: dropout probability of hidden-layer outputs (training)
 
     def layers(self) -> int:
         return len(self.layer_dims) - 1
@@ -126,7 +128,7 @@ class GcnConfig:
         c = mg_config(dims.ctypes.data_as(C.c_void_p), len(dims), self.lr, self.beta1, self.beta2, self.epsilon,
                       self.epochs, self.seed, int(self.permute), int(self.overlap),
                       int(self.skip_first_backward_spmm), int(self.order_swap), self.gemm_mode, self.spmm_mode,
-                      int(self.aggregate_input))
+                      int(self.aggregate_input), int(self.bias), float(self.dropout))
         c._keep = dims
         return c
 
@@ -573,6 +575,11 @@ class Group:
     def __exit__(self, *a):
         self.close()
 
+    def abort(self):
+        """DeviceGroup::abort (collectives.cpp:42-52): thread-safe; waits in progress and every later call on
+        the group raise ShutdownError."""
+        _check(lib().mg_group_abort(self._h))
+
     def init_params(self):
         _check(lib().mg_group_init_params(self._h))
 
@@ -639,6 +646,8 @@ class Group:
         d = self.dims
         if which in (T_W, T_WGRAD, T_ADAM_M, T_ADAM_V):
             return (d[layer], d[layer + 1])
+        if which in (T_BIAS, T_BIAS_GRAD):
+            return (1, d[layer + 1])
         if which == T_WSTAGE:
             return (8 * d[layer], d[layer + 1])
         rows = self.rows(rank)[1]

@@ -33,8 +33,12 @@ for task in "$@"; do
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${O}_launches.csv python bench.py --config ${arg:-c4} --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > ${O}_launches_bench.json 2>&1
       python scripts/ncu_launches.py ${O}_launches.csv > ${O}_launches.txt; head -16 ${O}_launches.txt ;;
     ncu_spmm)
-      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"spmm_" --launch-skip ${NCU_SKIP:-30} --launch-count ${NCU_COUNT:-10} -o ${O}_spmm -f python bench.py --config ${arg:-c4} --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > ${O}_spmm.log 2>&1; tail -1 ${O}_spmm.log
-      python scripts/ncu_summary.py ${O}_spmm.ncu-rep > ${O}_ncu_spmm.txt 2>&1; head -30 ${O}_ncu_spmm.txt; rm -f ${O}_spmm.ncu-rep ;;
+      # every SpMM launch of ONE step (ncu flushes caches between kernels, so no warm-up is needed)
+      c=${arg:-c4}
+      timeout 2400 ncu --set full --clock-control none --import-source on -k regex:"spmm_" -o ${O}_spmm_$c -f python bench.py --config $c --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > ${O}_spmm_$c.log 2>&1; tail -1 ${O}_spmm_$c.log
+      ncu -i ${O}_spmm_$c.ncu-rep --page raw --csv > ${O}_spmm_${c}_raw.csv 2>&1
+      python scripts/ncu_summary.py ${O}_spmm_$c.ncu-rep > ${O}_ncu_spmm_$c.txt 2>&1; head -30 ${O}_ncu_spmm_$c.txt
+      [ -n "${KEEP_REP:-}" ] || rm -f ${O}_spmm_$c.ncu-rep ;;
     ncu_gemm)
       timeout 1500 ncu --set full --clock-control none --import-source on -k regex:"gemm_tc|softmax" --launch-skip ${NCU_SKIP:-27} --launch-count ${NCU_COUNT:-9} -o ${O}_gemm -f python bench.py --config ${arg:-c4} --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > ${O}_gemm.log 2>&1; tail -1 ${O}_gemm.log
       python scripts/ncu_summary.py ${O}_gemm.ncu-rep > ${O}_ncu_gemm.txt 2>&1; head -30 ${O}_ncu_gemm.txt; rm -f ${O}_gemm.ncu-rep ;;

@@ -1,7 +1,7 @@
 """From an ncu --set full capture of one training step, write profiles/spmm_traffic.json: the SpMM
 kernels' measured DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per staged-SpMM launch, for
 bench.py's roofline.traffic.
-    python scripts/spmm_traffic.py gpurun_out/rNN_full.ncu-rep c4 5 [note]"""
+    python scripts/spmm_traffic.py gpurun_out/rNN_full.ncu-rep|raw.csv c4 5 [note]"""
 import csv
 import io
 import json
@@ -11,7 +11,8 @@ import sys
 
 rep, cfg, launches = sys.argv[1], sys.argv[2], int(sys.argv[3])
 note = sys.argv[4] if len(sys.argv) > 4 else ""
-out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+out = (open(rep).read() if rep.endswith(".csv") else
+       subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout)
 rows = list(csv.reader(io.StringIO(out)))
 hdr, units = rows[0], rows[1]
 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}

@@ -2,7 +2,7 @@
 
 Run in the build container (8+ cores, ~25 GB RAM for C4; /root/reference is not on the GPU box):
 
-    python tests/golden/make_scale_golden.py [partition] [traj] [c4step]
+    python tests/golden/make_scale_golden.py [partition] [traj] [c4step] [c4s16step]
 
 Writes, next to this script:
   scale_partition.json  sha256 of the reference's synth_graph output and of every prepare_data array
@@ -10,11 +10,13 @@ Writes, next to this script:
                         tile) for the (config, P) pairs of tests/scale_common.PARTITION_CASES
                         (inc/dataset.hpp:287-334, inc/driver.hpp:87-117)
   scale_traj.npz        3-epoch train_run of C2 (full 169K-vertex arxiv shape) and of the products 1/16
-                        sample: f64 and f32 losses, f32 final W, and the sha256 of the f32 forward
-                        activations (step_dump, EXACT parity) (inc/driver.hpp:140-206)
+                        sample: f64 and f32 losses, f32 and f64 final W, the sha256 of the f32 forward
+                        activations and the f32 W_G / W after Adam of the teacher-forced step 1 (step_dump)
+                        (inc/driver.hpp:140-206, inc/gcn.hpp:175-184)
   scale_c4step.npz      teacher-forced train_step(1) at full C4 (workers = 8): loss, W_G and W after Adam in
                         full; forward activations, loss gradient and H-grads on a row sample plus hub rows;
-                        per-tensor max |x| and per-column sums (inc/gcn.hpp:175-184)
+                        per-tensor max |x| and per-column sums (inc/gcn.hpp:175-184); the f64 build's W_G
+  scale_c4s16step.npz   the same step on the products 1/16 sample from the f32 and the f64 reference
 """
 import json
 import os
@@ -86,13 +88,45 @@ def traj(ref):
         dump = ref.step_dump(d32, make_cfg(dims, seed=1, permute=True), 1)
         for l, a in enumerate(dump["ahw_fwd"]):
             g[f"{name}_fwd_sha{l}"] = np.frombuffer(sha(np.asarray(a, np.float32)).encode(), np.uint8)
+        for l in range(len(dims) - 1):  # teacher-forced step 1: W_G (well conditioned) and W after Adam
+            g[f"{name}_f32_wgrad{l}"] = dump["w_grad"][l]
+            g[f"{name}_f32_wafter{l}"] = dump["w_after"][l]
         del d32, dump
         d64 = synth(ref, name, np.float64)
         r64 = ref.train_run(d64, cfg, 1, np.float64)
         g[f"{name}_f64_loss"] = r64["loss"]
+        for l, w in enumerate(r64["final_w"]):  # W after Adam is ill-conditioned: the reference's own f32
+            g[f"{name}_f64_w{l}"] = w          # build is the yardstick (tests/test_gpu_scale.py)
         log(name, "f64", r64["loss"])
         del d64
     np.savez_compressed(os.path.join(HERE, "scale_traj.npz"), **g)
+
+
+def step_stats(d, n, L, rows, prefix=""):
+    """A teacher-forced step dump reduced to what is committed: loss, W_G, W after Adam in full; every
+    row-indexed tensor on the sampled rows, with its max |x| and per-column sums / abs sums over all rows."""
+    g = {f"{prefix}loss": np.array([d["loss"]])}
+    for l in range(L):
+        g[f"{prefix}wgrad{l}"] = d["w_grad"][l]
+        g[f"{prefix}wafter{l}"] = d["w_after"][l]
+    tensors = {f"fwd{l}": d["ahw_fwd"][l] for l in range(L)}
+    tensors["loss_grad"] = d["loss_grad"]
+    tensors.update({f"bwd{l}": d["ahw_bwd"][l] for l in range(L - 1)})  # H-grads (relu-masked)
+    for k, a in tensors.items():
+        a = np.asarray(a).reshape(n, -1)
+        g[f"{prefix}{k}_rows"] = a[rows]
+        g[f"{prefix}{k}_max"] = np.array([np.max(np.abs(a))], np.float64)
+        s, sa = colsums(a)
+        g[f"{prefix}{k}_colsum"] = s
+        g[f"{prefix}{k}_colabs"] = sa
+    return g
+
+
+def sample_rows(ref, ds):
+    fwd, _ = ref.random_permutation(ds.n, 1)
+    deg_new = np.empty(ds.n, np.int64)
+    deg_new[fwd] = np.diff(ds.row_ptr)
+    return c4_sample_rows(ds.n, deg_new)
 
 
 def c4step(ref):
@@ -100,37 +134,47 @@ def c4step(ref):
     dims = SCALE[name]["dims"]
     L = len(dims) - 1
     ds = synth(ref, name)
-    fwd, _ = ref.random_permutation(ds.n, 1)
-    deg_new = np.empty(ds.n, np.int64)
-    deg_new[fwd] = np.diff(ds.row_ptr)
-    rows = c4_sample_rows(ds.n, deg_new)
+    rows = sample_rows(ref, ds)
     log("c4 synth; sample rows", len(rows))
-    d = ref.step_dump(ds, make_cfg(dims, seed=1, permute=True, overlap=True), 8)
+    cfg = make_cfg(dims, seed=1, permute=True, overlap=True)
+    d = ref.step_dump(ds, cfg, 8)
     log("c4 step_dump loss", d["loss"])
-    g = {"rows": rows, "loss": np.array([d["loss"]])}
+    g = {"rows": rows, **step_stats(d, ds.n, L, rows)}
+    del d, ds
+    # the f64 build's W_G: the yardstick for how far the f32 reference itself is from exact (K = 306K
+    # rows per canonical block)
+    d64 = synth(ref, name, np.float64)
+    r = ref.grad_run(d64, cfg, 8, np.float64)
     for l in range(L):
-        g[f"wgrad{l}"] = d["w_grad"][l]
-        g[f"wafter{l}"] = d["w_after"][l]
-    tensors = {f"fwd{l}": d["ahw_fwd"][l] for l in range(L)}
-    tensors["loss_grad"] = d["loss_grad"]
-    tensors.update({f"bwd{l}": d["ahw_bwd"][l] for l in range(L - 1)})  # H-grads (relu-masked)
-    for k, a in tensors.items():
-        a = np.asarray(a).reshape(ds.n, -1)
-        g[f"{k}_rows"] = a[rows]
-        g[f"{k}_max"] = np.array([np.max(np.abs(a))], np.float64)
-        s, sa = colsums(a)
-        g[f"{k}_colsum"] = s
-        g[f"{k}_colabs"] = sa
+        g[f"f64_wgrad{l}"] = r["w_grad"][l]
+    g["f64_loss"] = np.array([r["loss"]])
+    log("c4 f64 grad_run loss", r["loss"])
     np.savez_compressed(os.path.join(HERE, "scale_c4step.npz"), **g)
 
 
+def c4s16step(ref):
+    """The same teacher-forced step on the products 1/16 sample, dumped by the f32 AND the f64 reference:
+    per-tensor distances of ours and of the f32 reference to the f64 one (tests/test_gpu_scale.py)."""
+    name = "c4s16"
+    dims = SCALE[name]["dims"]
+    L = len(dims) - 1
+    g = {}
+    for dt, prefix in ((np.float32, ""), (np.float64, "f64_")):
+        ds = synth(ref, name, dt)
+        rows = sample_rows(ref, ds)
+        d = ref.step_dump(ds, make_cfg(dims, seed=1, permute=True), 1, dt)
+        g.update({"rows": rows, **step_stats(d, ds.n, L, rows, prefix)})
+        log(name, dt.__name__, "step_dump loss", d["loss"])
+    np.savez_compressed(os.path.join(HERE, "scale_c4s16step.npz"), **g)
+
+
 def main():
-    which = sys.argv[1:] or ["partition", "traj", "c4step"]
+    which = sys.argv[1:] or ["partition", "traj", "c4step", "c4s16step"]
     ref = Ref()
     ref.set_spmm_threads(max(1, (os.cpu_count() or 8)))
     for w in which:
         t = time.time()
-        {"partition": partition, "traj": traj, "c4step": c4step}[w](ref)
+        {"partition": partition, "traj": traj, "c4step": c4step, "c4s16step": c4s16step}[w](ref)
         log(w, f"{time.time() - t:.0f} s")
 
 

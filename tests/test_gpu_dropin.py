@@ -72,7 +72,7 @@ def test_reference_run_train_on_the_gpu(tmp_path):
     ds = R.synth_graph(3000, 10.0, 0.7, 7, 24, 5)
     rp, ci, _ = ds.graph
     with open(tmp_path / "g.edges", "w") as f:
-        for u in range(ds.n):
+        for u in range(ds.n()):
             for e in range(rp[u], rp[u + 1]):
                 f.write(f"{u} {ci[e]}\n")
     R.write_dense(tmp_path / "x.bin", ds.features)

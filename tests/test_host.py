@@ -31,10 +31,12 @@ def test_library_exports_every_header_symbol():
 
 def test_abi_version_and_defaults():
     from paper_2110_08688_b200._lib import lib, mg_config
-    assert lib().mg_abi_version() == 2
+    assert lib().mg_abi_version() == 3
+    assert ctypes.sizeof(mg_config) == 96  # mggcn.h layout (bias, dropout appended in ABI 3)
     c = mg_config()
     lib().mg_config_defaults(ctypes.byref(c))
     assert (c.lr, c.beta1, c.beta2, c.epsilon, c.epochs, c.seed) == (0.01, 0.9, 0.999, 1e-8, 100, 1)
+    assert (c.bias, c.dropout) == (0, 0.0)
 
 
 def test_config_validation_errors():
@@ -154,3 +156,16 @@ def test_aggregate_input_validation():
     d = mg_config()
     lib().mg_config_defaults(ctypes.byref(d))
     assert d.aggregate_input == 1 and d.spmm_mode == R.SPMM_FAST
+
+
+def test_csr_validation_reports_the_first_violation():
+    """CsrMatrix::validate (inc/sparse.hpp:37-54) scans rows in order: the first failing row wins, and an
+    out-of-range column is named in the message — also when the parallel scan meets later rows first."""
+    n = 200000
+    rp = np.arange(n + 1, dtype=np.int64)
+    ci = np.zeros(n, np.int64)
+    ci[150000] = n + 5          # out of range late
+    ci[3] = -1                  # out of range early: this one is reported
+    ds = R.Dataset.from_arrays(rp, ci, np.ones(n, np.float32), np.zeros((n, 1), np.float32), np.zeros(n, np.int32))
+    with pytest.raises(R.ValueError, match=r"^csr: col -1 out of range in row 3$"):
+        ds.validate()
