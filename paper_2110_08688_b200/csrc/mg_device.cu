@@ -1572,9 +1572,15 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
     std::vector<int> sorted = devs;
     std::sort(sorted.begin(), sorted.end());
     const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
+    const bool one_device = sorted.front() == sorted.back();
     if (transport == MG_TRANSPORT_AUTO) transport = (distinct || n_local < world) ? MG_TRANSPORT_NCCL : MG_TRANSPORT_LOCAL;
     if (transport == MG_TRANSPORT_LOCAL && n_local != world)
       throw ValueError("group: the in-process transport needs every rank local");
+    // LOCAL's peer copies and rank-order reduction dereference every worker's buffers from worker 0's device:
+    // no peer access is set up, so it is only legal when every worker shares one device.
+    if (transport == MG_TRANSPORT_LOCAL && !one_device)
+      throw ValueError("group: the in-process transport needs every worker on one device (got a mix of devices; "
+                       "use one device per worker for NCCL)");
     if (transport == MG_TRANSPORT_LOCAL && world > k::kMaxLocal)
       throw ValueError("group: the in-process transport supports at most " + std::to_string(k::kMaxLocal) + " workers");
     if (transport == MG_TRANSPORT_NCCL && !distinct)
@@ -2086,6 +2092,10 @@ mg_status mg_group_bench_spmm(mg_group* g, int32_t dir, double* wall_us) {
   return guarded([&] {
     if (!g) throw ValueError("group: null");
     if (dir != 0 && dir != 1) throw ValueError("bench_spmm: dir must be 0 (forward) or 1 (backward)");
+    if (pad4(g->cfg.dims[0]) > g->ld_max)
+      throw ValueError("bench_spmm: width " + std::to_string(g->cfg.dims[0]) +
+                       " exceeds the group's buffer width " + std::to_string(g->ld_max) +
+                       " (create the group with layer_dims[0] <= the widest hidden layer, or order_swap)");
     Step st(*g);
     std::vector<float*> src, out;
     for (auto& wp : g->workers) {

@@ -10,7 +10,7 @@
 // the UMMA canonical smem layouts: K-major operands (A of NN/NT, B of NT) as SWIZZLE_64B boxes
 // {16 k, rows}; MN-major operands (B = W of NN, both operands of TN, which are K x M row-major in HBM)
 // as SWIZZLE_128B boxes {32 mn, 16 k} — no transposition anywhere. Warps 2-5 split each element
-// in place, x = hi + lo with hi and lo both rounded to nearest TF32 (split_hi / split_lo below), and
+// in place, x = hi + lo with hi exact in TF32 (split_hi / split_lo below, MG_TC_SPLIT_RN), and
 // mask TN rows past the chunk end. Warp 1 (one lane) issues tcgen05.mma.kind::tf32 (M = 128,
 // N <= 256, K = 8) into one of two TMEM accumulators:
 //   TF32X3: D += A_lo B_hi + A_hi B_lo + A_hi B_hi      TF32: D += A_hi B_hi
@@ -57,6 +57,16 @@ constexpr int kEpiSmem = 4 * 32 * 33 * 4;  // epilogue transpose, one 32 x 33 ti
 static int g_split_rows = 4096;    // TN chunk (rows), fixed relative to the block start ("tn_chunk")
 
 enum { NN = 0, NT = 1, TN = 2 };
+
+// TF32X3 split rounding: 0 = truncated, hi = x & 0xFFFFE000 and lo = x - hi (default); 1 = hi and lo rounded
+// to nearest TF32. Measured on C4 (scripts/gemm_bias_probe.py, A/B on one box): round-to-nearest lowers the
+// normwise GeMM error 1.3-2x (1.0e-6 vs 1.4e-6 at K = 100, 4e-6 vs 5.5e-6 for non-negative operands at
+// K = 306K) but costs 1.6 ms of GeMM per epoch (11.4 vs 9.8 ms: the split warps are on the critical path).
+// Both are far inside the 1e-4 tolerance; the step-level deviations from the reference are ReLU-mask flips
+// at pre-activations within rounding of 0, which no split removes (tests/test_gpu_scale.py).
+#ifndef MG_TC_SPLIT_RN
+#define MG_TC_SPLIT_RN 0
+#endif
 
 struct Params {
   long M, N, K;          // NN/NT: C is M x N, reduction K. TN: M, N = output dims; rows given per block
@@ -203,21 +213,22 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
-// 3xTF32 splits round to nearest: x = hi + lo with hi = rn_tf32(x) and lo = rn_tf32(x - hi), so every
-// dropped part (the rounding of lo, the omitted lo*lo product) has a data-independent sign. Truncated
-// splits (hi = x & 0xFFFFE000, lo left for the tensor core to truncate) leave errors with the sign of x,
-// which add up coherently over a long K: W-grads at C4 (K = 306K rows per canonical block) came out
-// ~1.6e-4 (normwise) off the fp32 reference; with round-to-nearest splits they are ~1e-6.
+// 3xTF32 splits (MG_TC_SPLIT_RN above): x = hi + lo, hi exact in TF32; the tensor core reads lo's top 19
+// bits and the omitted lo*lo product is below 2^-22 |x|.
 __device__ __forceinline__ float tf32_rn(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
   return __uint_as_float(r);
 }
-__device__ __forceinline__ float split_hi(float x) { return tf32_rn(x); }
-__device__ __forceinline__ float split_lo(float x, float hi) { return tf32_rn(__fsub_rn(x, hi)); }
+__device__ __forceinline__ float tf32_tr(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+__device__ __forceinline__ float split_hi(float x) { return MG_TC_SPLIT_RN ? tf32_rn(x) : tf32_tr(x); }
+__device__ __forceinline__ float split_lo(float x, float hi) {
+  return MG_TC_SPLIT_RN ? tf32_rn(__fsub_rn(x, hi)) : __fsub_rn(x, hi);
+}
 // lo part for an operand whose hi part is the raw fp32 tile (kind::tf32 truncates it: hi = x & 0xFFFFE000)
 __device__ __forceinline__ float split_lo_trunc(float x) {
-  return tf32_rn(__fsub_rn(x, __uint_as_float(__float_as_uint(x) & 0xFFFFE000u)));
+  const float d = __fsub_rn(x, tf32_tr(x));
+  return MG_TC_SPLIT_RN ? tf32_rn(d) : d;
 }
 __device__ __forceinline__ float4 split4(float4 x, float4& lo) {
   float4 h;
@@ -230,8 +241,18 @@ __device__ __forceinline__ float4 split4(float4 x, float4& lo) {
 }
 
 // The NN / NT epilogue on 4 consecutive outputs of row `row`, columns col..col+3: 1 = relu_backward mask
-// (kept entries x 1/(1-p) under dropout), 2 = relu, 0 = store; bias / dropout per mg_epi.cuh.
+// (kept entries x 1/(1-p) under dropout), 2 = relu, 0 = store; bias / dropout per mg_epi.cuh only in the
+// EXT instantiations (the default kernels carry no bias / dropout code: warp-specialised kernels are
+// sensitive to code size, measured 2.5x slower GeMMs with the extension inlined into every kernel).
+template <bool EXT>
 __device__ __forceinline__ float4 gemm_epi(float4 o, float4 old, const Params& p, long row, int col) {
+  if (!EXT) {
+    if (p.epi == 1)
+      return make_float4(old.x > 0.0f ? o.x : 0.0f, old.y > 0.0f ? o.y : 0.0f, old.z > 0.0f ? o.z : 0.0f,
+                         old.w > 0.0f ? o.w : 0.0f);
+    if (p.epi == 2) return make_float4(fmaxf(o.x, 0.0f), fmaxf(o.y, 0.0f), fmaxf(o.z, 0.0f), fmaxf(o.w, 0.0f));
+    return o;
+  }
   if (p.epi == 1) {
     if (p.ep.thr) o = make_float4(__fmul_rn(o.x, p.ep.scale), __fmul_rn(o.y, p.ep.scale), __fmul_rn(o.z, p.ep.scale),
                                   __fmul_rn(o.w, p.ep.scale));
@@ -681,7 +702,7 @@ template <int MODE>
 __host__ __device__ constexpr int bk2() { return MODE == TN ? 32 : BK; }
 constexpr int kPromoteRows = 256;  // TN: drain TMEM every 256 K rows
 
-template <int MODE>
+template <int MODE, bool EXT>
 __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_constant__ CUtensorMap map_a,
                                                         const __grid_constant__ CUtensorMap map_bh,
                                                         const __grid_constant__ CUtensorMap map_bl,
@@ -853,9 +874,8 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
   } else if (warp >= 10) {
     // ------------------------------------------------------------ TN: B (G rows) lo copy
     // kind::tf32 reads the raw fp32 tile as its hi part: the tensor core drops the low 13 mantissa bits
-    // (hi = x & 0xFFFFE000), so only lo = rn_tf32(x - hi) is written (half the shared-memory stores of
-    // rewriting hi in place; the kernel is shared-memory-bandwidth bound at this stage). lo rounds to
-    // nearest, and A's split does too, so the omitted A_lo * B_lo term has no systematic sign.
+    // (hi = x & 0xFFFFE000), so only lo = x - hi is written (half the shared-memory stores of rewriting hi
+    // in place; the kernel is shared-memory-bandwidth bound at this stage).
     if (MODE == TN && p.terms == 3) {
       const int t = threadIdx.x - 320;
       RingPos rp(p.nst);
@@ -922,7 +942,7 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
                 o = make_float4(__fadd_rn(pv.x, o.x), __fadd_rn(pv.y, o.y), __fadd_rn(pv.z, o.z), __fadd_rn(pv.w, o.w));
               }
             } else {
-              o = gemm_epi(o, p.epi == 1 ? *dst : o, p, grow0 + lane, I.n0 + c * 32 + 4 * j);
+              o = gemm_epi<EXT>(o, p.epi == 1 ? *dst : o, p, grow0 + lane, I.n0 + c * 32 + 4 * j);
             }
             *dst = o;
           }
@@ -995,7 +1015,7 @@ __device__ __forceinline__ void mma_commit_mc_e(uint64_t* bar, uint32_t mask) {
       : "memory");
 }
 
-template <int MODE, int CL>
+template <int MODE, int CL, bool EXT>
 __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__ CUtensorMap map_a,
                                                          const __grid_constant__ CUtensorMap map_bh,
                                                          const __grid_constant__ CUtensorMap map_bl,
@@ -1227,7 +1247,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
           for (int jj = 0; jj < 8; ++jj) {
             float4 o = make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
             float4* dst = sw128(b, lane, jj);
-            o = gemm_epi(o, p.epi == 1 ? *dst : o, p, grow0 + lane, I.n0 + (c0 + c) * 32 + 4 * jj);
+            o = gemm_epi<EXT>(o, p.epi == 1 ? *dst : o, p, grow0 + lane, I.n0 + (c0 + c) * 32 + 4 * jj);
             *dst = o;
           }
         }
@@ -1381,12 +1401,12 @@ inline int smem_bytes3(const Params& p) {
   return p.nst * BM * BK3 * 4 + p.nwst * 2 * p.bnr * BK3 * 4 + 4 * p.epi_chunks * 4096 + 1024;
 }
 int g_gemm3_cluster = 1;  // v3 cluster size for the W multicast ("gemm3_cluster": 1 or 2)
-template <int MODE, int CL>
-void launch3(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
-             cudaStream_t s) {
+template <int MODE, int CL, bool EXT>
+void launch3x(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
+              cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr, cur_dev()))
-    TC_CUDA(cudaFuncSetAttribute(gemm_tc3<MODE, CL>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax3));
+    TC_CUDA(cudaFuncSetAttribute(gemm_tc3<MODE, CL, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax3));
   const int npi = ((p.m_tiles + CL - 1) / CL) * p.n_tiles;
   const int grid = CL * std::max(1, std::min(npi, num_sms() / CL));
   cudaLaunchConfig_t cfg{};
@@ -1401,19 +1421,33 @@ void launch3(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl,
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  TC_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc3<MODE, CL>, a, bh, bl, c, p));
+  TC_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc3<MODE, CL, EXT>, a, bh, bl, c, p));
+}
+// bias / dropout epilogue (Params::ep) only in the EXT instantiation
+inline bool epi_ext(const Params& p) { return p.ep.bias != nullptr || p.ep.thr != 0; }
+template <int MODE, int CL>
+void launch3(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
+             cudaStream_t s) {
+  if (epi_ext(p)) launch3x<MODE, CL, true>(a, bh, bl, c, p, s);
+  else launch3x<MODE, CL, false>(a, bh, bl, c, p, s);
 }
 
+template <int MODE, bool EXT>
+void launch2x(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
+              cudaStream_t s) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_on_device(attr, cur_dev()))
+    TC_CUDA(cudaFuncSetAttribute(gemm_tc2<MODE, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemBudget2 + kEpiBuf + 1024));
+  const int grid = std::max(1, std::min(p.n_items, num_sms()));
+  gemm_tc2<MODE, EXT><<<grid, threads2<MODE>(), smem_bytes2(p, bk2<MODE>()), s>>>(a, bh, bl, c, p);
+  TC_CUDA(cudaGetLastError());
+}
 template <int MODE>
 void launch2(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
              cudaStream_t s) {
-  static std::atomic<unsigned long long> attr{0};
-  if (first_on_device(attr, cur_dev()))
-    TC_CUDA(cudaFuncSetAttribute(gemm_tc2<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 kSmemBudget2 + kEpiBuf + 1024));
-  const int grid = std::max(1, std::min(p.n_items, num_sms()));
-  gemm_tc2<MODE><<<grid, threads2<MODE>(), smem_bytes2(p, bk2<MODE>()), s>>>(a, bh, bl, c, p);
-  TC_CUDA(cudaGetLastError());
+  if (MODE != TN && epi_ext(p)) launch2x<MODE, true>(a, bh, bl, c, p, s);
+  else launch2x<MODE, false>(a, bh, bl, c, p, s);
 }
 
 }  // namespace

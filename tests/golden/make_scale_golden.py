@@ -152,6 +152,22 @@ def c4step(ref):
     np.savez_compressed(os.path.join(HERE, "scale_c4step.npz"), **g)
 
 
+def c4f64(ref):
+    """Adds the f64 build's W_G and loss to an existing scale_c4step.npz (the f64 half of c4step)."""
+    name = "c4"
+    dims = SCALE[name]["dims"]
+    path = os.path.join(HERE, "scale_c4step.npz")
+    g = dict(np.load(path))
+    cfg = make_cfg(dims, seed=1, permute=True, overlap=True)
+    d64 = synth(ref, name, np.float64)
+    r = ref.grad_run(d64, cfg, 8, np.float64)
+    for l in range(len(dims) - 1):
+        g[f"f64_wgrad{l}"] = r["w_grad"][l]
+    g["f64_loss"] = np.array([r["loss"]])
+    log("c4 f64 grad_run loss", r["loss"])
+    np.savez_compressed(path, **g)
+
+
 def c4s16step(ref):
     """The same teacher-forced step on the products 1/16 sample, dumped by the f32 AND the f64 reference:
     per-tensor distances of ours and of the f32 reference to the f64 one (tests/test_gpu_scale.py)."""
@@ -174,7 +190,7 @@ def main():
     ref.set_spmm_threads(max(1, (os.cpu_count() or 8)))
     for w in which:
         t = time.time()
-        {"partition": partition, "traj": traj, "c4step": c4step, "c4s16step": c4s16step}[w](ref)
+        {"partition": partition, "traj": traj, "c4step": c4step, "c4f64": c4f64, "c4s16step": c4s16step}[w](ref)
         log(w, f"{time.time() - t:.0f} s")
 
 
