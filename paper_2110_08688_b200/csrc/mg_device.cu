@@ -93,10 +93,36 @@ struct DevTile {
   int4* hubs = nullptr;
   int n_hubs = 0;
   int n_segments = 0;
+  // MG_SPMM_FAST row-streaming pieces {r0, r1, e0, e1} (<= kPieceRows consecutive light rows) and hub-row
+  // segments {-(seg+1), 0, e0, e1}, by decreasing nonzeros (spmm_fast_stream)
+  int4* pieces = nullptr;
+  int n_pieces = 0;
   bool hubs_classed = false;  // FAST: column hub classes in the top 4 bits of each edge record
 };
 
 std::atomic<int> g_fast_segment{2048};
+std::atomic<int> g_adaptive_cuts{1};  // "adaptive_cuts": FAST hub threshold / segment scaled to the tile
+
+// MG_SPMM_FAST cut points of one tile: rows with >= ht nonzeros are hub rows cut into segments of seg
+// nonzeros. One work item's gathers are serial in one lane group (~12 nonzeros per memory latency), so an
+// item much longer than the launch's average share is the launch's tail: ncu of the C2 (arxiv-shaped)
+// SpMM showed every SM idle after ~30% of the launch while one group folded a ~4000-nonzero row. The
+// segment is therefore scaled to the tile: nnz / (SMs x 64) rounded down to a power of two, clamped to
+// [64, fast_segment], and rows from 2 segments up are hubs (never above heavy_row).
+struct FastCuts {
+  int ht, seg;
+};
+int num_sms();
+FastCuts fast_cuts(index_t nnz) {
+  FastCuts c{g_heavy_row.load(), g_fast_segment.load()};
+  if (!g_adaptive_cuts.load()) return c;
+  const index_t share = nnz / (static_cast<index_t>(num_sms()) * 64);
+  int seg = 64;
+  while (seg * 2 <= share && seg * 2 <= c.seg) seg *= 2;
+  c.seg = std::min(seg, c.seg);
+  c.ht = std::max(1, std::min(c.ht, 2 * c.seg));
+  return c;
+}
 
 // MGGCN_TIMING=1: host-side phase timings of group creation on stderr.
 struct Stopwatch {
@@ -116,7 +142,8 @@ struct Stopwatch {
 // by decreasing length.
 void build_fast_items(const std::vector<index_t>& rp, std::vector<int4>& items, std::vector<int4>& hubs, int& nseg) {
   const index_t rows = static_cast<index_t>(rp.size()) - 1;
-  const int ht = heavy_threshold(), seg = g_fast_segment.load();
+  const FastCuts cuts = fast_cuts(rp.back());
+  const int ht = cuts.ht, seg = cuts.seg;
   std::vector<int> light;
   items.clear();
   hubs.clear();
@@ -146,11 +173,38 @@ void build_fast_items(const std::vector<index_t>& rp, std::vector<int4>& items, 
         make_int4(static_cast<int>(rp[r]), static_cast<int>(rp[r + 1]), r, 0);
 }
 
+// Row-streaming work list (spmm_fast_stream): maximal runs of consecutive light rows cut into pieces of at
+// most kPieceRows rows and about piece_nnz nonzeros (a row is never split), plus one piece per hub-row
+// segment; ordered by decreasing nonzeros (stable), so the grid's first wave takes the longest pieces.
+constexpr int kPieceRows = 32;
+std::atomic<int> g_piece_nnz{1024};
+void build_stream_pieces(const std::vector<index_t>& rp, const std::vector<int4>& seg_items, std::vector<int4>& pieces) {
+  const index_t rows = static_cast<index_t>(rp.size()) - 1;
+  const FastCuts cuts = fast_cuts(rp.back());
+  const int ht = cuts.ht;
+  const index_t cap = std::min<index_t>(g_piece_nnz.load(), cuts.seg);
+  pieces.clear();
+  for (const int4& it : seg_items) pieces.push_back(make_int4(it.z, 0, it.x, it.y));
+  index_t r = 0;
+  while (r < rows) {
+    if (rp[r + 1] - rp[r] >= ht) {
+      ++r;
+      continue;
+    }
+    const index_t r0 = r;
+    while (r < rows && r - r0 < kPieceRows && rp[r + 1] - rp[r] < ht && (r == r0 || rp[r + 1] - rp[r0] <= cap)) ++r;
+    pieces.push_back(make_int4(static_cast<int>(r0), static_cast<int>(r), static_cast<int>(rp[r0]),
+                               static_cast<int>(rp[r])));
+  }
+  std::stable_sort(pieces.begin(), pieces.end(), [](const int4& a, const int4& b) { return a.w - a.z > b.w - b.z; });
+}
+
 // Hub-row half of build_fast_items: segment items + hub descriptors; *n_light = rows below the threshold.
 void build_hub_segments(const std::vector<index_t>& rp, std::vector<int4>& items, std::vector<int4>& hubs, int& nseg,
                         index_t& n_light) {
   const index_t rows = static_cast<index_t>(rp.size()) - 1;
-  const int ht = heavy_threshold(), seg = g_fast_segment.load();
+  const FastCuts cuts = fast_cuts(rp.back());
+  const int ht = cuts.ht, seg = cuts.seg;
   items.clear();
   hubs.clear();
   nseg = 0;
@@ -349,6 +403,10 @@ struct FastLaunch {
   float* scratch;  // n_segments x ld
   bool hubs_classed = false;  // edge records carry hub classes (upload_tile, FAST mode)
   index_t src_rows = 0;       // rows of the gathered block (the tile's columns)
+  const int4* pieces = nullptr;  // row-streaming work list (spmm_fast_stream)
+  int n_pieces = 0;
+  const int* row_ptr = nullptr;
+  double nnz_per_row = 0.0;
 };
 
 template <int G, int CPL>
@@ -424,6 +482,33 @@ static void launch_fast_async_v(const FastLaunch& t, const float* h, float* out,
   MG_LAUNCHED();
 }
 
+// MG_SPMM_FAST row-streaming kernel (spmm_fast_stream): 0 off, 1 on, 2 auto = tiles averaging fewer than
+// kStreamRowNnz nonzeros per row (measured: C4 P = 8 stage tiles, 6.3 per row, 12.8 -> 11.7 ms per rank;
+// slower on C2 / C3 / C4 at P = 1, 13.6-490 per row)
+std::atomic<int> g_spmm_stream{2};
+constexpr double kStreamRowNnz = 10.0;
+
+template <int G, int CPL, int E, int D, bool HINT>
+static void launch_fast_stream_v(const FastLaunch& t, const float* h, float* out, float* scratch, int ld, int nchunk,
+                                 int acc, int relu, int hub_max, const k::Epi& ep, cudaStream_t s) {
+  constexpr int kThreads = 128;
+  constexpr size_t smem = sizeof(float4) * kThreads * D * E * CPL;
+  static std::atomic<unsigned long long> attr{0};
+  static std::atomic<int> blocks_per_sm{1};
+  if (first_on_device(attr, cur_device())) {
+    MG_CUDA(cudaFuncSetAttribute(k::spmm_fast_stream<G, CPL, E, D, HINT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+    int b = 0;
+    MG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k::spmm_fast_stream<G, CPL, E, D, HINT>, kThreads, smem));
+    blocks_per_sm = std::max(1, b);
+  }
+  const int gpb = kThreads / G;
+  const int blocks = std::min(ceil_div(t.n_pieces, gpb), num_sms() * blocks_per_sm);
+  k::spmm_fast_stream<G, CPL, E, D, HINT><<<blocks, kThreads, smem, s>>>(t.pieces, t.n_pieces, t.row_ptr, t.edges, h, out,
+                                                                         scratch, ld, nchunk, acc, relu, hub_max, ep);
+  MG_LAUNCHED();
+}
+
 template <int G, int CPL, int E, int D>
 static void launch_fast_async(const FastLaunch& t, const float* h, float* out, float* scratch, int ld, int nchunk,
                               int acc, int relu, const k::Epi& ep, cudaStream_t s) {
@@ -431,6 +516,12 @@ static void launch_fast_async(const FastLaunch& t, const float* h, float* out, f
   // served by plain LRU, which then keeps a large share of every row resident)
   const bool big = static_cast<double>(t.src_rows) * ld * 4 > 4.0 * kL2Bytes;
   const int hub_max = t.hubs_classed && big ? hub_class_max(ld) : -1;
+  const int sm = g_spmm_stream.load();
+  if ((sm == 1 || (sm == 2 && t.nnz_per_row < kStreamRowNnz)) && t.pieces && t.n_pieces > 0) {
+    if (hub_max >= 0) launch_fast_stream_v<G, CPL, E, D, true>(t, h, out, scratch, ld, nchunk, acc, relu, hub_max, ep, s);
+    else launch_fast_stream_v<G, CPL, E, D, false>(t, h, out, scratch, ld, nchunk, acc, relu, -1, ep, s);
+    return;
+  }
   if (hub_max >= 0) launch_fast_async_v<G, CPL, E, D, true>(t, h, out, scratch, ld, nchunk, acc, relu, hub_max, ep, s);
   else launch_fast_async_v<G, CPL, E, D, false>(t, h, out, scratch, ld, nchunk, acc, relu, -1, ep, s);
 }
@@ -481,7 +572,8 @@ static int spmm_fast(const FastLaunch& t, const float* h, float* out, index_t ld
     }
   }
   if (t.n_hubs > 0) {
-    k::spmm_fast_hubs<<<t.n_hubs, 256, 0, s>>>(t.hubs, t.scratch, out, static_cast<int>(ld), acc, relu, ep0);
+    const int th = static_cast<int>(std::max<index_t>(32, std::min<index_t>(256, (ld / 4 + 31) / 32 * 32)));
+    k::spmm_fast_hubs<<<t.n_hubs, th, 0, s>>>(t.hubs, t.scratch, out, static_cast<int>(ld), acc, relu, ep0);
     MG_LAUNCHED();
     ++launches;
   }
@@ -844,7 +936,13 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d, const DevTil
     if (!seg_items.empty())
       MG_CUDA(cudaMemcpy(d.items, seg_items.data(), sizeof(int4) * seg_items.size(), cudaMemcpyHostToDevice));
     if (!hubs.empty()) MG_CUDA(cudaMemcpy(d.hubs, hubs.data(), sizeof(int4) * hubs.size(), cudaMemcpyHostToDevice));
-    if (n_light > 0) light_items_device(d.row_ptr, t.rows, heavy_threshold(), n_light, d.items + seg_items.size());
+    if (n_light > 0) light_items_device(d.row_ptr, t.rows, fast_cuts(d.nnz).ht, n_light, d.items + seg_items.size());
+    std::vector<int4> pieces;
+    build_stream_pieces(t.row_ptr, seg_items, pieces);
+    d.pieces = dalloc_t<int4>(g, w, std::max<size_t>(1, pieces.size()));
+    d.n_pieces = static_cast<int>(pieces.size());
+    if (!pieces.empty())
+      MG_CUDA(cudaMemcpy(d.pieces, pieces.data(), sizeof(int4) * pieces.size(), cudaMemcpyHostToDevice));
     sw.lap("  lists");
     return;
   }
@@ -1073,7 +1171,8 @@ class Step {
         const k::Epi ep = (epi_layer >= 0 && j == P_ - 1) ? out_epi(w, epi_layer, relu_last) : k::Epi{};
         const int pi = prof_begin(w);
         if (cfg_.spmm_mode == MG_SPMM_FAST) {
-          FastLaunch fl{t.items, t.n_items, t.hubs, t.n_hubs, t.edges, w.seg_scratch, t.hubs_classed, t.cols};
+          FastLaunch fl{t.items, t.n_items, t.hubs, t.n_hubs, t.edges, w.seg_scratch, t.hubs_classed, t.cols,
+                        t.pieces, t.n_pieces, t.row_ptr, t.rows ? static_cast<double>(t.nnz) / t.rows : 0.0};
           g_.kernels_last += spmm_fast(fl, recv[k], out[k], ld, acc, relu, ep, w.s0);
           prof_end(w, pi, 0);
           mult_task[k][j] = tl_end(k, ts);
@@ -1502,6 +1601,14 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
         for (int d = 0; d < 64 && d < mg_device_count(); ++d) block_cache().release(d);
     } else if (k == "bwd_transpose") {
       g_bwd_transpose = value != 0 ? 1 : 0;
+    } else if (k == "adaptive_cuts") {
+      g_adaptive_cuts = value != 0 ? 1 : 0;
+    } else if (k == "spmm_stream") {
+      if (value < 0 || value > 2) throw ValueError("tuning: spmm_stream must be 0 (off), 1 (on) or 2 (auto)");
+      g_spmm_stream = static_cast<int>(value);
+    } else if (k == "piece_nnz") {
+      if (value < 1) throw ValueError("tuning: piece_nnz must be >= 1");
+      g_piece_nnz = static_cast<int>(std::min<int64_t>(value, 1 << 30));
     } else if (k == "spmm_async") {
       g_spmm_async = value != 0 ? 1 : 0;
     } else if (k == "fast_segment") {
@@ -2136,13 +2243,22 @@ mg_status mg_dev_spmm(int64_t rows, const int32_t* row_ptr, const void* edges, c
       MG_CUDA(cudaMalloc(&sc, sizeof(float) * std::max<size_t>(1, static_cast<size_t>(nseg) * ld)));
       if (!items.empty()) MG_CUDA(cudaMemcpy(di, items.data(), sizeof(int4) * items.size(), cudaMemcpyHostToDevice));
       if (!hubs.empty()) MG_CUDA(cudaMemcpy(dh, hubs.data(), sizeof(int4) * hubs.size(), cudaMemcpyHostToDevice));
+      std::vector<int4> seg_items, pieces;
+      for (const int4& it : items)
+        if (it.z < 0) seg_items.push_back(it);
+      build_stream_pieces(rp, seg_items, pieces);
+      int4* dp = nullptr;
+      MG_CUDA(cudaMalloc(&dp, sizeof(int4) * std::max<size_t>(1, pieces.size())));
+      if (!pieces.empty()) MG_CUDA(cudaMemcpy(dp, pieces.data(), sizeof(int4) * pieces.size(), cudaMemcpyHostToDevice));
       FastLaunch fl{di, static_cast<int>(items.size()), dh, static_cast<int>(hubs.size()),
-                    static_cast<const int2*>(edges), sc};
+                    static_cast<const int2*>(edges), sc, false, 0, dp, static_cast<int>(pieces.size()), row_ptr,
+                    rows ? static_cast<double>(rp.back()) / rows : 0.0};
       spmm_fast(fl, h, out, ld, accumulate, relu, k::Epi{}, s);
       MG_CUDA(cudaStreamSynchronize(s));
       cudaFree(di);
       cudaFree(dh);
       cudaFree(sc);
+      cudaFree(dp);
       return;
     }
     std::vector<int> light, heavy;

@@ -324,6 +324,150 @@ __global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ 
   }
 }
 
+// MG_SPMM_FAST, row-streaming: the cp.async ring of spmm_fast_async kept full ACROSS rows. A work item is
+// a piece {r0, r1, e0, e1} of consecutive light rows (their edges contiguous, e0 = rp[r0], e1 = rp[r1])
+// or a hub-row segment {-(seg+1), 0, e0, e1}; the group streams the piece's nonzeros through the ring in
+// stages of E and closes a row (epilogue store, accumulator reset) when the consumption cursor crosses
+// the row's end, read from register windows of G row ends (lane l holds the end of row rb + l). Short rows no longer pay one DRAM latency each (spmm_fast_async drains its ring at every
+// row end): the pipeline drains once per piece. Per output element the FMA chain is the same as
+// spmm_fast_async's (acc = accumulate ? old : 0, then one fmaf per nonzero in column order), so results
+// are bitwise identical. With accumulate the next row's old output is prefetched into registers when a
+// row starts. Requires E | G and (D - 1) * E <= G.
+template <int G, int CPL, int E, int D, bool HINT>
+__global__ void __launch_bounds__(128) spmm_fast_stream(const int4* __restrict__ pieces, int n_pieces,
+                                                        const int* __restrict__ row_ptr, const int2* __restrict__ edges,
+                                                        const float* __restrict__ h, float* __restrict__ out,
+                                                        float* __restrict__ scratch, int ld, int nchunk, int accumulate,
+                                                        int relu, int hub_max, Epi ep) {
+  static_assert(G % E == 0 && (D - 1) * E <= G, "pipeline depth must stay within one record window");
+  uint64_t pol_last = 0, pol_first = 0;
+  if (HINT) {
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(pol_last));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol_first));
+  }
+  extern __shared__ float4 ring_all[];
+  const int lane = threadIdx.x & (G - 1);
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+  float4* ring = ring_all + (size_t)(threadIdx.x / G) * (D * E * CPL * G);  // [D][E][CPL][G]
+  const int groups = gridDim.x * (blockDim.x / G);
+  for (int idx = blockIdx.x * (blockDim.x / G) + threadIdx.x / G; idx < n_pieces; idx += groups) {
+    const int4 pc = __ldg(pieces + idx);
+    const bool seg = pc.x < 0;
+    const int e0 = pc.z, n = pc.w - pc.z;
+    const int nrows = seg ? 1 : pc.y - pc.x;
+    const bool acc_in = accumulate && !seg;
+    // row ends relative to e0 in two register windows of G rows (rows rb + lane, rb + G + lane; n past the
+    // piece); the window after next is loaded when consumption enters the second one
+    auto rwin = [&](int base) {
+      const int r = base + lane;
+      return (!seg && r < nrows) ? __ldg(row_ptr + pc.x + r + 1) - e0 : n;
+    };
+    int rb = 0, rend = rwin(0), rend2 = rwin(G);
+    auto orow = [&](int r) -> float* {
+      return seg ? scratch + (size_t)(-pc.x - 1) * ld : out + (size_t)(pc.x + r) * ld;
+    };
+    float4 acc[CPL], nxt[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) {
+      const int c = lane + k * G;
+      acc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+      nxt[k] = acc[k];
+      if (acc_in && c < nchunk) {
+        acc[k] = *reinterpret_cast<const float4*>(orow(0) + 4 * c);
+        if (nrows > 1) nxt[k] = *reinterpret_cast<const float4*>(orow(1) + 4 * c);
+      }
+    }
+    int cur = 0;
+    int cur_end = __shfl_sync(gmask, rend, 0, G);
+    // closes row `cur` and opens the next one (accumulator from the prefetched old output)
+    auto close_row = [&]() {
+      float* o = orow(cur);
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        const int c = lane + k * G;
+        if (c < nchunk) *reinterpret_cast<float4*>(o + 4 * c) = seg ? acc[k] : epi4(acc[k], relu, ep, pc.x + cur, 4 * c);
+      }
+      ++cur;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        const int c = lane + k * G;
+        acc[k] = acc_in ? nxt[k] : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (acc_in && cur + 1 < nrows && c < nchunk) nxt[k] = *reinterpret_cast<const float4*>(orow(cur + 1) + 4 * c);
+      }
+      if (cur - rb == G) {
+        rb += G;
+        rend = rend2;
+        rend2 = rwin(rb + G);
+      }
+      cur_end = __shfl_sync(gmask, rend, cur - rb, G);
+    };
+    auto win = [&](int w) {
+      const int i = w * G + lane;
+      return i < n ? ld_edge(edges + e0 + i) : make_int2(0, 0);
+    };
+    int2 wa = win(0), wb = win(1), wc = win(2);  // records of windows wi, wi + 1, wi + 2
+    int wi = 0;
+    const int nst = (n + E - 1) / E;
+    auto issue = [&](int t) {  // gathers of stage t (edges t*E .. t*E+E-1) into slot t % D
+      float4* slot = ring + (t % D) * (E * CPL * G);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = t * E + e;
+        const int src = (i / G == wi) ? wa.x : wb.x;
+        const int rec = __shfl_sync(gmask, src, i & (G - 1), G);
+        if (i < n) {
+          const float* hr = h + (size_t)(rec & kColMask) * ld;
+          if (HINT) {
+            const int cls = static_cast<int>(static_cast<unsigned>(rec) >> 28);
+            const uint64_t pol = (cls != 0 && cls <= hub_max) ? pol_last : pol_first;
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              const int c = lane + k * G;
+              if (c < nchunk) cp_async16_hint(slot + (e * CPL + k) * G + lane, hr + 4 * c, pol);
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              const int c = lane + k * G;
+              if (c < nchunk) cp_async16_cg(slot + (e * CPL + k) * G + lane, hr + 4 * c);
+            }
+          }
+        }
+      }
+    };
+#pragma unroll
+    for (int t = 0; t < D - 1; ++t) {
+      if (t < nst) issue(t);
+      cp_async_commit();
+    }
+    for (int t = 0; t < nst; ++t) {
+      if (t > 0 && (t * E) % G == 0) {  // consumption enters window wi + 1
+        wa = wb;
+        wb = wc;
+        ++wi;
+        wc = win(wi + 2);
+      }
+      if (t + D - 1 < nst) issue(t + D - 1);
+      cp_async_commit();
+      cp_async_wait<D - 1>();
+      const float4* slot = ring + (t % D) * (E * CPL * G);
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const int i = t * E + e;
+        const float v = __int_as_float(__shfl_sync(gmask, wa.y, i & (G - 1), G));
+        if (i < n) {
+          while (i >= cur_end) close_row();  // uniform across the group
+#pragma unroll
+          for (int k = 0; k < CPL; ++k)
+            if (lane + k * G < nchunk) fma4(acc[k], v, slot[(e * CPL + k) * G + lane]);
+        }
+      }
+    }
+    cp_async_wait<0>();
+    while (cur < nrows) close_row();  // the last row and trailing empty rows
+  }
+}
+
 // Upload time, FAST work lists: sort keys for the light rows (ht - length; hub rows 2 ht) and the items.
 __global__ void light_keys(const int* __restrict__ rp, int rows, int ht, int* __restrict__ keys, int* __restrict__ ids) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += gridDim.x * blockDim.x) {
@@ -380,7 +524,8 @@ __global__ void __launch_bounds__(256) spmm_fast_hubs(const int4* __restrict__ h
   float* orow = out + (size_t)hb.x * ld;
   for (int c = threadIdx.x; c < ld / 4; c += blockDim.x) {
     float4 s = accumulate ? *reinterpret_cast<const float4*>(orow + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int q = 0; q < hb.z; ++q) {
+#pragma unroll 8
+    for (int q = 0; q < hb.z; ++q) {  // unrolled: the segment loads go out together, the sum stays in order
       const float4 p = *reinterpret_cast<const float4*>(scratch + (size_t)(hb.y + q) * ld + 4 * c);
       s.x += p.x;
       s.y += p.y;

@@ -75,15 +75,20 @@ def test_spmm_async_pipeline_bitwise(w):
     R.set_tuning("heavy_row", 128)
     try:
         outs = {}
-        for on in (0, 1):
+        # register gather; cp.async ring per row (spmm_fast_async); row-streaming pieces (spmm_fast_stream)
+        for key, (on, stream) in {"reg": (0, 0), "async": (1, 0), "stream": (1, 1)}.items():  # 2 = auto
             R.set_tuning("spmm_async", on)
-            outs[on] = (run_spmm(rp, ci, v, h, mode=R.SPMM_FAST),
-                        run_spmm(rp, ci, v, h, True, o0, relu=True, mode=R.SPMM_FAST))
+            R.set_tuning("spmm_stream", stream)
+            outs[key] = (run_spmm(rp, ci, v, h, mode=R.SPMM_FAST),
+                         run_spmm(rp, ci, v, h, True, o0, relu=True, mode=R.SPMM_FAST))
     finally:
         R.set_tuning("spmm_async", 1)
+        R.set_tuning("spmm_stream", 2)
         R.set_tuning("heavy_row", 4096)
-    for a, b in zip(outs[0], outs[1]):
-        assert bits_equal(a, b)
+    for key in ("async", "stream"):
+        for a, b in zip(outs["reg"], outs[key]):
+            assert bits_equal(a, b), key
+    outs[1] = outs["stream"]
     ref = (rp, ci, v)
     dense = np.zeros((rows, cols), np.float64)
     for r in range(rows):
@@ -150,3 +155,51 @@ def test_block_cache_reuses_memory_across_groups():
         assert again.epoch_loss == first.epoch_loss
     free1, _ = torch.cuda.mem_get_info()
     assert free0 - free1 < 64 << 20  # the repeats ran out of the cache
+
+
+@pytest.mark.parametrize("w", [32, 40, 128, 256, 512])
+@pytest.mark.parametrize("density,piece_nnz", [(0.002, 1024), (0.002, 1), (0.02, 7), (0.02, 100000)])
+def test_spmm_stream_pieces_bitwise(w, density, piece_nnz):
+    """Row-streaming pieces (spmm_fast_stream): many empty and 1-2 nonzero rows, pieces of one row
+    (piece_nnz 1) up to 32 rows, hub segments in the same work list, accumulate (prefetched old rows) and
+    relu: bitwise equal to the per-row cp.async kernel."""
+    rng = np.random.default_rng(int(w / density) + piece_nnz)
+    rows, cols = 1000, 900
+    rp, ci, v = random_tile(rng, rows, cols, density, hub_rows=(0, 31, 32, 500, 999), hub_len=700)
+    h = rng.uniform(-1, 1, (cols, w)).astype(np.float32)
+    o0 = rng.uniform(-1, 1, (rows, w)).astype(np.float32)
+    R.set_tuning("heavy_row", 256)
+    R.set_tuning("fast_segment", 64)
+    R.set_tuning("piece_nnz", piece_nnz)
+    try:
+        outs = {}
+        for stream in (0, 1):
+            R.set_tuning("spmm_stream", stream)
+            outs[stream] = (run_spmm(rp, ci, v, h, mode=R.SPMM_FAST),
+                            run_spmm(rp, ci, v, h, True, o0, mode=R.SPMM_FAST),
+                            run_spmm(rp, ci, v, h, True, o0, relu=True, mode=R.SPMM_FAST))
+    finally:
+        R.set_tuning("spmm_stream", 2)
+        R.set_tuning("piece_nnz", 1024)
+        R.set_tuning("heavy_row", 4096)
+        R.set_tuning("fast_segment", 2048)
+    for a, b in zip(outs[0], outs[1]):
+        assert bits_equal(a, b)
+
+
+def test_spmm_stream_training_bitwise():
+    """Whole training steps (P = 1 and the staged P = 3 with accumulating stages) are bitwise identical with
+    the row-streaming kernel on and off."""
+    ds = R.synth_graph(20000, 9.0, 0.7, 4, 40, 6)
+    for P in (1, 3):
+        cfg = R.GcnConfig([40, 64, 64, 6], epochs=2, seed=2, permute=True, overlap=P > 1, gemm_mode=R.GEMM_TF32X3,
+                          spmm_mode=R.SPMM_FAST, aggregate_input=True)
+        opts = R.TrainOptions(workers=P, devices=[0] * P, transport=R.TRANSPORT_NCCL if P == 1 else R.TRANSPORT_LOCAL)
+        try:
+            R.set_tuning("spmm_stream", 0)
+            a = R.train_run(ds, cfg, opts)
+            R.set_tuning("spmm_stream", 1)
+            b = R.train_run(ds, cfg, opts)
+        finally:
+            R.set_tuning("spmm_stream", 2)
+        assert a.epoch_loss == b.epoch_loss and a.w_hashes == b.w_hashes, P
