@@ -215,10 +215,40 @@ mg_status mg_partition_tile_info(const mg_partition* p, int32_t dir, int32_t i, 
                                  int64_t* cols, int64_t* nnz);
 mg_status mg_partition_tile_export(const mg_partition* p, int32_t dir, int32_t i, int32_t j, int64_t* row_ptr,
                                    int64_t* col_idx, float* values);
-/* Permuted features (n x d0), labels, mask and the permutation's forward map (old id -> new id). */
+/* Permuted features, labels and mask of the stored rows (rows_info: [row0, row0 + rows); every row for
+ * mg_prepare / mg_prepare_device, the rank's row block for mg_synth_rank_finish) and the permutation's
+ * forward map over all n vertices (old id -> new id). */
 mg_status mg_partition_rows_export(const mg_partition* p, float* features, int32_t* labels, uint8_t* mask,
                                    int64_t* perm_forward);
+mg_status mg_partition_rows_info(const mg_partition* p, int64_t* row0, int64_t* rows);
 void mg_partition_free(mg_partition* p);
+
+/* ---------------------------------------------------------------- per-rank synthetic input (papers scale)
+ * synth_graph (inc/dataset.hpp:287-334) + prepare_data (inc/driver.hpp:87-117) fused for ONE rank of a
+ * P-way job, without materialising the whole graph or all features: the rank replays the generator's
+ * mt19937_64 stream (stub draws, then the feature and label draws with the other ranks' rows skipped),
+ * keeps the adjacency rows it owns after the permutation, and needs from the other ranks only the
+ * deduplicated degree of every vertex (normalize_in_degree's column sums; a symmetric graph's column sum
+ * is its row length). The partition it returns is bit-identical to row block `rank` of
+ * prepare_data(synth_graph(...), cfg, P) (only_rank = rank).
+ *   open    replays the stub stream, builds the rank's rows; flags MG_SYNTH_GRAPH_ONLY skips features
+ *   degrees the rank's row lengths (degrees of vertices row0 .. row0 + rows - 1, permuted ids)
+ *   block_degrees  the same for any row block b, computed from the kept stub stream (a lone process
+ *           derives every degree this way: P passes of 1/P of the graph each, no collective)
+ *   finish  takes every vertex's degree (n entries, permuted ids; NULL = compute via block_degrees) and
+ *           emits the rank's forward and backward tiles, rows and labels; the handle's graph state is
+ *           released. */
+typedef struct mg_synth_rank mg_synth_rank;
+#define MG_SYNTH_GRAPH_ONLY 1
+mg_status mg_synth_rank_open(int64_t n, double avg_degree, double exponent, uint64_t seed, int64_t feature_dim,
+                             int32_t classes, const mg_config* cfg, int32_t workers, int32_t rank, int32_t flags,
+                             mg_synth_rank** out);
+mg_status mg_synth_rank_info(const mg_synth_rank* h, int64_t* row0, int64_t* rows, int64_t* nnz,
+                             int64_t* stubs);
+mg_status mg_synth_rank_degrees(const mg_synth_rank* h, int32_t* degrees);
+mg_status mg_synth_rank_block_degrees(mg_synth_rank* h, int32_t block, int32_t* degrees);
+mg_status mg_synth_rank_finish(mg_synth_rank* h, const int32_t* degrees, mg_partition** out);
+void mg_synth_rank_free(mg_synth_rank* h);
 
 /* ---------------------------------------------------------------- device training group
  * The set of GcnWorkers (inc/gcn.hpp:101-398) living in this process, plus their communicator

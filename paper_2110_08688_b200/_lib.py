@@ -74,7 +74,15 @@ SIGNATURES = [
     ("mg_partition_tile_export", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                            C.c_void_p]),
     ("mg_partition_rows_export", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("mg_partition_rows_info", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("mg_partition_free", None, [C.c_void_p]),
+    ("mg_synth_rank_open", C.c_int, [C.c_int64, C.c_double, C.c_double, C.c_uint64, C.c_int64, C.c_int32,
+                                     C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p]),
+    ("mg_synth_rank_info", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("mg_synth_rank_degrees", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("mg_synth_rank_block_degrees", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    ("mg_synth_rank_finish", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("mg_synth_rank_free", None, [C.c_void_p]),
     ("mg_device_count", C.c_int32, []),
     ("mg_nccl_unique_id", C.c_int, [C.c_void_p]),
     ("mg_group_create", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,

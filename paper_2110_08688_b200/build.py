@@ -11,7 +11,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmggcn.so")
-SOURCES = ["mg_host.cpp", "mg_io.cpp", "mg_timeline.cpp", "mg_json.cpp", "mg_device.cu", "mg_tc_gemm.cu", "mg_prepare_dev.cu"]
+SOURCES = ["mg_host.cpp", "mg_io.cpp", "mg_timeline.cpp", "mg_json.cpp", "mg_synth_rank.cpp", "mg_device.cu", "mg_tc_gemm.cu", "mg_prepare_dev.cu"]
 HEADERS = ["mg_internal.hpp", "mg_kernels.cuh", "mg_tc_gemm.cuh", "mg_epi.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

@@ -1697,11 +1697,11 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
     g->transport = transport;
     // labels in range for masked rows (checked where the reference checks, at the loss: dense.hpp:263)
     const index_t C = cfg.dims.back();
-    for (index_t v = 0; v < p->n && g->labels_ok; ++v)
-      if (p->mask[v] && (p->labels[v] < 0 || p->labels[v] >= C)) {
+    for (index_t i = 0; i < p->rows_stored() && g->labels_ok; ++i)
+      if (p->mask[i] && (p->labels[i] < 0 || p->labels[i] >= C)) {
         g->labels_ok = false;
-        g->label_error = "softmax_xent: label " + std::to_string(p->labels[v]) + " out of range [0, " +
-                         std::to_string(C) + ") at row " + std::to_string(v);
+        g->label_error = "softmax_xent: label " + std::to_string(p->labels[i]) + " out of range [0, " +
+                         std::to_string(C) + ") at row " + std::to_string(p->row0 + i);
       }
     const int L = cfg.layers();
     Stopwatch sw;
@@ -1714,6 +1714,9 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       if (!p->has_row(w.rank)) throw ValueError("group: partition lacks row block " + std::to_string(w.rank));
       w.r0 = p->bounds[w.rank];
       w.rows = p->bounds[w.rank + 1] - w.r0;
+      if (w.r0 < p->row0 || w.r0 + w.rows > p->row0 + p->rows_stored())
+        throw ValueError("group: partition lacks the rows of block " + std::to_string(w.rank));
+      const index_t lr0 = w.r0 - p->row0;  // first row of this block in the partition's row storage
       MG_CUDA(cudaSetDevice(w.device));
       MG_CUDA(cudaStreamCreateWithFlags(&w.s0, cudaStreamNonBlocking));
       MG_CUDA(cudaStreamCreateWithFlags(&w.s1, cudaStreamNonBlocking));
@@ -1735,7 +1738,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       // while the backward tiles are processed (after the forward tiles' DMAs, so the two do not share
       // the link); otherwise synchronously after the tiles.
       w.x = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));
-      const float* xsrc = p->features.data() + w.r0 * p->d0;
+      const float* xsrc = p->features.data() + lr0 * p->d0;
       const bool x_async = p->d0 == g->ld[0] && w.rows > 0 && is_pinned_host(xsrc);
       cudaStream_t xs = nullptr;
       // tiles
@@ -1764,8 +1767,8 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       w.labels = dalloc_t<int>(*g, w, std::max<index_t>(1, w.rows));
       w.mask = dalloc_t<uint8_t>(*g, w, std::max<index_t>(1, w.rows));
       if (w.rows) {
-        MG_CUDA(cudaMemcpy(w.labels, p->labels.data() + w.r0, sizeof(int) * w.rows, cudaMemcpyHostToDevice));
-        MG_CUDA(cudaMemcpy(w.mask, p->mask.data() + w.r0, w.rows, cudaMemcpyHostToDevice));
+        MG_CUDA(cudaMemcpy(w.labels, p->labels.data() + lr0, sizeof(int) * w.rows, cudaMemcpyHostToDevice));
+        MG_CUDA(cudaMemcpy(w.mask, p->mask.data() + lr0, w.rows, cudaMemcpyHostToDevice));
       }
       sw.lap("rows");
       // the L + 3 buffer plan (gcn.hpp:134-140)

@@ -107,22 +107,39 @@ Rng::Rng(std::uint64_t seed) {
   idx_ = 312;
 }
 
-std::uint64_t Rng::next() {
-  if (idx_ >= 312) {
-    for (int i = 0; i < 312; ++i) {
-      const std::uint64_t x = (mt_[i] & 0xFFFFFFFF80000000ULL) | (mt_[(i + 1) % 312] & 0x7FFFFFFFULL);
-      std::uint64_t xa = x >> 1;
-      if (x & 1ULL) xa ^= 0xB5026F5AA96619E9ULL;
-      mt_[i] = mt_[(i + 156) % 312] ^ xa;
-    }
-    idx_ = 0;
+void Rng::twist() {  // the mt19937_64 recurrence, split so no index needs a modulo
+  constexpr std::uint64_t UM = 0xFFFFFFFF80000000ULL, LM = 0x7FFFFFFFULL, A = 0xB5026F5AA96619E9ULL;
+  int i = 0;
+  for (; i < 156; ++i) {
+    const std::uint64_t x = (mt_[i] & UM) | (mt_[i + 1] & LM);
+    mt_[i] = mt_[i + 156] ^ (x >> 1) ^ ((x & 1ULL) ? A : 0ULL);
   }
+  for (; i < 311; ++i) {
+    const std::uint64_t x = (mt_[i] & UM) | (mt_[i + 1] & LM);
+    mt_[i] = mt_[i - 156] ^ (x >> 1) ^ ((x & 1ULL) ? A : 0ULL);
+  }
+  const std::uint64_t x = (mt_[311] & UM) | (mt_[0] & LM);
+  mt_[311] = mt_[155] ^ (x >> 1) ^ ((x & 1ULL) ? A : 0ULL);
+  idx_ = 0;
+}
+
+std::uint64_t Rng::next() {
+  if (idx_ >= 312) twist();
   std::uint64_t y = mt_[idx_++];
   y ^= (y >> 29) & 0x5555555555555555ULL;
   y ^= (y << 17) & 0x71D67FFFEDA60000ULL;
   y ^= (y << 37) & 0xFFF7EEE000000000ULL;
   y ^= y >> 43;
   return y;
+}
+
+void Rng::discard(std::uint64_t k) {
+  while (k) {
+    if (idx_ >= 312) twist();
+    const std::uint64_t a = std::min<std::uint64_t>(k, static_cast<std::uint64_t>(312 - idx_));
+    idx_ += static_cast<int>(a);
+    k -= a;
+  }
 }
 
 // ---------------------------------------------------------------- config (inc/gcn.hpp:14-36)
@@ -718,6 +735,14 @@ mg_status mg_partition_rows_export(const mg_partition* p, float* features, int32
     if (labels) std::copy(p->labels.begin(), p->labels.end(), labels);
     if (mask) std::copy(p->mask.begin(), p->mask.end(), mask);
     if (perm_forward) std::copy(p->perm_forward.begin(), p->perm_forward.end(), perm_forward);
+  });
+}
+
+mg_status mg_partition_rows_info(const mg_partition* p, int64_t* row0, int64_t* rows) {
+  return guarded([&] {
+    if (!p) throw ValueError("partition: null");
+    if (row0) *row0 = p->row0;
+    if (rows) *rows = p->rows_stored();
   });
 }
 

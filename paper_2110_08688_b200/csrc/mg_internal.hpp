@@ -75,11 +75,17 @@ class Rng {
   std::uint64_t below(std::uint64_t n) { return next() % n; }
   double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
   double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+  // std::mt19937_64::discard(k): advances the stream by k draws (state twists only, no tempering).
+  void discard(std::uint64_t k);
 
  private:
+  void twist();
   std::uint64_t mt_[312];
   int idx_;
 };
+
+// rowgcn::random_permutation (inc/partition.hpp:69-79): forward map old id -> new id.
+void random_permutation(index_t n, std::uint64_t seed, std::vector<index_t>& forward);
 
 // ---------------------------------------------------------------- config
 struct Config {
@@ -174,10 +180,14 @@ struct mg_partition {
   int only_rank = -1;
   std::vector<mg::index_t> bounds;
   std::vector<mg::index_t> perm_forward;
-  mg::UploadVec<float> features;  // permuted, n x d0
+  // features / labels / mask hold permuted rows [row0, row0 + rows_stored()): every row for mg_prepare,
+  // the rank's row block for the per-rank synthetic path (mg_synth_rank_finish)
+  mg::index_t row0 = 0;
+  mg::UploadVec<float> features;  // permuted, rows_stored() x d0
   std::vector<std::int32_t> labels;
   std::vector<std::uint8_t> mask;
   // tiles[dir][i][j]; rows i != only_rank are left empty when only_rank >= 0
   std::vector<std::vector<mg::Tile>> tiles[2];
   bool has_row(int i) const { return only_rank < 0 || only_rank == i; }
+  mg::index_t rows_stored() const { return static_cast<mg::index_t>(labels.size()); }
 };

@@ -498,10 +498,18 @@ class PreparedData:
         _check(lib().mg_partition_tile_export(self._h, direction, i, j, _p(rp), _p(ci), _p(v)))
         return rp, ci[:z.value], v[:z.value]
 
+    def rows_info(self):
+        """(row0, rows): the permuted rows whose features / labels / mask this partition holds."""
+        r0, r = C.c_int64(), C.c_int64()
+        _check(lib().mg_partition_rows_info(self._h, C.byref(r0), C.byref(r)))
+        return r0.value, r.value
+
     def rows_export(self, d0: int):
-        x = np.zeros((self.n, d0), np.float32)
-        lab = np.zeros(self.n, np.int32)
-        m = np.zeros(self.n, np.uint8)
+        """Permuted features, labels and mask of the stored rows (rows_info), and the forward permutation."""
+        rows = self.rows_info()[1]
+        x = np.zeros((rows, d0), np.float32)
+        lab = np.zeros(rows, np.int32)
+        m = np.zeros(rows, np.uint8)
         pf = np.zeros(self.n, np.int64)
         _check(lib().mg_partition_rows_export(self._h, _p(x), _p(lab), _p(m), _p(pf)))
         return x, lab, m, pf
@@ -518,6 +526,63 @@ def prepare_data(ds: Dataset, cfg: GcnConfig, workers: int, only_rank: int = -1,
         _check(lib().mg_prepare_device(ds._h, C.byref(cfg._c()), int(workers), int(only_rank), int(device),
                                        C.byref(out)))
     return PreparedData(out.value, workers)
+
+
+class SynthRank:
+    """One rank's share of synth_graph + prepare_data without the whole graph (mg_synth_rank_*, mggcn.h):
+    open replays the generator's stream and keeps the rank's rows; degrees() are the rank's row lengths,
+    block_degrees(b) any block's (from the kept stub stream); finish(all_degrees) emits the partition."""
+
+    def __init__(self, n, avg_degree, exponent, seed, feature_dim, classes, cfg: GcnConfig, workers: int,
+                 rank: int, graph_only: bool = False):
+        out = C.c_void_p()
+        self._h = C.c_void_p()
+        _check(lib().mg_synth_rank_open(int(n), float(avg_degree), float(exponent), int(seed), int(feature_dim),
+                                        int(classes), C.byref(cfg._c()), int(workers), int(rank),
+                                        1 if graph_only else 0, C.byref(out)))
+        self._h = C.c_void_p(out.value)
+        self.n, self.workers, self.rank = int(n), int(workers), int(rank)
+        r0, r, z, st = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        _check(lib().mg_synth_rank_info(self._h, C.byref(r0), C.byref(r), C.byref(z), C.byref(st)))
+        self.row0, self.rows, self.nnz, self.stubs = r0.value, r.value, z.value, st.value
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and h.value and not _finalizing():
+            lib().mg_synth_rank_free(h)
+            self._h = C.c_void_p()
+
+    def degrees(self) -> np.ndarray:
+        d = np.zeros(max(self.rows, 1), np.int32)
+        _check(lib().mg_synth_rank_degrees(self._h, _p(d)))
+        return d[:self.rows]
+
+    def block_degrees(self, block: int) -> np.ndarray:
+        b0, b1 = int(block) * self.n // self.workers, (int(block) + 1) * self.n // self.workers
+        d = np.zeros(max(b1 - b0, 1), np.int32)
+        _check(lib().mg_synth_rank_block_degrees(self._h, int(block), _p(d)))
+        return d[:b1 - b0]
+
+    def finish(self, all_degrees: Optional[np.ndarray] = None) -> PreparedData:
+        out = C.c_void_p()
+        if all_degrees is not None:
+            all_degrees = np.ascontiguousarray(all_degrees, np.int32)
+            if all_degrees.shape != (self.n,):
+                raise ValueError(f"synth_rank: need {self.n} degrees, got {all_degrees.shape}")
+        _check(lib().mg_synth_rank_finish(self._h, _p(all_degrees) if all_degrees is not None else None,
+                                          C.byref(out)))
+        return PreparedData(out.value, self.workers)
+
+
+def synth_prepare_rank(n, avg_degree, exponent, seed, feature_dim, classes, cfg: GcnConfig, workers: int,
+                       rank: int, exchange=None) -> PreparedData:
+    """Row block `rank` of prepare_data(synth_graph(n, avg_degree, exponent, seed, feature_dim, classes), cfg,
+    workers) (inc/dataset.hpp:287-334, inc/driver.hpp:87-117), bit-identical, built from the generator's
+    stream without the rest of the graph. exchange(local_degrees) -> all n degrees (e.g. an all-gather
+    over the job's process group); None: this process derives every block's degrees itself."""
+    h = SynthRank(n, avg_degree, exponent, seed, feature_dim, classes, cfg, workers, rank)
+    degs = None if exchange is None else exchange(h.degrees())
+    return h.finish(degs)
 
 
 # ----------------------------------------------------------------------------- device group (gcn.hpp)

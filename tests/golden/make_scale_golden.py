@@ -17,6 +17,8 @@ Writes, next to this script:
                         full; forward activations, loss gradient and H-grads on a row sample plus hub rows;
                         per-tensor max |x| and per-column sums (inc/gcn.hpp:175-184); the f64 build's W_G
   scale_c4s16step.npz   the same step on the products 1/16 sample from the f32 and the f64 reference
+  scale_ranks.json      per-rank digests of prepare_data at papers shape, 1/64 scale, P = 8 (the rows and
+                        tiles one rank of the job holds): pins the per-rank input path mg_synth_rank_*
 """
 import json
 import os
@@ -30,7 +32,7 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.dirname(HERE))
 from oracle.pyoracle import Ref, make_cfg  # noqa: E402
-from scale_common import (PARTITION_CASES, SCALE, c4_sample_rows, colsums, dataset_digest, sha,  # noqa: E402
+from scale_common import (PARTITION_CASES, RANK_CASES, SCALE, c4_sample_rows, colsums, dataset_digest, sha,  # noqa: E402
                           tile_digest)
 
 EPOCHS = 3
@@ -184,13 +186,42 @@ def c4s16step(ref):
     np.savez_compressed(os.path.join(HERE, "scale_c4s16step.npz"), **g)
 
 
+def ranks(ref):
+    """scale_ranks.json: for each (config, P) of RANK_CASES, the reference's whole-graph prepare_data cut
+    into what one rank of a P-way job holds — per rank the bounds, its slices of the permuted features /
+    labels / mask, and its forward and backward tile row (inc/driver.hpp:87-117) — plus the permutation."""
+    out = {}
+    for name, P in RANK_CASES:
+        ds = synth(ref, name)
+        log(name, "synth", ds.n, ds.nnz)
+        d0 = SCALE[name]["dims"][0]
+        cfg = make_cfg(SCALE[name]["dims"], seed=1, permute=True, overlap=True)
+        p = ref.prepare(ds, cfg, P)
+        feats = np.asarray(p.features, np.float32).reshape(ds.n, d0)
+        e = {"n": ds.n, "nnz": ds.nnz, "P": P, "bounds": [int(b) for b in p.bounds],
+             "mask_count": int(p.mask_count), "perm_forward": sha(p.perm_forward), "ranks": {}}
+        for r in range(P):
+            b0, b1 = int(p.bounds[r]), int(p.bounds[r + 1])
+            e["ranks"][str(r)] = {
+                "features": sha(feats[b0:b1]), "labels": sha(np.asarray(p.labels, np.int32)[b0:b1]),
+                "mask": sha(np.asarray(p.mask, np.uint8)[b0:b1]),
+                "tiles": {f"{d},{j}": tile_digest(*p.tiles[d][r][j]) for d in (0, 1) for j in range(P)},
+                "nnz": {f"{d},{j}": int(p.tiles[d][r][j][0][-1]) for d in (0, 1) for j in range(P)}}
+        out[f"{name}:{P}"] = e
+        log(name, "P", P, "done")
+        del p, ds, feats
+    with open(os.path.join(HERE, "scale_ranks.json"), "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+
+
 def main():
     which = sys.argv[1:] or ["partition", "traj", "c4step", "c4s16step"]
     ref = Ref()
     ref.set_spmm_threads(max(1, (os.cpu_count() or 8)))
     for w in which:
         t = time.time()
-        {"partition": partition, "traj": traj, "c4step": c4step, "c4f64": c4f64, "c4s16step": c4s16step}[w](ref)
+        {"partition": partition, "traj": traj, "c4step": c4step, "c4f64": c4f64, "c4s16step": c4s16step,
+         "ranks": ranks}[w](ref)
         log(w, f"{time.time() - t:.0f} s")
 
 

@@ -16,7 +16,12 @@ SCALE = {
     "c4": dict(n=2449029, deg=50.6, dims=[100, 256, 256, 47]),
     # the reference arm's bounded sample of C4 (bench.py reference_epoch_sample: 1/16 of the vertices)
     "c4s16": dict(n=153064, deg=50.6, dims=[100, 256, 256, 47]),
+    # C5 papers-shaped at 1/64 of the vertices (same degree, dims, classes): the per-rank input path
+    # (mg_synth_rank_*) is pinned rank by rank at P = 8 against the reference's whole-graph prepare_data
+    "c5s64": dict(n=111059956 // 64, deg=28.8, dims=[128, 128, 128, 172]),
 }
+# per-rank digests (features / labels / mask slices of each rank's row block) are pinned for these
+RANK_CASES = [("c5s64", 8)]
 # partition digests are pinned for these (config, P) pairs (VERDICT r1 "next round" item 1)
 PARTITION_CASES = [("c2", 1), ("c2", 2), ("c3", 1), ("c3", 8), ("c4", 1), ("c4", 8)]
 # rows of the C4 teacher-forced step dump kept in full: a seeded uniform sample plus the top hub rows

@@ -50,6 +50,19 @@ def _worker(rank, world, port, q):
             for j in range(world):
                 for a, b in zip(mine.tile(d, rank, j), full.tile(d, rank, j)):
                     assert np.array_equal(a, b)
+        # 2b. the per-rank synthetic input path with the degree all-gather bench.py uses under torchrun
+        #     (mg_synth_rank_*): identical to the same row block of the whole-graph partition
+        from paper_2110_08688_b200.torchdist import degree_exchange
+        sr = R.synth_prepare_rank(n, 9.0, 0.7, 3, 5, 3, cfg, world, rank, exchange=degree_exchange(dist, n, world))
+        for d in (0, 1):
+            for j in range(world):
+                for a, b_ in zip(sr.tile(d, rank, j), full.tile(d, rank, j)):
+                    assert np.array_equal(a, b_)
+        xs, ls, _, _ = sr.rows_export(5)
+        xf, lf, _, _ = full.rows_export(5)
+        q0, q1 = int(full.bounds[rank]), int(full.bounds[rank + 1])
+        assert sr.rows_info() == (q0, q1 - q0)
+        assert np.array_equal(xs, xf[q0:q1]) and np.array_equal(ls, lf[q0:q1])
         b = mine.bounds
         r0, r1 = int(b[rank]), int(b[rank + 1])
         # 3. staged SpMM over torch.distributed broadcasts: out_i = sum_j tile(i, j) H^j, stages in order
