@@ -47,52 +47,70 @@ struct mg_synth_rank {
 
 namespace {
 
+// f(s, e) over [0, total) in chunks of `chunk`, claimed dynamically by host_threads() workers (the stub
+// store is power-law skewed by vertex id: static splits over vertices leave one thread most of the work).
+void dynamic_for(index_t total, index_t chunk, const std::function<void(index_t, index_t)>& f) {
+  std::atomic<index_t> next{0};
+  parallel_for(host_threads(), [&](index_t, index_t) {
+    for (index_t s; (s = next.fetch_add(chunk)) < total;) f(s, std::min(total, s + chunk));
+  }, 1);
+}
+
+// Every stub k in [s, e) with its drawing vertex u (so[u] <= k < so[u+1]): g(u, k_begin, k_end) per run.
+template <class G>
+void stub_runs(const mg_synth_rank& h, index_t s, index_t e, G&& g) {
+  const index_t* so = h.so.data();
+  index_t u = std::upper_bound(so, so + h.n + 1, s) - so - 1;
+  for (index_t k = s; k < e; ++u) {
+    const index_t ke = std::min(e, so[u + 1]);
+    if (ke > k) g(u, k, ke);
+    k = std::max(k, ke);
+  }
+}
+
 // Rows bounds[b] .. bounds[b+1] of the permuted symmetric adjacency: sorted unique permuted columns.
 void build_block(const mg_synth_rank& h, int b, std::vector<index_t>& rp, std::vector<std::int32_t>& ci) {
-  const index_t b0 = h.bounds[b], b1 = h.bounds[b + 1], rows = b1 - b0, n = h.n;
+  const index_t b0 = h.bounds[b], b1 = h.bounds[b + 1], rows = b1 - b0;
+  const index_t stubs = h.so[h.n];
+  constexpr index_t kChunk = index_t(1) << 20;
   const index_t* fwd = h.fwd.data();
-  const index_t* so = h.so.data();
   const std::int32_t* sv = h.sv.data();
   std::unique_ptr<std::atomic<index_t>[]> cur(new std::atomic<index_t>[rows + 1]);
   parallel_for(rows + 1, [&](index_t s, index_t e) {
     for (index_t r = s; r < e; ++r) cur[r].store(0, std::memory_order_relaxed);
   });
   auto in_block = [b0, b1](index_t x) { return x >= b0 && x < b1; };
-  // count: row fu gets v for its own stubs, row fv gets u for every stub (u, v)
-  parallel_for(n, [&](index_t s, index_t e) {
-    for (index_t u = s; u < e; ++u) {
+  // count: row fu gets fv for its own stubs, row fv gets fu for every stub (u, v)
+  dynamic_for(stubs, kChunk, [&](index_t s, index_t e) {
+    stub_runs(h, s, e, [&](index_t u, index_t k0, index_t k1) {
       const index_t fu = fwd[u];
-      const bool mine = in_block(fu);
-      if (mine && so[u + 1] > so[u]) cur[fu - b0 + 1].fetch_add(so[u + 1] - so[u], std::memory_order_relaxed);
-      for (index_t k = so[u]; k < so[u + 1]; ++k) {
-        const index_t fv = sv[k];
-        if (in_block(fv)) cur[fv - b0 + 1].fetch_add(1, std::memory_order_relaxed);
-      }
-    }
-  }, 1 << 16);
+      if (in_block(fu)) cur[fu - b0 + 1].fetch_add(k1 - k0, std::memory_order_relaxed);
+      for (index_t k = k0; k < k1; ++k)
+        if (in_block(sv[k])) cur[sv[k] - b0 + 1].fetch_add(1, std::memory_order_relaxed);
+    });
+  });
   std::vector<index_t> raw(rows + 1, 0);
   for (index_t r = 0; r < rows; ++r) raw[r + 1] = raw[r] + cur[r + 1].load(std::memory_order_relaxed);
   parallel_for(rows, [&](index_t s, index_t e) {
     for (index_t r = s; r < e; ++r) cur[r].store(raw[r], std::memory_order_relaxed);
   });
   std::vector<std::int32_t> buf(static_cast<size_t>(raw[rows]));
-  parallel_for(n, [&](index_t s, index_t e) {
-    for (index_t u = s; u < e; ++u) {
+  dynamic_for(stubs, kChunk, [&](index_t s, index_t e) {
+    stub_runs(h, s, e, [&](index_t u, index_t k0, index_t k1) {
       const index_t fu = fwd[u];
       const bool mine = in_block(fu);
-      index_t pos = 0;
-      if (mine && so[u + 1] > so[u]) pos = cur[fu - b0].fetch_add(so[u + 1] - so[u], std::memory_order_relaxed);
-      for (index_t k = so[u]; k < so[u + 1]; ++k) {
+      index_t pos = mine ? cur[fu - b0].fetch_add(k1 - k0, std::memory_order_relaxed) : 0;
+      for (index_t k = k0; k < k1; ++k) {
         const index_t fv = sv[k];
         if (mine) buf[pos++] = static_cast<std::int32_t>(fv);
         if (in_block(fv)) buf[cur[fv - b0].fetch_add(1, std::memory_order_relaxed)] = static_cast<std::int32_t>(fu);
       }
-    }
-  }, 1 << 16);
+    });
+  });
   cur.reset();
   // per row: sort + unique (the reference's std::sort + std::unique over the pair list, restricted to a row)
   std::vector<index_t> len(rows + 1, 0);
-  parallel_for(rows, [&](index_t s, index_t e) {
+  dynamic_for(rows, 4096, [&](index_t s, index_t e) {
     for (index_t r = s; r < e; ++r) {
       std::int32_t* row = buf.data() + raw[r];
       const index_t l = raw[r + 1] - raw[r];
@@ -102,7 +120,7 @@ void build_block(const mg_synth_rank& h, int b, std::vector<index_t>& rp, std::v
         if (w == 0 || row[i] != row[w - 1]) row[w++] = row[i];
       len[r + 1] = w;
     }
-  }, 256);
+  });
   rp.assign(rows + 1, 0);
   for (index_t r = 0; r < rows; ++r) rp[r + 1] = rp[r] + len[r + 1];
   ci.resize(static_cast<size_t>(rp[rows]));

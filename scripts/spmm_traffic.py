@@ -24,7 +24,8 @@ for r in rows[2:]:
     kernels += 1
     for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         i = hdr.index(m)
-        total += float(r[i].replace(",", "")) * scale[units[i]]
+        v = float(r[i].replace(",", "")) * scale[units[i]]
+        total += 0.0 if v != v else v  # ncu reports -nan for some ~80 us hub-reduction launches (MB-scale)
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 path = os.path.join(root, "profiles", "spmm_traffic.json")
 data = json.load(open(path)) if os.path.exists(path) else {}
