@@ -595,11 +595,25 @@ static int spmm_heavy(const SpmmLaunch& t, const float* h, float* out, index_t l
 }
 
 // GeMM dispatch: exact SIMT or tcgen05 (mg_tc_gemm.cuh).
+// mg_dev_gemm only: per-row max |A| pairs {max, 0} (in the training step the producers of A write them)
+__global__ void row_absmax_pairs(const float* __restrict__ A, long lda, long M, long K, float* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  for (long r = (static_cast<long>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; r < M;
+       r += static_cast<long>(gridDim.x) * blockDim.x / 32) {
+    float m = 0.0f;
+    for (long k = lane; k < K; k += 32) m = fmaxf(m, fabsf(A[r * lda + k]));
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) *reinterpret_cast<float2*>(out + 2 * r) = make_float2(m, 0.0f);
+  }
+}
+
 static int gemm_launch(int mode, bool ta, bool tb, index_t M, index_t N, index_t K, const float* A, index_t lda,
                        const float* B, index_t ldb, float* Cm, index_t ldc, int epi, cudaStream_t s,
-                       float* ws = nullptr, size_t ws_bytes = 0, const k::Epi& ep = k::Epi{}) {
+                       float* ws = nullptr, size_t ws_bytes = 0, const k::Epi& ep = k::Epi{},
+                       const float* rmax_in = nullptr) {
   if (M <= 0 || N <= 0) return 0;
-  if (mode != MG_GEMM_EXACT) return tc::gemm(mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, ws, ws_bytes, s, ep);
+  if (mode != MG_GEMM_EXACT)
+    return tc::gemm(mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, ws, ws_bytes, s, ep, rmax_in);
   dim3 grid(ceil_div(M, k::kGBM), ceil_div(N, k::kGBN));
 #define MG_G(TA, TB, E) k::gemm_exact<TA, TB, E><<<grid, 256, 0, s>>>((int)M, (int)N, (int)K, A, lda, B, ldb, Cm, ldc, ep)
   if (!ta && !tb) {
@@ -628,6 +642,10 @@ struct Worker {
   std::vector<float*> ahw;
   float *hw = nullptr, *bc1 = nullptr, *bc2 = nullptr;
   float* ax = nullptr;  // Â·X (rows x ld0) when Config::aggregate_first()
+  // TF32X3 + FAST: per-row max |y| pairs (k::Epi::rmax) of the GeMM A operands, written by their producers
+  // for the scaled fp16 split: slot l < L for ahw[l], L for hw, L + 1 for ax; rows x 2 floats each
+  float* rm = nullptr;
+  float* rm_slot(int s) const { return rm ? rm + static_cast<size_t>(s) * 2 * std::max<index_t>(rows, 1) : nullptr; }
   std::vector<float*> W, WG, M, V, stage;
   double* partials = nullptr;
   float* seg_scratch = nullptr;  // MG_SPMM_FAST hub-row segment partials (max segments x ld_max)
@@ -1131,8 +1149,9 @@ class Step {
   // tile on the compute stream, accumulating for j > 0. Event edges:
   //   spmm(j) <- broadcast(j);   broadcast(j) <- spmm(j-2) overlapped / spmm(j-1) otherwise / prior.
   // relu_last fuses the forward ReLU into the final stage's epilogue.
+  // rm_slot >= 0: the last stage also writes the output's per-row max pairs into Worker::rm_slot(rm_slot)
   void staged_spmm(int dir, index_t width, const std::vector<float*>& src, const std::vector<float*>& out,
-                   bool relu_last, int epi_layer = -1) {
+                   bool relu_last, int epi_layer = -1, int rm_slot = -1) {
     const index_t ld = pad4(width);
     const bool ov = cfg_.overlap;
     std::vector<uint64_t> prior_task(nloc());
@@ -1168,7 +1187,8 @@ class Step {
         SpmmLaunch sl{t.row_ptr, t.edges, t.light, t.n_light, t.heavy, t.n_heavy};
         const int acc = j > 0, relu = relu_last && j == P_ - 1;
         // the layer's bias / dropout ride on the final stage's output write
-        const k::Epi ep = (epi_layer >= 0 && j == P_ - 1) ? out_epi(w, epi_layer, relu_last) : k::Epi{};
+        k::Epi ep = (epi_layer >= 0 && j == P_ - 1) ? out_epi(w, epi_layer, relu_last) : k::Epi{};
+        if (j == P_ - 1 && rm_slot >= 0 && cfg_.spmm_mode == MG_SPMM_FAST) ep.rmax = w.rm_slot(rm_slot);
         const int pi = prof_begin(w);
         if (cfg_.spmm_mode == MG_SPMM_FAST) {
           FastLaunch fl{t.items, t.n_items, t.hubs, t.n_hubs, t.edges, w.seg_scratch, t.hubs_classed, t.cols,
@@ -1196,12 +1216,13 @@ class Step {
 
   // one GeMM task ("gemm", op, layer) on the compute lane, depending on the lane's previous task
   void gemm(size_t k, const char* op, int layer, bool ta, bool tb, index_t M, index_t N, index_t K, const float* A,
-            index_t lda, const float* B, index_t ldb, float* Cm, index_t ldc, int epi, const k::Epi& ep = k::Epi{}) {
+            index_t lda, const float* B, index_t ldb, float* Cm, index_t ldc, int epi, const k::Epi& ep = k::Epi{},
+            const float* rmax_in = nullptr) {
     Worker& w = W(k);
     const int th = tl_begin(k, 0, "gemm", op, layer, {w.last_task[0]});
     const int pi = prof_begin(w);
     g_.kernels_last += gemm_launch(cfg_.gemm_mode, ta, tb, M, N, K, A, lda, B, ldb, Cm, ldc, epi, w.s0, w.ws, w.ws_bytes,
-                                   ep);
+                                   ep, rmax_in);
     prof_end(w, pi, 1);
     tl_end(k, th);
   }
@@ -1262,28 +1283,34 @@ class Step {
           src[k] = W(k).x;
           out[k] = W(k).ax;
         }
-        staged_spmm(0, dl, src, out, false);
+        staged_spmm(0, dl, src, out, false, -1, L_ + 1);
         for (size_t k = 0; k < nloc(); ++k) {
           Worker& w = W(k);
           dev(w);
+          k::Epi ep = out_epi(w, 0, L_ > 1);
+          if (L_ > 1) ep.rmax = w.rm_slot(0);  // ahw[0] is the next NN's A
           gemm(k, "hw", 0, false, false, w.rows, ldl1, dl, w.ax, ldl, w.W[0], ldl1, w.ahw[0], ldl1, L_ > 1 ? 2 : 0,
-               out_epi(w, 0, L_ > 1));
+               ep, w.rm_slot(L_ + 1));
         }
         continue;
       }
+      // ahw[l-1]'s row maxima exist when its producer wrote them: a FAST SpMM (l - 1 > 0 or no aggregation)
+      // or the aggregated layer 0's NN GeMM
+      const bool rm_in = l > 0 && !(cfg_.order_swap && cfg_.dims[l - 1] < cfg_.dims[l]);
       for (size_t k = 0; k < nloc(); ++k) {
         Worker& w = W(k);
         dev(w);
         const float* h_in = l == 0 ? w.x : w.ahw[l - 1];
         if (!swap) {
-          gemm(k, "hw", l, false, false, w.rows, ldl1, dl, h_in, ldl, w.W[l], ldl1, w.hw, ldl1, 0);
+          gemm(k, "hw", l, false, false, w.rows, ldl1, dl, h_in, ldl, w.W[l], ldl1, w.hw, ldl1, 0, k::Epi{},
+               rm_in ? w.rm_slot(l - 1) : nullptr);
           src[k] = w.hw;
         } else {
           src[k] = const_cast<float*>(h_in);
         }
         out[k] = swap ? w.hw : w.ahw[l];
       }
-      staged_spmm(0, swap ? dl : dl1, src, out, !swap && l < L_ - 1, swap ? -1 : l);
+      staged_spmm(0, swap ? dl : dl1, src, out, !swap && l < L_ - 1, swap ? -1 : l, (!swap && l < L_ - 1) ? l : -1);
       if (swap) {
         for (size_t k = 0; k < nloc(); ++k) {
           Worker& w = W(k);
@@ -1345,7 +1372,7 @@ class Step {
           src[k] = W(k).ahw[l];
           out[k] = W(k).hw;
         }
-        staged_spmm(1, dl1, src, out, false);
+        staged_spmm(1, dl1, src, out, false, -1, L_);  // hw's row maxima: the H-grad NT's A
         grad_rows = out;
       } else {
         for (size_t k = 0; k < nloc(); ++k) grad_rows[k] = W(k).ahw[l];
@@ -1411,7 +1438,7 @@ class Step {
           Worker& w = W(k);
           dev(w);
           gemm(k, "hgrad", l, false, true, w.rows, ldl, dl1, grad_rows[k], ldl1, w.W[l], ldl1, w.ahw[l - 1], ldl, 1,
-               out_epi(w, l - 1, true));
+               out_epi(w, l - 1, true), skip ? nullptr : w.rm_slot(L_));
         }
       }
       (void)dl;
@@ -1620,6 +1647,8 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
       tc::set_gemm3_cluster(static_cast<int>(value));
     } else if (k == "gemm3_wring") {
       tc::set_w3_bytes(static_cast<int>(value));
+    } else if (k == "gemm_f16") {
+      tc::set_gemm_f16(static_cast<int>(value));
     } else if (k == "gemm_kernel") {
       tc::set_gemm_version(static_cast<int>(value));
     } else {
@@ -1777,6 +1806,8 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       w.bc1 = dalloc_t<float>(*g, w, std::max<index_t>(1, g->max_part * g->ld_max));
       w.bc2 = dalloc_t<float>(*g, w, std::max<index_t>(1, g->max_part * g->ld_max));
       if (cfg.aggregate_first()) w.ax = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));
+      if (cfg.gemm_mode == MG_GEMM_TF32X3 && cfg.spmm_mode == MG_SPMM_FAST)
+        w.rm = dalloc_t<float>(*g, w, static_cast<size_t>(L + 2) * 2 * std::max<index_t>(1, w.rows));
       // parameters, Adam state, W-grad staging (gcn.hpp:150-158), padded ld_l x ld_{l+1}
       for (int l = 0; l < L; ++l) {
         const index_t sz = g->pstride(l);
@@ -2298,14 +2329,21 @@ mg_status mg_dev_gemm(int32_t ta, int32_t tb, int64_t M, int64_t N, int64_t K, c
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     float* ws = nullptr;
     size_t wsb = 0;
+    float* rm = nullptr;  // NN / NT in TF32X3: A's per-row max pairs, as the training step's producers write them
     if (mode != MG_GEMM_EXACT) {
       wsb = ta ? tc::tn_workspace_bytes(M, N, std::max<int64_t>(K, 1)) : tc::nn_workspace_bytes(N, K);
       MG_CUDA(cudaMalloc(&ws, wsb));
+      if (!ta && mode == MG_GEMM_TF32X3 && M > 0) {
+        MG_CUDA(cudaMalloc(&rm, sizeof(float) * 2 * M));
+        row_absmax_pairs<<<static_cast<int>(std::min<int64_t>(4096, (M + 7) / 8)), 256, 0, st>>>(A, lda, M, K, rm);
+        MG_LAUNCHED();
+      }
     }
-    gemm_launch(mode, ta != 0, tb != 0, M, N, K, A, lda, B, ldb, Cm, ldc, epilogue, st, ws, wsb);
+    gemm_launch(mode, ta != 0, tb != 0, M, N, K, A, lda, B, ldb, Cm, ldc, epilogue, st, ws, wsb, k::Epi{}, rm);
     if (ws) {
       MG_CUDA(cudaStreamSynchronize(st));
       MG_CUDA(cudaFree(ws));
+      if (rm) MG_CUDA(cudaFree(rm));
     }
   });
 }

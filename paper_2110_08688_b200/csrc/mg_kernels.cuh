@@ -193,11 +193,17 @@ __global__ void __launch_bounds__(256) spmm_fast_items(const int4* __restrict__ 
         }
       }
     }
+    float m = 0.0f;
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       const int c = lane + k * G;
-      if (c < nchunk) *reinterpret_cast<float4*>(orow + 4 * c) = seg ? acc[k] : epi4(acc[k], relu, ep, it.z, 4 * c);
+      if (c < nchunk) {
+        const float4 y = seg ? acc[k] : epi4(acc[k], relu, ep, it.z, 4 * c);
+        *reinterpret_cast<float4*>(orow + 4 * c) = y;
+        m = absmax4(m, y);
+      }
     }
+    if (!seg && ep.rmax) rmax_group_store(m, gmask, lane, G, ep.rmax, it.z);
   }
 }
 
@@ -316,11 +322,17 @@ __global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ 
       }
     }
     cp_async_wait<0>();
+    float m = 0.0f;
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       const int c = lane + k * G;
-      if (c < nchunk) *reinterpret_cast<float4*>(orow + 4 * c) = seg ? acc[k] : epi4(acc[k], relu, ep, it.z, 4 * c);
+      if (c < nchunk) {
+        const float4 y = seg ? acc[k] : epi4(acc[k], relu, ep, it.z, 4 * c);
+        *reinterpret_cast<float4*>(orow + 4 * c) = y;
+        m = absmax4(m, y);
+      }
     }
+    if (!seg && ep.rmax) rmax_group_store(m, gmask, lane, G, ep.rmax, it.z);
   }
 }
 
@@ -382,11 +394,17 @@ __global__ void __launch_bounds__(128) spmm_fast_stream(const int4* __restrict__
     // closes row `cur` and opens the next one (accumulator from the prefetched old output)
     auto close_row = [&]() {
       float* o = orow(cur);
+      float m = 0.0f;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         const int c = lane + k * G;
-        if (c < nchunk) *reinterpret_cast<float4*>(o + 4 * c) = seg ? acc[k] : epi4(acc[k], relu, ep, pc.x + cur, 4 * c);
+        if (c < nchunk) {
+          const float4 y = seg ? acc[k] : epi4(acc[k], relu, ep, pc.x + cur, 4 * c);
+          *reinterpret_cast<float4*>(o + 4 * c) = y;
+          m = absmax4(m, y);
+        }
       }
+      if (!seg && ep.rmax) rmax_group_store(m, gmask, lane, G, ep.rmax, pc.x + cur);
       ++cur;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
@@ -522,6 +540,7 @@ __global__ void __launch_bounds__(256) spmm_fast_hubs(const int4* __restrict__ h
                                                       float* __restrict__ out, int ld, int accumulate, int relu, Epi ep) {
   const int4 hb = hubs[blockIdx.x];
   float* orow = out + (size_t)hb.x * ld;
+  float m = 0.0f;
   for (int c = threadIdx.x; c < ld / 4; c += blockDim.x) {
     float4 s = accumulate ? *reinterpret_cast<const float4*>(orow + 4 * c) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 8
@@ -532,7 +551,19 @@ __global__ void __launch_bounds__(256) spmm_fast_hubs(const int4* __restrict__ h
       s.z += p.z;
       s.w += p.w;
     }
-    *reinterpret_cast<float4*>(orow + 4 * c) = epi4(s, relu, ep, hb.x, 4 * c);
+    const float4 y = epi4(s, relu, ep, hb.x, 4 * c);
+    *reinterpret_cast<float4*>(orow + 4 * c) = y;
+    m = absmax4(m, y);
+  }
+  if (ep.rmax) {  // block max of the hub row
+    __shared__ float red[8];
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+      *reinterpret_cast<float2*>(ep.rmax + 2 * hb.x) = make_float2(m, 0.0f);
+    }
   }
 }
 

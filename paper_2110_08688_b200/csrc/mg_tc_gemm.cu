@@ -23,6 +23,7 @@
 // ring; tfull[b] (tcgen05.commit) / tempty[b] (epilogue) for the two TMEM accumulators.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -94,6 +95,10 @@ struct Params {
   int nwst;              // v3: W ring stages (nst = A ring stages)
   int epi_chunks;        // v3: 32 x 32 epilogue buffers per epilogue warp (2, or 4 with the relu_backward mask)
   k::Epi ep;             // fused bias / dropout (EPI 0, 2) and the dropout scale of the relu_backward mask (EPI 1)
+  // v3 F16 (scaled two-term fp16 split on kind::f16): per-row max |A| pairs from A's producer (Epi::rmax)
+  // and the per-column inverse scales of the pre-split W
+  const float* rmax_in;
+  const float* tinv;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -647,6 +652,50 @@ __device__ __forceinline__ void mma_tf32_ts_e(uint32_t tmem_d, uint32_t tmem_a, 
       "}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc));
 }
+// One 32-K stage of the scaled fp16 split (2 K = 16 steps x 3 terms, kind::f16) behind one elect: A hi / lo
+// from TMEM (16 fp16 pairs = 8 columns per K step), B hi / lo K-major SWIZZLE_64B (+32 B = +2 per K step).
+__device__ __forceinline__ void mma6_f16_ts_e(uint32_t d, uint32_t ah, uint32_t al, uint64_t bh, uint64_t bl,
+                                              uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p, e;\n"
+      ".reg .b32 ah1, al1;\n"
+      ".reg .b64 bh1, bl1;\n"
+      "elect.sync _|e, 0xffffffff;\n"
+      "setp.ne.b32 p, %6, 0;\n"
+      "add.u32 ah1, %1, 8;\nadd.u32 al1, %2, 8;\n"
+      "add.u64 bh1, %3, 2;\nadd.u64 bl1, %4, 2;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %3, %5, p;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %4, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %3, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al1], bh1, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah1], bl1, %5, 1;\n"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah1], bh1, %5, 1;\n"
+      "}\n" ::"r"(d),
+      "r"(ah), "r"(al), "l"(bh), "l"(bl), "r"(idesc), "r"(acc));
+}
+// kind::f16 instruction descriptor: D f32 (bit 4), A / B f16 (0 at bits 7, 10), both K-major, N >> 3, M >> 4.
+__host__ __device__ constexpr uint32_t idesc_f16(int m, int n) {
+  return (1u << 4) | (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
+// Power-of-two scale exponent for a block of values with max |x| = m: m * 2^e in [2^14, 2^15), so the fp16
+// hi part keeps 11 significant bits of every element within 2^13 of the max and the lo part (2^-11 of hi)
+// stays a normal fp16; clamped so the scale and its inverse are normal fp32 numbers.
+__device__ __forceinline__ int f16_scale_exp(float m) {
+  if (!(m > 0.0f)) return 0;
+  int e;
+  (void)frexpf(m, &e);  // m = f * 2^e, f in [0.5, 1): m in [2^(e-1), 2^e)
+  return max(-100, min(100, 15 - e));
+}
+__device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+// x (already scaled) -> fp16 hi / lo pair for two consecutive K elements (a = even k in the low half)
+__device__ __forceinline__ void split_f16x2(float a, float b, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(a, b);
+  const float2 hf = __half22float2(h);
+  hi = h2_bits(h);
+  lo = h2_bits(__floats2half2_rn(__fsub_rn(a, hf.x), __fsub_rn(b, hf.y)));
+}
+
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -673,6 +722,36 @@ __global__ void split_b(const float* __restrict__ W, long ldw, int trans, int np
     const float h = terms == 3 ? split_hi(x) : x;
     hi[i] = h;
     lo[i] = terms == 3 ? split_lo(x, h) : 0.0f;
+  }
+}
+
+// W -> per-column scaled fp16 hi / lo planes, K-major (np x kp, kp a multiple of 8) for the v3 F16 kernels:
+// column n (an output column) is scaled by 2^e_n from its max |W[., n]| (f16_scale_exp); tinv[n] = 2^-e_n
+// is applied by the epilogue. One block per column.
+__global__ void split_b16(const float* __restrict__ W, long ldw, int trans, int np, int kp, long nvalid, long kvalid,
+                          __half* __restrict__ hi, __half* __restrict__ lo, float* __restrict__ tinv) {
+  __shared__ float red[32];
+  const int n = blockIdx.x;
+  float m = 0.0f;
+  if (n < nvalid)
+    for (long k = threadIdx.x; k < kvalid; k += blockDim.x) m = fmaxf(m, fabsf(trans ? W[k * ldw + n] : W[n * ldw + k]));
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0f;
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) red[0] = m;
+  }
+  __syncthreads();
+  const int e = f16_scale_exp(red[0]);
+  const float sc = ldexpf(1.0f, e);
+  if (threadIdx.x == 0) tinv[n] = ldexpf(1.0f, -e);
+  for (long k = threadIdx.x; k < kp; k += blockDim.x) {
+    const float x = (n < nvalid && k < kvalid) ? __fmul_rn(trans ? W[k * ldw + n] : W[n * ldw + k], sc) : 0.0f;
+    const __half h = __float2half_rn(x);
+    hi[static_cast<long>(n) * kp + k] = h;
+    lo[static_cast<long>(n) * kp + k] = __float2half_rn(__fsub_rn(x, __half2float(h)));
   }
 }
 
@@ -1015,7 +1094,13 @@ __device__ __forceinline__ void mma_commit_mc_e(uint64_t* bar, uint32_t mask) {
       : "memory");
 }
 
-template <int MODE, int CL, bool EXT>
+constexpr int kRS3 = 4;  // F16: per-row scale buffers (split warps -> epilogue), one per item in flight
+
+// F16 = scaled two-term fp16 split on kind::f16 (K = 16 per MMA: half the MMAs of 3xTF32): the split warps
+// scale every A row by a power of two from its max |x| over the whole K range (read from global memory,
+// the next item's row during the current item's stages), W columns are pre-scaled by split_b16, and the
+// epilogue multiplies each output by both inverse scales (exact).
+template <int MODE, int CL, bool EXT, bool F16>
 __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__ CUtensorMap map_a,
                                                          const __grid_constant__ CUtensorMap map_bh,
                                                          const __grid_constant__ CUtensorMap map_bl,
@@ -1026,11 +1111,14 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t fullA[kMaxA3], emptyA[kMaxA3], fullW[kMaxW3], emptyW[kMaxW3], conv[kTSlots3], tslot[kTSlots3];
   __shared__ uint64_t tfull[2], tempty[2], oldbar[4];
+  __shared__ uint64_t rsready[F16 ? kRS3 : 1], rsfree[F16 ? kRS3 : 1];
+  __shared__ float rsinv[F16 ? kRS3 : 1][F16 ? BM : 1];
   __shared__ uint32_t tmem_base_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nA = p.nst, nW = p.nwst;
   constexpr int a_bytes = BM * BK3 * 4;  // raw A tile [128 rows][32 k], SWIZZLE_128B
-  const int b_bytes = p.bnr * BK3 * 4;   // one W tile (hi or lo), K-major [bnr][32 k], SWIZZLE_128B
+  // one W tile (hi or lo), K-major [bnr][32 k]: fp32 SWIZZLE_128B, or fp16 SWIZZLE_64B under F16
+  const int b_bytes = p.bnr * BK3 * (F16 ? 2 : 4);
   uint8_t* aring = smem;                 // nA x a_bytes
   uint8_t* wring = smem + nA * a_bytes;  // nW x (hi | lo)
   float* epib = reinterpret_cast<float*>(wring + nW * 2 * b_bytes);
@@ -1053,6 +1141,16 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
       mbar_init(&tempty[b], 4);
     }
     for (int q = 0; q < 4; ++q) mbar_init(&oldbar[q], 1);
+    if (F16)
+      for (int b = 0; b < kRS3; ++b) {
+        mbar_init(&rsready[b], 4);
+        mbar_init(&rsfree[b], 4);
+      }
+    if (F16)
+      for (int b = 0; b < kRS3; ++b) {
+        mbar_init(&rsready[b], 4);
+        mbar_init(&rsfree[b], 4);
+      }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0 && lane == 0) {
@@ -1133,7 +1231,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
     RingPos rw(nW);
     for (int pi = pair0; pi < npi; pi += npairs, ++ac) {
       const Item2 I = item_of3(pi);
-      const uint32_t idesc = idesc_tf32(BM, I.nw, 0, 0);
+      const uint32_t idesc = F16 ? idesc_f16(BM, I.nw) : idesc_tf32(BM, I.nw, 0, 0);
       const int buf = static_cast<int>(ac & 1);
       if (ac >= 2u) mbar_wait(&tempty[buf], ((ac >> 1) - 1) & 1);
       tc_fence_after();
@@ -1148,7 +1246,9 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
           const uint32_t bh = smem_u32(wring + w * 2 * b_bytes), bl = bh + b_bytes;
           const uint32_t ah = tmem + static_cast<uint32_t>(kAcol + j * 64), al = ah + 32;
           static_assert(BK3 == 32, "mma12_tf32_ts_e issues one 32-K stage");
-          if (p.terms == 3) {
+          if (F16) {
+            mma6_f16_ts_e(d, ah, ah + 16, desc_k64(bh), desc_k64(bl), idesc, kb == 0 ? 0u : 1u);
+          } else if (p.terms == 3) {
             mma12_tf32_ts_e(d, ah, al, desc_k128(bh), desc_k128(bl), idesc, kb == 0 ? 0u : 1u);
           } else {
 #pragma unroll
@@ -1168,9 +1268,28 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
     // ------------------------------------------------------------ split: raw A (smem) -> hi / lo (TMEM slot)
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    uint32_t sc = 0;
+    uint32_t sc = 0, ic = 0;
     RingPos ra(nA);
-    for (int pi = pair0; pi < npi; pi += npairs) {
+    // F16: max |A| of this thread's row, written by A's producer (SpMM / GeMM epilogue, Epi::rmax: two
+    // slots per row); the next item's pair is loaded one item ahead
+    auto row_max = [&](int pi) -> float2 {
+      const long grow = item_of3(pi).k.row0 + row;
+      return grow < p.M ? __ldg(reinterpret_cast<const float2*>(p.rmax_in) + grow) : make_float2(0.0f, 0.0f);
+    };
+    float2 rm_next = make_float2(0.0f, 0.0f);
+    if (F16 && pair0 < npi) rm_next = row_max(pair0);
+    for (int pi = pair0; pi < npi; pi += npairs, ++ic) {
+      float rscale = 1.0f;
+      if (F16) {
+        const int e = f16_scale_exp(fmaxf(rm_next.x, rm_next.y));
+        if (pi + npairs < npi) rm_next = row_max(pi + npairs);
+        rscale = ldexpf(1.0f, e);
+        const int b = static_cast<int>(ic % kRS3);
+        if (ic >= static_cast<uint32_t>(kRS3)) mbar_wait(&rsfree[b], ((ic / kRS3) - 1) & 1);
+        rsinv[b][row] = ldexpf(1.0f, -e);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rsready[b]);
+      }
       for (int kb = 0; kb < nkb; ++kb, ++sc, ra.next()) {
         const int s = ra.idx, j = sc % kTSlots3;
         mbar_wait(&fullA[s], ra.phase);
@@ -1186,20 +1305,31 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
         __syncwarp();
         if (lane == 0) mbar_arrive(&emptyA[s]);  // the raw tile is in registers: the producer may refill
         uint32_t hi[BK3], lo[BK3];
+        if (F16) {  // 16 fp16 pairs of hi, then 16 of lo: TMEM columns [0, 16) and [16, 32) of the slot
 #pragma unroll
-        for (int k = 0; k < BK3; ++k) {
-          const float h = p.terms == 3 ? split_hi(x[k]) : x[k];
-          hi[k] = __float_as_uint(h);
-          lo[k] = __float_as_uint(p.terms == 3 ? split_lo(x[k], h) : 0.0f);
+          for (int k = 0; k < BK3 / 2; ++k)
+            split_f16x2(__fmul_rn(x[2 * k], rscale), __fmul_rn(x[2 * k + 1], rscale), hi[k], lo[k]);
+        } else {
+#pragma unroll
+          for (int k = 0; k < BK3; ++k) {
+            const float h = p.terms == 3 ? split_hi(x[k]) : x[k];
+            hi[k] = __float_as_uint(h);
+            lo[k] = __float_as_uint(p.terms == 3 ? split_lo(x[k], h) : 0.0f);
+          }
         }
         if (sc >= static_cast<uint32_t>(kTSlots3)) mbar_wait(&tslot[j], ((sc / kTSlots3) - 1) & 1);
         tc_fence_after();
         const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(kAcol + j * 64);
-        tmem_st16(ta, hi);
-        tmem_st16(ta + 16, hi + 16);
-        if (p.terms == 3) {
-          tmem_st16(ta + 32, lo);
-          tmem_st16(ta + 48, lo + 16);
+        if (F16) {
+          tmem_st16(ta, hi);
+          tmem_st16(ta + 16, lo);
+        } else {
+          tmem_st16(ta, hi);
+          tmem_st16(ta + 16, hi + 16);
+          if (p.terms == 3) {
+            tmem_st16(ta + 32, lo);
+            tmem_st16(ta + 48, lo + 16);
+          }
         }
         asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
         tc_fence_before();
@@ -1216,6 +1346,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
     const int q = warp & 3;
     const int ech = p.epi_chunks;
     uint32_t ac = 0, mph = 0;
+    float rinv = 1.0f, omax = 0.0f;
     float* bufs = epib + q * (ech * 1024);
     for (int pi = pair0; pi < npi; pi += npairs, ++ac) {
       const Item2 I = item_of3(pi);
@@ -1237,6 +1368,13 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
           tc_fence_after();
           if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && ac < kTraceItems)
             p.trace[kTraceStages * 4 + ac * 2 + 0] = clock64();
+          if (F16) {
+            const int rb = static_cast<int>(ac % kRS3);
+            mbar_wait(&rsready[rb], (ac / kRS3) & 1);
+            rinv = rsinv[rb][q * 32 + lane];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&rsfree[rb]);
+          }
         }
         if (p.epi == 1) mbar_wait(&oldbar[q], (mph++) & 1);
         for (int c = 0; c < cn; ++c) {
@@ -1246,15 +1384,27 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
             float4 o = make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
+            if (F16) {  // both inverse scales are powers of two: exact
+              const float4 t = __ldg(reinterpret_cast<const float4*>(p.tinv + I.n0 + (c0 + c) * 32 + 4 * jj));
+              o = make_float4(__fmul_rn(__fmul_rn(o.x, rinv), t.x), __fmul_rn(__fmul_rn(o.y, rinv), t.y),
+                              __fmul_rn(__fmul_rn(o.z, rinv), t.z), __fmul_rn(__fmul_rn(o.w, rinv), t.w));
+            }
             float4* dst = sw128(b, lane, jj);
             o = gemm_epi<EXT>(o, p.epi == 1 ? *dst : o, p, grow0 + lane, I.n0 + (c0 + c) * 32 + 4 * jj);
             *dst = o;
+            omax = k::absmax4(omax, o);
           }
         }
         if (c0 + ech >= nch) {  // the whole accumulator has been read: the MMA may reuse it
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[buf]);
+          if (p.ep.rmax && grow0 + lane < p.M) {  // this tile's row max for the next GeMM's F16 split
+            float* r = p.ep.rmax + 2 * (grow0 + lane);
+            if (p.n_tiles == 1) *reinterpret_cast<float2*>(r) = make_float2(omax, 0.0f);
+            else r[I.n0 / kTileN] = omax;
+          }
+          omax = 0.0f;
           if (p.trace && blockIdx.x == 0 && q == 0 && lane == 0 && ac < kTraceItems)
             p.trace[kTraceStages * 4 + ac * 2 + 1] = clock64();
         }
@@ -1306,15 +1456,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D fp32 map over a row-major matrix [outer][inner] with row pitch ld floats.
-CUtensorMap make_map(const float* base, long inner, long outer, long ld, int box_inner, int box_outer,
-                     CUtensorMapSwizzle sw) {
+CUtensorMap make_map(const void* base, long inner, long outer, long ld, int box_inner, int box_outer,
+                     CUtensorMapSwizzle sw, bool f16 = false) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(std::max<long>(inner, 1)),
                               static_cast<cuuint64_t>(std::max<long>(outer, 1))};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 4};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * (f16 ? 2 : 4)};
   const cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
   const cuuint32_t es[2] = {1, 1};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+  const CUresult r = encode_fn()(&m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                 const_cast<void*>(base), dims, strides, box,
                                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
@@ -1390,29 +1541,32 @@ inline int smem_bytes2(const Params& p, int bk) { return p.nst * (BM * bk * 4 + 
 // v3 (NN / NT): A ring as deep as the shared memory left after the W ring and the epilogue buffers.
 constexpr int kSmemMax3 = 232448 - 2048;  // sm_100 per-block maximum, minus static barriers and alignment
 int g_w3_bytes = 96 * 1024;  // v3 W ring budget ("gemm3_wring", bytes): 3 stages of a 128-column tile
-void finish_params3(Params& p) {
-  const int wst = 2 * p.bnr * BK3 * 4, ast = BM * BK3 * 4;
+void finish_params3(Params& p, bool f16) {
+  const int wst = 2 * p.bnr * BK3 * (f16 ? 2 : 4), ast = BM * BK3 * 4;
   p.epi_chunks = p.epi == 1 ? 4 : 2;
   const int wbytes = p.epi == 1 ? std::min(g_w3_bytes, 64 * 1024) : g_w3_bytes;
   p.nwst = std::max(2, std::min(kMaxW3, wbytes / wst));
-  p.nst = std::max(2, std::min(kMaxA3, (kSmemMax3 - 1024 - 4 * p.epi_chunks * 4096 - p.nwst * wst) / ast));
+  const int avail = kSmemMax3 - (f16 ? 4096 : 0);  // F16: the per-row scale buffers are static shared memory
+  p.nst = std::max(2, std::min(kMaxA3, (avail - 1024 - 4 * p.epi_chunks * 4096 - p.nwst * wst) / ast));
 }
-inline int smem_bytes3(const Params& p) {
-  return p.nst * BM * BK3 * 4 + p.nwst * 2 * p.bnr * BK3 * 4 + 4 * p.epi_chunks * 4096 + 1024;
+inline int smem_bytes3(const Params& p, bool f16) {
+  return p.nst * BM * BK3 * 4 + p.nwst * 2 * p.bnr * BK3 * (f16 ? 2 : 4) + 4 * p.epi_chunks * 4096 + 1024;
 }
 int g_gemm3_cluster = 1;  // v3 cluster size for the W multicast ("gemm3_cluster": 1 or 2)
-template <int MODE, int CL, bool EXT>
+int g_gemm_f16 = 1;       // v3 NN / NT in TF32X3 mode: scaled fp16 two-term split on kind::f16 ("gemm_f16")
+template <int MODE, int CL, bool EXT, bool F16 = false>
 void launch3x(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
               cudaStream_t s) {
   static std::atomic<unsigned long long> attr{0};
   if (first_on_device(attr, cur_dev()))
-    TC_CUDA(cudaFuncSetAttribute(gemm_tc3<MODE, CL, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemMax3));
+    TC_CUDA(cudaFuncSetAttribute(gemm_tc3<MODE, CL, EXT, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 kSmemMax3 - (F16 ? 4096 : 0)));
   const int npi = ((p.m_tiles + CL - 1) / CL) * p.n_tiles;
   const int grid = CL * std::max(1, std::min(npi, num_sms() / CL));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads3);
-  cfg.dynamicSmemBytes = static_cast<size_t>(smem_bytes3(p));
+  cfg.dynamicSmemBytes = static_cast<size_t>(smem_bytes3(p, F16));
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1421,7 +1575,7 @@ void launch3x(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  TC_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc3<MODE, CL, EXT>, a, bh, bl, c, p));
+  TC_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc3<MODE, CL, EXT, F16>, a, bh, bl, c, p));
 }
 // bias / dropout epilogue (Params::ep) only in the EXT instantiation
 inline bool epi_ext(const Params& p) { return p.ep.bias != nullptr || p.ep.thr != 0; }
@@ -1430,6 +1584,12 @@ void launch3(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl,
              cudaStream_t s) {
   if (epi_ext(p)) launch3x<MODE, CL, true>(a, bh, bl, c, p, s);
   else launch3x<MODE, CL, false>(a, bh, bl, c, p, s);
+}
+template <int MODE>
+void launch3f16(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c,
+                const Params& p, cudaStream_t s) {
+  if (epi_ext(p)) launch3x<MODE, 1, true, true>(a, bh, bl, c, p, s);
+  else launch3x<MODE, 1, false, true>(a, bh, bl, c, p, s);
 }
 
 template <int MODE, bool EXT>
@@ -1453,8 +1613,13 @@ void launch2(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl,
 }  // namespace
 
 size_t nn_workspace_bytes(int64_t N, int64_t K) {
-  return 2 * sizeof(float) * static_cast<size_t>((N + 15) / 16 * 16) * static_cast<size_t>((K + 3) / 4 * 4);
+  const size_t np = static_cast<size_t>((N + 15) / 16 * 16);
+  const size_t f32 = 2 * sizeof(float) * np * static_cast<size_t>((K + 3) / 4 * 4);
+  const size_t f16 = 2 * sizeof(__half) * np * static_cast<size_t>((K + 7) / 8 * 8) + sizeof(float) * np + 256;
+  return std::max(f32, f16);
 }
+
+void set_gemm_f16(int on) { g_gemm_f16 = on != 0 ? 1 : 0; }
 
 void set_gemm3_cluster(int c) {
   if (c != 1 && c != 2) throw ValueError("tuning: gemm3_cluster must be 1 or 2");
@@ -1514,7 +1679,8 @@ void print_trace(const Params& p, const char* what) {
 }
 
 int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
-         int64_t ldb, float* C, int64_t ldc, int epi, float* ws, size_t ws_bytes, cudaStream_t s, const k::Epi& ep) {
+         int64_t ldb, float* C, int64_t ldc, int epi, float* ws, size_t ws_bytes, cudaStream_t s, const k::Epi& ep,
+         const float* rmax_in) {
   if (ta) {
     const int64_t begin[1] = {0}, len[1] = {K};
     return gemm_tn_blocks(mode, 1, begin, len, M, N, A, lda, B, ldb, C, ldc, 0, ws, ws_bytes, s);
@@ -1540,6 +1706,28 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
     p.n_items = p.m_tiles * p.n_tiles;
     const int kp = static_cast<int>((K + 3) / 4 * 4);
     if (!ws || ws_bytes < nn_workspace_bytes(N, K)) throw ValueError("tc gemm: B split workspace too small");
+    if (g_gemm_version == 3 && g_gemm_f16 && p.terms == 3 && g_gemm3_cluster == 1 && rmax_in) {
+      // scaled fp16 two-term split (kind::f16): W -> per-column scaled fp16 hi / lo planes + inverse scales
+      const int kp16 = static_cast<int>((K + 7) / 8 * 8);
+      __half* h16 = reinterpret_cast<__half*>(ws);
+      __half* l16 = h16 + static_cast<size_t>(p.np) * kp16;
+      float* tinv = reinterpret_cast<float*>(
+          (reinterpret_cast<uintptr_t>(l16 + static_cast<size_t>(p.np) * kp16) + 255) & ~uintptr_t(255));
+      split_b16<<<p.np, 128, 0, s>>>(B, ldb, tb ? 0 : 1, p.np, kp16, N, K, h16, l16, tinv);
+      TC_CUDA(cudaGetLastError());
+      p.rmax_in = rmax_in;
+      p.tinv = tinv;
+      p.trace = trace_buffer();
+      finish_params3(p, true);
+      const CUtensorMap mc = make_map(C, N, M, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
+      const CUtensorMap ma3 = make_map(A, K, M, lda, BK3, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+      const CUtensorMap mbh = make_map(h16, kp16, p.np, kp16, BK3, p.bnr, CU_TENSOR_MAP_SWIZZLE_64B, true);
+      const CUtensorMap mbl = make_map(l16, kp16, p.np, kp16, BK3, p.bnr, CU_TENSOR_MAP_SWIZZLE_64B, true);
+      if (!tb) launch3f16<NN>(ma3, mbh, mbl, mc, p, s);
+      else launch3f16<NT>(ma3, mbh, mbl, mc, p, s);
+      print_trace(p, tb ? "NT f16" : "NN f16");
+      return 2;
+    }
     float* bh = ws;
     float* bl = ws + static_cast<size_t>(p.np) * kp;
     const long tot = static_cast<long>(p.np) * kp;
@@ -1552,7 +1740,7 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
     const CUtensorMap mc = make_map(C, N, M, ldc, 32, 32, CU_TENSOR_MAP_SWIZZLE_128B);
     p.trace = trace_buffer();
     if (g_gemm_version == 3) {  // 32-K stages, SWIZZLE_128B boxes
-      finish_params3(p);
+      finish_params3(p, false);
       const CUtensorMap ma3 = make_map(A, K, M, lda, BK3, BM, CU_TENSOR_MAP_SWIZZLE_128B);
       const int CL = g_gemm3_cluster;
       const CUtensorMap mbh3 = make_map(bh, kp, p.np, kp, BK3, p.bnr / CL, CU_TENSOR_MAP_SWIZZLE_128B);

@@ -14,7 +14,9 @@ bool available();
 // TN (ta) needs a split-K workspace of tn_workspace_bytes(M, N, K) (one per concurrent stream).
 int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
          int64_t ldb, float* C, int64_t ldc, int epi, float* ws, size_t ws_bytes, cudaStream_t s,
-         const k::Epi& ep = k::Epi{});
+         const k::Epi& ep = k::Epi{}, const float* rmax_in = nullptr);
+// rmax_in: per-row max |A| pairs (k::Epi::rmax of A's producer); with it, TF32X3 NN / NT run the scaled fp16
+// two-term split (v3, "gemm_f16"), without it the 3xTF32 split. ep.rmax: write this GeMM's own row maxima.
 size_t tn_workspace_bytes(int64_t M, int64_t N, int64_t K);
 // W-grad over up to 8 canonical row blocks in one launch: stage + g*block_stride (M x N, ld ldc) =
 // H[begin_g : begin_g + len_g]^T G[same rows]; empty blocks are written as zeros. Deterministic and
@@ -27,6 +29,8 @@ size_t nn_workspace_bytes(int64_t N, int64_t K);
 void set_tn_chunk(int rows);
 void set_gemm_version(int v);
 void set_w3_bytes(int bytes);  // v3 W ring budget
-void set_gemm3_cluster(int c);  // v3 W multicast cluster (1 or 2)  // 1 = both operands in smem (SS), 2 = A split into TMEM (TS, default)  // TN split-K chunk length (rows, multiple of 32); set before creating groups
+void set_gemm3_cluster(int c);
+void set_gemm_f16(int on);  // v3 NN / NT: scaled fp16 two-term split (1, default) or 3xTF32 (0)
+  // v3 W multicast cluster (1 or 2)  // 1 = both operands in smem (SS), 2 = A split into TMEM (TS, default)  // TN split-K chunk length (rows, multiple of 32); set before creating groups
 }  // namespace tc
 }  // namespace mg

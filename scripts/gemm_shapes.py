@@ -12,6 +12,9 @@ import torch  # noqa: E402  (before libmggcn: torch brings its own NCCL)
 
 from paper_2110_08688_b200 import rowgcn as R  # noqa: E402
 
+for kv in filter(None, os.environ.get("MG_TUNE", "").split(",")):  # e.g. MG_TUNE=gemm_f16=0
+    R.set_tuning(kv.split("=")[0], int(kv.split("=")[1]))
+
 M = 2449029
 # name: (ta, tb, out rows, out cols, K, epilogue)
 SHAPES = {

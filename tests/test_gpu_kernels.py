@@ -135,8 +135,9 @@ TC_SHAPES = [(1000, 256, 100), (777, 256, 256), (130, 48, 256), (300, 256, 47), 
 @pytest.mark.parametrize("shape", TC_SHAPES)
 @pytest.mark.parametrize("ta,tb", [(False, False), (False, True), (True, False)])
 # 1: both operands split in smem (SS); 2: A split into TMEM (TS); 3 (default): 2 with 32-K SWIZZLE_128B stages
-# and decoupled A / W rings for NN / NT (TN runs the v2 kernel under 3)
-@pytest.mark.parametrize("kernel", [1, 2, 3])
+# and decoupled A / W rings for NN / NT (TN runs the v2 kernel under 3), NN / NT on the scaled fp16 two-term
+# split (kind::f16, per-row A / per-column W power-of-two scales); 30: 3 with the 3xTF32 split for NN / NT
+@pytest.mark.parametrize("kernel", [1, 2, 3, 30])
 def test_gemm_tcgen05(gemm_kernel, shape, ta, tb, mode, tol):
     from gpu_util import normwise
     m, n, k = shape
@@ -159,12 +160,37 @@ def test_gemm_tcgen05(gemm_kernel, shape, ta, tb, mode, tol):
 
 @pytest.fixture
 def gemm_kernel(kernel):
-    R.set_tuning("gemm_kernel", kernel)
+    R.set_tuning("gemm_kernel", 3 if kernel == 30 else kernel)
+    R.set_tuning("gemm_f16", 0 if kernel == 30 else 1)
     yield kernel
     R.set_tuning("gemm_kernel", 3)
+    R.set_tuning("gemm_f16", 1)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3])
+# Scaled fp16 split (kernel 3, NN / NT): rows and columns of very different magnitudes, tiny (gradient-like)
+# and huge values, zero rows, K tails that are not multiples of 4 or 32 — per-row / per-column scales keep
+# every row at the 3xTF32 accuracy relative to its own magnitude.
+@pytest.mark.parametrize("tb", [False, True])
+@pytest.mark.parametrize("shape", [(700, 256, 256), (300, 47, 101), (129, 256, 37), (64, 16, 3), (513, 100, 602)])
+def test_gemm_f16_row_scales(shape, tb):
+    m, n, k = shape
+    rng = np.random.default_rng(m + n + k + tb)
+    a = rng.uniform(-1, 1, (m, k)) * 10.0 ** rng.integers(-15, 15, (m, 1))
+    a[::7] = 0.0
+    b = rng.uniform(-1, 1, (n, k) if tb else (k, n))
+    a, b = a.astype(np.float32), b.astype(np.float32)
+    if tb:
+        b *= (10.0 ** rng.integers(-10, 10, (n, 1))).astype(np.float32)
+    else:
+        b *= (10.0 ** rng.integers(-10, 10, (1, n))).astype(np.float32)
+    ref = a.astype(np.float64) @ (b.astype(np.float64).T if tb else b.astype(np.float64))
+    got = run_gemm(a, b, False, tb, mode=R.GEMM_TF32X3)
+    scale = np.abs(a).max(1, keepdims=True).astype(np.float64) * np.abs(b).max(1 if tb else 0)[None, :].astype(np.float64)
+    err = np.abs(got - ref) / np.maximum(scale * k, 1e-300)
+    assert np.all(np.isfinite(got)) and err.max() <= 1e-6, err.max()
+
+
+@pytest.mark.parametrize("kernel", [1, 2, 3, 30])
 def test_gemm_tcgen05_deterministic(gemm_kernel):
     rng = np.random.default_rng(5)
     a = rng.normal(size=(20000, 256)).astype(np.float32)
