@@ -50,7 +50,8 @@ typedef struct mg_csr {
 /* Arithmetic modes of the device kernels (reported next to every number). */
 typedef enum mg_gemm_mode {
   MG_GEMM_EXACT = 0,  /* SIMT, k-ascending separate mul/add: bitwise equal to rowgcn::gemm (f32) */
-  MG_GEMM_TF32X3 = 1, /* tcgen05 kind::tf32, 3-term split (hi*hi + hi*lo + lo*hi): fp32-level accuracy */
+  MG_GEMM_TF32X3 = 1, /* tcgen05, 3-term split (hi*hi + hi*lo + lo*hi): fp32-level accuracy. kind::tf32 for the
+                       * W-grad; NN / NT fed by FAST SpMM: per-row / per-column scaled fp16 pairs on kind::f16 */
   MG_GEMM_TF32 = 2    /* tcgen05 kind::tf32, single term (reported separately, rel ~1e-3) */
 } mg_gemm_mode;
 
@@ -105,6 +106,12 @@ int32_t mg_abi_version(void);
  *   "gemm_kernel"  tcgen05 GeMM variant: 1 = both split operands in smem, 2 = A split into TMEM,
  *                  3 = 2 with 32-K stages and decoupled A / W rings for NN / NT (default)
  *   "gemm3_wring"  v3 W-ring budget in bytes (default 96 KiB), "gemm3_cluster" 1 or 2 (W multicast)
+ *   "gemm_f16"     1 (default): TF32X3 NN / NT whose A has producer-written row maxima (FAST SpMM) run the
+ *                  scaled fp16 two-term split on kind::f16; 0: the 3xTF32 split everywhere
+ *   "stage_fold"   1: MG_SPMM_FAST with P > 2 folds pairs of received stages into one SpMM launch over a
+ *                  merged tile (half the output read-modify-write passes); 0 (default): stage by stage
+ *   "spmm_stream" 0 / 1 / 2 (auto, default): the row-streaming FAST SpMM for short-row tiles
+ *   "adaptive_cuts" 1 (default): FAST hub-row cut points scaled to the tile; "piece_nnz" stream piece size
  *   "bwd_transpose"  one worker: build the backward tile on the device from the forward one (default 1)
  *   "block_cache"  1 (default): device blocks of destroyed groups are kept for reuse; 0: released (cold runs)
  *   "watchdog_ms"  host-wait timeout after which a group is aborted with MG_SHUTDOWN_ERROR (default 0 = none)
@@ -309,7 +316,9 @@ typedef enum mg_tensor {
   MG_T_ADAM_V = 6,
   MG_T_WSTAGE = 7, /* 8 d_l x d_{l+1}   the canonical-block W-grad staging buffer */
   MG_T_BIAS = 8,   /* 1 x d_{l+1}        bias row of layer l (cfg.bias) */
-  MG_T_BIAS_GRAD = 9 /* 1 x d_{l+1}      its gradient (like MG_T_WGRAD) */
+  MG_T_BIAS_GRAD = 9, /* 1 x d_{l+1}      its gradient (like MG_T_WGRAD) */
+  MG_T_ROWMAX = 10 /* local_rows x 2    row-max pairs of the f16 GeMM split, slot `layer` (l < L: ahw[l],
+                    * L: hw, L + 1: Â·X); TF32X3 + FAST groups only (diagnostics, read-only use) */
 } mg_tensor;
 
 /* Copies a tensor of local worker `rank` to/from host memory in the reference's dense layout

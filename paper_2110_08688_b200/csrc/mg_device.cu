@@ -101,6 +101,12 @@ struct DevTile {
 };
 
 std::atomic<int> g_fast_segment{2048};
+// "stage_fold" (MG_SPMM_FAST, P > 1): consecutive received stages (j, j + 1) are folded into one SpMM launch
+// over a merged tile (tile j's columns, then tile j + 1's shifted by the size of block j) reading both
+// blocks from one double-size receive buffer: the output is read-modified-written once per pair instead of
+// once per stage. A pair never contains the rank's own block (that stage reads its h in place). Off by
+// default (the reference's stage-by-stage schedule and timeline); read at group creation.
+std::atomic<int> g_stage_fold{0};
 std::atomic<int> g_adaptive_cuts{1};  // "adaptive_cuts": FAST hub threshold / segment scaled to the tile
 
 // MG_SPMM_FAST cut points of one tile: rows with >= ht nonzeros are hub rows cut into segments of seg
@@ -553,6 +559,7 @@ static int spmm_fast(const FastLaunch& t, const float* h, float* out, index_t ld
       const int L = static_cast<int>(ld);
       k::Epi ep = ep0;
       if (ep.bias) ep.bias += 4 * c0;
+      ep.rmax_acc = c0 > 0;  // column slabs: each pass folds its columns into the row maxima
       ep.key += static_cast<unsigned long long>(4 * c0) * 0x9E3779B97F4A7C15ull;  // column offset of the slab
       if (launch_fast_pipelined(t, hs, os, ss, L, nchunk, acc, relu, ep, s)) {
       } else if (nchunk <= 1) launch_fast<1, 1>(t, hs, os, ss, L, nchunk, acc, relu, ep, s);
@@ -636,6 +643,10 @@ struct Worker {
   index_t r0 = 0, rows = 0;
   cudaStream_t s0 = nullptr, s1 = nullptr, s2 = nullptr;  // compute (lane 0), comm (lane 1), heavy-row side
   std::vector<DevTile> tiles[2];
+  // stage folding: SpMM steps as [first, last] stage pairs (last == first: one stage), the step of every
+  // stage, and the merged tiles of the folded pairs (ftiles[dir][first])
+  std::vector<int> step_first, step_last, step_of;
+  std::vector<DevTile> ftiles[2];
   float* x = nullptr;
   int* labels = nullptr;
   uint8_t* mask = nullptr;
@@ -681,6 +692,7 @@ struct mg_group {
   mg::index_t wblocks[9] = {};  // canonical W-grad blocks uniform_partition(n, 8), driver.hpp:156
   std::vector<mg::index_t> ld;  // padded widths per dim
   mg::index_t ld_max = 4, max_part = 0;
+  bool fold = false;  // stage folding (g_stage_fold, FAST mode, P > 1)
   // floats per layer parameter array: W (ld_l x ld_{l+1}) plus, with cfg.bias, the bias row after it; the
   // same layout for W_G, Adam m / v and each canonical staging block, so the W-grad all-reduce, the block
   // sum and Adam cover the bias with no extra launches
@@ -974,6 +986,34 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d, const DevTil
   if (!heavy.empty()) MG_CUDA(cudaMemcpy(d.heavy, heavy.data(), sizeof(int) * heavy.size(), cudaMemcpyHostToDevice));
 }
 
+// Stage folding: tiles j and j + 1 of one row block side by side (row r = tile j's row r, then tile j + 1's
+// with its columns shifted by block j's size): a CSR over the two blocks stacked in one receive buffer.
+Tile merge_tiles(const Tile& a, const Tile& b) {
+  Tile m;
+  m.rows = a.rows;
+  m.cols = a.cols + b.cols;
+  m.row_ptr.assign(a.rows + 1, 0);
+  for (index_t r = 0; r < a.rows; ++r)
+    m.row_ptr[r + 1] = m.row_ptr[r] + (a.row_ptr[r + 1] - a.row_ptr[r]) + (b.row_ptr[r + 1] - b.row_ptr[r]);
+  m.col.resize(m.row_ptr[a.rows]);
+  m.val.resize(m.row_ptr[a.rows]);
+  const std::int32_t shift = static_cast<std::int32_t>(a.cols);
+  parallel_for(a.rows, [&](index_t s, index_t e) {
+    for (index_t r = s; r < e; ++r) {
+      index_t o = m.row_ptr[r];
+      for (index_t k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k, ++o) {
+        m.col[o] = a.col[k];
+        m.val[o] = a.val[k];
+      }
+      for (index_t k = b.row_ptr[r]; k < b.row_ptr[r + 1]; ++k, ++o) {
+        m.col[o] = b.col[k] + shift;
+        m.val[o] = b.val[k];
+      }
+    }
+  }, 4096);
+  return m;
+}
+
 // Copies rows x cols (host, dense) into a device buffer with leading dimension ld (padding = 0).
 void upload_padded(float* dst, const float* src, index_t rows, index_t cols, index_t ld) {
   if (cols == ld && rows * cols > 0 && is_pinned_host(src)) {
@@ -1167,12 +1207,18 @@ class Step {
       for (size_t k = 0; k < nloc(); ++k) {
         Worker& w = W(k);
         dev(w);
-        cudaEvent_t dep = ov ? (j >= 2 ? w.mult[j - 2] : w.prior) : (j >= 1 ? w.mult[j - 1] : w.prior);
+        // the step that consumes stage j and the buffer it reads (steps alternate BC1 / BC2 under overlap);
+        // without folding a step is a stage (inc/dist_spmm.hpp:75-88)
+        const int sj = w.step_of.empty() ? j : w.step_of[j];
+        const int first = w.step_of.empty() ? j : w.step_first[sj];
+        cudaEvent_t dep = ov ? (sj >= 2 ? w.mult[sj - 2] : w.prior) : (sj >= 1 ? w.mult[sj - 1] : w.prior);
         MG_CUDA(cudaStreamWaitEvent(w.s1, dep, 0));
-        const uint64_t dep_task = ov ? (j >= 2 ? mult_task[k][j - 2] : prior_task[k])
-                                     : (j >= 1 ? mult_task[k][j - 1] : prior_task[k]);
+        const uint64_t dep_task = ov ? (sj >= 2 ? mult_task[k][sj - 2] : prior_task[k])
+                                     : (sj >= 1 ? mult_task[k][sj - 1] : prior_task[k]);
         tb[k] = tl_begin(k, 1, "broadcast", "h_stage", j, {dep_task});
-        recv[k] = (w.rank == j) ? src[k] : ((!ov || j % 2 == 0) ? w.bc1 : w.bc2);
+        float* buf = (!ov || sj % 2 == 0) ? w.bc1 : w.bc2;
+        if (j != first) buf += (g_.bounds[first + 1] - g_.bounds[first]) * ld;  // second block of a folded pair
+        recv[k] = (w.rank == j) ? src[k] : buf;
       }
       const size_t count = static_cast<size_t>((g_.bounds[j + 1] - g_.bounds[j]) * ld);
       bcast(j, count, recv);
@@ -1182,10 +1228,15 @@ class Step {
         const uint64_t bc_task = tl_end(k, tb[k]);
         MG_CUDA(cudaEventRecord(w.bc_done[j], w.s1));
         MG_CUDA(cudaStreamWaitEvent(w.s0, w.bc_done[j], 0));
-        const int ts = tl_begin(k, 0, "spmm", "stage", j, {bc_task});
-        const DevTile& t = w.tiles[dir][j];
+        const int sj = w.step_of.empty() ? j : w.step_of[j];
+        if (!w.step_of.empty() && w.step_last[sj] != j) continue;  // the pair's SpMM waits for its second block
+        const bool folded = !w.step_of.empty() && w.step_first[sj] != j;
+        const int first = folded ? w.step_first[sj] : j;
+        const float* hsrc = folded ? ((!ov || sj % 2 == 0) ? w.bc1 : w.bc2) : recv[k];
+        const int ts = tl_begin(k, 0, "spmm", "stage", first, {bc_task});
+        const DevTile& t = folded ? w.ftiles[dir][first] : w.tiles[dir][j];
         SpmmLaunch sl{t.row_ptr, t.edges, t.light, t.n_light, t.heavy, t.n_heavy};
-        const int acc = j > 0, relu = relu_last && j == P_ - 1;
+        const int acc = sj > 0, relu = relu_last && j == P_ - 1;
         // the layer's bias / dropout ride on the final stage's output write
         k::Epi ep = (epi_layer >= 0 && j == P_ - 1) ? out_epi(w, epi_layer, relu_last) : k::Epi{};
         if (j == P_ - 1 && rm_slot >= 0 && cfg_.spmm_mode == MG_SPMM_FAST) ep.rmax = w.rm_slot(rm_slot);
@@ -1193,23 +1244,23 @@ class Step {
         if (cfg_.spmm_mode == MG_SPMM_FAST) {
           FastLaunch fl{t.items, t.n_items, t.hubs, t.n_hubs, t.edges, w.seg_scratch, t.hubs_classed, t.cols,
                         t.pieces, t.n_pieces, t.row_ptr, t.rows ? static_cast<double>(t.nnz) / t.rows : 0.0};
-          g_.kernels_last += spmm_fast(fl, recv[k], out[k], ld, acc, relu, ep, w.s0);
+          g_.kernels_last += spmm_fast(fl, hsrc, out[k], ld, acc, relu, ep, w.s0);
           prof_end(w, pi, 0);
-          mult_task[k][j] = tl_end(k, ts);
-          MG_CUDA(cudaEventRecord(w.mult[j], w.s0));
+          mult_task[k][sj] = tl_end(k, ts);
+          MG_CUDA(cudaEventRecord(w.mult[sj], w.s0));
           continue;
         }
         if (t.n_heavy > 0) {  // hub rows run beside the light rows on the side stream
           MG_CUDA(cudaEventRecord(w.heavy_fork, w.s0));
           MG_CUDA(cudaStreamWaitEvent(w.s2, w.heavy_fork, 0));
-          g_.kernels_last += spmm_heavy(sl, recv[k], out[k], ld, acc, relu, ep, w.s2);
+          g_.kernels_last += spmm_heavy(sl, hsrc, out[k], ld, acc, relu, ep, w.s2);
           MG_CUDA(cudaEventRecord(w.heavy_join, w.s2));
         }
-        g_.kernels_last += spmm_light(sl, recv[k], out[k], ld, acc, relu, ep, w.s0);
+        g_.kernels_last += spmm_light(sl, hsrc, out[k], ld, acc, relu, ep, w.s0);
         if (t.n_heavy > 0) MG_CUDA(cudaStreamWaitEvent(w.s0, w.heavy_join, 0));
         prof_end(w, pi, 0);
-        mult_task[k][j] = tl_end(k, ts);
-        MG_CUDA(cudaEventRecord(w.mult[j], w.s0));
+        mult_task[k][sj] = tl_end(k, ts);
+        MG_CUDA(cudaEventRecord(w.mult[sj], w.s0));
       }
     }
   }
@@ -1647,6 +1698,8 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
       tc::set_gemm3_cluster(static_cast<int>(value));
     } else if (k == "gemm3_wring") {
       tc::set_w3_bytes(static_cast<int>(value));
+    } else if (k == "stage_fold") {
+      g_stage_fold = value != 0 ? 1 : 0;
     } else if (k == "gemm_f16") {
       tc::set_gemm_f16(static_cast<int>(value));
     } else if (k == "gemm_kernel") {
@@ -1695,6 +1748,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
     if (cfg.gemm_mode != MG_GEMM_EXACT && !tc::available())
       throw ValueError("gemm_mode " + std::to_string(cfg.gemm_mode) + " needs the tcgen05 kernels (sm_100a)");
     g->world = world;
+    g->fold = g_stage_fold.load() != 0 && cfg.spmm_mode == MG_SPMM_FAST && world > 2;
     g->n = p->n;
     g->mask_count = p->mask_count;
     g->bounds = p->bounds;
@@ -1763,6 +1817,17 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       }
       w.t_start = mk_event(true);
       w.t_end = mk_event(true);
+      if (g->fold) {  // SpMM steps: pairs of consecutive received stages, single stages around the own block
+        w.step_of.assign(world, 0);
+        for (int j = 0; j < world;) {
+          const bool pair = j + 1 < world && j != w.rank && j + 1 != w.rank;
+          w.step_first.push_back(j);
+          w.step_last.push_back(pair ? j + 1 : j);
+          w.step_of[j] = static_cast<int>(w.step_first.size()) - 1;
+          if (pair) w.step_of[j + 1] = w.step_of[j];
+          j += pair ? 2 : 1;
+        }
+      }
       // rows: x_local (gcn.hpp:127-132). Page-locked features of the padded width go up on a copy stream
       // while the backward tiles are processed (after the forward tiles' DMAs, so the two do not share
       // the link); otherwise synchronously after the tiles.
@@ -1784,6 +1849,15 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
           upload_tile(*g, w, p->tiles[d][w.rank][j], w.tiles[d][j], tr ? &w.tiles[0][0] : nullptr);
           max_segments = std::max(max_segments, w.tiles[d][j].n_segments);
         }
+        if (g->fold) {  // merged tiles of the folded stage pairs
+          w.ftiles[d].resize(world);
+          for (size_t st = 0; st < w.step_first.size(); ++st) {
+            const int j0 = w.step_first[st], j1 = w.step_last[st];
+            if (j1 == j0) continue;
+            upload_tile(*g, w, merge_tiles(p->tiles[d][w.rank][j0], p->tiles[d][w.rank][j1]), w.ftiles[d][j0]);
+            max_segments = std::max(max_segments, w.ftiles[d][j0].n_segments);
+          }
+        }
       }
       if (max_segments > 0) w.seg_scratch = dalloc_t<float>(*g, w, static_cast<size_t>(max_segments) * g->ld_max);
       sw.lap("tiles");
@@ -1803,11 +1877,15 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       // the L + 3 buffer plan (gcn.hpp:134-140)
       for (int l = 0; l < L; ++l) w.ahw.push_back(dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[l + 1])));
       w.hw = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld_max));
-      w.bc1 = dalloc_t<float>(*g, w, std::max<index_t>(1, g->max_part * g->ld_max));
-      w.bc2 = dalloc_t<float>(*g, w, std::max<index_t>(1, g->max_part * g->ld_max));
+      const index_t bc_rows = (g->fold ? 2 : 1) * g->max_part;  // a folded pair's two blocks stacked
+      w.bc1 = dalloc_t<float>(*g, w, std::max<index_t>(1, bc_rows * g->ld_max));
+      w.bc2 = dalloc_t<float>(*g, w, std::max<index_t>(1, bc_rows * g->ld_max));
       if (cfg.aggregate_first()) w.ax = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));
-      if (cfg.gemm_mode == MG_GEMM_TF32X3 && cfg.spmm_mode == MG_SPMM_FAST)
-        w.rm = dalloc_t<float>(*g, w, static_cast<size_t>(L + 2) * 2 * std::max<index_t>(1, w.rows));
+      if (cfg.gemm_mode == MG_GEMM_TF32X3 && cfg.spmm_mode == MG_SPMM_FAST) {
+        const size_t n_rm = static_cast<size_t>(L + 2) * 2 * std::max<index_t>(1, w.rows);
+        w.rm = dalloc_t<float>(*g, w, n_rm);
+        if (std::getenv("MGGCN_POISON_RM")) MG_CUDA(cudaMemset(w.rm, 0x7E, sizeof(float) * n_rm));  // debug aid
+      }
       // parameters, Adam state, W-grad staging (gcn.hpp:150-158), padded ld_l x ld_{l+1}
       for (int l = 0; l < L; ++l) {
         const index_t sz = g->pstride(l);
@@ -2054,6 +2132,11 @@ static TensorView tensor_view(mg_group* g, Worker& w, int which, int layer) {
       if (!g->cfg.bias) throw ValueError("tensor: the group has no bias (config bias = 0)");
       float* base = which == MG_T_BIAS ? w.W[layer] : w.WG[layer];
       return {base + g->ld[layer] * g->ld[layer + 1], 1, g->cfg.dims[layer + 1], g->ld[layer + 1]};
+    }
+    case MG_T_ROWMAX: {  // the f16 split's per-row max pairs of slot `layer` (rows x 2; diagnostics)
+      if (!w.rm) throw ValueError("tensor: the group keeps no row maxima (TF32X3 + FAST only)");
+      if (layer < 0 || layer > g->cfg.layers() + 1) throw ValueError("tensor: row-max slot out of range");
+      return {w.rm_slot(layer), w.rows, 2, 2};
     }
     default: throw ValueError("tensor: unknown id " + std::to_string(which));
   }

@@ -29,14 +29,18 @@ struct Epi {
   // rmax[2 * row + slot] = max |y| over the values it stored in that row (local row index). A SpMM writes
   // slot 0 and zeroes slot 1; an NN GeMM tile writes slot = its 128-column tile (at most two tiles).
   float* rmax = nullptr;
+  int rmax_acc = 0;  // 1: a later column slab of the same rows — fold the stored max in instead of overwriting
 };
 __device__ __forceinline__ float absmax4(float m, float4 v) {
   return fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
 }
 // max over the G lanes of a row group; lane 0 of the group writes {max, 0} for local row `row`
-__device__ __forceinline__ void rmax_group_store(float m, unsigned gmask, int lane, int G, float* rmax, long long row) {
+__device__ __forceinline__ void rmax_group_store(float m, unsigned gmask, int lane, int G, const Epi& e, long long row) {
   for (int o = G / 2; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(gmask, m, o, G));
-  if (lane == 0) *reinterpret_cast<float2*>(rmax + 2 * row) = make_float2(m, 0.0f);
+  if (lane == 0) {
+    float* r = e.rmax + 2 * row;
+    *reinterpret_cast<float2*>(r) = make_float2(e.rmax_acc ? fmaxf(m, r[0]) : m, 0.0f);
+  }
 }
 __host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {  // splitmix64 finaliser
   z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) spmm_fast_items(const int4* __restrict__ 
         m = absmax4(m, y);
       }
     }
-    if (!seg && ep.rmax) rmax_group_store(m, gmask, lane, G, ep.rmax, it.z);
+    if (!seg && ep.rmax) rmax_group_store(m, gmask, lane, G, ep, it.z);
   }
 }
 
@@ -332,7 +332,7 @@ __global__ void __launch_bounds__(128) spmm_fast_async(const int4* __restrict__ 
         m = absmax4(m, y);
       }
     }
-    if (!seg && ep.rmax) rmax_group_store(m, gmask, lane, G, ep.rmax, it.z);
+    if (!seg && ep.rmax) rmax_group_store(m, gmask, lane, G, ep, it.z);
   }
 }
 
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(128) spmm_fast_stream(const int4* __restrict__
           m = absmax4(m, y);
         }
       }
-      if (!seg && ep.rmax) rmax_group_store(m, gmask, lane, G, ep.rmax, pc.x + cur);
+      if (!seg && ep.rmax) rmax_group_store(m, gmask, lane, G, ep, pc.x + cur);
       ++cur;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {

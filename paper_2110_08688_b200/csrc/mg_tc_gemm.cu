@@ -1384,15 +1384,19 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
 #pragma unroll
           for (int jj = 0; jj < 8; ++jj) {
             float4 o = make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
+            const int col = I.n0 + (c0 + c) * 32 + 4 * jj;  // columns >= nw are stale TMEM: never stored
             if (F16) {  // both inverse scales are powers of two: exact
-              const float4 t = __ldg(reinterpret_cast<const float4*>(p.tinv + I.n0 + (c0 + c) * 32 + 4 * jj));
+              const float4 t = col < p.np ? __ldg(reinterpret_cast<const float4*>(p.tinv + col))
+                                          : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
               o = make_float4(__fmul_rn(__fmul_rn(o.x, rinv), t.x), __fmul_rn(__fmul_rn(o.y, rinv), t.y),
                               __fmul_rn(__fmul_rn(o.z, rinv), t.z), __fmul_rn(__fmul_rn(o.w, rinv), t.w));
             }
             float4* dst = sw128(b, lane, jj);
-            o = gemm_epi<EXT>(o, p.epi == 1 ? *dst : o, p, grow0 + lane, I.n0 + (c0 + c) * 32 + 4 * jj);
+            o = gemm_epi<EXT>(o, p.epi == 1 ? *dst : o, p, grow0 + lane, col);
             *dst = o;
-            omax = k::absmax4(omax, o);
+            if (col + 3 < p.N) omax = k::absmax4(omax, o);
+            else if (col < p.N)
+              omax = k::absmax4(omax, make_float4(o.x, col + 1 < p.N ? o.y : 0.0f, col + 2 < p.N ? o.z : 0.0f, 0.0f));
           }
         }
         if (c0 + ech >= nch) {  // the whole accumulator has been read: the MMA may reuse it

@@ -216,6 +216,9 @@ def test_gemm_v3_variants_bitwise(knob, value):
         base.append((a, b, tb, c0, [run_gemm(a, b, False, tb, epi=e, c0=c0 if e == 1 else None, mode=R.GEMM_TF32X3)
                                     for e in (0, 1, 2)]))
     default = 96 << 10 if knob == "gemm3_wring" else 1
+    R.set_tuning("gemm_f16", 0)  # the variants are of the 3xTF32 pipeline (the fp16 split runs without a cluster)
+    base = [(a, b, tb, c0, [run_gemm(a, b, False, tb, epi=e, c0=c0 if e == 1 else None, mode=R.GEMM_TF32X3)
+                            for e in (0, 1, 2)]) for a, b, tb, c0, _ in base]
     R.set_tuning(knob, value)
     try:
         for a, b, tb, c0, outs in base:
@@ -224,6 +227,7 @@ def test_gemm_v3_variants_bitwise(knob, value):
                 assert bits_equal(got, ref), (knob, value, a.shape, tb, e)
     finally:
         R.set_tuning(knob, default)
+        R.set_tuning("gemm_f16", 1)
 
 
 # ---------------------------------------------------------------------------- MG_SPMM_FAST

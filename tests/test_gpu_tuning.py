@@ -203,3 +203,42 @@ def test_spmm_stream_training_bitwise():
         finally:
             R.set_tuning("spmm_stream", 2)
         assert a.epoch_loss == b.epoch_loss and a.w_hashes == b.w_hashes, P
+
+
+@pytest.mark.parametrize("P,overlap", [(3, True), (4, False), (8, True)])
+def test_stage_fold(ref, P, overlap):
+    """stage_fold (FAST, P > 2): pairs of received stages in one SpMM over a merged tile — the same sums in
+    another association. Teacher-forced step 1: W_G and the H-grads within 1e-5 (normwise) of the
+    stage-by-stage schedule; 3 epochs: losses of both schedules within 1e-4 of the f64 reference (the
+    product contract; W after Adam amplifies the reassociation of tiny gradients, so the two trajectories are
+    compared through the reference, not to each other). In-process transport."""
+    from gpu_util import normwise
+    from oracle.pyoracle import make_cfg
+    dims = [24, 64, 32, 6]
+    ds = R.synth_graph(6000, 20.0, 0.9, 3, dims[0], dims[-1])
+    cfg = R.GcnConfig(dims, epochs=3, seed=5, permute=True, overlap=overlap,
+                      gemm_mode=R.GEMM_TF32X3, spmm_mode=R.SPMM_FAST, aggregate_input=True)
+    opts = dict(workers=P, devices=[0] * P, transport=R.TRANSPORT_LOCAL)
+    prep = R.prepare_data(ds, cfg, P)
+
+    def step1():
+        with R.Group(cfg, prep, P, devices=[0] * P, transport=R.TRANSPORT_LOCAL) as g:
+            g.init_params()
+            loss = g.compute_gradients()
+            return loss, [g.read(R.T_WGRAD, l) for l in range(3)], [g.read(R.T_AHW, l, r) for l in range(2) for r in range(P)]
+
+    base1, base = step1(), R.train_run(ds, cfg, R.TrainOptions(**opts))
+    R.set_tuning("stage_fold", 1)
+    try:
+        fold1, fold = step1(), R.train_run(ds, cfg, R.TrainOptions(**opts))
+    finally:
+        R.set_tuning("stage_fold", 0)
+    assert abs(fold1[0] - base1[0]) <= 1e-6 * abs(base1[0])
+    for a, b in zip(fold1[1] + fold1[2], base1[1] + base1[2]):
+        assert normwise(a, b) <= 1e-5
+    assert fold1[1][0].tobytes() != base1[1][0].tobytes()  # the folded schedule ran (another association)
+    r64 = ref.train_run(ref.synth(6000, 20.0, 0.9, 3, dims[0], dims[-1], dtype=np.float64),
+                        make_cfg(dims, epochs=3, seed=5, permute=True, overlap=overlap), P, np.float64)
+    for e in range(3):
+        assert abs(base.epoch_loss[e] - r64["loss"][e]) <= 1e-4 * abs(r64["loss"][e])
+        assert abs(fold.epoch_loss[e] - r64["loss"][e]) <= 1e-4 * abs(r64["loss"][e])
