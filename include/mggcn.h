@@ -271,7 +271,16 @@ void mg_synth_rank_free(mg_synth_rank* h);
  *              device — the reference's DeviceGroup semantics, used to test P > #GPUs). */
 typedef struct mg_group mg_group;
 
-typedef enum mg_transport { MG_TRANSPORT_AUTO = 0, MG_TRANSPORT_NCCL = 1, MG_TRANSPORT_LOCAL = 2 } mg_transport;
+/* MG_TRANSPORT_SOLO (measurement only): ONE rank of a P-way job alone in the process, its collectives
+ * skipped (the receive buffers keep whatever they hold): times one rank's device work on its real
+ * partition — e.g. rank 0 of the papers-shaped graph at P = 8 on one GPU — without the other ranks. The
+ * numbers it computes are not a training result. */
+typedef enum mg_transport {
+  MG_TRANSPORT_AUTO = 0,
+  MG_TRANSPORT_NCCL = 1,
+  MG_TRANSPORT_LOCAL = 2,
+  MG_TRANSPORT_SOLO = 3
+} mg_transport;
 
 /* Number of visible CUDA devices (0 without a driver/GPU: the host half of the library still works). */
 int32_t mg_device_count(void);

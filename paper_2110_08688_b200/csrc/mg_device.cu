@@ -1113,7 +1113,7 @@ class Step {
   // -------------------------------------------------------------- collectives
   // DeviceGroup::broadcast_bytes (collectives.cpp:110-125) on the comm streams.
   void bcast(int root, size_t count, const std::vector<float*>& bufs) {
-    if (P_ == 1 && !W(0).comm) return;
+    if ((P_ == 1 && !W(0).comm) || g_.transport == MG_TRANSPORT_SOLO) return;
     if (g_.transport == MG_TRANSPORT_NCCL) {
       MG_NCCL(ncclGroupStart());
       for (size_t k = 0; k < nloc(); ++k) {
@@ -1148,7 +1148,7 @@ class Step {
   // DeviceGroup::all_reduce_sum (collectives.hpp:76-94), no-op at P == 1.
   template <class T>
   void allreduce(size_t count, const std::vector<T*>& bufs) {
-    if ((P_ == 1 && !W(0).comm) || count == 0) return;
+    if ((P_ == 1 && !W(0).comm) || count == 0 || g_.transport == MG_TRANSPORT_SOLO) return;
     if (g_.transport == MG_TRANSPORT_NCCL) {
       MG_NCCL(ncclGroupStart());
       for (size_t k = 0; k < nloc(); ++k) {
@@ -1764,6 +1764,9 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
     const bool distinct = std::adjacent_find(sorted.begin(), sorted.end()) == sorted.end();
     const bool one_device = sorted.front() == sorted.back();
     if (transport == MG_TRANSPORT_AUTO) transport = (distinct || n_local < world) ? MG_TRANSPORT_NCCL : MG_TRANSPORT_LOCAL;
+    if (transport == MG_TRANSPORT_SOLO && n_local != 1)
+      throw ValueError("group: the solo transport (measurement only) drives exactly one rank");
+    if (transport < MG_TRANSPORT_NCCL || transport > MG_TRANSPORT_SOLO) throw ValueError("group: unknown transport");
     if (transport == MG_TRANSPORT_LOCAL && n_local != world)
       throw ValueError("group: the in-process transport needs every rank local");
     // LOCAL's peer copies and rank-order reduction dereference every worker's buffers from worker 0's device:

@@ -84,7 +84,7 @@ _STATUS = {1: ShapeError, 2: ValueError, 3: ProtocolError, 4: ShutdownError, 5: 
 
 GEMM_EXACT, GEMM_TF32X3, GEMM_TF32 = 0, 1, 2
 SPMM_EXACT, SPMM_FAST = 0, 1
-TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_LOCAL = 0, 1, 2
+TRANSPORT_AUTO, TRANSPORT_NCCL, TRANSPORT_LOCAL, TRANSPORT_SOLO = 0, 1, 2, 3
 T_W, T_WGRAD, T_AHW, T_HW, T_X, T_ADAM_M, T_ADAM_V, T_WSTAGE, T_BIAS, T_BIAS_GRAD, T_ROWMAX = range(11)
 
 
