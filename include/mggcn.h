@@ -108,8 +108,9 @@ int32_t mg_abi_version(void);
  *   "gemm3_wring"  v3 W-ring budget in bytes (default 96 KiB), "gemm3_cluster" 1 or 2 (W multicast)
  *   "gemm_f16"     1 (default): TF32X3 NN / NT whose A has producer-written row maxima (FAST SpMM) run the
  *                  scaled fp16 two-term split on kind::f16; 0: the 3xTF32 split everywhere
- *   "stage_fold"   1: MG_SPMM_FAST with P > 2 folds pairs of received stages into one SpMM launch over a
- *                  merged tile (half the output read-modify-write passes); 0 (default): stage by stage
+ *   "stage_fold"   k >= 2: MG_SPMM_FAST with P > 2 folds up to k consecutive received stages into one SpMM
+ *                  launch over a merged tile (one output read-modify-write pass per group; receive buffers
+ *                  k blocks deep); 0 (default) or 1: stage by stage
  *   "spmm_stream" 0 / 1 / 2 (auto, default): the row-streaming FAST SpMM for short-row tiles
  *   "adaptive_cuts" 1 (default): FAST hub-row cut points scaled to the tile; "piece_nnz" stream piece size
  *   "bwd_transpose"  one worker: build the backward tile on the device from the forward one (default 1)

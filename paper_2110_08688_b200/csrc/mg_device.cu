@@ -101,11 +101,12 @@ struct DevTile {
 };
 
 std::atomic<int> g_fast_segment{2048};
-// "stage_fold" (MG_SPMM_FAST, P > 1): consecutive received stages (j, j + 1) are folded into one SpMM launch
-// over a merged tile (tile j's columns, then tile j + 1's shifted by the size of block j) reading both
-// blocks from one double-size receive buffer: the output is read-modified-written once per pair instead of
-// once per stage. A pair never contains the rank's own block (that stage reads its h in place). Off by
-// default (the reference's stage-by-stage schedule and timeline); read at group creation.
+// "stage_fold" = k (MG_SPMM_FAST, P > 2; 0 / 1 = off): up to k consecutive received stages are folded into
+// one SpMM launch over a merged tile (the stages' tiles side by side, each block's columns shifted by the
+// sizes of the blocks before it) reading the blocks from one k-block receive buffer: the output is
+// read-modified-written once per group instead of once per stage. A group never contains the rank's own
+// block (that stage reads its h in place). Off by default (the reference's stage-by-stage schedule and
+// timeline); read at group creation.
 std::atomic<int> g_stage_fold{0};
 std::atomic<int> g_adaptive_cuts{1};  // "adaptive_cuts": FAST hub threshold / segment scaled to the tile
 
@@ -692,7 +693,7 @@ struct mg_group {
   mg::index_t wblocks[9] = {};  // canonical W-grad blocks uniform_partition(n, 8), driver.hpp:156
   std::vector<mg::index_t> ld;  // padded widths per dim
   mg::index_t ld_max = 4, max_part = 0;
-  bool fold = false;  // stage folding (g_stage_fold, FAST mode, P > 1)
+  int fold = 0;  // stage folding group size (g_stage_fold >= 2, FAST mode, P > 2), 0 = off
   // floats per layer parameter array: W (ld_l x ld_{l+1}) plus, with cfg.bias, the bias row after it; the
   // same layout for W_G, Adam m / v and each canonical staging block, so the W-grad all-reduce, the block
   // sum and Adam cover the bias with no extra launches
@@ -986,29 +987,33 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d, const DevTil
   if (!heavy.empty()) MG_CUDA(cudaMemcpy(d.heavy, heavy.data(), sizeof(int) * heavy.size(), cudaMemcpyHostToDevice));
 }
 
-// Stage folding: tiles j and j + 1 of one row block side by side (row r = tile j's row r, then tile j + 1's
-// with its columns shifted by block j's size): a CSR over the two blocks stacked in one receive buffer.
-Tile merge_tiles(const Tile& a, const Tile& b) {
+// Stage folding: tiles j0..j1 of one row block side by side (row r = tile j0's row r, then tile j0 + 1's with
+// its columns shifted by block j0's size, ...): a CSR over the blocks stacked in one receive buffer.
+Tile merge_tiles(const std::vector<const Tile*>& t) {
   Tile m;
-  m.rows = a.rows;
-  m.cols = a.cols + b.cols;
-  m.row_ptr.assign(a.rows + 1, 0);
-  for (index_t r = 0; r < a.rows; ++r)
-    m.row_ptr[r + 1] = m.row_ptr[r] + (a.row_ptr[r + 1] - a.row_ptr[r]) + (b.row_ptr[r + 1] - b.row_ptr[r]);
-  m.col.resize(m.row_ptr[a.rows]);
-  m.val.resize(m.row_ptr[a.rows]);
-  const std::int32_t shift = static_cast<std::int32_t>(a.cols);
-  parallel_for(a.rows, [&](index_t s, index_t e) {
-    for (index_t r = s; r < e; ++r) {
+  const index_t rows = t[0]->rows;
+  m.rows = rows;
+  std::vector<std::int32_t> shift(t.size(), 0);
+  for (size_t q = 0; q < t.size(); ++q) {
+    if (q) shift[q] = shift[q - 1] + static_cast<std::int32_t>(t[q - 1]->cols);
+    m.cols += t[q]->cols;
+  }
+  m.row_ptr.assign(rows + 1, 0);
+  for (index_t r = 0; r < rows; ++r) {
+    index_t len = 0;
+    for (const Tile* x : t) len += x->row_ptr[r + 1] - x->row_ptr[r];
+    m.row_ptr[r + 1] = m.row_ptr[r] + len;
+  }
+  m.col.resize(m.row_ptr[rows]);
+  m.val.resize(m.row_ptr[rows]);
+  parallel_for(rows, [&](index_t s0, index_t e0) {
+    for (index_t r = s0; r < e0; ++r) {
       index_t o = m.row_ptr[r];
-      for (index_t k = a.row_ptr[r]; k < a.row_ptr[r + 1]; ++k, ++o) {
-        m.col[o] = a.col[k];
-        m.val[o] = a.val[k];
-      }
-      for (index_t k = b.row_ptr[r]; k < b.row_ptr[r + 1]; ++k, ++o) {
-        m.col[o] = b.col[k] + shift;
-        m.val[o] = b.val[k];
-      }
+      for (size_t q = 0; q < t.size(); ++q)
+        for (index_t k = t[q]->row_ptr[r]; k < t[q]->row_ptr[r + 1]; ++k, ++o) {
+          m.col[o] = t[q]->col[k] + shift[q];
+          m.val[o] = t[q]->val[k];
+        }
     }
   }, 4096);
   return m;
@@ -1217,7 +1222,7 @@ class Step {
                                      : (sj >= 1 ? mult_task[k][sj - 1] : prior_task[k]);
         tb[k] = tl_begin(k, 1, "broadcast", "h_stage", j, {dep_task});
         float* buf = (!ov || sj % 2 == 0) ? w.bc1 : w.bc2;
-        if (j != first) buf += (g_.bounds[first + 1] - g_.bounds[first]) * ld;  // second block of a folded pair
+        buf += (g_.bounds[j] - g_.bounds[first]) * ld;  // block j's place in a folded group (0 if unfolded)
         recv[k] = (w.rank == j) ? src[k] : buf;
       }
       const size_t count = static_cast<size_t>((g_.bounds[j + 1] - g_.bounds[j]) * ld);
@@ -1229,7 +1234,7 @@ class Step {
         MG_CUDA(cudaEventRecord(w.bc_done[j], w.s1));
         MG_CUDA(cudaStreamWaitEvent(w.s0, w.bc_done[j], 0));
         const int sj = w.step_of.empty() ? j : w.step_of[j];
-        if (!w.step_of.empty() && w.step_last[sj] != j) continue;  // the pair's SpMM waits for its second block
+        if (!w.step_of.empty() && w.step_last[sj] != j) continue;  // a group's SpMM waits for its last block
         const bool folded = !w.step_of.empty() && w.step_first[sj] != j;
         const int first = folded ? w.step_first[sj] : j;
         const float* hsrc = folded ? ((!ov || sj % 2 == 0) ? w.bc1 : w.bc2) : recv[k];
@@ -1699,7 +1704,8 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
     } else if (k == "gemm3_wring") {
       tc::set_w3_bytes(static_cast<int>(value));
     } else if (k == "stage_fold") {
-      g_stage_fold = value != 0 ? 1 : 0;
+      if (value < 0 || value > 64) throw ValueError("tuning: stage_fold must be 0 (off) or a group size 2..64");
+      g_stage_fold = static_cast<int>(value);
     } else if (k == "gemm_f16") {
       tc::set_gemm_f16(static_cast<int>(value));
     } else if (k == "gemm_kernel") {
@@ -1748,7 +1754,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
     if (cfg.gemm_mode != MG_GEMM_EXACT && !tc::available())
       throw ValueError("gemm_mode " + std::to_string(cfg.gemm_mode) + " needs the tcgen05 kernels (sm_100a)");
     g->world = world;
-    g->fold = g_stage_fold.load() != 0 && cfg.spmm_mode == MG_SPMM_FAST && world > 2;
+    g->fold = (g_stage_fold.load() >= 2 && cfg.spmm_mode == MG_SPMM_FAST && world > 2) ? g_stage_fold.load() : 0;
     g->n = p->n;
     g->mask_count = p->mask_count;
     g->bounds = p->bounds;
@@ -1820,15 +1826,16 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       }
       w.t_start = mk_event(true);
       w.t_end = mk_event(true);
-      if (g->fold) {  // SpMM steps: pairs of consecutive received stages, single stages around the own block
+      if (g->fold) {  // SpMM steps: groups of <= fold consecutive received stages, the own stage alone
         w.step_of.assign(world, 0);
         for (int j = 0; j < world;) {
-          const bool pair = j + 1 < world && j != w.rank && j + 1 != w.rank;
+          int e = j + 1;
+          if (j != w.rank)
+            while (e < world && e - j < g->fold && e != w.rank) ++e;
           w.step_first.push_back(j);
-          w.step_last.push_back(pair ? j + 1 : j);
-          w.step_of[j] = static_cast<int>(w.step_first.size()) - 1;
-          if (pair) w.step_of[j + 1] = w.step_of[j];
-          j += pair ? 2 : 1;
+          w.step_last.push_back(e - 1);
+          for (int q = j; q < e; ++q) w.step_of[q] = static_cast<int>(w.step_first.size()) - 1;
+          j = e;
         }
       }
       // rows: x_local (gcn.hpp:127-132). Page-locked features of the padded width go up on a copy stream
@@ -1857,7 +1864,9 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
           for (size_t st = 0; st < w.step_first.size(); ++st) {
             const int j0 = w.step_first[st], j1 = w.step_last[st];
             if (j1 == j0) continue;
-            upload_tile(*g, w, merge_tiles(p->tiles[d][w.rank][j0], p->tiles[d][w.rank][j1]), w.ftiles[d][j0]);
+            std::vector<const Tile*> parts;
+            for (int q = j0; q <= j1; ++q) parts.push_back(&p->tiles[d][w.rank][q]);
+            upload_tile(*g, w, merge_tiles(parts), w.ftiles[d][j0]);
             max_segments = std::max(max_segments, w.ftiles[d][j0].n_segments);
           }
         }
@@ -1880,7 +1889,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       // the L + 3 buffer plan (gcn.hpp:134-140)
       for (int l = 0; l < L; ++l) w.ahw.push_back(dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[l + 1])));
       w.hw = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld_max));
-      const index_t bc_rows = (g->fold ? 2 : 1) * g->max_part;  // a folded pair's two blocks stacked
+      const index_t bc_rows = std::max(1, g->fold) * g->max_part;  // a folded group's blocks stacked
       w.bc1 = dalloc_t<float>(*g, w, std::max<index_t>(1, bc_rows * g->ld_max));
       w.bc2 = dalloc_t<float>(*g, w, std::max<index_t>(1, bc_rows * g->ld_max));
       if (cfg.aggregate_first()) w.ax = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));

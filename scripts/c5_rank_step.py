@@ -3,7 +3,7 @@ B200: rank `r`'s real partition (mg_synth_rank_*, bit-identical to that row bloc
 prepare_data) in a group created with the measurement-only solo transport (mggcn.h MG_TRANSPORT_SOLO: the
 broadcasts / all-reduces are skipped, the receive buffers keep what they hold). Times the rank's device
 work per training step (CUDA events, after warm-up) with the per-kind breakdown, for stage folding off and
-on — the compute side of the 8-GPU epoch; the exchange adds n_p-row blocks over NVLink.
+in groups of 2 and 4 — the compute side of the 8-GPU epoch; the exchange adds n_p-row blocks over NVLink.
 
     python scripts/c5_rank_step.py [rank] [--scale K] [--steps S]
 """
@@ -30,7 +30,7 @@ t_prep = time.time() - t0
 out = {"n": n, "P": P, "rank": rank, "rows": int(prep.bounds[rank + 1] - prep.bounds[rank]), "prepare_s": round(t_prep, 1)}
 out["rank_nnz"] = int(sum(prep.tile(0, rank, j)[0][-1] for j in range(P)))
 import ctypes as C  # noqa: E402
-for fold in (0, 1):
+for fold in (0, 2, 4):
     R.set_tuning("stage_fold", fold)
     R.set_tuning("profile", 1)
     t1 = time.time()

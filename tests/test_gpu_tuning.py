@@ -205,9 +205,9 @@ def test_spmm_stream_training_bitwise():
         assert a.epoch_loss == b.epoch_loss and a.w_hashes == b.w_hashes, P
 
 
-@pytest.mark.parametrize("P,overlap", [(3, True), (4, False), (8, True)])
-def test_stage_fold(ref, P, overlap):
-    """stage_fold (FAST, P > 2): pairs of received stages in one SpMM over a merged tile — the same sums in
+@pytest.mark.parametrize("P,overlap,k", [(3, True, 2), (4, False, 2), (8, True, 2), (8, True, 4), (8, False, 7)])
+def test_stage_fold(ref, P, overlap, k):
+    """stage_fold = k (FAST, P > 2): up to k received stages in one SpMM over a merged tile — the same sums in
     another association. Teacher-forced step 1: W_G and the H-grads within 1e-5 (normwise) of the
     stage-by-stage schedule; 3 epochs: losses of both schedules within 1e-4 of the f64 reference (the
     product contract; W after Adam amplifies the reassociation of tiny gradients, so the two trajectories are
@@ -228,7 +228,7 @@ def test_stage_fold(ref, P, overlap):
             return loss, [g.read(R.T_WGRAD, l) for l in range(3)], [g.read(R.T_AHW, l, r) for l in range(2) for r in range(P)]
 
     base1, base = step1(), R.train_run(ds, cfg, R.TrainOptions(**opts))
-    R.set_tuning("stage_fold", 1)
+    R.set_tuning("stage_fold", k)
     try:
         fold1, fold = step1(), R.train_run(ds, cfg, R.TrainOptions(**opts))
     finally:
@@ -242,3 +242,19 @@ def test_stage_fold(ref, P, overlap):
     for e in range(3):
         assert abs(base.epoch_loss[e] - r64["loss"][e]) <= 1e-4 * abs(r64["loss"][e])
         assert abs(fold.epoch_loss[e] - r64["loss"][e]) <= 1e-4 * abs(r64["loss"][e])
+
+
+def test_solo_transport_steps():
+    """MG_TRANSPORT_SOLO (measurement only): one rank of a P-way job alone, collectives skipped — it creates,
+    steps and reports; more than one local rank is refused."""
+    ds = R.synth_graph(4000, 10.0, 0.7, 2, 16, 4)
+    cfg = R.GcnConfig([16, 32, 4], epochs=2, seed=2, permute=True, overlap=True, gemm_mode=R.GEMM_TF32X3,
+                      spmm_mode=R.SPMM_FAST, aggregate_input=True)
+    prep = R.synth_prepare_rank(4000, 10.0, 0.7, 2, 16, 4, cfg, 4, 1)
+    with R.Group(cfg, prep, 4, local_ranks=[1], devices=[0], transport=R.TRANSPORT_SOLO) as g:
+        g.init_params()
+        for t in (1, 2):
+            g.train_step(t)
+    full = R.prepare_data(ds, cfg, 4)
+    with pytest.raises(R.ValueError, match="solo"):
+        R.Group(cfg, full, 4, local_ranks=[0, 1], devices=[0, 0], transport=R.TRANSPORT_SOLO)
