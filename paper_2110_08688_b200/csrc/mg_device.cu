@@ -1706,6 +1706,8 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
     } else if (k == "stage_fold") {
       if (value < 0 || value > 64) throw ValueError("tuning: stage_fold must be 0 (off) or a group size 2..64");
       g_stage_fold = static_cast<int>(value);
+    } else if (k == "gemm_f16_min_k") {
+      tc::set_gemm_f16_min_k(static_cast<int>(value));
     } else if (k == "gemm_f16") {
       tc::set_gemm_f16(static_cast<int>(value));
     } else if (k == "gemm_kernel") {

@@ -685,7 +685,9 @@ __device__ __forceinline__ int f16_scale_exp(float m) {
   if (!(m > 0.0f)) return 0;
   int e;
   (void)frexpf(m, &e);  // m = f * 2^e, f in [0.5, 1): m in [2^(e-1), 2^e)
-  return max(-100, min(100, 15 - e));
+  // +-60: the epilogue multiplies by the product of a row's and a column's inverse scales, which then stays
+  // a normal fp32 power of two (exact)
+  return max(-60, min(60, 15 - e));
 }
 __device__ __forceinline__ uint32_t h2_bits(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 // x (already scaled) -> fp16 hi / lo pair for two consecutive K elements (a = even k in the low half)
@@ -1385,18 +1387,20 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
           for (int jj = 0; jj < 8; ++jj) {
             float4 o = make_float4(v[4 * jj], v[4 * jj + 1], v[4 * jj + 2], v[4 * jj + 3]);
             const int col = I.n0 + (c0 + c) * 32 + 4 * jj;  // columns >= nw are stale TMEM: never stored
-            if (F16) {  // both inverse scales are powers of two: exact
+            if (F16) {  // row x column inverse scale: a power of two within 2^+-120, so one exact multiply
               const float4 t = col < p.np ? __ldg(reinterpret_cast<const float4*>(p.tinv + col))
                                           : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-              o = make_float4(__fmul_rn(__fmul_rn(o.x, rinv), t.x), __fmul_rn(__fmul_rn(o.y, rinv), t.y),
-                              __fmul_rn(__fmul_rn(o.z, rinv), t.z), __fmul_rn(__fmul_rn(o.w, rinv), t.w));
+              o = make_float4(__fmul_rn(o.x, __fmul_rn(rinv, t.x)), __fmul_rn(o.y, __fmul_rn(rinv, t.y)),
+                              __fmul_rn(o.z, __fmul_rn(rinv, t.z)), __fmul_rn(o.w, __fmul_rn(rinv, t.w)));
             }
             float4* dst = sw128(b, lane, jj);
             o = gemm_epi<EXT>(o, p.epi == 1 ? *dst : o, p, grow0 + lane, col);
             *dst = o;
-            if (col + 3 < p.N) omax = k::absmax4(omax, o);
-            else if (col < p.N)
-              omax = k::absmax4(omax, make_float4(o.x, col + 1 < p.N ? o.y : 0.0f, col + 2 < p.N ? o.z : 0.0f, 0.0f));
+            if (p.ep.rmax) {
+              if (col + 3 < p.N) omax = k::absmax4(omax, o);
+              else if (col < p.N)
+                omax = k::absmax4(omax, make_float4(o.x, col + 1 < p.N ? o.y : 0.0f, col + 2 < p.N ? o.z : 0.0f, 0.0f));
+            }
           }
         }
         if (c0 + ech >= nch) {  // the whole accumulator has been read: the MMA may reuse it
@@ -1558,6 +1562,10 @@ inline int smem_bytes3(const Params& p, bool f16) {
 }
 int g_gemm3_cluster = 1;  // v3 cluster size for the W multicast ("gemm3_cluster": 1 or 2)
 int g_gemm_f16 = 1;       // v3 NN / NT in TF32X3 mode: scaled fp16 two-term split on kind::f16 ("gemm_f16")
+// ... only above this K ("gemm_f16_min_k"): with <= 4 32-K stages per 128-row tile the per-tile epilogue,
+// not the MMA issue, paces the kernel and the split's extra epilogue work made it slower (ncu, C4:
+// NN K = 100 1.09 -> 1.21 ms, NT K = 47 1.09 -> 1.19 ms; K = 256: 1.52 -> 1.40 and 1.71 -> 1.46 ms)
+int g_f16_min_k = 128;
 template <int MODE, int CL, bool EXT, bool F16 = false>
 void launch3x(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, const CUtensorMap& c, const Params& p,
               cudaStream_t s) {
@@ -1624,6 +1632,10 @@ size_t nn_workspace_bytes(int64_t N, int64_t K) {
 }
 
 void set_gemm_f16(int on) { g_gemm_f16 = on != 0 ? 1 : 0; }
+void set_gemm_f16_min_k(int k) {
+  if (k < 0) throw ValueError("tuning: gemm_f16_min_k must be >= 0");
+  g_f16_min_k = k;
+}
 
 void set_gemm3_cluster(int c) {
   if (c != 1 && c != 2) throw ValueError("tuning: gemm3_cluster must be 1 or 2");
@@ -1710,7 +1722,7 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
     p.n_items = p.m_tiles * p.n_tiles;
     const int kp = static_cast<int>((K + 3) / 4 * 4);
     if (!ws || ws_bytes < nn_workspace_bytes(N, K)) throw ValueError("tc gemm: B split workspace too small");
-    if (g_gemm_version == 3 && g_gemm_f16 && p.terms == 3 && g_gemm3_cluster == 1 && rmax_in) {
+    if (g_gemm_version == 3 && g_gemm_f16 && p.terms == 3 && g_gemm3_cluster == 1 && rmax_in && K > g_f16_min_k) {
       // scaled fp16 two-term split (kind::f16): W -> per-column scaled fp16 hi / lo planes + inverse scales
       const int kp16 = static_cast<int>((K + 7) / 8 * 8);
       __half* h16 = reinterpret_cast<__half*>(ws);

@@ -162,9 +162,11 @@ def test_gemm_tcgen05(gemm_kernel, shape, ta, tb, mode, tol):
 def gemm_kernel(kernel):
     R.set_tuning("gemm_kernel", 3 if kernel == 30 else kernel)
     R.set_tuning("gemm_f16", 0 if kernel == 30 else 1)
+    R.set_tuning("gemm_f16_min_k", 0)  # the fp16 split at every K (the step uses it above K = 128)
     yield kernel
     R.set_tuning("gemm_kernel", 3)
     R.set_tuning("gemm_f16", 1)
+    R.set_tuning("gemm_f16_min_k", 128)
 
 
 # Scaled fp16 split (kernel 3, NN / NT): rows and columns of very different magnitudes, tiny (gradient-like)
@@ -184,7 +186,11 @@ def test_gemm_f16_row_scales(shape, tb):
     else:
         b *= (10.0 ** rng.integers(-10, 10, (1, n))).astype(np.float32)
     ref = a.astype(np.float64) @ (b.astype(np.float64).T if tb else b.astype(np.float64))
-    got = run_gemm(a, b, False, tb, mode=R.GEMM_TF32X3)
+    R.set_tuning("gemm_f16_min_k", 0)
+    try:
+        got = run_gemm(a, b, False, tb, mode=R.GEMM_TF32X3)
+    finally:
+        R.set_tuning("gemm_f16_min_k", 128)
     scale = np.abs(a).max(1, keepdims=True).astype(np.float64) * np.abs(b).max(1 if tb else 0)[None, :].astype(np.float64)
     err = np.abs(got - ref) / np.maximum(scale * k, 1e-300)
     assert np.all(np.isfinite(got)) and err.max() <= 1e-6, err.max()
