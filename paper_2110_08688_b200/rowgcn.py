@@ -34,7 +34,7 @@ from ._lib import lib, mg_config, mg_csr, mg_timeline_event
 def _finalizing() -> bool:
     """True during interpreter shutdown, when module globals (lib, ctypes) may already be torn down: the
     process exit releases the native objects then."""
-    return sys is None or sys.is_finalizing()
+    return sys is None or sys.is_finalizing() or lib is None or C is None
 
 # ----------------------------------------------------------------------------- errors (inc/errors.hpp)
 
@@ -252,7 +252,10 @@ class Dataset:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h and h.value and not _finalizing():
-            lib().mg_dataset_free(h)
+            try:
+                lib().mg_dataset_free(h)
+            except Exception:  # interpreter teardown: the process exit releases the native object
+                return
             self._h = C.c_void_p()
 
     def _view(self):
@@ -485,7 +488,10 @@ class PreparedData:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h and h.value and not _finalizing():
-            lib().mg_partition_free(h)
+            try:
+                lib().mg_partition_free(h)
+            except Exception:  # interpreter teardown: the process exit releases the native object
+                return
             self._h = C.c_void_p()
 
     def tile(self, direction: int, i: int, j: int):
@@ -549,7 +555,10 @@ class SynthRank:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h and h.value and not _finalizing():
-            lib().mg_synth_rank_free(h)
+            try:
+                lib().mg_synth_rank_free(h)
+            except Exception:  # interpreter teardown: the process exit releases the native object
+                return
             self._h = C.c_void_p()
 
     def degrees(self) -> np.ndarray:
@@ -632,7 +641,10 @@ class Group:
 
     def __del__(self):
         if not _finalizing():
-            self.close()
+            try:
+                self.close()
+            except Exception:  # interpreter teardown
+                pass
 
     def __enter__(self):
         return self
