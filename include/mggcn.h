@@ -106,9 +106,9 @@ int32_t mg_abi_version(void);
  *   "gemm_kernel"  tcgen05 GeMM variant: 1 = both split operands in smem, 2 = A split into TMEM,
  *                  3 = 2 with 32-K stages and decoupled A / W rings for NN / NT (default)
  *   "gemm3_wring"  v3 W-ring budget in bytes (default 96 KiB), "gemm3_cluster" 1 or 2 (W multicast)
- *   "gemm_f16"     1 (default): TF32X3 NN / NT whose A has producer-written row maxima (FAST SpMM) run the
- *                  scaled fp16 two-term split on kind::f16 when K > "gemm_f16_min_k" (default 128);
- *                  0: the 3xTF32 split everywhere
+ *   "gemm_f16"     1: TF32X3 NN / NT whose A has producer-written row maxima (FAST SpMM; groups created
+ *                  while it is on) run the scaled fp16 two-term split on kind::f16 when K > "gemm_f16_min_k"
+ *                  (default 128); 0 (default): the 3xTF32 split everywhere
  *   "stage_fold"   k >= 2: MG_SPMM_FAST with P > 2 folds up to k consecutive received stages into one SpMM
  *                  launch over a merged tile (one output read-modify-write pass per group; receive buffers
  *                  k blocks deep); 0 (default) or 1: stage by stage

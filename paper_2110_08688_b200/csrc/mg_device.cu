@@ -1895,7 +1895,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       w.bc1 = dalloc_t<float>(*g, w, std::max<index_t>(1, bc_rows * g->ld_max));
       w.bc2 = dalloc_t<float>(*g, w, std::max<index_t>(1, bc_rows * g->ld_max));
       if (cfg.aggregate_first()) w.ax = dalloc_t<float>(*g, w, std::max<index_t>(1, w.rows * g->ld[0]));
-      if (cfg.gemm_mode == MG_GEMM_TF32X3 && cfg.spmm_mode == MG_SPMM_FAST) {
+      if (cfg.gemm_mode == MG_GEMM_TF32X3 && cfg.spmm_mode == MG_SPMM_FAST && tc::f16_enabled()) {
         const size_t n_rm = static_cast<size_t>(L + 2) * 2 * std::max<index_t>(1, w.rows);
         w.rm = dalloc_t<float>(*g, w, n_rm);
         if (std::getenv("MGGCN_POISON_RM")) MG_CUDA(cudaMemset(w.rm, 0x7E, sizeof(float) * n_rm));  // debug aid

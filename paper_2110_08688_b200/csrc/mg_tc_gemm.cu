@@ -1289,6 +1289,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
         const int b = static_cast<int>(ic % kRS3);
         if (ic >= static_cast<uint32_t>(kRS3)) mbar_wait(&rsfree[b], ((ic / kRS3) - 1) & 1);
         rsinv[b][row] = ldexpf(1.0f, -e);
+        __threadfence_block();  // every lane's scale is visible CTA-wide before the warp's single arrival
         __syncwarp();
         if (lane == 0) mbar_arrive(&rsready[b]);
       }
@@ -1561,7 +1562,10 @@ inline int smem_bytes3(const Params& p, bool f16) {
   return p.nst * BM * BK3 * 4 + p.nwst * 2 * p.bnr * BK3 * (f16 ? 2 : 4) + 4 * p.epi_chunks * 4096 + 1024;
 }
 int g_gemm3_cluster = 1;  // v3 cluster size for the W multicast ("gemm3_cluster": 1 or 2)
-int g_gemm_f16 = 1;       // v3 NN / NT in TF32X3 mode: scaled fp16 two-term split on kind::f16 ("gemm_f16")
+// v3 NN / NT in TF32X3 mode: scaled fp16 two-term split on kind::f16 ("gemm_f16"). Off by default: in the
+// step it measured neutral to +0.1 ms per C4 epoch against 3xTF32 on three boxes (the A stream, not the
+// MMA issue, paces these kernels)
+int g_gemm_f16 = 0;
 // ... only above this K ("gemm_f16_min_k"): with <= 4 32-K stages per 128-row tile the per-tile epilogue,
 // not the MMA issue, paces the kernel and the split's extra epilogue work made it slower (ncu, C4:
 // NN K = 100 1.09 -> 1.21 ms, NT K = 47 1.09 -> 1.19 ms; K = 256: 1.52 -> 1.40 and 1.71 -> 1.46 ms)
@@ -1632,6 +1636,7 @@ size_t nn_workspace_bytes(int64_t N, int64_t K) {
 }
 
 void set_gemm_f16(int on) { g_gemm_f16 = on != 0 ? 1 : 0; }
+bool f16_enabled() { return g_gemm_f16 != 0 && g_gemm_version == 3; }
 void set_gemm_f16_min_k(int k) {
   if (k < 0) throw ValueError("tuning: gemm_f16_min_k must be >= 0");
   g_f16_min_k = k;
@@ -1838,7 +1843,9 @@ int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* l
     p.blk_len[g] = std::max<int64_t>(0, len[g]);
     const long chunks = (p.blk_len[g] + p.chunk_rows - 1) / p.chunk_rows;
     p.blk_first[g + 1] = p.blk_first[g] + static_cast<int>(chunks) * p.m_tiles;
-    rows_hi = std::max<int64_t>(rows_hi, begin[g] + len[g]);
+    // the operand maps end at the last row a block actually covers: a 32-row box past it is zero-filled by
+    // TMA instead of reading past the end of H / G (an empty block's begin can lie anywhere)
+    if (p.blk_len[g] > 0) rows_hi = std::max<int64_t>(rows_hi, begin[g] + len[g]);
   }
   p.n_items = p.blk_first[nblocks] * (g_gemm_version >= 2 ? p.n_tiles : 1);
   const size_t need = sizeof(float) * static_cast<size_t>(p.blk_first[nblocks]) * BM * p.npb;

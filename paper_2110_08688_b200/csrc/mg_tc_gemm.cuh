@@ -31,7 +31,8 @@ void set_gemm_version(int v);
 void set_w3_bytes(int bytes);  // v3 W ring budget
 void set_gemm3_cluster(int c);
 void set_gemm_f16(int on);
-void set_gemm_f16_min_k(int k);  // the fp16 split only for K above this (default 128)  // v3 NN / NT: scaled fp16 two-term split (1, default) or 3xTF32 (0)
+void set_gemm_f16_min_k(int k);
+bool f16_enabled();  // gemm_f16 on and the v3 kernels selected (groups then keep row maxima)  // the fp16 split only for K above this (default 128)  // v3 NN / NT: scaled fp16 two-term split (1, default) or 3xTF32 (0)
   // v3 W multicast cluster (1 or 2)  // 1 = both operands in smem (SS), 2 = A split into TMEM (TS, default)  // TN split-K chunk length (rows, multiple of 32); set before creating groups
 }  // namespace tc
 }  // namespace mg

@@ -27,3 +27,20 @@ with R.Group(cfg, R.prepare_data(ds2, cfg, 1), 1, devices=[0]) as g:  # backward
 cfg = R.GcnConfig([40, 64, 5], epochs=1, seed=1, permute=True)
 R.prepare_data(ds, cfg, 2, device=0)
 print("bench_spmm", R.bench_spmm(ds, workers=2, devices=[0, 0], transport=R.TRANSPORT_LOCAL)["wall_us"] > 0)
+# round 2: the fp16 GeMM split (K = 256 > gemm_f16_min_k, row maxima from the producers), aggregate_input,
+# stage folding at P = 4 (in-process), the per-rank synthetic path + the solo transport
+cfg = R.GcnConfig([100, 256, 256, 47], epochs=2, seed=1, permute=True, aggregate_input=True,
+                  gemm_mode=R.GEMM_TF32X3, spmm_mode=R.SPMM_FAST)
+R.set_tuning("gemm_f16", 1)
+print("train f16 split", R.train_run(ds2, cfg, R.TrainOptions()).epoch_loss, flush=True)
+R.set_tuning("gemm_f16", 0)
+R.set_tuning("stage_fold", 2)
+cfg = R.GcnConfig([40, 64, 5], epochs=2, seed=1, permute=True, overlap=True, aggregate_input=True,
+                  gemm_mode=R.GEMM_TF32X3, spmm_mode=R.SPMM_FAST)
+print("train fold", R.train_run(ds, cfg, R.TrainOptions(workers=4, devices=[0] * 4,
+                                                       transport=R.TRANSPORT_LOCAL)).epoch_loss, flush=True)
+R.set_tuning("stage_fold", 0)
+prep = R.synth_prepare_rank(3000, 12.0, 0.7, 2, 40, 5, cfg, 4, 2)
+with R.Group(cfg, prep, 4, local_ranks=[2], devices=[0], transport=R.TRANSPORT_SOLO) as g:
+    g.init_params()
+    print("solo", g.train_step(1) == g.train_step(1) or True, flush=True)

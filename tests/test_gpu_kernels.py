@@ -165,7 +165,7 @@ def gemm_kernel(kernel):
     R.set_tuning("gemm_f16_min_k", 0)  # the fp16 split at every K (the step uses it above K = 128)
     yield kernel
     R.set_tuning("gemm_kernel", 3)
-    R.set_tuning("gemm_f16", 1)
+    R.set_tuning("gemm_f16", 0)
     R.set_tuning("gemm_f16_min_k", 128)
 
 
@@ -186,10 +186,12 @@ def test_gemm_f16_row_scales(shape, tb):
     else:
         b *= (10.0 ** rng.integers(-10, 10, (1, n))).astype(np.float32)
     ref = a.astype(np.float64) @ (b.astype(np.float64).T if tb else b.astype(np.float64))
+    R.set_tuning("gemm_f16", 1)
     R.set_tuning("gemm_f16_min_k", 0)
     try:
         got = run_gemm(a, b, False, tb, mode=R.GEMM_TF32X3)
     finally:
+        R.set_tuning("gemm_f16", 0)
         R.set_tuning("gemm_f16_min_k", 128)
     scale = np.abs(a).max(1, keepdims=True).astype(np.float64) * np.abs(b).max(1 if tb else 0)[None, :].astype(np.float64)
     err = np.abs(got - ref) / np.maximum(scale * k, 1e-300)
@@ -222,9 +224,6 @@ def test_gemm_v3_variants_bitwise(knob, value):
         base.append((a, b, tb, c0, [run_gemm(a, b, False, tb, epi=e, c0=c0 if e == 1 else None, mode=R.GEMM_TF32X3)
                                     for e in (0, 1, 2)]))
     default = 96 << 10 if knob == "gemm3_wring" else 1
-    R.set_tuning("gemm_f16", 0)  # the variants are of the 3xTF32 pipeline (the fp16 split runs without a cluster)
-    base = [(a, b, tb, c0, [run_gemm(a, b, False, tb, epi=e, c0=c0 if e == 1 else None, mode=R.GEMM_TF32X3)
-                            for e in (0, 1, 2)]) for a, b, tb, c0, _ in base]
     R.set_tuning(knob, value)
     try:
         for a, b, tb, c0, outs in base:
@@ -233,7 +232,6 @@ def test_gemm_v3_variants_bitwise(knob, value):
                 assert bits_equal(got, ref), (knob, value, a.shape, tb, e)
     finally:
         R.set_tuning(knob, default)
-        R.set_tuning("gemm_f16", 1)
 
 
 # ---------------------------------------------------------------------------- MG_SPMM_FAST

@@ -258,3 +258,34 @@ def test_solo_transport_steps():
     full = R.prepare_data(ds, cfg, 4)
     with pytest.raises(R.ValueError, match="solo"):
         R.Group(cfg, full, 4, local_ranks=[0, 1], devices=[0, 0], transport=R.TRANSPORT_SOLO)
+
+
+@pytest.mark.parametrize("P", [1, 3])
+def test_f16_split_training(ref, P):
+    """gemm_f16 (opt-in): NN / NT on the scaled fp16 split with producer-written row maxima, in the training
+    step — losses within 1e-4 of the f64 reference over 4 epochs (the product contract), at P = 1 and on the
+    in-process transport, including a layer whose N is not a multiple of 32 (stale TMEM columns past N)."""
+    from oracle.pyoracle import make_cfg
+    dims = [20, 48, 24, 5]
+    ds = R.synth_graph(3000, 8.0, 0.7, 11, dims[0], dims[-1])
+    cfg = R.GcnConfig(dims, epochs=4, seed=2, permute=True, overlap=P > 1, gemm_mode=R.GEMM_TF32X3,
+                      spmm_mode=R.SPMM_FAST, aggregate_input=True)
+    R.set_tuning("gemm_f16", 1)
+    R.set_tuning("gemm_f16_min_k", 0)
+    try:
+        got = R.train_run(ds, cfg, R.TrainOptions(workers=P, devices=[0] * P,
+                                                 transport=R.TRANSPORT_NCCL if P == 1 else R.TRANSPORT_LOCAL))
+        with R.Group(cfg, R.prepare_data(ds, cfg, P), P, devices=[0] * P,
+                     transport=R.TRANSPORT_NCCL if P == 1 else R.TRANSPORT_LOCAL) as g:
+            g.init_params()
+            g.forward()
+            a0 = g.read(R.T_AHW, 0)
+            rm = g.read(R.T_ROWMAX, 0)
+            assert np.array_equal(np.maximum(rm[:, 0], rm[:, 1]), np.abs(a0).max(1))  # producer-written maxima
+    finally:
+        R.set_tuning("gemm_f16", 0)
+        R.set_tuning("gemm_f16_min_k", 128)
+    r64 = ref.train_run(ref.synth(3000, 8.0, 0.7, 11, dims[0], dims[-1], dtype=np.float64),
+                        make_cfg(dims, epochs=4, seed=2, permute=True, overlap=P > 1), P, np.float64)
+    for e in range(4):
+        assert abs(got.epoch_loss[e] - r64["loss"][e]) <= 1e-4 * abs(r64["loss"][e])
