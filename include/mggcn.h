@@ -51,7 +51,8 @@ typedef struct mg_csr {
 typedef enum mg_gemm_mode {
   MG_GEMM_EXACT = 0,  /* SIMT, k-ascending separate mul/add: bitwise equal to rowgcn::gemm (f32) */
   MG_GEMM_TF32X3 = 1, /* tcgen05, 3-term split (hi*hi + hi*lo + lo*hi): fp32-level accuracy. kind::tf32 for the
-                       * W-grad; NN / NT fed by FAST SpMM: per-row / per-column scaled fp16 pairs on kind::f16 */
+                       * W-grad and (default) NN / NT; opt-in "gemm_f16": NN / NT fed by FAST SpMM on per-row /
+                       * per-column scaled fp16 pairs, kind::f16 */
   MG_GEMM_TF32 = 2    /* tcgen05 kind::tf32, single term (reported separately, rel ~1e-3) */
 } mg_gemm_mode;
 
