@@ -106,7 +106,9 @@ int32_t mg_abi_version(void);
  *   "spmm_hub_bytes"  L2 footprint of the rows given evict_last priority (default 96 MiB; 0 = no hints)
  *   "gemm_kernel"  tcgen05 GeMM variant: 1 = both split operands in smem, 2 = A split into TMEM,
  *                  3 = 2 with 32-K stages and decoupled A / W rings for NN / NT (default)
- *   "gemm3_wring"  v3 W-ring budget in bytes (default 96 KiB), "gemm3_cluster" 1 or 2 (W multicast)
+ *   "gemm3_wring"  v3 W-ring budget in bytes (default 96 KiB); "gemm3_cluster" 2: NN / NT with two 128-column
+ *                  tiles run as 2-CTA clusters that multicast each A stage to both tiles (one A read from
+ *                  HBM / L2 per row tile), 1: one CTA per tile
  *   "gemm_f16"     1: TF32X3 NN / NT whose A has producer-written row maxima (FAST SpMM; groups created
  *                  while it is on) run the scaled fp16 two-term split on kind::f16 when K > "gemm_f16_min_k"
  *                  (default 128); 0 (default): the 3xTF32 split everywhere

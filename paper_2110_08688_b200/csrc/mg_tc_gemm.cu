@@ -1102,6 +1102,18 @@ constexpr int kRS3 = 4;  // F16: per-row scale buffers (split warps -> epilogue)
 // scale every A row by a power of two from its max |x| over the whole K range (read from global memory,
 // the next item's row during the current item's stages), W columns are pre-scaled by split_b16, and the
 // epilogue multiplies each output by both inverse scales (exact).
+// arrive on the mbarrier at the same shared-memory offset in CTA `peer` of the cluster (release, cluster scope)
+__device__ __forceinline__ void mbar_arrive_peer(uint64_t* bar, uint32_t peer) {
+  asm volatile(
+      "{\n"
+      ".reg .b32 ra;\n"
+      "mapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(peer)
+      : "memory");
+}
+
 template <int MODE, int CL, bool EXT, bool F16>
 __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__ CUtensorMap map_a,
                                                          const __grid_constant__ CUtensorMap map_bh,
@@ -1128,11 +1140,11 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
   if (threadIdx.x == 0) {
     for (int s = 0; s < nA; ++s) {
       mbar_init(&fullA[s], 1);
-      mbar_init(&emptyA[s], 4);
+      mbar_init(&emptyA[s], 4 * CL);  // CL = 2: both CTAs' split warps (A is multicast into both)
     }
     for (int s = 0; s < nW; ++s) {
       mbar_init(&fullW[s], 1);
-      mbar_init(&emptyW[s], CL);  // every CTA of the cluster reads the slot (W is multicast)
+      mbar_init(&emptyW[s], 1);
     }
     for (int s = 0; s < kTSlots3; ++s) {
       mbar_init(&conv[s], 4);
@@ -1170,15 +1182,15 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
   tc_fence_after();
   const uint32_t tmem = tmem_base_s;
   const int nkb = static_cast<int>((p.K + BK3 - 1) / BK3);
-  // cluster-synchronous work list: the CL CTAs of a cluster take CL adjacent row tiles of the same
-  // output-column tile, so they consume the same W tiles in the same order (multicast once per cluster)
+  // CL = 2 (N > 128): the two CTAs of a cluster take the two 128-column tiles of the same row tile, so they
+  // stream the same A tiles in the same order: each loads half of every A stage and multicasts it to both
   const int rank = static_cast<int>(blockIdx.x % CL), pair0 = static_cast<int>(blockIdx.x / CL);
   const int npairs = static_cast<int>(gridDim.x / CL);
-  const int npi = ((p.m_tiles + CL - 1) / CL) * p.n_tiles;
+  const int npi = CL == 1 ? p.m_tiles * p.n_tiles : p.m_tiles;
   auto item_of3 = [&](int pi) {
     Item2 r;
-    const int nt = pi % p.n_tiles;
-    r.mi = (pi / p.n_tiles) * CL + rank;
+    const int nt = CL == 1 ? pi % p.n_tiles : rank;
+    r.mi = CL == 1 ? pi / p.n_tiles : pi;
     r.n0 = nt * kTileN;
     r.nw = min(kTileN, p.np - r.n0);
     r.k.row0 = static_cast<long>(r.mi) * BM;
@@ -1198,7 +1210,11 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
           if (r.wrapped) mbar_wait(&emptyA[s], r.phase ^ 1u);
           if (p.trace && blockIdx.x == 0 && sc < kTraceStages) p.trace[sc * 4 + 0] = clock64();
           mbar_arrive_tx(&fullA[s], static_cast<uint32_t>(a_bytes));
-          tma_load_2d(aring + s * a_bytes, &map_a, kb * BK3, static_cast<int>(I.k.row0), &fullA[s]);
+          if (CL == 1)
+            tma_load_2d(aring + s * a_bytes, &map_a, kb * BK3, static_cast<int>(I.k.row0), &fullA[s]);
+          else  // this CTA's half of the rows, into both CTAs' slot s
+            tma_load_2d_mc(aring + s * a_bytes + rank * (a_bytes / 2), &map_a, kb * BK3,
+                           static_cast<int>(I.k.row0) + rank * (BM / 2), &fullA[s], 3u);
         }
       }
     }
@@ -1207,7 +1223,6 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
     if (lane == 0) {
       RingPos r(nW);
       const uint32_t tx = static_cast<uint32_t>(p.terms == 3 ? 2 * b_bytes : b_bytes);
-      const int half = p.bnr / CL;  // rows of the W tile this CTA loads (and multicasts to its peers)
       for (int pi = pair0; pi < npi; pi += npairs) {
         const Item2 I = item_of3(pi);
         for (int kb = 0; kb < nkb; ++kb, r.next()) {
@@ -1215,15 +1230,8 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
           if (r.wrapped) mbar_wait(&emptyW[s], r.phase ^ 1u);
           uint8_t* b = wring + s * 2 * b_bytes;
           mbar_arrive_tx(&fullW[s], tx);
-          if (CL == 1) {
-            tma_load_2d(b, &map_bh, kb * BK3, I.n0, &fullW[s]);
-            if (p.terms == 3) tma_load_2d(b + b_bytes, &map_bl, kb * BK3, I.n0, &fullW[s]);
-          } else {
-            const uint32_t off = static_cast<uint32_t>(rank * half * BK3 * 4);
-            tma_load_2d_mc(b + off, &map_bh, kb * BK3, I.n0 + rank * half, &fullW[s], (1u << CL) - 1u);
-            if (p.terms == 3)
-              tma_load_2d_mc(b + b_bytes + off, &map_bl, kb * BK3, I.n0 + rank * half, &fullW[s], (1u << CL) - 1u);
-          }
+          tma_load_2d(b, &map_bh, kb * BK3, I.n0, &fullW[s]);  // this CTA's own column tile
+          if (p.terms == 3) tma_load_2d(b + b_bytes, &map_bl, kb * BK3, I.n0, &fullW[s]);
         }
       }
     }
@@ -1258,8 +1266,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
               mma_tf32_ts_e(d, ah + kk * 8, desc_k128(bh + kk * 32), idesc, (kb == 0 && kk == 0) ? 0u : 1u);
           }
           mma_commit_e(&tslot[j]);  // TMEM A slot j reusable
-          if (CL == 1) mma_commit_e(&emptyW[w]);  // W slot w reusable
-          else mma_commit_mc_e(&emptyW[w], (1u << CL) - 1u);  // ... in every CTA of the cluster
+          mma_commit_e(&emptyW[w]);  // W slot w reusable
         }
         __syncwarp();
       }
@@ -1306,7 +1313,10 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
                        : "=f"(x[4 * c]), "=f"(x[4 * c + 1]), "=f"(x[4 * c + 2]), "=f"(x[4 * c + 3])
                        : "r"(rbase + static_cast<uint32_t>(((c ^ (row & 7)) << 4))));
         __syncwarp();
-        if (lane == 0) mbar_arrive(&emptyA[s]);  // the raw tile is in registers: the producer may refill
+        if (lane == 0) {  // the raw tile is in registers: the producer(s) may refill (CL = 2: both write it)
+          mbar_arrive(&emptyA[s]);
+          if (CL == 2) mbar_arrive_peer(&emptyA[s], static_cast<uint32_t>(rank ^ 1));
+        }
         uint32_t hi[BK3], lo[BK3];
         if (F16) {  // 16 fp16 pairs of hi, then 16 of lo: TMEM columns [0, 16) and [16, 32) of the slot
 #pragma unroll
@@ -1561,7 +1571,7 @@ void finish_params3(Params& p, bool f16) {
 inline int smem_bytes3(const Params& p, bool f16) {
   return p.nst * BM * BK3 * 4 + p.nwst * 2 * p.bnr * BK3 * (f16 ? 2 : 4) + 4 * p.epi_chunks * 4096 + 1024;
 }
-int g_gemm3_cluster = 1;  // v3 cluster size for the W multicast ("gemm3_cluster": 1 or 2)
+int g_gemm3_cluster = 1;  // v3 NN / NT: 2 = 2-CTA clusters multicasting A to both column tiles ("gemm3_cluster")
 // v3 NN / NT in TF32X3 mode: scaled fp16 two-term split on kind::f16 ("gemm_f16"). Off by default: in the
 // step it measured neutral to +0.1 ms per C4 epoch against 3xTF32 on three boxes (the A stream, not the
 // MMA issue, paces these kernels)
@@ -1577,7 +1587,7 @@ void launch3x(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl
   if (first_on_device(attr, cur_dev()))
     TC_CUDA(cudaFuncSetAttribute(gemm_tc3<MODE, CL, EXT, F16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemMax3 - (F16 ? 4096 : 0)));
-  const int npi = ((p.m_tiles + CL - 1) / CL) * p.n_tiles;
+  const int npi = CL == 1 ? p.m_tiles * p.n_tiles : p.m_tiles;  // CL = 2: one row tile per cluster item
   const int grid = CL * std::max(1, std::min(npi, num_sms() / CL));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
@@ -1763,12 +1773,13 @@ int gemm(int mode, bool ta, bool tb, int64_t M, int64_t N, int64_t K, const floa
     if (g_gemm_version == 3) {  // 32-K stages, SWIZZLE_128B boxes
       finish_params3(p, false);
       const CUtensorMap ma3 = make_map(A, K, M, lda, BK3, BM, CU_TENSOR_MAP_SWIZZLE_128B);
-      const int CL = g_gemm3_cluster;
-      const CUtensorMap mbh3 = make_map(bh, kp, p.np, kp, BK3, p.bnr / CL, CU_TENSOR_MAP_SWIZZLE_128B);
-      const CUtensorMap mbl3 = make_map(bl, kp, p.np, kp, BK3, p.bnr / CL, CU_TENSOR_MAP_SWIZZLE_128B);
+      const int CL = (g_gemm3_cluster == 2 && p.n_tiles == 2) ? 2 : 1;  // A multicast needs two column tiles
+      const CUtensorMap mbh3 = make_map(bh, kp, p.np, kp, BK3, p.bnr, CU_TENSOR_MAP_SWIZZLE_128B);
+      const CUtensorMap mbl3 = make_map(bl, kp, p.np, kp, BK3, p.bnr, CU_TENSOR_MAP_SWIZZLE_128B);
+      const CUtensorMap ma3h = make_map(A, K, M, lda, BK3, BM / 2, CU_TENSOR_MAP_SWIZZLE_128B);  // CL = 2 halves
       if (CL == 2) {
-        if (!tb) launch3<NN, 2>(ma3, mbh3, mbl3, mc, p, s);
-        else launch3<NT, 2>(ma3, mbh3, mbl3, mc, p, s);
+        if (!tb) launch3<NN, 2>(ma3h, mbh3, mbl3, mc, p, s);
+        else launch3<NT, 2>(ma3h, mbh3, mbl3, mc, p, s);
       } else {
         if (!tb) launch3<NN, 1>(ma3, mbh3, mbl3, mc, p, s);
         else launch3<NT, 1>(ma3, mbh3, mbl3, mc, p, s);
