@@ -1703,6 +1703,13 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
       tc::set_gemm3_cluster(static_cast<int>(value));
     } else if (k == "gemm3_wring") {
       tc::set_w3_bytes(static_cast<int>(value));
+    } else if (k == "l2_persist_mb") {  // L2 set-aside for persisting (evict_last) lines on the current device
+      if (value < 0) throw ValueError("tuning: l2_persist_mb must be >= 0");
+      int dev = 0, maxp = 0;
+      MG_CUDA(cudaGetDevice(&dev));
+      MG_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+      MG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize,
+                                 std::min<size_t>(static_cast<size_t>(value) << 20, static_cast<size_t>(maxp))));
     } else if (k == "stage_fold") {
       if (value < 0 || value > 64) throw ValueError("tuning: stage_fold must be 0 (off) or a group size 2..64");
       g_stage_fold = static_cast<int>(value);
