@@ -968,8 +968,11 @@ void upload_tile(mg_group& g, Worker& w, const Tile& t, DevTile& d, const DevTil
       MG_CUDA(cudaMemcpy(d.items, seg_items.data(), sizeof(int4) * seg_items.size(), cudaMemcpyHostToDevice));
     if (!hubs.empty()) MG_CUDA(cudaMemcpy(d.hubs, hubs.data(), sizeof(int4) * hubs.size(), cudaMemcpyHostToDevice));
     if (n_light > 0) light_items_device(d.row_ptr, t.rows, fast_cuts(d.nnz).ht, n_light, d.items + seg_items.size());
+    // row-streaming pieces only where the stream kernel will run ("spmm_stream", read here at creation)
     std::vector<int4> pieces;
-    build_stream_pieces(t.row_ptr, seg_items, pieces);
+    const int smode = g_spmm_stream.load();
+    const double avg_nnz = t.rows ? static_cast<double>(d.nnz) / static_cast<double>(t.rows) : 0.0;
+    if (smode == 1 || (smode == 2 && avg_nnz < kStreamRowNnz)) build_stream_pieces(t.row_ptr, seg_items, pieces);
     d.pieces = dalloc_t<int4>(g, w, std::max<size_t>(1, pieces.size()));
     d.n_pieces = static_cast<int>(pieces.size());
     if (!pieces.empty())
