@@ -1704,6 +1704,8 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
       tc::set_tn_chunk(static_cast<int>(value));
     } else if (k == "gemm3_cluster") {
       tc::set_gemm3_cluster(static_cast<int>(value));
+    } else if (k == "gemm3_epi") {
+      tc::set_epi_chunks3(static_cast<int>(value));
     } else if (k == "gemm3_wring") {
       tc::set_w3_bytes(static_cast<int>(value));
     } else if (k == "l2_persist_mb") {  // L2 set-aside for persisting (evict_last) lines on the current device

@@ -1559,10 +1559,11 @@ inline int smem_bytes2(const Params& p, int bk) { return p.nst * (BM * bk * 4 + 
 
 // v3 (NN / NT): A ring as deep as the shared memory left after the W ring and the epilogue buffers.
 constexpr int kSmemMax3 = 232448 - 2048;  // sm_100 per-block maximum, minus static barriers and alignment
+int g_epi_chunks3 = 2;  // v3 NN / NT epilogue buffers per warp without the relu_backward mask ("gemm3_epi", 1 or 2)
 int g_w3_bytes = 96 * 1024;  // v3 W ring budget ("gemm3_wring", bytes): 3 stages of a 128-column tile
 void finish_params3(Params& p, bool f16) {
   const int wst = 2 * p.bnr * BK3 * (f16 ? 2 : 4), ast = BM * BK3 * 4;
-  p.epi_chunks = p.epi == 1 ? 4 : 2;
+  p.epi_chunks = p.epi == 1 ? 4 : g_epi_chunks3;
   const int wbytes = p.epi == 1 ? std::min(g_w3_bytes, 64 * 1024) : g_w3_bytes;
   p.nwst = std::max(2, std::min(kMaxW3, wbytes / wst));
   const int avail = kSmemMax3 - (f16 ? 4096 : 0);  // F16: the per-row scale buffers are static shared memory
@@ -1655,6 +1656,11 @@ void set_gemm_f16_min_k(int k) {
 void set_gemm3_cluster(int c) {
   if (c != 1 && c != 2) throw ValueError("tuning: gemm3_cluster must be 1 or 2");
   g_gemm3_cluster = c;
+}
+
+void set_epi_chunks3(int c) {
+  if (c != 1 && c != 2) throw ValueError("tuning: gemm3_epi must be 1 or 2");
+  g_epi_chunks3 = c;
 }
 
 void set_w3_bytes(int bytes) {

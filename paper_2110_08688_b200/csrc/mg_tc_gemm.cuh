@@ -28,7 +28,8 @@ int gemm_tn_blocks(int mode, int nblocks, const int64_t* begin, const int64_t* l
 size_t nn_workspace_bytes(int64_t N, int64_t K);
 void set_tn_chunk(int rows);
 void set_gemm_version(int v);
-void set_w3_bytes(int bytes);  // v3 W ring budget
+void set_w3_bytes(int bytes);
+void set_epi_chunks3(int c);  // v3 epilogue 32x32 buffers per warp (1 or 2) without the relu_backward mask  // v3 W ring budget
 void set_gemm3_cluster(int c);
 void set_gemm_f16(int on);
 void set_gemm_f16_min_k(int k);
