@@ -1869,6 +1869,8 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
           MG_CUDA(cudaMemcpyAsync(w.x, xsrc, sizeof(float) * w.rows * p->d0, cudaMemcpyHostToDevice, xs));
         }
         for (int j = 0; j < world; ++j) {
+          // a stage folded into a group is only ever read through the group's merged tile (below)
+          if (g->fold && w.step_first[w.step_of[j]] != w.step_last[w.step_of[j]]) continue;
           const bool tr = d == 1 && world == 1 && g_bwd_transpose.load();
           upload_tile(*g, w, p->tiles[d][w.rank][j], w.tiles[d][j], tr ? &w.tiles[0][0] : nullptr);
           max_segments = std::max(max_segments, w.tiles[d][j].n_segments);

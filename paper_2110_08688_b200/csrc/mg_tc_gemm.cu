@@ -1157,13 +1157,8 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
     for (int q = 0; q < 4; ++q) mbar_init(&oldbar[q], 1);
     if (F16)
       for (int b = 0; b < kRS3; ++b) {
-        mbar_init(&rsready[b], 4);
-        mbar_init(&rsfree[b], 4);
-      }
-    if (F16)
-      for (int b = 0; b < kRS3; ++b) {
-        mbar_init(&rsready[b], 4);
-        mbar_init(&rsfree[b], 4);
+        mbar_init(&rsready[b], 128);  // every split thread releases its own row's scale
+        mbar_init(&rsfree[b], 128);   // every epilogue thread has read its row's scale
       }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -1296,9 +1291,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
         const int b = static_cast<int>(ic % kRS3);
         if (ic >= static_cast<uint32_t>(kRS3)) mbar_wait(&rsfree[b], ((ic / kRS3) - 1) & 1);
         rsinv[b][row] = ldexpf(1.0f, -e);
-        __threadfence_block();  // every lane's scale is visible CTA-wide before the warp's single arrival
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&rsready[b]);
+        mbar_arrive(&rsready[b]);  // per thread: each arrival releases exactly the write it orders
       }
       for (int kb = 0; kb < nkb; ++kb, ++sc, ra.next()) {
         const int s = ra.idx, j = sc % kTSlots3;
@@ -1385,8 +1378,7 @@ __global__ void __launch_bounds__(kThreads3, 1) gemm_tc3(const __grid_constant__
             const int rb = static_cast<int>(ac % kRS3);
             mbar_wait(&rsready[rb], (ac / kRS3) & 1);
             rinv = rsinv[rb][q * 32 + lane];
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&rsfree[rb]);
+            mbar_arrive(&rsfree[rb]);
           }
         }
         if (p.epi == 1) mbar_wait(&oldbar[q], (mph++) & 1);
