@@ -873,11 +873,12 @@ __global__ void __launch_bounds__(256) softmax_xent(float* __restrict__ logits, 
           my_loss += (double)(logf(se) - (zlab - mx));
           my_corr += (arg == label) ? 1.0 : 0.0;
         }
+        const float scale = __fdiv_rn(inv_denom, se);  // one division per row: g = e^(z - max) * (1/denom) / sum
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
           const int j = lr + LPR * q;
           if (j < C) {
-            float g = __fmul_rn(__fdiv_rn(ex[q], se), inv_denom);
+            float g = __fmul_rn(ex[q], scale);
             if (j == label) g = __fsub_rn(g, inv_denom);
             row[j] = g;
           }
