@@ -1912,7 +1912,8 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       if (cfg.gemm_mode == MG_GEMM_TF32X3 && cfg.spmm_mode == MG_SPMM_FAST && tc::f16_enabled()) {
         const size_t n_rm = static_cast<size_t>(L + 2) * 2 * std::max<index_t>(1, w.rows);
         w.rm = dalloc_t<float>(*g, w, n_rm);
-        if (std::getenv("MGGCN_POISON_RM")) MG_CUDA(cudaMemset(w.rm, 0x7E, sizeof(float) * n_rm));  // debug aid
+        // test hook: row maxima start as 8e37, so a row read before its producer wrote it breaks training
+        if (std::getenv("MGGCN_POISON_RM")) MG_CUDA(cudaMemset(w.rm, 0x7E, sizeof(float) * n_rm));
       }
       // parameters, Adam state, W-grad staging (gcn.hpp:150-158), padded ld_l x ld_{l+1}
       for (int l = 0; l < L; ++l) {

@@ -270,9 +270,11 @@ def test_f16_split_training(ref, P):
     ds = R.synth_graph(3000, 8.0, 0.7, 11, dims[0], dims[-1])
     cfg = R.GcnConfig(dims, epochs=4, seed=2, permute=True, overlap=P > 1, gemm_mode=R.GEMM_TF32X3,
                       spmm_mode=R.SPMM_FAST, aggregate_input=True)
+    import os
     R.set_tuning("gemm_f16", 1)
     R.set_tuning("gemm_f16_min_k", 0)
-    try:
+    os.environ["MGGCN_POISON_RM"] = "1"  # row maxima start as 8e37: any row read before its producer wrote it
+    try:                                  # would scale its A row to zero and break the trajectory
         got = R.train_run(ds, cfg, R.TrainOptions(workers=P, devices=[0] * P,
                                                  transport=R.TRANSPORT_NCCL if P == 1 else R.TRANSPORT_LOCAL))
         with R.Group(cfg, R.prepare_data(ds, cfg, P), P, devices=[0] * P,
@@ -283,6 +285,7 @@ def test_f16_split_training(ref, P):
             rm = g.read(R.T_ROWMAX, 0)
             assert np.array_equal(np.maximum(rm[:, 0], rm[:, 1]), np.abs(a0).max(1))  # producer-written maxima
     finally:
+        os.environ.pop("MGGCN_POISON_RM", None)
         R.set_tuning("gemm_f16", 0)
         R.set_tuning("gemm_f16_min_k", 128)
     r64 = ref.train_run(ref.synth(3000, 8.0, 0.7, 11, dims[0], dims[-1], dtype=np.float64),
