@@ -99,6 +99,9 @@ int32_t mg_abi_version(void);
 /* Process-wide tuning knobs (no reference analogue; defaults in DESIGN.md):
  *   "heavy_row"  nonzeros from which a tile row takes the cp.async hub-row SpMM path (default 4096)
  *   "profile"    1 = record per-kernel CUDA events during steps (mg_group_last_profile)
+ *   "step_graph" 1 (default): training steps of one-worker groups (no collectives) are captured once as a
+ *                CUDA graph and replayed (Adam's per-step constants patched into the graph); not used with
+ *                the timeline, "profile", dropout or the stall hook; 0: every kernel launched per step
  *   "tn_chunk"   W-grad split-K chunk in rows (multiple of 256, default 4096)
  *   "fast_segment"  hub-row segment length of MG_SPMM_FAST (default 2048)
  *   "spmm_slab" / "spmm_narrow_group"  SpMM launch-geometry experiments (default 0 = off)
@@ -356,6 +359,8 @@ mg_status mg_group_buffer_audit(mg_group* g, int32_t* large_buffers, int64_t* st
  * of kernels this library launched over the same steps (always counted). */
 mg_status mg_group_last_profile(mg_group* g, double* spmm_us, double* gemm_us, double* other_us,
                                 int64_t* kernels);
+/* Training steps of this group replayed from its captured CUDA graph ("step_graph"), and captures made. */
+mg_status mg_group_graph_steps(mg_group* g, int64_t* replays, int64_t* captures);
 void mg_group_destroy(mg_group* g);
 
 /* ---------------------------------------------------------------- timeline

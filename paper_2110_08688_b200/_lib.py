@@ -101,6 +101,7 @@ SIGNATURES = [
     ("mg_group_rows", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     ("mg_group_buffer_audit", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("mg_group_last_profile", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("mg_group_graph_steps", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("mg_group_backward", C.c_int, [C.c_void_p]),
     ("mg_group_destroy", None, [C.c_void_p]),
     ("mg_group_set_timeline", C.c_int, [C.c_void_p, C.c_int32]),

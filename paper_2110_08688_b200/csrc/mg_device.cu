@@ -60,6 +60,8 @@ std::atomic<long long> g_watchdog_ms{0};  // host-wait timeout before the group 
 std::atomic<long long> g_debug_stall_us{0};  // test hook: a spin kernel of this length at every step start
 std::atomic<int> g_nccl_single{0};  // test hook: one-rank groups also get an NCCL communicator (exercised path)
 std::atomic<int> g_profile{0};
+std::atomic<int> g_step_graph{1};  // one-worker training steps replayed from a captured CUDA graph
+std::atomic<uint64_t> g_tuning_epoch{1};  // bumped by every mg_set_tuning: a captured step graph is stale
 std::atomic<int> g_spmm_slab{0};  // floats per column-slab pass of the SpMM (0 = the whole width, <= 1024)
 std::atomic<int> g_narrow_group{0};  // lanes per row for widths of 33..64 floats (0 = 16, or 4 / 8)
 int narrow_group() { return g_narrow_group.load(); }
@@ -671,6 +673,7 @@ struct Worker {
   ncclComm_t comm = nullptr;
   // events (reused every step)
   cudaEvent_t prior, heavy_fork, heavy_join, loss_done, stats_done, src_ready, copy_done, ar_ready, ar_done;
+  cudaEvent_t join1 = nullptr, join2 = nullptr;  // step graph: s1 / s2 work enqueued before a graph launch
   std::vector<cudaEvent_t> bc_done, mult, wg_done, red_done;
   cudaEvent_t t_start, t_end;
   // timeline recorder (mg_group_set_timeline): timing events on the task's lane stream, base on s0
@@ -727,6 +730,25 @@ struct mg_group {
   uint64_t tl_next = 1;
   std::vector<TlRec> tl;
   std::vector<mg_timeline_event> tl_out;  // last drained events (deps point into tl)
+  // The training step captured once as a CUDA graph (one-worker groups, `step_graph` tuning): replayed
+  // with cudaGraphLaunch, the Adam launches' step-dependent constants patched per step.
+  struct StepGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    struct AdamNode {
+      cudaGraphNode_t node;
+      cudaKernelNodeParams p;
+      int size, blocks, run;
+      const float* stage;
+      float *w, *g, *m, *v;
+      mg::k::AdamConsts c;
+      void* args[9];
+    };
+    std::vector<AdamNode> adam;
+    int kernels = 0;
+    uint64_t epoch = 0;
+  } sg;
+  int64_t graph_replays = 0, graph_captures = 0;
 };
 
 namespace mg {
@@ -1648,6 +1670,134 @@ void read_stats(mg_group& g) {
   g.last_acc = w.h_stats[1] / static_cast<double>(g.mask_count);
 }
 
+// ---------------------------------------------------------------- the step as a CUDA graph
+// One-worker groups (no collectives) replay a captured graph of the whole step: at small sizes (C1, C2) the
+// step is ~30 launches of a few microseconds each, and the graph removes the per-launch host cost and
+// the inter-kernel launch gaps. The step's schedule depends only on the group and the tuning (captured
+// again after any mg_set_tuning); what changes from step to step — Adam's bias corrections — is
+// patched into the captured finalize_adam nodes. Not used with the timeline, the profiler (their events
+// are per step), dropout (its key depends on t), the stall hook or the GeMM debug environment.
+bool step_graph_ok(const mg_group& g) {
+  static const bool debug_env = std::getenv("MGGCN_TC_TRACE") || std::getenv("MGGCN_TC_DEBUG");
+  return g_step_graph.load() && !debug_env && g.workers.size() == 1 && g.world == 1 && !g.workers[0]->comm &&
+         !g.tl_on && !g_profile.load() && !g_debug_stall_us.load() && !(g.cfg.dropout > 0.0);
+}
+
+void set_adam_nodes(mg_group& g, int t) {
+  const Config& c = g.cfg;
+  const k::AdamConsts ac = adam_consts(c.lr, c.beta1, c.beta2, c.epsilon, t);
+  for (auto& a : g.sg.adam) {
+    a.c = ac;
+    MG_CUDA(cudaGraphExecKernelNodeSetParams(g.sg.exec, a.node, &a.p));
+  }
+}
+
+void capture_step(mg_group& g, Step& st) {
+  Worker& w = *g.workers[0];
+  if (g.sg.exec) MG_CUDA(cudaGraphExecDestroy(g.sg.exec));
+  if (g.sg.graph) MG_CUDA(cudaGraphDestroy(g.sg.graph));
+  g.sg = mg_group::StepGraph{};
+  g.kernels_last = 0;
+  MG_CUDA(cudaStreamBeginCapture(w.s0, cudaStreamCaptureModeRelaxed));
+  cudaGraph_t graph = nullptr;
+  try {
+    st.forward();
+    st.loss_grad();
+    st.backward();
+    st.finalize(true, 1);
+    // every forked stream joins s0 before the capture ends
+    cudaStreamCaptureStatus cs;
+    for (auto [s, e] : {std::pair{w.s1, w.join1}, std::pair{w.s2, w.join2}}) {
+      MG_CUDA(cudaStreamIsCapturing(s, &cs));
+      if (cs != cudaStreamCaptureStatusActive) continue;
+      MG_CUDA(cudaEventRecord(e, s));
+      MG_CUDA(cudaStreamWaitEvent(w.s0, e, 0));
+    }
+  } catch (...) {
+    cudaStreamEndCapture(w.s0, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    (void)cudaGetLastError();
+    throw;
+  }
+  MG_CUDA(cudaStreamEndCapture(w.s0, &graph));
+  g.sg.graph = graph;
+  // events recorded inside the capture can only be waited on inside it: record each once outside
+  for (cudaEvent_t e : {w.prior, w.heavy_fork, w.heavy_join, w.loss_done, w.stats_done, w.src_ready, w.copy_done,
+                        w.ar_ready, w.ar_done, w.join1, w.join2})
+    MG_CUDA(cudaEventRecord(e, w.s0));
+  for (auto* vec : {&w.bc_done, &w.mult, &w.wg_done, &w.red_done})
+    for (cudaEvent_t e : *vec) MG_CUDA(cudaEventRecord(e, w.s0));
+  MG_CUDA(cudaGraphInstantiate(&g.sg.exec, graph, 0));
+  g.sg.kernels = g.kernels_last;
+  g.sg.epoch = g_tuning_epoch.load();
+  g.graph_captures++;
+  size_t n = 0;
+  MG_CUDA(cudaGraphGetNodes(graph, nullptr, &n));
+  std::vector<cudaGraphNode_t> nodes(n);
+  MG_CUDA(cudaGraphGetNodes(graph, nodes.data(), &n));
+  for (cudaGraphNode_t nd : nodes) {
+    cudaGraphNodeType ty;
+    MG_CUDA(cudaGraphNodeGetType(nd, &ty));
+    if (ty != cudaGraphNodeTypeKernel) continue;
+    cudaKernelNodeParams kp{};
+    MG_CUDA(cudaGraphKernelNodeGetParams(nd, &kp));
+    if (kp.func != reinterpret_cast<void*>(k::finalize_adam)) continue;
+    g.sg.adam.emplace_back();
+    auto& a = g.sg.adam.back();
+    a.node = nd;
+    a.p = kp;
+    void** v = kp.kernelParams;
+    a.size = *static_cast<int*>(v[0]);
+    a.blocks = *static_cast<int*>(v[1]);
+    a.stage = *static_cast<const float**>(v[2]);
+    a.w = *static_cast<float**>(v[3]);
+    a.g = *static_cast<float**>(v[4]);
+    a.m = *static_cast<float**>(v[5]);
+    a.v = *static_cast<float**>(v[6]);
+    a.run = *static_cast<int*>(v[7]);
+    a.c = *static_cast<k::AdamConsts*>(v[8]);
+  }
+  // argument storage lives in the vector's final elements
+  for (auto& a : g.sg.adam) {
+    void* args[9] = {&a.size, &a.blocks, &a.stage, &a.w, &a.g, &a.m, &a.v, &a.run, &a.c};
+    std::copy(args, args + 9, a.args);
+    a.p.kernelParams = a.args;
+    a.p.extra = nullptr;
+  }
+  if (static_cast<int>(g.sg.adam.size()) != g.cfg.layers())
+    throw CudaError("step graph: expected one Adam launch per layer, captured " + std::to_string(g.sg.adam.size()));
+}
+
+void enqueue_train_graph(mg_group& g, int t) {
+  Worker& w = *g.workers[0];
+  MG_CUDA(cudaSetDevice(w.device));
+  check_alive(g);
+  if (!g.labels_ok) throw ValueError(g.label_error);
+  if (!g.sg.exec || g.sg.epoch != g_tuning_epoch.load()) {
+    Step st(g);
+    st.set_training(t);
+    capture_step(g, st);
+  }
+  set_adam_nodes(g, t);
+  // the graph runs on s0 after everything enqueued before on s0 / s1 / s2 (the previous step's stats
+  // read-back included), and later s1 / s2 work runs after it
+  MG_CUDA(cudaEventRecord(w.join1, w.s1));
+  MG_CUDA(cudaEventRecord(w.join2, w.s2));
+  MG_CUDA(cudaStreamWaitEvent(w.s0, w.join1, 0));
+  MG_CUDA(cudaStreamWaitEvent(w.s0, w.join2, 0));
+  MG_CUDA(cudaStreamWaitEvent(w.s0, w.stats_done, 0));
+  MG_CUDA(cudaEventRecord(w.t_start, w.s0));
+  MG_CUDA(cudaGraphLaunch(g.sg.exec, w.s0));
+  MG_CUDA(cudaEventRecord(w.stats_done, w.s0));
+  MG_CUDA(cudaEventRecord(w.t_end, w.s0));
+  MG_CUDA(cudaStreamWaitEvent(w.s1, w.t_end, 0));
+  MG_CUDA(cudaStreamWaitEvent(w.s2, w.t_end, 0));
+  g.kernels_last = g.sg.kernels;
+  g.kernels_total += g.sg.kernels;
+  g.graph_replays++;
+  g.stats_pending = true;
+}
+
 }  // namespace
 }  // namespace mg
 
@@ -1659,6 +1809,7 @@ extern "C" {
 mg_status mg_set_tuning(const char* key, int64_t value) {
   return guarded([&] {
     const std::string k = key ? key : "";
+    g_tuning_epoch.fetch_add(1);
     if (k == "heavy_row") {
       if (value < 1) throw ValueError("tuning: heavy_row must be >= 1");
       g_heavy_row = static_cast<int>(std::min<int64_t>(value, 1 << 30));
@@ -1672,6 +1823,8 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
       g_nccl_single = value != 0 ? 1 : 0;
     } else if (k == "profile") {
       g_profile = value != 0 ? 1 : 0;
+    } else if (k == "step_graph") {
+      g_step_graph = value != 0 ? 1 : 0;
     } else if (k == "spmm_narrow_group") {
       if (value != 0 && value != 4 && value != 8) throw ValueError("tuning: spmm_narrow_group must be 0, 4 or 8");
       g_narrow_group = static_cast<int>(value);
@@ -1828,7 +1981,7 @@ mg_status mg_group_create(const mg_config* cfgp, const mg_partition* p, int32_t 
       MG_CUDA(cudaStreamCreateWithFlags(&w.s1, cudaStreamNonBlocking));
       MG_CUDA(cudaStreamCreateWithFlags(&w.s2, cudaStreamNonBlocking));
       for (auto* e : {&w.prior, &w.heavy_fork, &w.heavy_join, &w.loss_done, &w.stats_done, &w.src_ready, &w.copy_done,
-                      &w.ar_ready, &w.ar_done})
+                      &w.ar_ready, &w.ar_done, &w.join1, &w.join2})
         *e = mk_event();
       for (int j = 0; j < world; ++j) {
         w.bc_done.push_back(mk_event());
@@ -2013,6 +2166,10 @@ mg_status mg_group_init_params(mg_group* g) {
 }
 
 static void enqueue_train(mg_group* g, int t, bool adam) {
+  if (adam && mg::step_graph_ok(*g)) {
+    mg::enqueue_train_graph(*g, t);
+    return;
+  }
   Step st(*g);
   st.set_training(t);
   st.begin();
@@ -2264,6 +2421,14 @@ mg_status mg_group_last_profile(mg_group* g, double* spmm_us, double* gemm_us, d
   });
 }
 
+mg_status mg_group_graph_steps(mg_group* g, int64_t* replays, int64_t* captures) {
+  return guarded([&] {
+    if (!g) throw ValueError("group: null");
+    if (replays) *replays = g->graph_replays;
+    if (captures) *captures = g->graph_captures;
+  });
+}
+
 void mg_group_destroy(mg_group* g) {
   if (!g) return;
   for (auto& wp : g->workers) {
@@ -2276,7 +2441,7 @@ void mg_group_destroy(mg_group* g) {
     for (auto& a : w.allocs) block_cache().put(w.device, a.first, a.second);
     if (w.h_stats) cudaFreeHost(w.h_stats);
     for (cudaEvent_t e : {w.prior, w.heavy_fork, w.heavy_join, w.loss_done, w.stats_done, w.src_ready, w.copy_done,
-                          w.ar_ready, w.ar_done, w.t_start, w.t_end})
+                          w.ar_ready, w.ar_done, w.join1, w.join2, w.t_start, w.t_end})
       if (e) cudaEventDestroy(e);
     for (auto* vec : {&w.bc_done, &w.mult, &w.wg_done, &w.red_done, &w.tl_pool})
       for (cudaEvent_t e : *vec) cudaEventDestroy(e);
@@ -2285,6 +2450,8 @@ void mg_group_destroy(mg_group* g) {
       if (st) cudaStreamDestroy(st);
   }
   if (!g->workers.empty()) cudaSetDevice(g->workers[0]->device);
+  if (g->sg.exec) cudaGraphExecDestroy(g->sg.exec);
+  if (g->sg.graph) cudaGraphDestroy(g->sg.graph);
   for (cudaEvent_t e : g->prof_pool) cudaEventDestroy(e);
   delete g;
 }

@@ -773,6 +773,12 @@ class Group:
         _check(lib().mg_group_last_profile(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(kk)))
         return kk.value
 
+    def graph_steps(self):
+        """(steps replayed from the captured CUDA graph, captures made) — see the "step_graph" tuning."""
+        r, c = C.c_int64(), C.c_int64()
+        _check(lib().mg_group_graph_steps(self._h, C.byref(r), C.byref(c)))
+        return r.value, c.value
+
     def logits(self, rank: Optional[int] = None):
         return self.read(T_AHW, len(self.dims) - 2, rank)
 

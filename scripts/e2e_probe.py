@@ -9,6 +9,9 @@ from paper_2110_08688_b200 import rowgcn as R  # noqa: E402
 
 SHAPES = {"c4": (2449029, 50.6, [100, 256, 256, 47]), "c2": (169343, 13.6, [128, 256, 256, 40]),
           "c1": (2708, 3.9, [1433, 16, 7])}
+for kv in filter(None, os.environ.get("MG_TUNE", "").split(",")):  # e.g. MG_TUNE=step_graph=0
+    k, v = kv.split("=")
+    R.set_tuning(k, int(v))
 n, deg, dims = SHAPES[sys.argv[1] if len(sys.argv) > 1 else "c4"]
 t0 = time.time()
 ds = R.synth_graph(n, deg, 0.7, 1, dims[0], dims[-1])
