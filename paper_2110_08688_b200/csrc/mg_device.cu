@@ -2606,23 +2606,35 @@ mg_status mg_dev_gemm(int32_t ta, int32_t tb, int64_t M, int64_t N, int64_t K, c
   return guarded([&] {
     if (epilogue < 0 || epilogue > 2) throw ValueError("gemm: unknown epilogue");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    // workspaces come from the block cache (no cudaMalloc / cudaFree per call) and go back to it after a
+    // stream synchronise
+    const int dev = cur_device();
     float* ws = nullptr;
-    size_t wsb = 0;
-    float* rm = nullptr;  // NN / NT in TF32X3: A's per-row max pairs, as the training step's producers write them
+    size_t wsb = 0, wsr = 0, rmr = 0;
+    float* rm = nullptr;  // NN / NT fp16 split: A's per-row max pairs, as the training step's producers write them
     if (mode != MG_GEMM_EXACT) {
       wsb = ta ? tc::tn_workspace_bytes(M, N, std::max<int64_t>(K, 1)) : tc::nn_workspace_bytes(N, K);
-      MG_CUDA(cudaMalloc(&ws, wsb));
-      if (!ta && mode == MG_GEMM_TF32X3 && M > 0) {
-        MG_CUDA(cudaMalloc(&rm, sizeof(float) * 2 * M));
+      wsr = BlockCache::round(wsb);
+      ws = static_cast<float*>(block_cache().get(dev, wsr));
+      if (!ta && mode == MG_GEMM_TF32X3 && M > 0 && tc::f16_enabled()) {
+        rmr = BlockCache::round(sizeof(float) * 2 * M);
+        rm = static_cast<float*>(block_cache().get(dev, rmr));
         row_absmax_pairs<<<static_cast<int>(std::min<int64_t>(4096, (M + 7) / 8)), 256, 0, st>>>(A, lda, M, K, rm);
         MG_LAUNCHED();
       }
     }
-    gemm_launch(mode, ta != 0, tb != 0, M, N, K, A, lda, B, ldb, Cm, ldc, epilogue, st, ws, wsb, k::Epi{}, rm);
+    try {
+      gemm_launch(mode, ta != 0, tb != 0, M, N, K, A, lda, B, ldb, Cm, ldc, epilogue, st, ws, wsb, k::Epi{}, rm);
+    } catch (...) {
+      cudaStreamSynchronize(st);
+      block_cache().put(dev, ws, wsr);
+      block_cache().put(dev, rm, rmr);
+      throw;
+    }
     if (ws) {
       MG_CUDA(cudaStreamSynchronize(st));
-      MG_CUDA(cudaFree(ws));
-      if (rm) MG_CUDA(cudaFree(rm));
+      block_cache().put(dev, ws, wsr);
+      block_cache().put(dev, rm, rmr);
     }
   });
 }
