@@ -1692,6 +1692,17 @@ void set_adam_nodes(mg_group& g, int t) {
   }
 }
 
+// Events recorded inside a stream capture can only be waited on inside it: record each once outside, so
+// the stream path (and the host waits) can use them again.
+void release_captured_events(Worker& w) {
+  for (cudaEvent_t e : {w.prior, w.heavy_fork, w.heavy_join, w.loss_done, w.stats_done, w.src_ready, w.copy_done,
+                        w.ar_ready, w.ar_done, w.join1, w.join2})
+    cudaEventRecord(e, w.s0);
+  for (auto* vec : {&w.bc_done, &w.mult, &w.wg_done, &w.red_done})
+    for (cudaEvent_t e : *vec) cudaEventRecord(e, w.s0);
+  MG_LAUNCHED();
+}
+
 void capture_step(mg_group& g, Step& st) {
   Worker& w = *g.workers[0];
   if (g.sg.exec) MG_CUDA(cudaGraphExecDestroy(g.sg.exec));
@@ -1717,16 +1728,12 @@ void capture_step(mg_group& g, Step& st) {
     cudaStreamEndCapture(w.s0, &graph);
     if (graph) cudaGraphDestroy(graph);
     (void)cudaGetLastError();
+    release_captured_events(w);
     throw;
   }
   MG_CUDA(cudaStreamEndCapture(w.s0, &graph));
   g.sg.graph = graph;
-  // events recorded inside the capture can only be waited on inside it: record each once outside
-  for (cudaEvent_t e : {w.prior, w.heavy_fork, w.heavy_join, w.loss_done, w.stats_done, w.src_ready, w.copy_done,
-                        w.ar_ready, w.ar_done, w.join1, w.join2})
-    MG_CUDA(cudaEventRecord(e, w.s0));
-  for (auto* vec : {&w.bc_done, &w.mult, &w.wg_done, &w.red_done})
-    for (cudaEvent_t e : *vec) MG_CUDA(cudaEventRecord(e, w.s0));
+  release_captured_events(w);
   MG_CUDA(cudaGraphInstantiate(&g.sg.exec, graph, 0));
   g.sg.kernels = g.kernels_last;
   g.sg.epoch = g_tuning_epoch.load();
