@@ -102,6 +102,10 @@ int32_t mg_abi_version(void);
  *   "step_graph" 1 (default): training steps of one-worker groups (no collectives) are captured once as a
  *                CUDA graph and replayed (Adam's per-step constants patched into the graph); not used with
  *                the timeline, "profile", dropout or the stall hook; 0: every kernel launched per step
+ *   "ax_cache"   1: under aggregate_input (MG_SPMM_FAST), a one-process group computes layer 0's Â·X once
+ *                and reuses it until the features are written (mg_group_write MG_T_X) or the tuning changes
+ *                (bitwise the same steps; one d0-wide SpMM fewer per step); 0 (default): every step, like
+ *                the reference
  *   "tn_chunk"   W-grad split-K chunk in rows (multiple of 256, default 4096)
  *   "fast_segment"  hub-row segment length of MG_SPMM_FAST (default 2048)
  *   "spmm_slab" / "spmm_narrow_group"  SpMM launch-geometry experiments (default 0 = off)

@@ -61,6 +61,11 @@ std::atomic<long long> g_debug_stall_us{0};  // test hook: a spin kernel of this
 std::atomic<int> g_nccl_single{0};  // test hook: one-rank groups also get an NCCL communicator (exercised path)
 std::atomic<int> g_profile{0};
 std::atomic<int> g_step_graph{1};  // one-worker training steps replayed from a captured CUDA graph
+// Opt-in ("ax_cache", default off; the bench headline never uses it): under aggregate_first, layer 0's SpMM
+// Â·X depends on the inputs only, so a one-process group computes it once and keeps it until the features
+// are written (mg_group_write) or the tuning changes. Results are bitwise those of the uncached step (the
+// same kernel wrote the same buffer); the reference recomputes it every epoch (its order_swap path).
+std::atomic<int> g_ax_cache{0};
 std::atomic<uint64_t> g_tuning_epoch{1};  // bumped by every mg_set_tuning: a captured step graph is stale
 std::atomic<int> g_spmm_slab{0};  // floats per column-slab pass of the SpMM (0 = the whole width, <= 1024)
 std::atomic<int> g_narrow_group{0};  // lanes per row for widths of 33..64 floats (0 = 16, or 4 / 8)
@@ -747,8 +752,10 @@ struct mg_group {
     std::vector<AdamNode> adam;
     int kernels = 0;
     uint64_t epoch = 0;
+    bool ax_cached = false;  // captured without layer 0's Â·X SpMM
   } sg;
   int64_t graph_replays = 0, graph_captures = 0;
+  uint64_t ax_epoch = 0;  // g_tuning_epoch when Â·X was last computed under "ax_cache" (0: not cached)
 };
 
 namespace mg {
@@ -1112,6 +1119,13 @@ __global__ void stall_kernel(long long ns) {
   }
 }
 
+// "ax_cache": groups whose ranks all live in this process only (a write to one rank's features must not
+// let the ranks of a multi-process job disagree on whether the layer-0 broadcasts run)
+bool ax_cache_applies(const mg_group& g) {
+  return g_ax_cache.load() && g.cfg.aggregate_first() && static_cast<int>(g.workers.size()) == g.world;
+}
+bool ax_cached(const mg_group& g) { return ax_cache_applies(g) && g.ax_epoch == g_tuning_epoch.load(); }
+
 // ---------------------------------------------------------------- the step (one process, all local workers)
 class Step {
  public:
@@ -1360,11 +1374,14 @@ class Step {
       const bool swap = cfg_.order_swap && dl < dl1;  // gcn.hpp:145-148
       std::vector<float*> src(nloc()), out(nloc());
       if (l == 0 && cfg_.aggregate_first()) {  // ax = Â·X (d0 wide), ahw[0] = ax·W0 (+ReLU)
-        for (size_t k = 0; k < nloc(); ++k) {
-          src[k] = W(k).x;
-          out[k] = W(k).ax;
+        if (!ax_cached(g_)) {
+          for (size_t k = 0; k < nloc(); ++k) {
+            src[k] = W(k).x;
+            out[k] = W(k).ax;
+          }
+          staged_spmm(0, dl, src, out, false, -1, L_ + 1);
+          if (ax_cache_applies(g_)) g_.ax_epoch = g_tuning_epoch.load();
         }
-        staged_spmm(0, dl, src, out, false, -1, L_ + 1);
         for (size_t k = 0; k < nloc(); ++k) {
           Worker& w = W(k);
           dev(w);
@@ -1737,6 +1754,7 @@ void capture_step(mg_group& g, Step& st) {
   MG_CUDA(cudaGraphInstantiate(&g.sg.exec, graph, 0));
   g.sg.kernels = g.kernels_last;
   g.sg.epoch = g_tuning_epoch.load();
+  g.sg.ax_cached = ax_cached(g);
   g.graph_captures++;
   size_t n = 0;
   MG_CUDA(cudaGraphGetNodes(graph, nullptr, &n));
@@ -1780,7 +1798,7 @@ void enqueue_train_graph(mg_group& g, int t) {
   MG_CUDA(cudaSetDevice(w.device));
   check_alive(g);
   if (!g.labels_ok) throw ValueError(g.label_error);
-  if (!g.sg.exec || g.sg.epoch != g_tuning_epoch.load()) {
+  if (!g.sg.exec || g.sg.epoch != g_tuning_epoch.load() || g.sg.ax_cached != ax_cached(g)) {
     Step st(g);
     st.set_training(t);
     capture_step(g, st);
@@ -1832,6 +1850,8 @@ mg_status mg_set_tuning(const char* key, int64_t value) {
       g_profile = value != 0 ? 1 : 0;
     } else if (k == "step_graph") {
       g_step_graph = value != 0 ? 1 : 0;
+    } else if (k == "ax_cache") {
+      g_ax_cache = value != 0 ? 1 : 0;
     } else if (k == "spmm_narrow_group") {
       if (value != 0 && value != 4 && value != 8) throw ValueError("tuning: spmm_narrow_group must be 0, 4 or 8");
       g_narrow_group = static_cast<int>(value);
@@ -2173,7 +2193,8 @@ mg_status mg_group_init_params(mg_group* g) {
 }
 
 static void enqueue_train(mg_group* g, int t, bool adam) {
-  if (adam && mg::step_graph_ok(*g)) {
+  // a step that has to (re)compute the cached Â·X runs on the stream path; the graph is captured without it
+  if (adam && mg::step_graph_ok(*g) && (!mg::ax_cache_applies(*g) || mg::ax_cached(*g))) {
     mg::enqueue_train_graph(*g, t);
     return;
   }
@@ -2363,6 +2384,7 @@ mg_status mg_group_write(mg_group* g, int32_t rank, int32_t which, int32_t layer
       upload_padded(v.p, src, v.rows, v.cols, v.ld);
     };
     sync_all(*g);
+    if (which == MG_T_X) g->ax_epoch = 0;  // the cached Â·X is stale
     if (rank < 0) {  // replicated tensors: write every local worker
       for (auto& wp : g->workers) write_one(*wp);
     } else {
