@@ -6,7 +6,8 @@ import ctypes as C
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libmggcn.so")
+# MGGCN_RACECHECK=1 loads the racecheck variant of the same sources (build.py --racecheck; sanitizer runs only)
+LIB_PATH = os.path.join(PKG, "libmggcn_rc.so" if os.environ.get("MGGCN_RACECHECK") == "1" else "libmggcn.so")
 
 c_i64p = C.POINTER(C.c_int64)
 

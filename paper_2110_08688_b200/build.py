@@ -11,6 +11,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libmggcn.so")
+LIB_RC = os.path.join(PKG, "libmggcn_rc.so")
 SOURCES = ["mg_host.cpp", "mg_io.cpp", "mg_timeline.cpp", "mg_json.cpp", "mg_synth_rank.cpp", "mg_device.cu", "mg_tc_gemm.cu", "mg_prepare_dev.cu"]
 HEADERS = ["mg_internal.hpp", "mg_kernels.cuh", "mg_tc_gemm.cuh", "mg_epi.cuh"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -31,15 +32,21 @@ def needs_build():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
+def build(force=False, verbose=False, racecheck=False):
+    """racecheck=True: libmggcn_rc.so, the compute-sanitizer racecheck variant (MG_RACECHECK_PLAIN_COPIES:
+    the EXACT hub-row SpMM's cp.async copies become plain loads / stores with the same ring protocol)."""
+    lib_out = LIB_RC if racecheck else LIB
+    if not racecheck and not force and not needs_build():
         return LIB
     objs = []
-    os.makedirs(os.path.join(PKG, "build"), exist_ok=True)
+    bdir = os.path.join(PKG, "build_rc" if racecheck else "build")
+    os.makedirs(bdir, exist_ok=True)
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    if racecheck:
+        common += ["-DMG_RACECHECK_PLAIN_COPIES"]
     procs = []
     for src in SOURCES:
-        obj = os.path.join(PKG, "build", src + ".o")
+        obj = os.path.join(bdir, src + ".o")
         cmd = [nvcc(), *ARCH, "-lineinfo", *common, "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
@@ -51,14 +58,14 @@ def build(force=False, verbose=False):
             raise RuntimeError("build failed: " + " ".join(cmd) + "\n" + out)
         if verbose and out:
             print(out)
-    tmp = LIB + ".tmp"
+    tmp = lib_out + ".tmp"
     link = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-lnccl", "-lpthread"]
     r = subprocess.run(link, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed: " + " ".join(link) + "\n" + r.stdout)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib_out)
+    return lib_out
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, racecheck="--racecheck" in sys.argv))

@@ -634,7 +634,7 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __r
   if (threadIdx.x == 0) {
     for (int s = 0; s < kHeavyNst; ++s) {
       mbar_init(&full[s], 64);  // one cp.async.mbarrier.arrive.noinc per producer thread
-      mbar_init(&empty[s], 2);
+      mbar_init(&empty[s], 64);
     }
     for (int s = 0; s < kHeavyEslots; ++s) mbar_init(&efull[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -668,9 +668,20 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __r
       float* dst = buf + (size_t)s * kHeavyB * kHeavySlab;
       for (int q = pt; q < cnt * (kHeavySlab / 4); q += 64) {
         const int b = q / (kHeavySlab / 4), c = q % (kHeavySlab / 4);
+#ifdef MG_RACECHECK_PLAIN_COPIES
+        // racecheck build only (build.py --racecheck): the same ring protocol with plain loads / stores and a
+        // per-thread arrival, a form compute-sanitizer racecheck models (it does not model cp.async
+        // completion through mbarriers)
+        if (c < nchunk)
+          *reinterpret_cast<float4*>(dst + b * kHeavySlab + 4 * c) =
+              *reinterpret_cast<const float4*>(h + (size_t)er[b].x * ld + col0 + 4 * c);
+      }
+      mbar_arrive(&full[s]);
+#else
         if (c < nchunk) cp_async16(dst + b * kHeavySlab + 4 * c, h + (size_t)er[b].x * ld + col0 + 4 * c);
       }
       asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_addr(&full[s])) : "memory");
+#endif
     }
   } else {  // consumers: one column each
     const int t = threadIdx.x;
@@ -699,8 +710,7 @@ __global__ void __launch_bounds__(kHeavyThreads) spmm_exact_heavy(const int* __r
           for (int b = 0; b < cnt; ++b) acc = fma_free(acc, __int_as_float(er[b].y), bs[b * kHeavySlab]);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      mbar_arrive(&empty[s]);  // per consumer thread (an elected arrival after __syncwarp is not modelled by racecheck)
     }
     if (active) out[(size_t)r * ld + my_col] = (ep.bias || ep.thr) ? epi1(acc, relu, ep, r, my_col) : (relu ? relu1(acc) : acc);
   }

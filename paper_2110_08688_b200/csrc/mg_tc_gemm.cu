@@ -791,7 +791,6 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t full[kMaxStages], conv[kMaxStages], empty[kMaxStages], tfull[2], tempty[2], oldbar[4];
-  __shared__ uint64_t afree[kMaxStages];  // TN: A raw of the stage read by all four split warps
   __shared__ uint32_t tmem_base_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr bool B_MN = MODE == TN;  // NN/NT read the pre-split K-major B
@@ -800,16 +799,13 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
   constexpr uint32_t kBox = 32 * BKV * 4;      // TN: bytes of one {32 n, BKV k} B box (LBO along N)
   const int a_bytes = BM * BKV * 4;    // raw A tile (no swizzle): NN/NT [128 rows][16 k], TN [32 k][128 m]
   const int b_bytes = p.bnr * BKV * 4;  // one B tile (bnr = tile columns held per stage)
-  // NN / NT: A raw | B hi | B lo. TN: A raw | B raw, and B lo is written over A raw once the split warps
-  // hold A in registers (afree): a third less shared memory per stage, so a 4-deep ring instead of 3.
-  const int stage = MODE == TN ? a_bytes + b_bytes : a_bytes + 2 * b_bytes;
+  const int stage = a_bytes + 2 * b_bytes;  // A raw | B hi | B lo
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&conv[s], MODE == TN && p.terms == 3 ? 8 : 4);
       mbar_init(&empty[s], 1);
-      mbar_init(&afree[s], 4);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -882,8 +878,7 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
           tc_fence_after();
           if (p.trace && blockIdx.x == 0 && lane == 0 && sc < kTraceStages) p.trace[sc * 4 + 3] = clock64();
           {  // whole warp, elected issue (see mma_tf32_e)
-            const uint32_t bh = smem_u32(smem + s * stage + a_bytes);
-            const uint32_t bl = MODE == TN ? smem_u32(smem + s * stage) : bh + b_bytes;
+            const uint32_t bh = smem_u32(smem + s * stage + a_bytes), bl = bh + b_bytes;
             const uint32_t ah = tmem + static_cast<uint32_t>(kAcol + s * 2 * BKV), al = ah + BKV;
             if (p.terms == 3) {
               const uint64_t dbh = B_MN ? desc_mn128(bh, kBox) : desc_k64(bh);
@@ -944,10 +939,6 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
           hi[k] = __float_as_uint(h);
           lo[k] = __float_as_uint(p.terms == 3 ? split_lo(x[k], h) : 0.0f);
         }
-        if (MODE == TN) {  // every lane's A loads have returned (their values are in hi / lo): B lo may overwrite
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&afree[s]);
-        }
         const uint32_t ta = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(kAcol + s * 2 * BKV);
 #pragma unroll
         for (int c = 0; c < BKV / 16; ++c) {
@@ -975,8 +966,7 @@ __global__ void __launch_bounds__(threads2<MODE>(), 1) gemm_tc2(const __grid_con
           const int s = rp.idx;
           mbar_wait(&full[s], rp.phase);
           const uint32_t bh = smem_u32(smem + s * stage + a_bytes);
-          const uint32_t bl = smem_u32(smem + s * stage);  // over A raw (b_bytes <= a_bytes)
-          mbar_wait(&afree[s], rp.phase);
+          const uint32_t bl = bh + static_cast<uint32_t>(b_bytes);
           for (int q4 = t; q4 < b_bytes / 16; q4 += 128) {
             float4 v, l;
             asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
@@ -1551,15 +1541,13 @@ void finish_params2(Params& p, long N, bool tn, int terms) {
   p.bnr = std::min(p.np, kTileN);
   if (tn) p.bnr = (p.bnr + 31) / 32 * 32;
   const int bk = tn ? bk2<TN>() : bk2<NN>();
-  const int stage = BM * bk * 4 + (tn ? 1 : 2) * p.bnr * bk * 4;  // TN: B lo over A raw (gemm_tc2)
+  const int stage = BM * bk * 4 + 2 * p.bnr * bk * 4;
   // TMEM: the A slots (2 * bk columns each, hi | lo) live above the two 128-column accumulators
   const int tmem_slots = (512 - kAcol) / (2 * bk);
   p.nst = std::max(2, std::min({kMaxStages, tmem_slots, kSmemBudget2 / stage}));
 }
 
-inline int smem_bytes2(const Params& p, int bk, bool tn) {
-  return p.nst * (BM * bk * 4 + (tn ? 1 : 2) * p.bnr * bk * 4) + kEpiBuf + 1024;
-}
+inline int smem_bytes2(const Params& p, int bk) { return p.nst * (BM * bk * 4 + 2 * p.bnr * bk * 4) + kEpiBuf + 1024; }
 
 // v3 (NN / NT): A ring as deep as the shared memory left after the W ring and the epilogue buffers.
 constexpr int kSmemMax3 = 232448 - 2048;  // sm_100 per-block maximum, minus static barriers and alignment
@@ -1631,7 +1619,7 @@ void launch2x(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl
     TC_CUDA(cudaFuncSetAttribute(gemm_tc2<MODE, EXT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  kSmemBudget2 + kEpiBuf + 1024));
   const int grid = std::max(1, std::min(p.n_items, num_sms()));
-  gemm_tc2<MODE, EXT><<<grid, threads2<MODE>(), smem_bytes2(p, bk2<MODE>(), MODE == TN), s>>>(a, bh, bl, c, p);
+  gemm_tc2<MODE, EXT><<<grid, threads2<MODE>(), smem_bytes2(p, bk2<MODE>()), s>>>(a, bh, bl, c, p);
   TC_CUDA(cudaGetLastError());
 }
 template <int MODE>
