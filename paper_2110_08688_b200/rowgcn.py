@@ -249,9 +249,9 @@ class Dataset:
                                             C.byref(out)))
         return cls(out.value, name)
 
-    def __del__(self):
+    def __del__(self, _fin=_finalizing):  # bound at definition: module globals may be gone at exit
         h = getattr(self, "_h", None)
-        if h and h.value and not _finalizing():
+        if h and h.value and not _fin():
             try:
                 lib().mg_dataset_free(h)
             except Exception:  # interpreter teardown: the process exit releases the native object
@@ -485,9 +485,9 @@ class PreparedData:
         self.mask_count = mc.value
         self.bounds = b
 
-    def __del__(self):
+    def __del__(self, _fin=_finalizing):  # bound at definition: module globals may be gone at exit
         h = getattr(self, "_h", None)
-        if h and h.value and not _finalizing():
+        if h and h.value and not _fin():
             try:
                 lib().mg_partition_free(h)
             except Exception:  # interpreter teardown: the process exit releases the native object
@@ -552,9 +552,9 @@ class SynthRank:
         _check(lib().mg_synth_rank_info(self._h, C.byref(r0), C.byref(r), C.byref(z), C.byref(st)))
         self.row0, self.rows, self.nnz, self.stubs = r0.value, r.value, z.value, st.value
 
-    def __del__(self):
+    def __del__(self, _fin=_finalizing):  # bound at definition: module globals may be gone at exit
         h = getattr(self, "_h", None)
-        if h and h.value and not _finalizing():
+        if h and h.value and not _fin():
             try:
                 lib().mg_synth_rank_free(h)
             except Exception:  # interpreter teardown: the process exit releases the native object
@@ -639,8 +639,8 @@ class Group:
             lib().mg_group_destroy(h)
             self._h = C.c_void_p()
 
-    def __del__(self):
-        if not _finalizing():
+    def __del__(self, _fin=_finalizing):  # bound at definition: module globals may be gone at exit
+        if not _fin():
             try:
                 self.close()
             except Exception:  # interpreter teardown

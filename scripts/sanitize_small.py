@@ -44,3 +44,14 @@ prep = R.synth_prepare_rank(3000, 12.0, 0.7, 2, 40, 5, cfg, 4, 2)
 with R.Group(cfg, prep, 4, local_ranks=[2], devices=[0], transport=R.TRANSPORT_SOLO) as g:
     g.init_params()
     print("solo", g.train_step(1) == g.train_step(1) or True, flush=True)
+# late round 2: the step as a CUDA graph (default) with the opt-in Â·X cache, a feature write in between
+R.set_tuning("ax_cache", 1)
+cfg = R.GcnConfig([100, 256, 256, 47], epochs=3, seed=1, permute=True, aggregate_input=True,
+                  gemm_mode=R.GEMM_TF32X3, spmm_mode=R.SPMM_FAST)
+with R.Group(cfg, R.prepare_data(ds2, cfg, 1), 1, devices=[0]) as g:
+    g.init_params()
+    losses = [g.train_step(t) for t in (1, 2)]
+    g.write(R.T_X, 0, g.read(R.T_X, 0) * np.float32(0.5))
+    losses.append(g.train_step(3))
+    print("ax_cache + graph", losses, g.graph_steps(), flush=True)
+R.set_tuning("ax_cache", 0)
